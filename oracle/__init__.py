@@ -1,0 +1,255 @@
+"""CPU oracle of the HetuMoE (arXiv 2203.14685) token-routing path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_2203_14685_b200`` never imports it, and
+it imports nothing from the product package.
+
+This module is argument marshalling (numpy <-> ctypes) around ``liboracle.so``,
+a plain single-threaded C11 implementation compiled with
+``-O2 -ffp-contract=off`` (see ``oracle/oracle.c`` for the arithmetic and its
+PAPER.md citations).  The only logic written here in Python is the composition
+of the C calls into Algorithm 1's six steps for P simulated
+ranks (``route_multi``), which adds no arithmetic of its own.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+TOPK, KTOP1, HASH = 0, 1, 2
+RENORM, SOFTMAX = 0, 1
+PRIO_TOKEN, PRIO_SLOT = 0, 1
+F32, BF16 = 0, 1
+
+KINDS = {"topk": TOPK, "ktop1": KTOP1, "hash": HASH}
+MODES = {"renorm": RENORM, "softmax": SOFTMAX}
+PRIOS = {"token": PRIO_TOKEN, "slot": PRIO_SLOT}
+DTYPES = {"f32": F32, "bf16": BF16}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc, C11, -O2 -ffp-contract=off, no fast-math)."""
+    hdr = os.path.join(_HERE, "oracle.h")
+    if (not force and os.path.exists(_SO)
+            and os.path.getmtime(_SO) >= max(os.path.getmtime(_SRC), os.path.getmtime(hdr))):
+        return _SO
+    tmp = _SO + ".tmp%d" % os.getpid()
+    subprocess.check_call(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math",
+                           "-Wall", "-Wextra", "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
+    os.replace(tmp, _SO)
+    return _SO
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("intra_msgs", ctypes.c_int64), ("inter_msgs", ctypes.c_int64),
+                ("inter_msg_bytes", ctypes.c_int64), ("intra_bytes", ctypes.c_int64),
+                ("inter_bytes", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i32, i64 = ctypes.c_int32, ctypes.c_int64
+        L.orc_capacity.argtypes = [i32, i32, i32, ctypes.c_double]
+        L.orc_capacity.restype = i32
+        L.orc_gate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i32, i32, i32, i32,
+                               P, P, P, i32, P, P, P, P, P]
+        L.orc_gate.restype = i64
+        L.orc_layout.argtypes = [i32, i32, i32, i32, i64, P, P, P, P]
+        L.orc_layout.restype = None
+        L.orc_reverse_layout.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P, P, P, P]
+        L.orc_reverse_layout.restype = None
+        L.orc_expert_scale.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P]
+        L.orc_expert_scale.restype = None
+        L.orc_alltoall_flat.argtypes = [i32, i64, ctypes.POINTER(P), ctypes.POINTER(P)]
+        L.orc_alltoall_flat.restype = None
+        L.orc_alltoall_hier.argtypes = [i32, i32, i64, ctypes.POINTER(P), ctypes.POINTER(P),
+                                        ctypes.POINTER(_Stats)]
+        L.orc_alltoall_hier.restype = ctypes.c_int
+        L.orc_alltoall_flat_stats.argtypes = [i32, i32, i64, ctypes.POINTER(_Stats)]
+        L.orc_alltoall_flat_stats.restype = None
+        L.orc_bf16_to_f64.argtypes = [ctypes.c_uint16]
+        L.orc_bf16_to_f64.restype = ctypes.c_double
+        L.orc_f64_to_bf16.argtypes = [ctypes.c_double]
+        L.orc_f64_to_bf16.restype = ctypes.c_uint16
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def _c(a, dtype):
+    return None if a is None else np.ascontiguousarray(a, dtype=dtype)
+
+
+def capacity(S, E, k, C) -> int:
+    return int(lib().orc_capacity(S, E, k, float(C)))
+
+
+@dataclass
+class Routing:
+    expert_idx: np.ndarray  # [S, k] int32
+    slot_idx: np.ndarray    # [S, k] int32
+    weight: np.ndarray      # [S, k] float32
+    load: np.ndarray        # [E]    int32
+    slot_src: np.ndarray    # [E*cap] int32
+    S: int
+    E: int
+    k: int
+    cap: int
+    bad: int
+
+
+def gate(logits=None, *, S=None, E, k, cap, kind="topk", weight_mode="renorm",
+         priority="token", token_ids=None, table=None) -> Routing:
+    kind_i = KINDS[kind]
+    logits = _c(logits, np.float32)
+    if logits is not None:
+        S = logits.shape[0]
+        assert logits.shape == (S, E)
+    else:
+        token_ids = _c(token_ids, np.int32)
+        S = token_ids.shape[0]
+    token_ids = _c(token_ids, np.int32)
+    table = _c(table, np.int32)
+    vocab = 0 if table is None else int(table.shape[0])
+    ei = np.empty((S, k), np.int32)
+    si = np.empty((S, k), np.int32)
+    w = np.empty((S, k), np.float32)
+    load = np.empty((E,), np.int32)
+    ss = np.empty((E * cap,), np.int32)
+    bad = lib().orc_gate(kind_i, MODES[weight_mode], PRIOS[priority], S, E, k, cap,
+                         _ptr(logits), _ptr(token_ids), _ptr(table), vocab,
+                         _ptr(ei), _ptr(si), _ptr(w), _ptr(load), _ptr(ss))
+    if bad < 0:
+        raise ValueError("orc_gate rejected its arguments")
+    return Routing(ei, si, w, load, ss, S, E, k, cap, int(bad))
+
+
+def layout(x: np.ndarray, r: Routing) -> np.ndarray:
+    """x: [S, d] of any element type -> dispatch [E, cap, d] of the same type."""
+    x = np.ascontiguousarray(x)
+    S, d = x.shape
+    out = np.empty((r.E, r.cap, d), x.dtype)
+    lib().orc_layout(S, r.E, r.k, r.cap, d * x.itemsize, _ptr(r.expert_idx), _ptr(r.slot_idx),
+                     _ptr(x), _ptr(out))
+    return out
+
+
+def _dt(a):
+    if a.dtype == np.float32:
+        return F32
+    if a.dtype == np.uint16:  # raw bf16 bits
+        return BF16
+    raise TypeError("oracle data must be float32 or uint16 (bf16 bits)")
+
+
+def reverse_layout(back: np.ndarray, r: Routing) -> np.ndarray:
+    back = np.ascontiguousarray(back)
+    E, cap, d = back.shape
+    assert E == r.E and cap == r.cap
+    y = np.empty((r.S, d), back.dtype)
+    lib().orc_reverse_layout(_dt(back), r.S, r.E, r.k, r.cap, d, _ptr(r.expert_idx),
+                             _ptr(r.slot_idx), _ptr(r.weight), _ptr(back), _ptr(y))
+    return y
+
+
+def expert_scale(buf: np.ndarray, e_base: int) -> np.ndarray:
+    """buf: [nsrc, E_local, cap, d] -> s_e * buf."""
+    buf = np.ascontiguousarray(buf)
+    nsrc, El, cap, d = buf.shape
+    out = np.empty_like(buf)
+    lib().orc_expert_scale(_dt(buf), nsrc, El, e_base, cap, d, _ptr(buf), _ptr(out))
+    return out
+
+
+def _ptrs(bufs):
+    arr = (ctypes.c_void_p * len(bufs))()
+    for i, b in enumerate(bufs):
+        arr[i] = b.ctypes.data
+    return arr
+
+
+def alltoall_flat(sends):
+    P = len(sends)
+    sends = [np.ascontiguousarray(s) for s in sends]
+    nbytes = sends[0].nbytes
+    assert all(s.nbytes == nbytes for s in sends) and nbytes % P == 0
+    recvs = [np.empty_like(s) for s in sends]
+    lib().orc_alltoall_flat(P, nbytes // P, _ptrs(sends), _ptrs(recvs))
+    return recvs
+
+
+def alltoall_hier(sends, G):
+    P = len(sends)
+    sends = [np.ascontiguousarray(s) for s in sends]
+    nbytes = sends[0].nbytes
+    assert all(s.nbytes == nbytes for s in sends) and nbytes % P == 0
+    recvs = [np.empty_like(s) for s in sends]
+    st = _Stats()
+    rc = lib().orc_alltoall_hier(P, G, nbytes // P, _ptrs(sends), _ptrs(recvs), ctypes.byref(st))
+    if rc != 0:
+        raise ValueError("P % G != 0")
+    return recvs, {f: getattr(st, f) for f, _ in _Stats._fields_}
+
+
+def alltoall_flat_stats(P, G, bytes_per_peer):
+    st = _Stats()
+    lib().orc_alltoall_flat_stats(P, G, bytes_per_peer, ctypes.byref(st))
+    return {f: getattr(st, f) for f, _ in _Stats._fields_}
+
+
+def bf16_to_f64(h: int) -> float:
+    return float(lib().orc_bf16_to_f64(h))
+
+
+def f64_to_bf16(v: float) -> int:
+    return int(lib().orc_f64_to_bf16(float(v)))
+
+
+def route_multi(xs, logits_list, *, E, k, cap, kind="topk", weight_mode="renorm",
+                priority="token", token_ids_list=None, table=None, algo="flat", G=None,
+                scale=True):
+    """Algorithm 1 for P simulated ranks, experts in contiguous
+    blocks of E/P per rank (R10).  Returns (routings, dispatches, recvs, ys).
+
+    Step 1 Gate -> 2 Layout_Transform -> 3 AllToAll -> 4 expert (fixed scale,
+    R16; identity if scale=False) -> 5 AllToAll -> 6 Reverse_Layout_Transform.
+    """
+    P = len(xs)
+    assert E % P == 0
+    El = E // P
+    routings, disp, ys = [], [], []
+    for r in range(P):
+        rt = gate(None if logits_list is None else logits_list[r], E=E, k=k, cap=cap, kind=kind,
+                  weight_mode=weight_mode, priority=priority,
+                  token_ids=None if token_ids_list is None else token_ids_list[r], table=table)
+        routings.append(rt)
+        disp.append(layout(xs[r], rt))
+    a2a = alltoall_flat if algo == "flat" else (lambda s: alltoall_hier(s, G)[0])
+    recvs = a2a(disp)  # recv_r: [P_src][El][cap][d] viewed as [E, cap, d]
+    outs = []
+    for r in range(P):
+        rv = recvs[r].reshape(P, El, cap, -1)
+        outs.append(expert_scale(rv, r * El).reshape(recvs[r].shape) if scale else recvs[r])
+    backs = a2a(outs)
+    for r in range(P):
+        ys.append(reverse_layout(backs[r], routings[r]))
+    return routings, disp, recvs, ys
