@@ -1,0 +1,248 @@
+/*
+ * moe.h -- C ABI of libmoe_b200.so: the HetuMoE (arXiv 2203.14685) token-
+ * routing hot path, hand-written for B200 (sm_100a).
+ *
+ * The calls follow Algorithm 1, "General MoE Training Process"
+ * (PAPER.md:41-68):
+ *
+ *   W_(S,E), id_S = Gate(x_S)                    step 1  -> moe_gate
+ *   x'_S = Layout_Transform(x_S, id_S)           step 2  -> moe_layout
+ *   x'_S = AllToAll(x'_S)                        step 3  -> moe_alltoall
+ *   y_i += w_(i,idx) * e_idx(x_i)                step 4  (experts: out of scope;
+ *                                                         bench stand-in moe_expert_scale)
+ *   y_S = AllToAll(y_S)                          step 5  -> moe_alltoall
+ *   y_S = Reverse_Layout_Transform(y_S, id_S)    step 6  -> moe_reverse_layout
+ *
+ * Conventions (apply to every call unless stated otherwise):
+ *  - Pointers named as tensors are DEVICE pointers (cudaMalloc / torch CUDA
+ *    memory of the current device).  Host-only calls say "host".
+ *  - Every device call is asynchronous on `stream` (a cudaStream_t; NULL =
+ *    legacy default stream) and enqueues no host synchronisation.
+ *  - All memory is caller-owned.  The library allocates nothing on the hot
+ *    path; it only owns moe_comm_t (the NCCL communicator).
+ *  - Arguments are validated on the host BEFORE anything is enqueued: on any
+ *    error nothing was launched, the status says which class of error, and
+ *    moe_last_error() (thread-local) names the argument and the values.
+ *  - Index arrays are int32, row-major, item index i = t*k + j for token t
+ *    and slot j (j = 0 is the best-scoring choice).
+ *  - Readings of points the paper leaves open are DESIGN.md §3 "R<n>".
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Binary compatible with cudaStream_t (driver_types.h declares the same). */
+typedef struct CUstream_st* moe_stream_t;
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARG = 1, /* bad size, enum, NULL pointer, shape mismatch   */
+  MOE_ERR_UNSUPPORTED = 2, /* valid but outside this build's limits          */
+  MOE_ERR_ALIGNMENT = 3,   /* pointer or row size not 16-byte aligned        */
+  MOE_ERR_WORKSPACE = 4,   /* workspace NULL or smaller than *_workspace_bytes */
+  MOE_ERR_CUDA = 5,        /* a CUDA launch / runtime call failed            */
+  MOE_ERR_NCCL = 6         /* an NCCL call failed                            */
+} moe_status_t;
+
+typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype_t;
+
+/* Gate kinds (§3.1):
+ *   TOPK  : Eq. 1 top-k; k=1 is Switch, k=2 is GShard
+ *   KTOP1 : M6-T k-top-1, k prototypes of E/k contiguous experts each, top-1
+ *           inside every prototype, outputs summed (R11)
+ *   HASH  : Hash layer, expert = table[token_id], k = 1 */
+typedef enum { MOE_GATE_TOPK = 0, MOE_GATE_KTOP1 = 1, MOE_GATE_HASH = 2 } moe_gate_kind_t;
+
+/* Combine weights (R1):
+ *   RENORM  : Eq. 1 literally, g = softmax over the k selected logits
+ *             (k-top-1: softmax of one logit = 1; hash: 1)
+ *   SOFTMAX : full-row (k-top-1: prototype-slice) softmax evaluated at the
+ *             selected experts, not renormalised (Switch-paper convention) */
+typedef enum { MOE_W_RENORM = 0, MOE_W_SOFTMAX = 1 } moe_weight_mode_t;
+
+/* Capacity admission order (R5): TOKEN = items (t,j) t-major;
+ * SLOT = j-major, all first choices before any second choice (GShard). */
+typedef enum { MOE_PRIO_TOKEN = 0, MOE_PRIO_SLOT = 1 } moe_priority_t;
+
+/* AllToAll algorithms:
+ *   FLAT        : one grouped send/recv to every peer (Fig. 5)
+ *   HIER_LEADER : the paper's hierarchical scheme mimicked with groups of
+ *                 `group_size` consecutive ranks on one box (Fig. 6, R13) */
+typedef enum { MOE_A2A_FLAT = 0, MOE_A2A_HIER_LEADER = 1 } moe_a2a_algo_t;
+
+/* Gate problem description.  Enums are carried as int32 for a fixed ABI. */
+typedef struct {
+  int32_t S;           /* tokens on this rank (x_S of Alg. 1), >= 1          */
+  int32_t E;           /* number of experts, 1..256                          */
+  int32_t k;           /* slots per token: top-k k; k-top-1 prototypes; hash 1 */
+  int32_t capacity;    /* per-expert capacity cap >= 1 (see moe_capacity)    */
+  int32_t kind;        /* moe_gate_kind_t                                    */
+  int32_t weight_mode; /* moe_weight_mode_t                                  */
+  int32_t priority;    /* moe_priority_t                                     */
+} moe_gate_desc_t;
+
+/* Routing decision W_(S,E), id_S of Alg. 1, stored sparsely.
+ * All arrays are caller-allocated device memory. */
+typedef struct {
+  int32_t* expert_idx; /* [S*k] chosen expert, descending logit order
+                          (ties -> lower index, R3); -1 only for an invalid
+                          hash id                                            */
+  int32_t* slot_idx;   /* [S*k] row inside the expert's buffer, in [0,cap),
+                          or -1 = dropped by capacity                        */
+  float* weight;       /* [S*k] combine weight w_(t,idx); 0 where dropped,
+                          survivors NOT renormalised (R6)                    */
+  int32_t* load;       /* [E]   requests per expert before capacity          */
+  int32_t* slot_src;   /* [E*cap] inverse map t*k+j, -1 for an empty slot;
+                          may be NULL (not produced)                         */
+} moe_routing_t;
+
+/* ---------------------------------------------------------------- gate */
+
+/* host.  cap = ceil(C*S*k/E) evaluated in double ("capacity
+ * factor C to force the max received tokens by each expert"; formula
+ * SPEC.md:138; R4).  S is this rank's token count.  Returns -1 if S, E, k < 1,
+ * C <= 0 or the result does not fit in int32. */
+int32_t moe_capacity(int32_t S, int32_t E, int32_t k, double C);
+
+/* host.  Device workspace moe_gate needs for `desc` (0 if desc is invalid).
+ * The workspace must be ZERO-FILLED before its first use; after that every
+ * moe_gate call leaves it ready for the next one (it carries an epoch), so
+ * it may be reused across calls and CUDA-graph replays on one stream.  Do
+ * not use one workspace from two streams concurrently. */
+size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc);
+
+/* Step 1 of Algorithm 1 plus capacity:
+ * selection (TOPK: Eq. 1 TopK on raw fp32 logits, R2; KTOP1: per-prototype
+ * argmax; HASH: table lookup), weights (Eq. 1 softmax, R1) and capacity
+ * slots (per-expert prefix sum in admission order, slot >= cap -> dropped).
+ *   logits    [S,E] fp32 row-major (TOPK, KTOP1; ignored for HASH)
+ *   token_ids [S] int32, table [vocab] int32 (HASH only; else may be NULL)
+ *   out       routing arrays (see moe_routing_t); all written
+ *   ws        workspace of >= moe_gate_workspace_bytes(desc) bytes
+ * Device-side preconditions (not checked synchronously): logits finite;
+ * for HASH 0 <= token_ids[t] < vocab and 0 <= table[v] < E -- a violating
+ * token is routed as dropped (expert_idx = slot_idx = -1, weight 0) and
+ * counted in ws (read it with moe_gate_check).
+ * Errors: INVALID_ARG (S<1, E<1, k<1 or k>E, cap<1, KTOP1 with E%k != 0,
+ * HASH with k != 1 or missing ids/table/vocab, bad enum, NULL output),
+ * UNSUPPORTED (E > 256; SLOT priority with k*E > 2048), WORKSPACE. */
+moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits,
+                      const int32_t* token_ids, const int32_t* table, int32_t vocab,
+                      const moe_routing_t* out, void* ws, size_t ws_bytes,
+                      moe_stream_t stream);
+
+/* host, SYNCHRONISES `stream`.  Number of invalid hash tokens seen since the
+ * last check (the counter is reset to 0). */
+moe_status_t moe_gate_check(void* ws, moe_stream_t stream, int32_t* bad_count);
+
+/* ---------------------------------------------------------------- layout */
+
+/* Step 2, Layout_Transform (§3.2 "tokens assigned to the same
+ * expert need to be put in physically continuous memory locations",
+ * PAPER.md:175-177), padded form (R9):
+ *   dispatch[e][s][:] = x[t][:]  for every admitted item (t,j) with
+ *                                e = expert_idx[t*k+j], s = slot_idx[t*k+j];
+ *   dispatch[e][s][:] = 0        for s in [min(load[e],cap), cap).
+ * x [S,d] and dispatch [E,cap,d] have element type `dtype`; the copy is
+ * bit-exact.  Uses expert_idx, slot_idx, load of `routing`.
+ * Errors: INVALID_ARG, ALIGNMENT (x/dispatch not 16-byte aligned or d*size
+ * not a multiple of 16 bytes). */
+moe_status_t moe_layout(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                        const void* x, int32_t d, int32_t dtype, void* dispatch,
+                        moe_stream_t stream);
+
+/* Step 6 with the weighted combine of step 4, Reverse_Layout_Transform
+ * (PAPER.md:56-59, 64-65):
+ *   y[t][:] = sum_{j = 0..k-1, slot_idx >= 0} weight[t*k+j] * back[e][s][:]
+ * accumulated in fp32 in ascending j from 0, rounded once to dtype (RNE);
+ * a token with every slot dropped gets y[t] = 0 (R7).
+ * back [E,cap,d], y [S,d] of `dtype`.  Uses expert_idx, slot_idx, weight.
+ * Errors: as moe_layout. */
+moe_status_t moe_reverse_layout(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                const void* back, int32_t d, int32_t dtype, void* y,
+                                moe_stream_t stream);
+
+/* Bench stand-in for the expert (step 4; R16), NOT part of the method:
+ *   out[src][le][s][:] = s_e * in[src][le][s][:],  e = e_base + le,
+ *   s_e = 1 + (e mod 8)/8  (bit-reproducible: one rounding of an exact product)
+ * in/out [nsrc][E_local][cap][d] of dtype; in == out is allowed. */
+moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E_local,
+                              int32_t e_base, int32_t cap, int32_t d, int32_t dtype,
+                              moe_stream_t stream);
+
+/* ---------------------------------------------------------------- AllToAll */
+
+typedef struct moe_comm moe_comm_t;
+
+/* host.  A fresh NCCL unique id (128 bytes) on rank 0, to be broadcast to the
+ * other ranks by the caller (e.g. torch.distributed over gloo). */
+moe_status_t moe_comm_unique_id(uint8_t id[128]);
+
+/* host, collective over all ranks, blocking.  Creates the library-owned NCCL
+ * communicator on the CURRENT CUDA device.  *out is owned by the caller until
+ * moe_comm_destroy. */
+moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank,
+                           moe_comm_t** out);
+moe_status_t moe_comm_destroy(moe_comm_t* comm);
+moe_status_t moe_comm_size(const moe_comm_t* comm, int32_t* nranks, int32_t* rank);
+
+/* host.  Device workspace moe_alltoall needs (0 for FLAT; for HIER_LEADER the
+ * leader's staging, 2 * group_size * nranks * bytes_per_peer). */
+size_t moe_alltoall_workspace_bytes(int32_t nranks, int32_t algo, int32_t group_size,
+                                    size_t bytes_per_peer);
+
+/* Steps 3 and 5 (§3.2 "each GPU sends its data to all
+ * GPUs ... where each data will be divided equally into n parts",
+ * PAPER.md:179).  send and recv are [P][bytes_per_peer]:
+ *   recv[q] (on rank r) = send[r] (on rank q)   for all q
+ * i.e. chunks arrive in ascending source rank.  With the padded
+ * layout [E][cap][d] = [P][E/P][cap][d] and experts in contiguous blocks of
+ * E/P per rank (R10), dispatch and combine are this same call.
+ * FLAT: one NCCL group of send/recv pairs with every peer (self included).
+ * HIER_LEADER: groups of group_size consecutive ranks; (1) members send to
+ * their leader (local rank 0) sub-messages addressed by destination group,
+ * (3) leaders exchange one aggregated message per group pair (B*G/N bytes,
+ * PAPER.md:213), (4) the leader permutes chunks by destination device, (5)
+ * scatters.  Result byte-identical to FLAT (R13).
+ * Collective: every rank must call it with the same algo, group_size and
+ * bytes_per_peer, in the same order relative to its other NCCL calls.
+ * send != recv when nranks > 1 (nranks == 1: a device copy, or nothing if
+ * send == recv).  Errors: INVALID_ARG (nranks % group_size, in-place),
+ * WORKSPACE (HIER_LEADER on a leader), NCCL. */
+moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size,
+                          const void* send, void* recv, size_t bytes_per_peer,
+                          void* ws, size_t ws_bytes, moe_stream_t stream);
+
+/* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
+ * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,
+ * 1 = recv, 2 = ws staging A, 3 = ws staging B (each G*P*bytes_per_peer).
+ * Offsets/bytes are in units of bytes_per_peer chunks. */
+typedef struct {
+  int32_t phase; /* ops of one phase run as one NCCL group; phases in order */
+  int32_t op;    /* 0 = SEND, 1 = RECV, 2 = COPY (local), 3 = PERMUTE      */
+  int32_t peer;  /* SEND/RECV: peer rank; PERMUTE: N (groups)              */
+  int32_t src_buf, dst_buf;
+  int64_t src_off, dst_off, chunks; /* PERMUTE: chunks = G (group size)   */
+} moe_a2a_op_t;
+
+/* host.  Fills ops[0..*n_ops) with rank `rank`'s schedule; returns
+ * INVALID_ARG if capacity is too small (*n_ops then holds the count needed). */
+moe_status_t moe_alltoall_plan(int32_t nranks, int32_t rank, int32_t algo, int32_t group_size,
+                               moe_a2a_op_t* ops, int32_t capacity, int32_t* n_ops);
+
+/* ---------------------------------------------------------------- misc */
+
+const char* moe_status_str(moe_status_t s);
+const char* moe_last_error(void);   /* thread-local detail of the last error */
+const char* moe_version(void);      /* build string: arch, NCCL version      */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

@@ -1,0 +1,17 @@
+"""paper_2203_14685_b200 -- the HetuMoE (arXiv 2203.14685) token-routing hot
+path, B200-native: a thin Python binding over libmoe_b200.so (include/moe.h).
+
+Importing this package loads the CUDA library; if it is not built the import
+fails (there is no CPU fallback).
+"""
+from ._lib import MoeError, lib as _lib
+
+_lib()  # fail loudly now if libmoe_b200.so is missing
+
+from .api import (ALGOS, KINDS, MODES, PRIOS, Comm, Gate, Routing, alltoall_plan,  # noqa: E402
+                  capacity, expert_scale, gate, layout, reverse_layout, version)
+from .route import RoutePipeline  # noqa: E402
+
+__all__ = ["MoeError", "Comm", "Gate", "Routing", "RoutePipeline", "alltoall_plan", "capacity",
+           "expert_scale", "gate", "layout", "reverse_layout", "version", "KINDS", "MODES",
+           "PRIOS", "ALGOS"]

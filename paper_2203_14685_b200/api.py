@@ -1,0 +1,258 @@
+"""Python face of libmoe_b200: the four calls of Algorithm 1's routing path on
+torch CUDA tensors and the current torch stream.
+
+PyTorch is used for device memory, streams and torch.distributed bootstrap
+only; these functions check dtype/contiguity/device/alignment, pass
+``data_ptr()`` and the stream handle to the C ABI, and return tensors.  Every
+byte of routing work is done by the library's kernels (or NCCL).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from ._lib import A2AOp, GateDesc, RoutingC, check, lib
+
+KINDS = {"topk": 0, "ktop1": 1, "hash": 2}
+MODES = {"renorm": 0, "softmax": 1}
+PRIOS = {"token": 0, "slot": 1}
+ALGOS = {"flat": 0, "hier": 1}
+_DT = {torch.float32: 0, torch.bfloat16: 1}
+
+
+def _stream(device=None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need_cuda(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError("%s must be a CUDA tensor (no CPU fallback)" % name)
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError("%s must be %s, got %s" % (name, dtype, t.dtype))
+
+
+def capacity(S: int, E: int, k: int, C: float) -> int:
+    """cap = ceil(C*S*k/E) (R4)."""
+    c = lib().moe_capacity(S, E, k, float(C))
+    if c < 0:
+        raise ValueError("invalid capacity arguments S=%d E=%d k=%d C=%r" % (S, E, k, C))
+    return c
+
+
+@dataclass
+class Routing:
+    """W_(S,E), id_S of Algorithm 1, sparse: index t*k+j."""
+    expert_idx: torch.Tensor   # [S, k] int32
+    slot_idx: torch.Tensor     # [S, k] int32, -1 = dropped
+    weight: torch.Tensor       # [S, k] float32
+    load: torch.Tensor         # [E] int32
+    slot_src: Optional[torch.Tensor]  # [E*cap] int32 or None
+    S: int
+    E: int
+    k: int
+    cap: int
+    kind: int = 0
+    weight_mode: int = 0
+    priority: int = 0
+
+    def desc(self) -> GateDesc:
+        return GateDesc(self.S, self.E, self.k, self.cap, self.kind, self.weight_mode,
+                        self.priority)
+
+    def c(self) -> RoutingC:
+        return RoutingC(self.expert_idx.data_ptr(), self.slot_idx.data_ptr(),
+                        self.weight.data_ptr(), self.load.data_ptr(),
+                        None if self.slot_src is None else self.slot_src.data_ptr())
+
+    @staticmethod
+    def empty(S, E, k, cap, device, kind=0, weight_mode=0, priority=0, slot_src=True):
+        i32 = dict(dtype=torch.int32, device=device)
+        return Routing(torch.empty((S, k), **i32), torch.empty((S, k), **i32),
+                       torch.empty((S, k), dtype=torch.float32, device=device),
+                       torch.empty((E,), **i32),
+                       torch.empty((E * cap,), **i32) if slot_src else None,
+                       S, E, k, cap, kind, weight_mode, priority)
+
+
+class Gate:
+    """moe_gate with its persistent (self-resetting) workspace."""
+
+    def __init__(self, S: int, E: int, k: int, capacity: int, kind: str = "topk",
+                 weight_mode: str = "renorm", priority: str = "token", device=None):
+        self.S, self.E, self.k, self.cap = S, E, k, capacity
+        self.kind, self.mode, self.prio = KINDS[kind], MODES[weight_mode], PRIOS[priority]
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        d = GateDesc(S, E, k, capacity, self.kind, self.mode, self.prio)
+        nb = lib().moe_gate_workspace_bytes(ctypes.byref(d))
+        if nb == 0:
+            # let moe_gate produce the precise error message
+            check(lib().moe_gate(ctypes.byref(d), None, None, None, 0, None, None, 0, None),
+                  "moe_gate")
+        self.ws = torch.zeros(nb, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, logits: Optional[torch.Tensor] = None, token_ids=None, table=None,
+                 out: Optional[Routing] = None, slot_src: bool = True) -> Routing:
+        if out is None:
+            out = Routing.empty(self.S, self.E, self.k, self.cap, self.device, self.kind,
+                                self.mode, self.prio, slot_src)
+        vocab = 0
+        if self.kind == KINDS["hash"]:
+            _need_cuda(token_ids, "token_ids", torch.int32)
+            _need_cuda(table, "table", torch.int32)
+            vocab = table.numel()
+        else:
+            _need_cuda(logits, "logits", torch.float32)
+            if tuple(logits.shape) != (self.S, self.E):
+                raise ValueError("logits shape %s != (S=%d, E=%d)" % (tuple(logits.shape),
+                                                                     self.S, self.E))
+        d = out.desc()
+        rc = out.c()
+        check(lib().moe_gate(ctypes.byref(d), _p(logits), _p(token_ids), _p(table), vocab,
+                             ctypes.byref(rc), _p(self.ws), self.ws.numel(),
+                             _stream(self.device)), "moe_gate")
+        return out
+
+    def check(self) -> int:
+        """Invalid hash ids since the last check (synchronises the stream)."""
+        n = ctypes.c_int32(0)
+        check(lib().moe_gate_check(_p(self.ws), _stream(self.device), ctypes.byref(n)),
+              "moe_gate_check")
+        return n.value
+
+
+def gate(logits: Optional[torch.Tensor] = None, *, E: Optional[int] = None, k: int = 1,
+         capacity_factor: float = 1.0, capacity_: Optional[int] = None, kind: str = "topk",
+         weight_mode: str = "renorm", priority: str = "token", token_ids=None, table=None,
+         slot_src: bool = True) -> Routing:
+    """One-shot convenience wrapper around Gate (allocates a workspace)."""
+    if logits is not None:
+        S, E = logits.shape
+        dev = logits.device
+    else:
+        S = token_ids.numel()
+        dev = token_ids.device
+    cap = capacity_ if capacity_ is not None else capacity(S, E, k, capacity_factor)
+    g = Gate(S, E, k, cap, kind, weight_mode, priority, dev)
+    return g(logits, token_ids, table, slot_src=slot_src)
+
+
+def layout(x: torch.Tensor, r: Routing, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Layout_Transform (Alg. 1 step 2): [S,d] -> padded [E,cap,d]."""
+    _need_cuda(x, "x")
+    if x.dtype not in _DT:
+        raise TypeError("x must be float32 or bfloat16")
+    S, d = x.shape
+    if S != r.S:
+        raise ValueError("x has %d rows, routing has S=%d" % (S, r.S))
+    if out is None:
+        out = torch.empty((r.E, r.cap, d), dtype=x.dtype, device=x.device)
+    _need_cuda(out, "dispatch", x.dtype)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_layout(ctypes.byref(desc), ctypes.byref(rc), _p(x), d, _DT[x.dtype], _p(out),
+                           _stream(x.device)), "moe_layout")
+    return out
+
+
+def reverse_layout(back: torch.Tensor, r: Routing,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Reverse_Layout_Transform + weighted combine (Alg. 1 steps 4/6)."""
+    _need_cuda(back, "back")
+    if back.dtype not in _DT:
+        raise TypeError("back must be float32 or bfloat16")
+    d = back.shape[-1]
+    if back.numel() != r.E * r.cap * d:
+        raise ValueError("back must hold [E=%d, cap=%d, d] rows" % (r.E, r.cap))
+    if out is None:
+        out = torch.empty((r.S, d), dtype=back.dtype, device=back.device)
+    _need_cuda(out, "y", back.dtype)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_reverse_layout(ctypes.byref(desc), ctypes.byref(rc), _p(back), d,
+                                   _DT[back.dtype], _p(out), _stream(back.device)),
+          "moe_reverse_layout")
+    return out
+
+
+def expert_scale(buf: torch.Tensor, nsrc: int, E_local: int, e_base: int,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Bench stand-in expert (R16): s_e * buf over [nsrc][E_local][cap][d]."""
+    _need_cuda(buf, "buf")
+    d = buf.shape[-1]
+    cap = buf.numel() // (nsrc * E_local * d)
+    if out is None:
+        out = buf
+    check(lib().moe_expert_scale(_p(buf), _p(out), nsrc, E_local, e_base, cap, d,
+                                 _DT[buf.dtype], _stream(buf.device)), "moe_expert_scale")
+    return out
+
+
+def alltoall_plan(nranks: int, rank: int, algo: str = "flat", group_size: int = 1):
+    """The schedule moe_alltoall executes on `rank` (host only)."""
+    n = ctypes.c_int32(0)
+    L = lib()
+    L.moe_alltoall_plan(nranks, rank, ALGOS[algo], group_size, None, 0, ctypes.byref(n))
+    ops = (A2AOp * max(1, n.value))()
+    check(L.moe_alltoall_plan(nranks, rank, ALGOS[algo], group_size, ops, n.value,
+                              ctypes.byref(n)), "moe_alltoall_plan")
+    return [{f: getattr(o, f) for f, _ in A2AOp._fields_} for o in ops[:n.value]]
+
+
+class Comm:
+    """The library-owned NCCL communicator (moe_comm_t)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        self.nranks, self.rank = nranks, rank
+        h = ctypes.c_void_p()
+        check(lib().moe_comm_init(unique_id, nranks, rank, ctypes.byref(h)), "moe_comm_init")
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().moe_comm_unique_id(buf), "moe_comm_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        """Bootstrap over torch.distributed: rank 0 makes the NCCL id and
+        broadcasts it (object broadcast over the default group's backend)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world, rank)
+
+    def workspace_bytes(self, algo: str, group_size: int, bytes_per_peer: int) -> int:
+        return lib().moe_alltoall_workspace_bytes(self.nranks, ALGOS[algo], group_size,
+                                                  bytes_per_peer)
+
+    def alltoall(self, send: torch.Tensor, recv: torch.Tensor, algo: str = "flat",
+                 group_size: int = 1, ws: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """AllToAll (Alg. 1 steps 3/5): recv[q] on rank r = send[r] on rank q."""
+        _need_cuda(send, "send")
+        _need_cuda(recv, "recv")
+        nb = send.numel() * send.element_size()
+        if nb != recv.numel() * recv.element_size() or nb % self.nranks:
+            raise ValueError("send/recv must be equal and divisible into nranks chunks")
+        check(lib().moe_alltoall(self._h, ALGOS[algo], group_size, _p(send), _p(recv),
+                                 nb // self.nranks, _p(ws),
+                                 0 if ws is None else ws.numel() * ws.element_size(),
+                                 _stream(send.device)), "moe_alltoall")
+        return recv
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            check(lib().moe_comm_destroy(self._h), "moe_comm_destroy")
+            self._h = None
+
+
+def version() -> str:
+    return lib().moe_version().decode()

@@ -1,0 +1,255 @@
+// api.cu -- the C ABI of libmoe_b200.so (include/moe.h): host-side argument
+// validation (before anything is enqueued), error reporting, and dispatch to
+// the kernels of gate.cu / layout.cu.  moe_alltoall lives in comm.cu.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace moe {
+
+size_t gate_workspace_bytes(const moe_gate_desc_t& d);
+moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const int32_t* ids,
+                         const int32_t* table, int32_t vocab, const moe_routing_t& out, void* ws,
+                         cudaStream_t stream);
+moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);
+moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
+                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream);
+moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
+                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream);
+moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
+                                 int cap, int dcols, int dtype, int dtype_size,
+                                 cudaStream_t stream);
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+moe_status_t cuda_status(cudaError_t e, const char* what) {
+  set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+  return MOE_ERR_CUDA;
+}
+
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static int dtype_size(int32_t dt) { return dt == MOE_F32 ? 4 : dt == MOE_BF16 ? 2 : 0; }
+
+// Checks shared by every call that takes a gate description.
+static moe_status_t check_desc(const char* fn, const moe_gate_desc_t* d) {
+  if (!d) {
+    set_error("%s: desc is NULL", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->S < 1 || d->E < 1 || d->k < 1 || d->k > d->E || d->capacity < 1) {
+    set_error("%s: need S>=1, E>=1, 1<=k<=E, capacity>=1 (S=%d E=%d k=%d capacity=%d)", fn, d->S,
+              d->E, d->k, d->capacity);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->kind < MOE_GATE_TOPK || d->kind > MOE_GATE_HASH) {
+    set_error("%s: invalid gate kind %d", fn, d->kind);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->weight_mode != MOE_W_RENORM && d->weight_mode != MOE_W_SOFTMAX) {
+    set_error("%s: invalid weight_mode %d", fn, d->weight_mode);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->priority != MOE_PRIO_TOKEN && d->priority != MOE_PRIO_SLOT) {
+    set_error("%s: invalid priority %d", fn, d->priority);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->kind == MOE_GATE_KTOP1 && d->E % d->k != 0) {
+    set_error("%s: k-top-1 needs E %% k == 0 (E=%d, k=%d prototypes)", fn, d->E, d->k);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->kind == MOE_GATE_HASH && d->k != 1) {
+    set_error("%s: hash gate needs k == 1 (k=%d)", fn, d->k);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->E > 256) {
+    set_error("%s: E=%d > 256 is not supported", fn, d->E);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  if ((long long)d->S * d->k >= (1ll << 31) || (long long)d->E * d->capacity >= (1ll << 31)) {
+    set_error("%s: S*k and E*capacity must be < 2^31 (S=%d k=%d E=%d capacity=%d)", fn, d->S, d->k,
+              d->E, d->capacity);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  return MOE_OK;
+}
+
+static moe_status_t check_rows(const char* fn, const moe_gate_desc_t* d, const moe_routing_t* r,
+                               const void* a, const char* an, const void* b, const char* bn,
+                               int32_t dcols, int32_t dtype, bool need_weight, bool need_load) {
+  moe_status_t s = check_desc(fn, d);
+  if (s != MOE_OK) return s;
+  if (!r || !r->expert_idx || !r->slot_idx || (need_weight && !r->weight) ||
+      (need_load && !r->load)) {
+    set_error("%s: routing or one of its required arrays is NULL", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!a || !b) {
+    set_error("%s: %s or %s is NULL", fn, an, bn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int ds = dtype_size(dtype);
+  if (!ds) {
+    set_error("%s: invalid dtype %d", fn, dtype);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (dcols < 1) {
+    set_error("%s: d=%d < 1", fn, dcols);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (((long long)dcols * ds) % 16 != 0) {
+    set_error("%s: row of d=%d x %d bytes is not a multiple of 16 bytes", fn, dcols, ds);
+    return MOE_ERR_ALIGNMENT;
+  }
+  if (!aligned(a, 16) || !aligned(b, 16)) {
+    set_error("%s: %s (%p) and %s (%p) must be 16-byte aligned", fn, an, a, bn, b);
+    return MOE_ERR_ALIGNMENT;
+  }
+  return MOE_OK;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+int32_t moe_capacity(int32_t S, int32_t E, int32_t k, double C) {
+  if (S < 1 || E < 1 || k < 1 || !(C > 0.0)) return -1;
+  const double c = std::ceil(C * (double)S * (double)k / (double)E);
+  if (!(c >= 1.0) || c > 2147483647.0) return -1;
+  return (int32_t)c;
+}
+
+size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc) {
+  if (check_desc("moe_gate_workspace_bytes", desc) != MOE_OK) return 0;
+  return gate_workspace_bytes(*desc);
+}
+
+moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const int32_t* token_ids,
+                      const int32_t* table, int32_t vocab, const moe_routing_t* out, void* ws,
+                      size_t ws_bytes, moe_stream_t stream) {
+  moe_status_t s = check_desc("moe_gate", desc);
+  if (s != MOE_OK) return s;
+  if (!out || !out->expert_idx || !out->slot_idx || !out->weight || !out->load) {
+    set_error("moe_gate: out or one of expert_idx/slot_idx/weight/load is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (desc->kind == MOE_GATE_HASH) {
+    if (!token_ids || !table || vocab < 1) {
+      set_error("moe_gate: hash gate needs token_ids, table and vocab >= 1 (vocab=%d)", vocab);
+      return MOE_ERR_INVALID_ARG;
+    }
+  } else if (!logits) {
+    set_error("moe_gate: logits is NULL");
+    return MOE_ERR_INVALID_ARG;
+  } else if (!aligned(logits, 4)) {
+    set_error("moe_gate: logits must be 4-byte aligned");
+    return MOE_ERR_ALIGNMENT;
+  }
+  const size_t need = gate_workspace_bytes(*desc);
+  if (!ws || ws_bytes < need) {
+    set_error("moe_gate: workspace %zu bytes < %zu needed (or NULL)", ws_bytes, need);
+    return MOE_ERR_WORKSPACE;
+  }
+  if (!aligned(ws, 16)) {
+    set_error("moe_gate: workspace must be 16-byte aligned");
+    return MOE_ERR_ALIGNMENT;
+  }
+  return gate_launch(*desc, logits, token_ids, table, vocab, *out, ws,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_gate_check(void* ws, moe_stream_t stream, int32_t* bad_count) {
+  if (!ws || !bad_count) {
+    set_error("moe_gate_check: NULL ws or bad_count");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return gate_check(ws, reinterpret_cast<cudaStream_t>(stream), bad_count);
+}
+
+moe_status_t moe_layout(const moe_gate_desc_t* desc, const moe_routing_t* routing, const void* x,
+                        int32_t d, int32_t dtype, void* dispatch, moe_stream_t stream) {
+  moe_status_t s =
+      check_rows("moe_layout", desc, routing, x, "x", dispatch, "dispatch", d, dtype, false, true);
+  if (s != MOE_OK) return s;
+  return layout_launch(*desc, *routing, x, dtype_size(dtype), d, dispatch,
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_reverse_layout(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                const void* back, int32_t d, int32_t dtype, void* y,
+                                moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_reverse_layout", desc, routing, back, "back", y, "y", d, dtype,
+                              true, false);
+  if (s != MOE_OK) return s;
+  return reverse_launch(*desc, *routing, back, dtype, dtype_size(dtype), d, y,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E_local,
+                              int32_t e_base, int32_t cap, int32_t d, int32_t dtype,
+                              moe_stream_t stream) {
+  const int ds = dtype_size(dtype);
+  if (!in || !out || nsrc < 1 || E_local < 1 || e_base < 0 || cap < 1 || d < 1 || !ds) {
+    set_error("moe_expert_scale: bad arguments (nsrc=%d E_local=%d e_base=%d cap=%d d=%d dtype=%d)",
+              nsrc, E_local, e_base, cap, d, dtype);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (((long long)d * ds) % 16 != 0 || !aligned(in, 16) || !aligned(out, 16)) {
+    set_error("moe_expert_scale: rows and pointers must be 16-byte aligned");
+    return MOE_ERR_ALIGNMENT;
+  }
+  return expert_scale_launch(in, out, nsrc, E_local, e_base, cap, d, dtype, ds,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* moe_status_str(moe_status_t s) {
+  switch (s) {
+    case MOE_OK: return "MOE_OK";
+    case MOE_ERR_INVALID_ARG: return "MOE_ERR_INVALID_ARG";
+    case MOE_ERR_UNSUPPORTED: return "MOE_ERR_UNSUPPORTED";
+    case MOE_ERR_ALIGNMENT: return "MOE_ERR_ALIGNMENT";
+    case MOE_ERR_WORKSPACE: return "MOE_ERR_WORKSPACE";
+    case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
+    case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
+  }
+  return "MOE_ERR_UNKNOWN";
+}
+
+const char* moe_last_error(void) { return g_err; }
+
+const char* moe_version(void) {
+  static char v[128];
+  if (!v[0])
+    snprintf(v, sizeof v, "libmoe_b200 sm_100a nccl-%d.%d.%d cuda-%d", NCCL_MAJOR, NCCL_MINOR,
+             NCCL_PATCH, CUDART_VERSION);
+  return v;
+}
+
+}  // extern "C"

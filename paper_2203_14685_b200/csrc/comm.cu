@@ -1,0 +1,290 @@
+// comm.cu -- moe_alltoall: Alg. 1 steps 3 and 5 over
+// NCCL point-to-point on NVLink 5 / NVSwitch, flat (Fig. 5) and
+// the paper's hierarchical scheme (Fig. 6) mimicked with
+// groups of G consecutive ranks on one box (R13).
+//
+// Both algorithms are written as a host-side schedule of ops (moe_a2a_op_t):
+// every op of one `phase` is issued inside one ncclGroupStart/End (local
+// copies and the permute kernel are stream-ordered between phases).  The
+// schedule is exported (moe_alltoall_plan) so the multi-process tests can
+// execute the very same plan over gloo on CPUs.
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace moe {
+
+moe_status_t chunk_permute_launch(const void* src, void* dst, int N, int G, long long chunk_bytes,
+                                  cudaStream_t stream);
+
+}  // namespace moe
+
+struct moe_comm {
+  ncclComm_t nccl;
+  int nranks, rank, device;
+};
+
+namespace moe {
+
+static moe_status_t nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return MOE_OK;
+  set_error("%s: NCCL error %d (%s)", what, (int)r, ncclGetErrorString(r));
+  return MOE_ERR_NCCL;
+}
+
+enum { OP_SEND = 0, OP_RECV = 1, OP_COPY = 2, OP_PERMUTE = 3 };
+enum { BUF_SEND = 0, BUF_RECV = 1, BUF_A = 2, BUF_B = 3 };
+
+static void push(std::vector<moe_a2a_op_t>& v, int phase, int op, int peer, int sb, int db,
+                 long long so, long long dof, long long n) {
+  moe_a2a_op_t o;
+  o.phase = phase;
+  o.op = op;
+  o.peer = peer;
+  o.src_buf = sb;
+  o.dst_buf = db;
+  o.src_off = so;
+  o.dst_off = dof;
+  o.chunks = n;
+  v.push_back(o);
+}
+
+// FLAT: one phase; rank r sends chunk q of its send buffer to q and receives
+// chunk q of its recv buffer from q (self included: NCCL copies it in the
+// same group, overlapped with the peer transfers).
+//
+// HIER_LEADER (N = P/G groups, leader = local rank 0 of each group):
+//  phase 0  (1)+(2) members -> leader: member m of group g sends, for every
+//           destination group h, its G chunks [hG, hG+G) into leader staging
+//           A[h][m][0..G)  ("reorder by destination node" costs nothing);
+//  phase 1  (3) leader g sends A[h] (G*G chunks = B*G/N bytes)
+//           to leader h and receives leader h's block into B[h]:
+//           B[g'][m][n] = chunk for (dst local n) from source rank g'G+m;
+//  phase 2  (4) permute B[g'][m][n] -> A[n][g'][m]   (k_chunk_permute)
+//  phase 3  (5) leader sends A[n] (P chunks, ascending source rank) to member
+//           n; its own A[0] is copied into its recv buffer.
+static std::vector<moe_a2a_op_t> make_plan(int P, int r, int algo, int G) {
+  std::vector<moe_a2a_op_t> v;
+  if (algo == MOE_A2A_FLAT || P == 1) {
+    for (int q = 0; q < P; ++q) {
+      push(v, 0, OP_SEND, q, BUF_SEND, -1, q, 0, 1);
+      push(v, 0, OP_RECV, q, -1, BUF_RECV, 0, q, 1);
+    }
+    return v;
+  }
+  // G == 1 (every rank a leader) and G == P (one group: gather + scatter
+  // only) are valid degenerate forms of the same schedule.
+  const int N = P / G, g = r / G, m = r % G, leader = g * G;
+  const long long GG = (long long)G * G;
+  // phase 0
+  if (m != 0) {
+    for (int h = 0; h < N; ++h) push(v, 0, OP_SEND, leader, BUF_SEND, -1, (long long)h * G, 0, G);
+  } else {
+    for (int mm = 0; mm < G; ++mm)
+      for (int h = 0; h < N; ++h) {
+        const long long dst = (long long)h * GG + (long long)mm * G;
+        if (mm == 0)
+          push(v, 0, OP_COPY, -1, BUF_SEND, BUF_A, (long long)h * G, dst, G);
+        else
+          push(v, 0, OP_RECV, leader + mm, -1, BUF_A, 0, dst, G);
+      }
+    // phase 1: leader <-> leader
+    for (int h = 0; h < N; ++h) {
+      if (h == g) {
+        push(v, 1, OP_COPY, -1, BUF_A, BUF_B, (long long)h * GG, (long long)g * GG, GG);
+      } else {
+        push(v, 1, OP_SEND, h * G, BUF_A, -1, (long long)h * GG, 0, GG);
+        push(v, 1, OP_RECV, h * G, -1, BUF_B, 0, (long long)h * GG, GG);
+      }
+    }
+    // phase 2: permute B -> A
+    push(v, 2, OP_PERMUTE, N, BUF_B, BUF_A, 0, 0, G);
+    // phase 3: scatter
+    for (int n = 0; n < G; ++n) {
+      if (n == 0)
+        push(v, 3, OP_COPY, -1, BUF_A, BUF_RECV, 0, 0, P);
+      else
+        push(v, 3, OP_SEND, leader + n, BUF_A, -1, (long long)n * P, 0, P);
+    }
+  }
+  if (m != 0) push(v, 3, OP_RECV, leader, -1, BUF_RECV, 0, 0, P);
+  return v;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+moe_status_t moe_comm_unique_id(uint8_t id[128]) {
+  if (!id) {
+    set_error("moe_comm_unique_id: id is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  moe_status_t s = nccl_status(ncclGetUniqueId(&u), "moe_comm_unique_id");
+  if (s == MOE_OK) std::memcpy(id, &u, 128);
+  return s;
+}
+
+moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, moe_comm_t** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error("moe_comm_init: bad arguments (nranks=%d rank=%d)", nranks, rank);
+    return MOE_ERR_INVALID_ARG;
+  }
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_status(ce, "moe_comm_init: cudaGetDevice");
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 1;
+  ncclComm_t c;
+  moe_status_t s = nccl_status(ncclCommInitRankConfig(&c, nranks, u, rank, &cfg), "moe_comm_init");
+  if (s != MOE_OK) return s;
+  moe_comm_t* m = new moe_comm_t{c, nranks, rank, dev};
+  *out = m;
+  return MOE_OK;
+}
+
+moe_status_t moe_comm_destroy(moe_comm_t* comm) {
+  if (!comm) return MOE_OK;
+  moe_status_t s = nccl_status(ncclCommDestroy(comm->nccl), "moe_comm_destroy");
+  delete comm;
+  return s;
+}
+
+moe_status_t moe_comm_size(const moe_comm_t* comm, int32_t* nranks, int32_t* rank) {
+  if (!comm || !nranks || !rank) {
+    set_error("moe_comm_size: NULL argument");
+    return MOE_ERR_INVALID_ARG;
+  }
+  *nranks = comm->nranks;
+  *rank = comm->rank;
+  return MOE_OK;
+}
+
+size_t moe_alltoall_workspace_bytes(int32_t nranks, int32_t algo, int32_t group_size,
+                                    size_t bytes_per_peer) {
+  if (algo != MOE_A2A_HIER_LEADER || nranks < 1 || group_size < 1) return 0;
+  return 2 * (size_t)group_size * (size_t)nranks * bytes_per_peer;
+}
+
+moe_status_t moe_alltoall_plan(int32_t nranks, int32_t rank, int32_t algo, int32_t group_size,
+                               moe_a2a_op_t* ops, int32_t capacity, int32_t* n_ops) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !n_ops ||
+      (algo != MOE_A2A_FLAT && algo != MOE_A2A_HIER_LEADER) ||
+      (algo == MOE_A2A_HIER_LEADER && (group_size < 1 || nranks % group_size != 0))) {
+    set_error("moe_alltoall_plan: bad arguments (nranks=%d rank=%d algo=%d group_size=%d)", nranks,
+              rank, algo, group_size);
+    return MOE_ERR_INVALID_ARG;
+  }
+  std::vector<moe_a2a_op_t> v = make_plan(nranks, rank, algo, group_size);
+  *n_ops = (int32_t)v.size();
+  if (!ops || capacity < (int32_t)v.size()) {
+    set_error("moe_alltoall_plan: need room for %d ops", (int)v.size());
+    return MOE_ERR_INVALID_ARG;
+  }
+  std::memcpy(ops, v.data(), v.size() * sizeof(moe_a2a_op_t));
+  return MOE_OK;
+}
+
+moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, const void* send,
+                          void* recv, size_t bytes_per_peer, void* ws, size_t ws_bytes,
+                          moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (!comm || !send || !recv) {
+    set_error("moe_alltoall: NULL comm/send/recv");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks, r = comm->rank;
+  if (algo != MOE_A2A_FLAT && algo != MOE_A2A_HIER_LEADER) {
+    set_error("moe_alltoall: invalid algo %d", algo);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (algo == MOE_A2A_HIER_LEADER && (group_size < 1 || P % group_size != 0)) {
+    set_error("moe_alltoall: nranks %d not divisible by group_size %d", P, group_size);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (bytes_per_peer == 0) return MOE_OK;
+  if (P == 1) {
+    if (send == recv) return MOE_OK;
+    cudaError_t e = cudaMemcpyAsync(recv, send, bytes_per_peer, cudaMemcpyDeviceToDevice, stream);
+    return e == cudaSuccess ? MOE_OK : cuda_status(e, "moe_alltoall: self copy");
+  }
+  if (send == recv) {
+    set_error("moe_alltoall: in-place (send == recv) is not supported for nranks > 1");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const bool hier = algo == MOE_A2A_HIER_LEADER;
+  if (hier && r % group_size == 0) {
+    const size_t need = moe_alltoall_workspace_bytes(P, algo, group_size, bytes_per_peer);
+    if (!ws || ws_bytes < need) {
+      set_error("moe_alltoall: leader workspace %zu < %zu bytes", ws_bytes, need);
+      return MOE_ERR_WORKSPACE;
+    }
+    if (bytes_per_peer % 16 != 0) {
+      set_error("moe_alltoall: HIER_LEADER needs bytes_per_peer %% 16 == 0 (got %zu)",
+                bytes_per_peer);
+      return MOE_ERR_ALIGNMENT;
+    }
+  }
+  std::vector<moe_a2a_op_t> plan = make_plan(P, r, algo, group_size);
+  const size_t b = bytes_per_peer;
+  const size_t stage = (size_t)group_size * P * b;
+  char* bufs[4] = {const_cast<char*>(static_cast<const char*>(send)), static_cast<char*>(recv),
+                   static_cast<char*>(ws), ws ? static_cast<char*>(ws) + stage : nullptr};
+  size_t i = 0;
+  while (i < plan.size()) {
+    const int phase = plan[i].phase;
+    size_t jend = i;
+    while (jend < plan.size() && plan[jend].phase == phase) ++jend;
+    bool grouped = false;
+    for (size_t j = i; j < jend; ++j) {
+      const moe_a2a_op_t& o = plan[j];
+      if (o.op == OP_SEND || o.op == OP_RECV) {
+        if (!grouped) {
+          moe_status_t s = nccl_status(ncclGroupStart(), "moe_alltoall: ncclGroupStart");
+          if (s != MOE_OK) return s;
+          grouped = true;
+        }
+        ncclResult_t nr =
+            o.op == OP_SEND
+                ? ncclSend(bufs[o.src_buf] + o.src_off * b, (size_t)o.chunks * b, ncclInt8, o.peer,
+                           comm->nccl, stream)
+                : ncclRecv(bufs[o.dst_buf] + o.dst_off * b, (size_t)o.chunks * b, ncclInt8, o.peer,
+                           comm->nccl, stream);
+        if (nr != ncclSuccess) {
+          ncclGroupEnd();
+          return nccl_status(nr, "moe_alltoall: send/recv");
+        }
+      }
+    }
+    if (grouped) {
+      moe_status_t s = nccl_status(ncclGroupEnd(), "moe_alltoall: ncclGroupEnd");
+      if (s != MOE_OK) return s;
+    }
+    for (size_t j = i; j < jend; ++j) {
+      const moe_a2a_op_t& o = plan[j];
+      if (o.op == OP_COPY) {
+        cudaError_t e = cudaMemcpyAsync(bufs[o.dst_buf] + o.dst_off * b,
+                                        bufs[o.src_buf] + o.src_off * b, (size_t)o.chunks * b,
+                                        cudaMemcpyDeviceToDevice, stream);
+        if (e != cudaSuccess) return cuda_status(e, "moe_alltoall: local copy");
+      } else if (o.op == OP_PERMUTE) {
+        moe_status_t s = chunk_permute_launch(bufs[o.src_buf], bufs[o.dst_buf], o.peer,
+                                              (int)o.chunks, (long long)b, stream);
+        if (s != MOE_OK) return s;
+      }
+    }
+    i = jend;
+  }
+  return MOE_OK;
+}
+
+}  // extern "C"

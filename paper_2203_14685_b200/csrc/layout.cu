@@ -1,0 +1,404 @@
+// layout.cu -- moe_layout (Alg. 1 step 2),
+// moe_reverse_layout (step 6 + the weighted combine of step 4,
+// PAPER.md:56-59, 64-65), the bench expert stand-in (R16) and the chunk
+// permutation used by the hierarchical AllToAll.
+//
+// All four are HBM-bound row movers.  Design:
+//  - persistent grid (SMs x resident CTAs), one warp per row task;
+//  - 32-byte vector loads/stores (LDG/STG.E.256) when the row is a multiple
+//    of 32 bytes, else 16-byte; streaming loads bypass L1 and are marked
+//    evict-first in L2;
+//  - layout is token-centric: each x row is read ONCE and written to its <= k
+//    admitted slots; the zero-fill of the padding rows is appended to the same
+//    launch as extra row tasks (no separate memset);
+//  - reverse is token-centric: <= k row loads, fp32 FMA in ascending j from
+//    0, one RNE store; fully dropped tokens store zeros.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+
+struct RowArgs {
+  const char* src;
+  char* dst;
+  const int32_t* expert_idx;
+  const int32_t* slot_idx;
+  const float* weight;
+  const int32_t* load;
+  int S, E, k, cap;
+  int row_bytes;
+  int d;
+};
+
+template <int VB>
+struct Vec;
+template <>
+struct Vec<32> {
+  using T = V8;
+  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v8(p); }
+  static __device__ __forceinline__ T ld(const void* p) { return ld_v8(p); }
+  static __device__ __forceinline__ void st(void* p, const T& v) { st_v8(p, v); }
+  static __device__ __forceinline__ T zero() { return V8{{0, 0, 0, 0, 0, 0, 0, 0}}; }
+};
+template <>
+struct Vec<16> {
+  using T = V4;
+  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v4(p); }
+  static __device__ __forceinline__ T ld(const void* p) {
+    V4 r;
+    asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "l"(p));
+    return r;
+  }
+  static __device__ __forceinline__ void st(void* p, const T& v) { st_v4(p, v); }
+  static __device__ __forceinline__ T zero() { return V4{{0, 0, 0, 0}}; }
+};
+
+// Exclusive prefix of the padding-row counts cap - min(load[e], cap) into
+// s_beg[0..E] (E <= 256), computed by every CTA (tiny).
+__device__ __forceinline__ void pad_prefix(const RowArgs& a, int* s_beg) {
+  __shared__ int s_cnt[257];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < a.E; e += blockDim.x) s_cnt[e] = a.cap - min(__ldg(a.load + e), a.cap);
+  __syncthreads();
+  if (tid < 32) {
+    int carry = 0;
+    for (int base = 0; base < a.E; base += 32) {
+      const int e = base + tid;
+      int v = e < a.E ? s_cnt[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (tid >= m) incl += o;
+      }
+      if (e < a.E) s_beg[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) s_beg[a.E] = carry;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ Layout_Transform
+template <int VB, int U>
+__global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
+  using V = Vec<VB>;
+  __shared__ int s_beg[257];
+  pad_prefix(a, s_beg);
+  const int lane = threadIdx.x & 31;
+  const long long n_tasks = (long long)a.S + s_beg[a.E];
+  const long long wstride = (long long)gridDim.x * kRowWarps;
+  constexpr int SEG = 32 * U * VB;  // bytes one warp moves per segment
+  for (long long task = (long long)blockIdx.x * kRowWarps + (threadIdx.x >> 5); task < n_tasks;
+       task += wstride) {
+    if (task < a.S) {
+      const int t = (int)task;
+      const char* srow = a.src + (size_t)t * a.row_bytes;
+      for (int seg = 0; seg < a.row_bytes; seg += SEG) {
+        typename V::T r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (off < a.row_bytes) r[u] = V::ld_stream(srow + off);
+        }
+        for (int j = 0; j < a.k; ++j) {
+          const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
+          if (s < 0) continue;
+          const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
+          char* drow = a.dst + ((size_t)e * a.cap + s) * a.row_bytes;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int off = seg + (lane + 32 * u) * VB;
+            if (off < a.row_bytes) V::st(drow + off, r[u]);
+          }
+        }
+      }
+    } else {
+      // padding row: binary search its expert in the prefix
+      const int p = (int)(task - a.S);
+      int lo = 0, hi = a.E - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
+      }
+      const int e = lo;
+      const int s = min(__ldg(a.load + e), a.cap) + (p - s_beg[e]);
+      char* drow = a.dst + ((size_t)e * a.cap + s) * a.row_bytes;
+      const typename V::T z = V::zero();
+      for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
+    }
+  }
+}
+
+// ------------------------------------------------------------ Reverse + combine
+struct F32Acc {
+  static constexpr int kPerVec = 8;  // fp32 per 32 bytes
+};
+
+template <int DT>  // MOE_F32 or MOE_BF16; 32-byte vectors
+__device__ __forceinline__ void fma_vec(float* acc, float w, const V8& v) {
+  if constexpr (DT == MOE_F32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc[2 * q] = fmaf(w, bf16lo(v.w[q]), acc[2 * q]);
+      acc[2 * q + 1] = fmaf(w, bf16hi(v.w[q]), acc[2 * q + 1]);
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ V8 pack_vec(const float* acc) {
+  V8 o;
+  if constexpr (DT == MOE_F32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o.w[q] = __float_as_uint(acc[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o.w[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
+  }
+  return o;
+}
+
+template <int DT, int U>
+__global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
+  constexpr int VB = 32;
+  constexpr int NA = DT == MOE_F32 ? 8 : 16;  // accumulators per vector
+  constexpr int SEG = 32 * U * VB;
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * kRowWarps;
+  for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
+    char* yrow = a.dst + (size_t)t * a.row_bytes;
+    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
+      float acc[U][NA];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < NA; ++q) acc[u][q] = 0.f;
+      for (int j = 0; j < a.k; j += 2) {
+        // two slots per round so both rows' loads are in flight together
+        int s0 = __ldg(a.slot_idx + (size_t)t * a.k + j);
+        int s1 = j + 1 < a.k ? __ldg(a.slot_idx + (size_t)t * a.k + j + 1) : -1;
+        V8 r0[U], r1[U];
+        float w0 = 0.f, w1 = 0.f;
+        if (s0 >= 0) {
+          const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
+          w0 = __ldg(a.weight + (size_t)t * a.k + j);
+          const char* b = a.src + ((size_t)e * a.cap + s0) * a.row_bytes;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int off = seg + (lane + 32 * u) * VB;
+            if (off < a.row_bytes) r0[u] = ld_stream_v8(b + off);
+          }
+        }
+        if (s1 >= 0) {
+          const int e = __ldg(a.expert_idx + (size_t)t * a.k + j + 1);
+          w1 = __ldg(a.weight + (size_t)t * a.k + j + 1);
+          const char* b = a.src + ((size_t)e * a.cap + s1) * a.row_bytes;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int off = seg + (lane + 32 * u) * VB;
+            if (off < a.row_bytes) r1[u] = ld_stream_v8(b + off);
+          }
+        }
+        if (s0 >= 0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (seg + (lane + 32 * u) * VB < a.row_bytes) fma_vec<DT>(acc[u], w0, r0[u]);
+        }
+        if (s1 >= 0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (seg + (lane + 32 * u) * VB < a.row_bytes) fma_vec<DT>(acc[u], w1, r1[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int off = seg + (lane + 32 * u) * VB;
+        if (off < a.row_bytes) st_v8(yrow + off, pack_vec<DT>(acc[u]));
+      }
+    }
+  }
+}
+
+// 16-byte fallback of the combine for rows that are not a multiple of 32 B.
+template <int DT>
+__global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * kRowWarps;
+  constexpr int NA = DT == MOE_F32 ? 4 : 8;
+  for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
+    char* yrow = a.dst + (size_t)t * a.row_bytes;
+    for (int off = lane * 16; off < a.row_bytes; off += 32 * 16) {
+      float acc[NA];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) acc[q] = 0.f;
+      for (int j = 0; j < a.k; ++j) {
+        const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
+        if (s < 0) continue;
+        const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
+        const float w = __ldg(a.weight + (size_t)t * a.k + j);
+        const V4 v = ld_stream_v4(a.src + ((size_t)e * a.cap + s) * a.row_bytes + off);
+        if constexpr (DT == MOE_F32) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[2 * q] = fmaf(w, bf16lo(v.w[q]), acc[2 * q]);
+            acc[2 * q + 1] = fmaf(w, bf16hi(v.w[q]), acc[2 * q + 1]);
+          }
+        }
+      }
+      V4 o;
+      if constexpr (DT == MOE_F32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o.w[q] = __float_as_uint(acc[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o.w[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
+      }
+      st_v4(yrow + off, o);
+    }
+  }
+}
+
+// ------------------------------------------------------------ expert stand-in
+template <int DT>
+__global__ void __launch_bounds__(kRowThreads) k_expert_scale(const char* in, char* out,
+                                                              long long n_vec, int row_vecs,
+                                                              int cap, int E_local, int e_base) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n_vec; v += stride) {
+    const long long row = v / row_vecs;
+    const int le = (int)((row / cap) % E_local);
+    const float s = 1.0f + (float)((e_base + le) % 8) * 0.125f;  // exact
+    V4 x = ld_stream_v4(in + v * 16);
+    V4 o;
+    if constexpr (DT == MOE_F32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o.w[q] = __float_as_uint(__fmul_rn(__uint_as_float(x.w[q]), s));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o.w[q] = pack_bf16x2(__fmul_rn(bf16lo(x.w[q]), s), __fmul_rn(bf16hi(x.w[q]), s));
+    }
+    st_v4(out + v * 16, o);
+  }
+}
+
+// ------------------------------------------------------------ chunk permute
+// dst chunk (n, g, m) <- src chunk (g, m, n) for n, m < G and g < N:
+// phase (4) of the hierarchical AllToAll, "reorder by destination device".
+__global__ void __launch_bounds__(kRowThreads) k_chunk_permute(const char* src, char* dst, int N,
+                                                               int G, long long chunk_bytes) {
+  const long long vecs = chunk_bytes / 16;
+  const long long total = (long long)N * G * G * vecs;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long c = i / vecs, v = i % vecs;  // c = destination chunk (n, g, m)
+    const int m = (int)(c % G);
+    const int g = (int)((c / G) % N);
+    const int n = (int)(c / ((long long)G * N));
+    const long long sc = ((long long)g * G + m) * G + n;
+    st_v4(dst + c * chunk_bytes + v * 16, ld_stream_v4(src + sc * chunk_bytes + v * 16));
+  }
+}
+
+// ------------------------------------------------------------ host side
+static int row_grid(const void* kern) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);
+  return std::max(1, per_sm) * device_sm_count();
+}
+
+moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
+                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream) {
+  RowArgs a{};
+  a.src = static_cast<const char*>(x);
+  a.dst = static_cast<char*>(dispatch);
+  a.expert_idx = r.expert_idx;
+  a.slot_idx = r.slot_idx;
+  a.load = r.load;
+  a.S = d.S;
+  a.E = d.E;
+  a.k = d.k;
+  a.cap = d.capacity;
+  a.row_bytes = dtype_size * dcols;
+  a.d = dcols;
+  if (a.row_bytes % 32 == 0) {
+    auto kern = k_layout<32, 4>;
+    kern<<<row_grid((const void*)kern), kRowThreads, 0, stream>>>(a);
+  } else {
+    auto kern = k_layout<16, 4>;
+    kern<<<row_grid((const void*)kern), kRowThreads, 0, stream>>>(a);
+  }
+  MOE_CHECK_LAUNCH("moe_layout: k_layout launch");
+  return MOE_OK;
+}
+
+moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
+                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream) {
+  RowArgs a{};
+  a.src = static_cast<const char*>(back);
+  a.dst = static_cast<char*>(y);
+  a.expert_idx = r.expert_idx;
+  a.slot_idx = r.slot_idx;
+  a.weight = r.weight;
+  a.S = d.S;
+  a.E = d.E;
+  a.k = d.k;
+  a.cap = d.capacity;
+  a.row_bytes = dtype_size * dcols;
+  a.d = dcols;
+  const void* kern;
+  if (a.row_bytes % 32 == 0) {
+    kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 2> : (const void*)k_reverse<MOE_BF16, 2>;
+  } else {
+    kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
+  }
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernel(kern, dim3(row_grid(kern)), dim3(kRowThreads), args, 0, stream);
+  if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
+  return MOE_OK;
+}
+
+moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
+                                 int cap, int dcols, int dtype, int dtype_size,
+                                 cudaStream_t stream) {
+  const long long row_bytes = (long long)dcols * dtype_size;
+  const long long n_vec = (long long)nsrc * E_local * cap * row_bytes / 16;
+  const int row_vecs = (int)(row_bytes / 16);
+  const void* kern =
+      dtype == MOE_F32 ? (const void*)k_expert_scale<MOE_F32> : (const void*)k_expert_scale<MOE_BF16>;
+  const char* pin = static_cast<const char*>(in);
+  char* pout = static_cast<char*>(out);
+  void* args[] = {&pin, &pout, (void*)&n_vec, (void*)&row_vecs, &cap, &E_local, &e_base};
+  int grid = (int)std::min<long long>((n_vec + kRowThreads - 1) / kRowThreads,
+                                      (long long)row_grid(kern));
+  if (grid < 1) return MOE_OK;
+  cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(kRowThreads), args, 0, stream);
+  if (e != cudaSuccess) return cuda_status(e, "moe_expert_scale: launch");
+  return MOE_OK;
+}
+
+moe_status_t chunk_permute_launch(const void* src, void* dst, int N, int G, long long chunk_bytes,
+                                  cudaStream_t stream) {
+  const long long total = (long long)N * G * G * (chunk_bytes / 16);
+  int grid = (int)std::min<long long>((total + kRowThreads - 1) / kRowThreads,
+                                      (long long)row_grid((const void*)k_chunk_permute));
+  if (grid < 1) return MOE_OK;
+  k_chunk_permute<<<grid, kRowThreads, 0, stream>>>(static_cast<const char*>(src),
+                                                    static_cast<char*>(dst), N, G, chunk_bytes);
+  MOE_CHECK_LAUNCH("moe_alltoall: k_chunk_permute launch");
+  return MOE_OK;
+}
+
+}  // namespace moe

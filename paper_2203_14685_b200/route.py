@@ -1,0 +1,60 @@
+"""Algorithm 1's routing path on one rank, with every buffer
+resident in HBM and sized once: gate -> Layout_Transform -> AllToAll ->
+(expert stand-in) -> AllToAll -> Reverse_Layout_Transform.
+
+Orchestration only: each step is one call into libmoe_b200 (kernels) or its
+NCCL communicator, all enqueued on the current torch stream with no host
+synchronisation (the padded layout makes every size static, R9).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from .api import Comm, Gate, Routing, expert_scale, layout, reverse_layout
+
+
+class RoutePipeline:
+    def __init__(self, S: int, d: int, E: int, k: int, cap: int, dtype=torch.bfloat16,
+                 kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
+                 comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
+                 device=None, slot_src: bool = True):
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.comm = comm
+        self.P = comm.nranks if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        if E % self.P:
+            raise ValueError("E=%d experts do not shard over %d ranks (R10)" % (E, self.P))
+        self.S, self.d, self.E, self.k, self.cap = S, d, E, k, cap
+        self.E_local = E // self.P
+        self.algo, self.group_size = algo, group_size
+        self.gate = Gate(S, E, k, cap, kind, weight_mode, priority, self.device)
+        self.routing = Routing.empty(S, E, k, cap, self.device, self.gate.kind, self.gate.mode,
+                                     self.gate.prio, slot_src)
+        mk = lambda *shape: torch.empty(shape, dtype=dtype, device=self.device)
+        self.dispatch = mk(E, cap, d)
+        if self.P > 1:
+            self.recv = mk(E, cap, d)
+            self.back = mk(E, cap, d)
+        else:
+            self.recv = self.back = self.dispatch
+        self.y = mk(S, d)
+        self.ws = None
+        if self.P > 1 and algo == "hier":
+            nb = comm.workspace_bytes(algo, group_size, self.dispatch.nbytes // self.P)
+            self.ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+
+    def alltoall(self, send, recv):
+        if self.P > 1:
+            self.comm.alltoall(send, recv, self.algo, self.group_size, self.ws)
+
+    def step(self, logits=None, x=None, token_ids=None, table=None, expert: bool = False):
+        r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
+        layout(x, r, out=self.dispatch)                                    # step 2
+        self.alltoall(self.dispatch, self.recv)                            # step 3
+        if expert:                                                         # step 4 (stand-in)
+            expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
+        self.alltoall(self.recv, self.back)                                # step 5
+        reverse_layout(self.back, r, out=self.y)                           # step 6
+        return self.y
