@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py -- MoE dispatch+combine tokens/s of the HetuMoE routing path on
+B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+                    [--algo flat|hier] [--group-size G] [--impl ours|reference]
+    # N > 1: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+
+A step is one pass of the whole routing path on one batch of S tokens per
+rank (Algorithm 1): gate (select + weights + capacity) ->
+Layout_Transform -> AllToAll dispatch -> AllToAll combine ->
+Reverse_Layout_Transform.  The expert is the identity inside the timed step
+(routing isolated, north_star); the s_e stand-in is timed separately
+(`expert_ms`).  Inputs are synthetic (synthgen, seeded) and resident in HBM;
+the L2 is flushed (a 2x-L2 memset) between timed steps, outside the events.
+Each step is timed with CUDA events on the launching stream; the reported
+time is the max over ranks.  `value` = tokens of all ranks / time.
+
+--impl reference runs the CPU oracle (oracle/, plain single-threaded C) on a
+bounded sample of the same workload -- the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "MoE dispatch+combine tokens/s"
+UNIT = "tokens/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+NVLINK_GBS = 770.0         # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--algo", default="flat", choices=["flat", "hier"])
+    ap.add_argument("--group-size", type=int, default=0, help="hier group size (default N/2)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the
+    timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-i", ",".join(map(str, self.gpus)), "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def rejected(clocks):
+    if not clocks:
+        return False
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(clocks["reasons"]):
+        return True
+    return clocks["sm_mhz"] < 0.5 * clocks["sm_max_mhz"] and not clocks["reasons"]
+
+
+def algorithmic_bytes(w, S, cap, P, row):
+    """Per-launch algorithmic bytes."""
+    return {
+        "gate": S * (4 * w.E if w.kind != "hash" else 8) + 12 * S * w.k + 4 * w.E + 4 * w.E * cap,
+        "layout": S * row + w.E * cap * row + 8 * S * w.k,
+        "reverse": None,   # needs the admitted count: filled in at run time
+        "a2a": (P - 1) * (w.E * cap * row // P),
+    }
+
+
+# ---------------------------------------------------------------- reference arm
+def oracle_step(orc, w, inputs, cap, P):
+    xs = [i[3] for i in inputs]
+    lgs = None if w.kind == "hash" else [i[0] for i in inputs]
+    ids = None if w.kind != "hash" else [i[1] for i in inputs]
+    table = None if w.kind != "hash" else inputs[0][2]
+    return orc.route_multi(xs, lgs, E=w.E, k=w.k, cap=cap, kind=w.kind, token_ids_list=ids,
+                           table=table, scale=False)
+
+
+def cpu_sample(w, P, target_s):
+    """A bounded sample of the workload for the oracle: S_s tokens per rank
+    (the full S if one P-rank step costs <= ~1.5 s on one core)."""
+    per_tok = 14e-6 * w.d / 1024 * max(1, w.k)   # measured ~0.45 s for C2 (32768 tok) per rank
+    S_s = w.S
+    while S_s > 256 and P * S_s * per_tok > 1.5:
+        S_s //= 2
+    return S_s
+
+
+def run_reference(a, w, world, rank):
+    import oracle
+    import synthgen
+    if rank != 0:
+        return
+    P = world
+    S_s = cpu_sample(w, P, a.cpu_seconds)
+    cap = oracle.capacity(S_s, w.E, w.k, w.C)
+    inputs = [synthgen.workload_inputs(w, r, S=S_s) for r in range(P)]
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    for _ in range(max(0, a.warmup)):
+        oracle_step(oracle, w, inputs, cap, P)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        oracle_step(oracle, w, inputs, cap, P)
+    dt = (time.perf_counter() - t0) / max(1, a.steps)
+    value = P * S_s / dt
+    sample = ("oracle route (gate+layout+AllToAll sim+AllToAll sim+reverse) on %d simulated "
+              "rank(s) x %d tokens per rank of %s (full S=%d), 1 thread" % (P, S_s, w.name, w.S))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)", "data": "synthetic",
+        "config": {"workload": w.name, "S_per_rank": S_s, "d": w.d, "E": w.E, "k": w.k,
+                   "gate": w.kind, "capacity_factor": w.C, "parallelism": "ep%d" % P},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    import synthgen
+    w = synthgen.WORKLOADS[a.workload]
+    world, rank, local = dist_env()
+    if a.impl == "reference":
+        run_reference(a, w, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2203_14685_b200 as moe
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
+    P = world
+    G = a.group_size or max(1, P // 2)
+    comm = moe.Comm.from_process_group() if P > 1 else None
+    S = w.S
+    cap = moe.capacity(S, w.E, w.k, w.C)
+    dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    row = w.d * (2 if w.dtype == "bf16" else 4)
+    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm,
+                             algo=a.algo if P > 1 else "flat", group_size=G, device=dev)
+
+    lg, ids, table, x = synthgen.workload_inputs(w, rank)
+
+    def pinned(arr):
+        if arr is None:
+            return None
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if arr.dtype == np.uint16:
+            t = t.view(torch.int16).view(torch.bfloat16)
+        return t.pin_memory()
+
+    host = {"logits": pinned(lg), "x": pinned(x), "token_ids": pinned(ids), "table": pinned(table)}
+    d_in = {k: (None if v is None else v.to(dev)) for k, v in host.items()}
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if P > 1:
+            dist.barrier()
+
+    def step(mark=None):
+        return pipe.step(d_in["logits"], d_in["x"], d_in["token_ids"], d_in["table"],
+                         expert=False, mark=mark)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    stages = ["gate", "layout", "a2a_dispatch", "a2a_combine", "reverse"]
+
+    def timed(K):
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+              for _ in range(K)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(K):
+            flush.zero_()                       # L2 flush, outside the events
+            marks = iter(ev[i][1:])
+            ev[i][0].record()
+            step(lambda name: next(marks).record())
+        torch.cuda.synchronize()
+        barrier()
+        tot = [ev[i][0].elapsed_time(ev[i][-1]) for i in range(K)]
+        st = [[ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(K)] for j in range(len(stages))]
+        return tot, st
+
+    gpus = list(range(torch.cuda.device_count())) if P > 1 else [local]
+    clocks = None
+    for attempt in range(2):
+        sampler = ClockSampler(gpus) if (rank == 0 and not a.no_clocks) else None
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        tot, st = timed(a.steps)
+        if sampler:
+            clocks = sampler.stop()
+        bad = torch.tensor([1.0 if rejected(clocks) else 0.0])
+        if P > 1:
+            dist.broadcast(bad, 0)
+        if bad.item() == 0:
+            break
+    # max over ranks (per step mean, per stage mean)
+    vals = torch.tensor([statistics.mean(tot)] + [statistics.mean(s) for s in st] +
+                        [min(tot)], dtype=torch.float64)
+    if P > 1:
+        vals_d = vals.to(dev)
+        dist.all_reduce(vals_d, op=dist.ReduceOp.MAX)
+        vals = vals_d.cpu()
+    ms = float(vals[0])
+    stage_ms = {s: float(vals[1 + j]) for j, s in enumerate(stages)}
+    value = P * S / (ms / 1e3)
+
+    # expert stand-in, timed on its own (not part of the step)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    e0.record()
+    moe.expert_scale(pipe.recv, P, w.E // P, rank * (w.E // P), out=pipe.recv)
+    e1.record()
+    torch.cuda.synchronize()
+    expert_ms = e0.elapsed_time(e1)
+
+    # ---- end to end through the public API from pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        y_h = torch.empty((S, w.d), dtype=dt, pin_memory=True)
+        staging = {}
+        for _ in range(2):
+            pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
+                           inputs=staging)
+        torch.cuda.synchronize()
+        K2 = max(3, a.steps // 2)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K2)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(K2):
+            flush.zero_()
+            evs[i][0].record()
+            pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
+                           inputs=staging)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        barrier()
+        t_e2e = torch.tensor([statistics.mean(s.elapsed_time(e) for s, e in evs)],
+                             dtype=torch.float64)
+        if P > 1:
+            t_d = t_e2e.to(dev)
+            dist.all_reduce(t_d, op=dist.ReduceOp.MAX)
+            t_e2e = t_d.cpu()
+        h2d = sum(v.numel() * v.element_size() for k, v in host.items()
+                  if v is not None and k != "table") + (
+            host["table"].numel() * 4 if host["table"] is not None else 0)
+        e2e = {"value": P * S / (float(t_e2e[0]) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(S * row),
+               "ms_per_step": float(t_e2e[0])}
+
+    # ---- roofline of the dominant kernel (layout or reverse; HBM-bound)
+    admitted = int((pipe.routing.slot_idx >= 0).sum().item())
+    ab = algorithmic_bytes(w, S, cap, P, row)
+    ab["reverse"] = admitted * row + S * row + 12 * S * w.k
+    dom = "layout" if stage_ms["layout"] >= stage_ms["reverse"] else "reverse"
+    peak, peak_src = measured_peaks()
+    achieved = ab[dom] / (stage_ms[dom] / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get("%s/%s" % (w.name, dom))
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "kernel": "k_" + dom, "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_bytes": ab[dom], "peak_source": peak_src,
+            "per_kernel_gbs": {
+                "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+                "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
+                "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9}}
+    a2a = None
+    if P > 1:
+        a2a = {"bytes_out_per_rank": ab["a2a"],
+               "busbw_gbs": {s: ab["a2a"] / (stage_ms[s] / 1e3) / 1e9
+                             for s in ("a2a_dispatch", "a2a_combine")},
+               "peak_gbs": NVLINK_GBS, "algo": a.algo, "group_size": G if a.algo == "hier" else None}
+        a2a["frac"] = min(a2a["busbw_gbs"].values()) / NVLINK_GBS
+
+    # ---- CPU baseline: the oracle, rank 0, N=1 only, bounded sample
+    cpu = None
+    if rank == 0 and P == 1 and not a.no_cpu_baseline:
+        import oracle
+        S_s = cpu_sample(w, 1, a.cpu_seconds)
+        capo = oracle.capacity(S_s, w.E, w.k, w.C)
+        inputs = [synthgen.workload_inputs(w, 0, S=S_s)]
+        try:
+            aff = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {sorted(aff)[0]})
+        except Exception:
+            aff = None
+        oracle_step(oracle, w, inputs, capo, 1)
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < a.cpu_seconds or n < 2:
+            oracle_step(oracle, w, inputs, capo, 1)
+            n += 1
+        dtc = (time.perf_counter() - t0) / n
+        if aff:
+            os.sched_setaffinity(0, aff)
+        cpu = {"value": S_s / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": "%d oracle steps (gate+layout+reverse, AllToAll identity at P=1) on "
+                         "%d of %d tokens of %s, single thread pinned to one core; %d host cores "
+                         "present" % (n, S_s, w.S, w.name, os.cpu_count())}
+
+    # our kernels per step: gate (+ finalize for SLOT priority), layout, reverse,
+    # and on hierarchical leaders one chunk permute per AllToAll
+    launches_per_step = 3 + (2 if (P > 1 and a.algo == "hier" and rank % G == 0) else 0)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
+            "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+            "data": "synthetic (synthgen: seeded N(0,1) logits/tokens, no near ties)",
+            "config": {"workload": w.name, "desc": w.note, "S_per_rank": S, "d": w.d, "E": w.E,
+                       "k": w.k, "gate": w.kind, "capacity_factor": w.C, "capacity": cap,
+                       "a2a": a.algo if P > 1 else None,
+                       "parallelism": "ep%d (experts sharded, tokens data-parallel)" % P,
+                       "l2": "flushed between timed steps (2x L2 memset, outside events)",
+                       "expert": "identity in the timed step; s_e stand-in timed separately"},
+            "stages_ms": stage_ms, "expert_ms": expert_ms, "min_ms_per_step": float(vals[-1]),
+            "admitted_slots": admitted, "roofline": roof, "alltoall": a2a, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches_per_step * a.steps,
+            "library": moe.version(),
+        }
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if P > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -49,12 +49,44 @@ class RoutePipeline:
         if self.P > 1:
             self.comm.alltoall(send, recv, self.algo, self.group_size, self.ws)
 
-    def step(self, logits=None, x=None, token_ids=None, table=None, expert: bool = False):
+    def step(self, logits=None, x=None, token_ids=None, table=None, expert: bool = False,
+             mark=None):
+        """One pass of Algorithm 1 on device-resident inputs; returns y.
+        `mark(name)` (optional) is called after each stage is enqueued (the
+        bench records a CUDA event there)."""
+        mark = mark or (lambda name: None)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
+        mark("gate")
         layout(x, r, out=self.dispatch)                                    # step 2
+        mark("layout")
         self.alltoall(self.dispatch, self.recv)                            # step 3
+        mark("a2a_dispatch")
         if expert:                                                         # step 4 (stand-in)
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
+            mark("expert")
         self.alltoall(self.recv, self.back)                                # step 5
+        mark("a2a_combine")
         reverse_layout(self.back, r, out=self.y)                           # step 6
+        mark("reverse")
         return self.y
+
+    def step_host(self, logits_h=None, x_h=None, y_h=None, token_ids_h=None, table_h=None,
+                  expert: bool = False, inputs=None):
+        """The same pass from HOST buffers (pinned for async copies): copy the
+        step's inputs host->device, run it, copy y device->host into y_h.
+        `inputs` (optional) are device staging tensors to reuse."""
+        dev_in = inputs or {}
+        def up(name, h):
+            if h is None:
+                return None
+            t = dev_in.get(name)
+            if t is None:
+                t = dev_in[name] = torch.empty(h.shape, dtype=h.dtype, device=self.device)
+            t.copy_(h, non_blocking=True)
+            return t
+        y = self.step(up("logits", logits_h), up("x", x_h), up("token_ids", token_ids_h),
+                      up("table", table_h), expert)
+        if y_h is None:
+            y_h = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+        y_h.copy_(y, non_blocking=True)
+        return y_h
