@@ -17,6 +17,23 @@ void set_error(const char* fmt, ...);  // thread-local detail (api.cu)
 moe_status_t cuda_status(cudaError_t e, const char* what);
 int device_sm_count();                 // cached per device
 
+// Launch with the PDL attribute (kernel args passed as a void* array).
+inline cudaError_t launch_pdl(const void* kern, dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, kern, args);
+}
+int env_int(const char* name, int dflt);  // tuning knobs (api.cu)
+
 #define MOE_CHECK_LAUNCH(what)                                   \
   do {                                                           \
     cudaError_t _e = cudaGetLastError();                         \
@@ -68,6 +85,18 @@ __device__ __forceinline__ void st_v4(void* p, const V4& r) {
                : "memory");
 }
 
+// ------------------------------------------------------------ gpu-scope words
+// Relaxed gpu-scope accesses go to L2 (coherent across SMs) without a fence;
+// enough for status words that carry their own payload.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // ------------------------------------------------------------ acquire / release
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -76,6 +105,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 }
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ------------------------------------------------------------ PDL
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; it must call pdl_wait() before touching the
+// predecessor's output.  pdl_trigger() lets our own dependent launch early
+// (it still waits for our completion in its pdl_wait()).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

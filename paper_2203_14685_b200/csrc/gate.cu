@@ -15,7 +15,8 @@
 //            items of the same expert column (__match_any_sync, 32 items at a
 //            time, per-warp histograms), then a decoupled look-back across
 //            tiles per column: 64-bit status words (epoch | flag | value)
-//            published with st.release and read with ld.acquire.  slot =
+//            that carry their own payload, so relaxed gpu-scope stores and
+//            loads suffice (no fences on the critical path).  slot =
 //            tiles-before + warps-before + rank-in-warp; >= cap -> dropped.
 //            SLOT priority (j-major) runs the same scan per (j, e) column and
 //            k_gate_slot_finalize adds the totals of earlier j afterwards.
@@ -49,7 +50,7 @@ struct GateArgs {
   int32_t* load;
   int32_t* slot_src;
   GateCtrl* ctrl;
-  unsigned long long* status;  // [n_tiles][ncols]
+  unsigned long long* status;  // [ncols][n_tiles] (column-major: warp look-back)
   int32_t* totals;             // [ncols] (SLOT priority)
 };
 
@@ -69,7 +70,10 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   GatePlan p{};
   p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.E);
   p.K = d.k <= 1 ? 1 : d.k <= 2 ? 2 : d.k <= 4 ? 4 : d.k <= 8 ? 8 : 0;
+  // >= 256 tiles when S allows (about 1.7 CTAs per SM on 148 SMs), tiles of
+  // 32..256 tokens, at most kMaxTileItems items per tile
   int tt = 256;
+  while (tt > 32 && (d.S + tt - 1) / tt < 256) tt >>= 1;
   while (tt > 1 && tt * d.k > kMaxTileItems) tt >>= 1;
   p.tile_tokens = tt;
   p.n_tiles = (d.S + tt - 1) / tt;
@@ -159,15 +163,23 @@ __device__ __forceinline__ void select_topk_reg(const GateArgs& a, int t, bool v
   if (valid) for_lane_logits(row, l, epl, vec4, [&](float x, int e) { top.insert(x, e); });
 #pragma unroll
   for (int m = 1; m < L; m <<= 1) {
+    // snapshot the partner's whole list first: both lanes mutate their own
+    float ov[K];
+    int oi[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      float ov = __shfl_xor_sync(0xffffffffu, top.v[p], m);
-      int oi = __shfl_xor_sync(0xffffffffu, top.i[p], m);
-      top.insert(ov, oi);
+      ov[p] = __shfl_xor_sync(0xffffffffu, top.v[p], m);
+      oi[p] = __shfl_xor_sync(0xffffffffu, top.i[p], m);
     }
+#pragma unroll
+    for (int p = 0; p < K; ++p) top.insert(ov[p], oi[p]);
   }
-  // weights in fp64 (R1); m = the row maximum = top.v[0]
+  // weights in fp64 (R1); m = the row maximum = top.v[0], exp(0) = 1 exactly
   const double mx = (double)top.v[0];
+  double ex[K];
+  ex[0] = 1.0;
+#pragma unroll
+  for (int p = 1; p < K; ++p) ex[p] = (p < a.k) ? exp((double)top.v[p] - mx) : 0.0;
   double den = 0.0;
   if (a.mode == MOE_W_SOFTMAX) {
     double part = 0.0;
@@ -175,8 +187,7 @@ __device__ __forceinline__ void select_topk_reg(const GateArgs& a, int t, bool v
     den = group_sum<L>(part);
   } else {
 #pragma unroll
-    for (int p = 0; p < K; ++p)
-      if (p < a.k) den += exp((double)top.v[p] - mx);
+    for (int p = 0; p < K; ++p) den += ex[p];
   }
   if (valid && l == 0) {
     const size_t o = (size_t)t * a.k;
@@ -184,7 +195,7 @@ __device__ __forceinline__ void select_topk_reg(const GateArgs& a, int t, bool v
     for (int p = 0; p < K; ++p) {
       if (p < a.k) {
         a.expert_idx[o + p] = top.i[p];
-        a.weight[o + p] = (float)(exp((double)top.v[p] - mx) / den);
+        a.weight[o + p] = (float)(ex[p] / den);
         s_sel[p] = top.i[p];
       }
     }
@@ -322,10 +333,12 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   int* s_rank = s_exp + items;                // [items] rank inside its warp
   int* s_hist = s_rank + items;               // [warps][ncols]
   int* s_excl = s_hist + kGateWarps * a.ncols;  // [ncols] tiles-before
-  int* s_tot = s_excl + a.ncols;              // [ncols] inclusive (last tile)
+  int* s_tot = s_excl + a.ncols;              // [ncols] aggregate, then inclusive
   __shared__ unsigned s_tile, s_epoch, s_bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();     // the producer of the logits / the previous step must be done
+  pdl_trigger();  // moe_layout may launch now; it waits for our completion
   if (tid == 0) {
     s_tile = atomicAdd(&a.ctrl->ticket, 1u);
     s_epoch = *((volatile unsigned*)&a.ctrl->epoch) & 0x3FFFFFFFu;
@@ -409,7 +422,11 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   }
   __syncthreads();
 
-  // ---------------- Phase B2: warp prefix + decoupled look-back per column
+  // ---------------- Phase B2: warp prefix, then a decoupled look-back per
+  // column.  Aggregates are published first (successors never wait on our
+  // look-back); then one warp per column scans 32 predecessor tiles at a time
+  // (status is column-major, so the 32 lanes read 256 contiguous bytes) and
+  // stops at the nearest tile that already carries an inclusive prefix.
   const bool last_tile = tile == a.n_tiles - 1;
   for (int c = tid; c < a.ncols; c += kGateThreads) {
     int run = 0;
@@ -419,26 +436,45 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
       s_hist[w * a.ncols + c] = run;
       run += v;
     }
-    const unsigned agg = (unsigned)run;
-    unsigned long long* my = a.status + (size_t)tile * a.ncols + c;
+    s_tot[c] = run;  // tile aggregate (overwritten by the inclusive total below)
+    st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
+                   (epoch << 34) | ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)run);
+  }
+  __syncthreads();
+  for (int c = warp; c < a.ncols; c += kGateWarps) {
+    const unsigned agg = (unsigned)s_tot[c];
     unsigned excl = 0;
-    if (tile == 0) {
-      st_release_u64(my, (epoch << 34) | (2ull << 32) | agg);
-    } else {
-      st_release_u64(my, (epoch << 34) | (1ull << 32) | agg);
-      int p = tile - 1;
+    if (tile > 0) {
+      const unsigned long long* col = a.status + (size_t)c * a.n_tiles;
+      int hi = tile - 1;
       while (true) {
-        const unsigned long long w = ld_acquire_u64(a.status + (size_t)p * a.ncols + c);
-        const unsigned flag = (unsigned)(w >> 32) & 3u;
-        if ((w >> 34) != epoch || flag == 0) continue;  // predecessor not published yet
-        excl += (unsigned)w;
-        if (flag == 2) break;
-        --p;
+        const int p = hi - lane;  // lane 0 = nearest predecessor
+        unsigned flag = 2, val = 0;
+        if (p >= 0) {
+          unsigned long long w;
+          do {
+            w = ld_relaxed_u64(col + p);
+            flag = (unsigned)(w >> 32) & 3u;
+          } while ((w >> 34) != epoch || flag == 0);
+          val = (unsigned)w;
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+        const int first = incl ? __ffs(incl) - 1 : 31;
+        unsigned contrib = lane <= first ? val : 0u;
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, m);
+        excl += contrib;
+        if (incl) break;
+        hi -= 32;
       }
-      st_release_u64(my, (epoch << 34) | (2ull << 32) | (excl + agg));
+      if (lane == 0)
+        st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
+                       (epoch << 34) | (2ull << 32) | (excl + agg));
     }
-    s_excl[c] = (int)excl;
-    if (last_tile) s_tot[c] = (int)(excl + agg);
+    if (lane == 0) {
+      s_excl[c] = (int)excl;
+      s_tot[c] = (int)(excl + agg);
+    }
   }
   __syncthreads();
 
@@ -478,15 +514,15 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
 
   // ---------------- reset the control block for the next call
   __syncthreads();
+  // Every CTA read the epoch before it incremented `done`, so the last one
+  // may reset the block without a fence; the next launch sees it.
   if (tid == 0) {
     if (s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-    __threadfence();
     const unsigned prev = atomicAdd(&a.ctrl->done, 1u);
     if (prev == gridDim.x - 1) {
       a.ctrl->ticket = 0;
       a.ctrl->done = 0;
       a.ctrl->epoch = (unsigned)((epoch + 1) & 0x3FFFFFFFu);
-      __threadfence();
     }
   }
 }
@@ -595,8 +631,12 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
                                          (int)p.smem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
   }
-  kern<<<p.n_tiles, kGateThreads, p.smem, stream>>>(a);
-  MOE_CHECK_LAUNCH("moe_gate: k_gate launch");
+  {
+    void* args[] = {&a};
+    cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
+                               stream, args);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate launch");
+  }
   if (d.priority == MOE_PRIO_SLOT) {
     const size_t n = std::max((size_t)d.S * d.k, (size_t)d.E * d.capacity);
     int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)device_sm_count() * 8);

@@ -90,6 +90,8 @@ template <int VB, int U>
 __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   using V = Vec<VB>;
   __shared__ int s_beg[257];
+  pdl_wait();     // routing comes from moe_gate
+  pdl_trigger();
   pad_prefix(a, s_beg);
   const int lane = threadIdx.x & 31;
   const long long n_tasks = (long long)a.S + s_beg[a.E];
@@ -174,6 +176,8 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
   constexpr int SEG = 32 * U * VB;
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * kRowWarps;
+  pdl_wait();     // expert outputs come from the AllToAll / the layout
+  pdl_trigger();
   for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
     char* yrow = a.dst + (size_t)t * a.row_bytes;
     for (int seg = 0; seg < a.row_bytes; seg += SEG) {
@@ -234,6 +238,8 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * kRowWarps;
   constexpr int NA = DT == MOE_F32 ? 4 : 8;
+  pdl_wait();
+  pdl_trigger();
   for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
     char* yrow = a.dst + (size_t)t * a.row_bytes;
     for (int off = lane * 16; off < a.row_bytes; off += 32 * 16) {
@@ -271,26 +277,33 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
 }
 
 // ------------------------------------------------------------ expert stand-in
+// One warp per row of [nsrc][E_local][cap] rows; s_e = 1 + (e mod 8)/8 is
+// exact, and one fp32 multiply of a bf16 (or fp32) value rounds once.
 template <int DT>
 __global__ void __launch_bounds__(kRowThreads) k_expert_scale(const char* in, char* out,
-                                                              long long n_vec, int row_vecs,
+                                                              long long n_rows, int row_bytes,
                                                               int cap, int E_local, int e_base) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n_vec; v += stride) {
-    const long long row = v / row_vecs;
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * kRowWarps;
+  for (long long row = (long long)blockIdx.x * kRowWarps + (threadIdx.x >> 5); row < n_rows;
+       row += wstride) {
     const int le = (int)((row / cap) % E_local);
     const float s = 1.0f + (float)((e_base + le) % 8) * 0.125f;  // exact
-    V4 x = ld_stream_v4(in + v * 16);
-    V4 o;
-    if constexpr (DT == MOE_F32) {
+    const char* src = in + row * row_bytes;
+    char* dst = out + row * row_bytes;
+    for (int off = lane * 16; off < row_bytes; off += 32 * 16) {
+      V4 x = ld_stream_v4(src + off);
+      V4 o;
+      if constexpr (DT == MOE_F32) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o.w[q] = __float_as_uint(__fmul_rn(__uint_as_float(x.w[q]), s));
-    } else {
+        for (int q = 0; q < 4; ++q) o.w[q] = __float_as_uint(__fmul_rn(__uint_as_float(x.w[q]), s));
+      } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        o.w[q] = pack_bf16x2(__fmul_rn(bf16lo(x.w[q]), s), __fmul_rn(bf16hi(x.w[q]), s));
+        for (int q = 0; q < 4; ++q)
+          o.w[q] = pack_bf16x2(__fmul_rn(bf16lo(x.w[q]), s), __fmul_rn(bf16hi(x.w[q]), s));
+      }
+      st_v4(dst + off, o);
     }
-    st_v4(out + v * 16, o);
   }
 }
 
@@ -333,14 +346,16 @@ moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, con
   a.cap = d.capacity;
   a.row_bytes = dtype_size * dcols;
   a.d = dcols;
-  if (a.row_bytes % 32 == 0) {
-    auto kern = k_layout<32, 4>;
-    kern<<<row_grid((const void*)kern), kRowThreads, 0, stream>>>(a);
-  } else {
-    auto kern = k_layout<16, 4>;
-    kern<<<row_grid((const void*)kern), kRowThreads, 0, stream>>>(a);
-  }
-  MOE_CHECK_LAUNCH("moe_layout: k_layout launch");
+  const void* kern;
+  if (a.row_bytes % 32 == 0)
+    kern = env_int("MOE_LAYOUT_U", 4) == 2 ? (const void*)k_layout<32, 2> : (const void*)k_layout<32, 4>;
+  else
+    kern = (const void*)k_layout<16, 4>;
+  void* args[] = {&a};
+  const int occ = env_int("MOE_LAYOUT_CTAS_PER_SM", 0);
+  const int grid = occ > 0 ? occ * device_sm_count() : row_grid(kern);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout launch");
   return MOE_OK;
 }
 
@@ -359,13 +374,19 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
   a.row_bytes = dtype_size * dcols;
   a.d = dcols;
   const void* kern;
+  const int U = env_int("MOE_REVERSE_U", 2);
   if (a.row_bytes % 32 == 0) {
-    kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 2> : (const void*)k_reverse<MOE_BF16, 2>;
+    if (U == 1)
+      kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
+    else
+      kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 2> : (const void*)k_reverse<MOE_BF16, 2>;
   } else {
     kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
   }
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernel(kern, dim3(row_grid(kern)), dim3(kRowThreads), args, 0, stream);
+  const int occ = env_int("MOE_REVERSE_CTAS_PER_SM", 0);
+  const int grid = occ > 0 ? occ * device_sm_count() : row_grid(kern);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
   return MOE_OK;
 }
@@ -373,15 +394,14 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
                                  int cap, int dcols, int dtype, int dtype_size,
                                  cudaStream_t stream) {
-  const long long row_bytes = (long long)dcols * dtype_size;
-  const long long n_vec = (long long)nsrc * E_local * cap * row_bytes / 16;
-  const int row_vecs = (int)(row_bytes / 16);
+  const int row_bytes = dcols * dtype_size;
+  const long long n_rows = (long long)nsrc * E_local * cap;
   const void* kern =
       dtype == MOE_F32 ? (const void*)k_expert_scale<MOE_F32> : (const void*)k_expert_scale<MOE_BF16>;
   const char* pin = static_cast<const char*>(in);
   char* pout = static_cast<char*>(out);
-  void* args[] = {&pin, &pout, (void*)&n_vec, (void*)&row_vecs, &cap, &E_local, &e_base};
-  int grid = (int)std::min<long long>((n_vec + kRowThreads - 1) / kRowThreads,
+  void* args[] = {&pin, &pout, (void*)&n_rows, (void*)&row_bytes, &cap, &E_local, &e_base};
+  int grid = (int)std::min<long long>((n_rows + kRowWarps - 1) / kRowWarps,
                                       (long long)row_grid(kern));
   if (grid < 1) return MOE_OK;
   cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(kRowThreads), args, 0, stream);

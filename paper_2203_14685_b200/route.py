@@ -70,6 +70,50 @@ class RoutePipeline:
         mark("reverse")
         return self.y
 
+    STAGES = ("gate", "layout", "a2a_dispatch", "a2a_combine", "reverse")
+
+    def capture(self, logits=None, x=None, token_ids=None, table=None, expert: bool = False,
+                stages: bool = False, events=None):
+        """Capture the step into CUDA graph(s) bound to these input tensors
+        (refill them in place between replays).  stages=False: one graph for
+        the whole step; with `events` (len(STAGES)+1 torch.cuda.Event(
+        enable_timing=True, external=True)) event-record nodes bracket every
+        stage inside that graph.  stages=True: {stage: graph}.  Run one eager
+        step first (NCCL's lazy setup must not happen inside a capture)."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        graphs = {}
+        with torch.cuda.stream(s):
+            if not stages:
+                g = torch.cuda.CUDAGraph()
+                mark = None
+                if events is not None:
+                    order = {n: i + 1 for i, n in enumerate(self.STAGES)}
+                    mark = lambda name: events[order[name]].record() if name in order else None
+                with torch.cuda.graph(g, stream=s):
+                    if events is not None:
+                        events[0].record()
+                    self.step(logits, x, token_ids, table, expert, mark=mark)
+                graphs = g
+            else:
+                r = self.routing
+                fns = {
+                    "gate": lambda: self.gate(logits, token_ids, table, out=r),
+                    "layout": lambda: layout(x, r, out=self.dispatch),
+                    "a2a_dispatch": lambda: self.alltoall(self.dispatch, self.recv),
+                    "a2a_combine": lambda: self.alltoall(self.recv, self.back),
+                    "reverse": lambda: reverse_layout(self.back, r, out=self.y),
+                }
+                for name in self.STAGES:
+                    if self.P == 1 and name.startswith("a2a"):
+                        continue   # nothing to launch at P=1 (recv/back alias dispatch)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=s):
+                        fns[name]()
+                    graphs[name] = g
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return graphs
+
     def step_host(self, logits_h=None, x_h=None, y_h=None, token_ids_h=None, table_h=None,
                   expert: bool = False, inputs=None):
         """The same pass from HOST buffers (pinned for async copies): copy the
