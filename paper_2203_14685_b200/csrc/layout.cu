@@ -374,7 +374,7 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
   a.row_bytes = dtype_size * dcols;
   a.d = dcols;
   const void* kern;
-  const int U = env_int("MOE_REVERSE_U", 2);
+  const int U = env_int("MOE_REVERSE_U", 1);
   if (a.row_bytes % 32 == 0) {
     if (U == 1)
       kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
