@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--verbose", action="store_true", help="progress on stderr")
     return ap.parse_args()
 
 
@@ -218,13 +219,22 @@ def main():
     import torch.distributed as dist
     import paper_2203_14685_b200 as moe
 
+    t_start = time.time()
+
+    def log(msg):
+        if a.verbose:
+            sys.stderr.write("[bench r%d %.1fs] %s\n" % (rank, time.time() - t_start, msg))
+            sys.stderr.flush()
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
     P = world
     G = a.group_size or max(1, P // 2)
+    log("process group up")
     comm = moe.Comm.from_process_group() if P > 1 else None
+    log("moe comm up")
     S = w.S
     cap = moe.capacity(S, w.E, w.k, w.C)
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
@@ -258,6 +268,7 @@ def main():
     for _ in range(max(3, a.warmup)):
         step()
     torch.cuda.synchronize()
+    log("eager warm-up done")
 
     stages = list(pipe.STAGES)
     # The timed step is ONE CUDA graph replay (gate, layout, AllToAll x2,
@@ -267,10 +278,12 @@ def main():
     ev_in = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(stages) + 1)]
     g_timed = pipe.capture(d_in["logits"], d_in["x"], d_in["token_ids"], d_in["table"],
                            events=ev_in)
+    log("graphs captured")
     for _ in range(2):
         g_step.replay()
         g_timed.replay()
     torch.cuda.synchronize()
+    log("graph warm-up done")
 
     def timed(K):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -331,8 +344,11 @@ def main():
             dist.broadcast(bad, 0)
         if bad.item() == 0:
             break
+    log("timed steps done")
     st = timed_stages(a.steps)
+    log("stage timing done")
     eager = timed_eager(max(3, a.steps // 2))
+    log("eager timing done")
     # max over ranks (per step mean, per stage mean)
     vals = torch.tensor([statistics.mean(tot)] + [statistics.mean(s) for s in st] +
                         [min(tot), statistics.mean(eager)], dtype=torch.float64)
@@ -465,6 +481,10 @@ def main():
             "library": moe.version(),
         }
         print(json.dumps(out), flush=True)
+    # CUDA graphs that captured NCCL work must go before the communicator
+    del g_step, g_timed
+    torch.cuda.synchronize()
+    barrier()
     if comm is not None:
         comm.destroy()
     if P > 1:

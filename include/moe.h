@@ -19,7 +19,8 @@
  *  - Every device call is asynchronous on `stream` (a cudaStream_t; NULL =
  *    legacy default stream) and enqueues no host synchronisation.
  *  - All memory is caller-owned.  The library allocates nothing on the hot
- *    path; it only owns moe_comm_t (the NCCL communicator).
+ *    path; it only owns moe_comm_t (the NCCL communicator) and the symmetric
+ *    peer-mapped buffers of the one-sided NVLink path (moe_comm_symm_alloc).
  *  - Arguments are validated on the host BEFORE anything is enqueued: on any
  *    error nothing was launched, the status says which class of error, and
  *    moe_last_error() (thread-local) names the argument and the values.
@@ -73,8 +74,11 @@ typedef enum { MOE_PRIO_TOKEN = 0, MOE_PRIO_SLOT = 1 } moe_priority_t;
 /* AllToAll algorithms:
  *   FLAT        : one grouped send/recv to every peer (Fig. 5)
  *   HIER_LEADER : the paper's hierarchical scheme mimicked with groups of
- *                 `group_size` consecutive ranks on one box (Fig. 6, R13) */
-typedef enum { MOE_A2A_FLAT = 0, MOE_A2A_HIER_LEADER = 1 } moe_a2a_algo_t;
+ *                 `group_size` consecutive ranks on one box (Fig. 6, R13)
+ *   P2P         : one-sided: SM stores straight into the peers' receive
+ *                 buffers over NVLink (recv must be a symmetric buffer,
+ *                 moe_comm_symm_alloc), then a device-side barrier */
+typedef enum { MOE_A2A_FLAT = 0, MOE_A2A_HIER_LEADER = 1, MOE_A2A_P2P = 2 } moe_a2a_algo_t;
 
 /* Gate problem description.  Enums are carried as int32 for a fixed ABI. */
 typedef struct {
@@ -218,6 +222,45 @@ size_t moe_alltoall_workspace_bytes(int32_t nranks, int32_t algo, int32_t group_
 moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size,
                           const void* send, void* recv, size_t bytes_per_peer,
                           void* ws, size_t ws_bytes, moe_stream_t stream);
+
+/* ---------------------------------------------------------------- one-sided NVLink path
+ * the layout transform fused with the dispatch AllToAll,
+ * with rows stored by the SMs straight into the owner rank's memory over
+ * NVLink peer mappings.  Needs GPUs that can map each other's memory (all
+ * GPUs of an NVSwitch box); otherwise these calls return UNSUPPORTED. */
+
+/* host, collective, blocking.  Allocates `bytes` of device memory on every
+ * rank, zero-filled, mapped into every peer (CUDA IPC).  The library owns it;
+ * free it with moe_comm_symm_free (collective) or moe_comm_destroy. */
+moe_status_t moe_comm_symm_alloc(moe_comm_t* comm, size_t bytes, void** local);
+moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* local);
+
+/* Device-side barrier of all ranks, enqueued on `stream`: returns (in stream
+ * order) once every rank's stream has reached its matching barrier; all
+ * memory writes made before it (including stores into peers' symmetric
+ * buffers) are visible to every rank after it. */
+moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream);
+
+/* Steps 2+3 fused: for every admitted item (t,j) with
+ * expert e and slot s, the row x[t] is stored into rank q = e/(E/P)'s
+ * `recv` at [r][e mod E/P][s] (r = this rank); padding rows
+ * [min(load[e],cap), cap) are zeroed there; then moe_comm_barrier.  The
+ * resulting recv buffers are byte-identical to moe_layout followed by
+ * moe_alltoall(FLAT).  recv: symmetric, [P][E/P][cap][d] of dtype. */
+moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                              const moe_routing_t* routing, const void* x, int32_t d,
+                              int32_t dtype, void* recv, moe_stream_t stream);
+
+/* Steps 5+6 fused: moe_comm_barrier (every rank's experts
+ * are done), then y[t] = sum_j w[t,j] * expert_out_q[r][e mod E/P][s] with
+ * every admitted row read straight from its owner rank q's `expert_out` over
+ * NVLink (fp32 accumulate in ascending j, one RNE store, 0 if all slots
+ * dropped), then moe_comm_barrier (the buffers may be reused).  Same result
+ * as moe_alltoall(FLAT) back + moe_reverse_layout.  expert_out: symmetric,
+ * [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
+moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                             const moe_routing_t* routing, const void* expert_out, int32_t d,
+                             int32_t dtype, void* y, moe_stream_t stream);
 
 /* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
  * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,

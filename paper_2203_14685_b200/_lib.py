@@ -52,6 +52,13 @@ SIGNATURES = [
     ("moe_alltoall", ctypes.c_int, [vp, i32, i32, vp, vp, sz, vp, sz, vp]),
     ("moe_alltoall_plan", ctypes.c_int, [i32, i32, i32, i32, ctypes.POINTER(A2AOp), i32,
                                          ctypes.POINTER(i32)]),
+    ("moe_comm_symm_alloc", ctypes.c_int, [vp, sz, ctypes.POINTER(vp)]),
+    ("moe_comm_symm_free", ctypes.c_int, [vp, vp]),
+    ("moe_comm_barrier", ctypes.c_int, [vp, vp]),
+    ("moe_dispatch_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
+                                        i32, i32, vp, vp]),
+    ("moe_combine_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
+                                       i32, i32, vp, vp]),
     ("moe_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("moe_last_error", ctypes.c_char_p, []),
     ("moe_version", ctypes.c_char_p, []),

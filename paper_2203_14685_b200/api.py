@@ -19,7 +19,7 @@ from ._lib import A2AOp, GateDesc, RoutingC, check, lib
 KINDS = {"topk": 0, "ktop1": 1, "hash": 2}
 MODES = {"renorm": 0, "softmax": 1}
 PRIOS = {"token": 0, "slot": 1}
-ALGOS = {"flat": 0, "hier": 1}
+ALGOS = {"flat": 0, "hier": 1, "p2p": 2}
 _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 
@@ -248,10 +248,64 @@ class Comm:
                                  _stream(send.device)), "moe_alltoall")
         return recv
 
+    def symm_empty(self, shape, dtype) -> torch.Tensor:
+        """A tensor over a library-owned symmetric buffer (mapped into every
+        peer; collective).  Freed by symm_free or destroy."""
+        nb = int(torch.Size(shape).numel()) * torch.empty((), dtype=dtype).element_size()
+        p = ctypes.c_void_p()
+        check(lib().moe_comm_symm_alloc(self._h, nb, ctypes.byref(p)), "moe_comm_symm_alloc")
+        return _tensor_from_ptr(p.value, shape, dtype, torch.cuda.current_device())
+
+    def symm_free(self, t: torch.Tensor):
+        check(lib().moe_comm_symm_free(self._h, _p(t)), "moe_comm_symm_free")
+
+    def barrier(self):
+        """Device-side barrier of all ranks on the current stream."""
+        check(lib().moe_comm_barrier(self._h, _stream()), "moe_comm_barrier")
+
+    def dispatch_p2p(self, x: torch.Tensor, r: "Routing", recv: torch.Tensor) -> torch.Tensor:
+        """Layout_Transform fused with the dispatch AllToAll over NVLink:
+        rows land directly in the owner rank's symmetric `recv`."""
+        _need_cuda(x, "x")
+        d = x.shape[-1]
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_dispatch_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(x), d,
+                                     _DT[x.dtype], _p(recv), _stream(x.device)),
+              "moe_dispatch_p2p")
+        return recv
+
+    def combine_p2p(self, expert_out: torch.Tensor, r: "Routing",
+                    y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """AllToAll combine fused with Reverse_Layout_Transform over NVLink:
+        every admitted row is read from its owner's symmetric `expert_out`."""
+        d = expert_out.shape[-1]
+        if y is None:
+            y = torch.empty((r.S, d), dtype=expert_out.dtype, device=expert_out.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_combine_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(expert_out),
+                                    d, _DT[expert_out.dtype], _p(y), _stream(y.device)),
+              "moe_combine_p2p")
+        return y
+
     def destroy(self):
         if getattr(self, "_h", None):
             check(lib().moe_comm_destroy(self._h), "moe_comm_destroy")
             self._h = None
+
+
+def _tensor_from_ptr(ptr: int, shape, dtype, device_index: int) -> torch.Tensor:
+    """Wrap library-owned device memory as a torch tensor (no copy, no free)."""
+    n = int(torch.Size(shape).numel())
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.int32: "<i4",
+               torch.uint8: "|u1"}[dtype]
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    t = torch.as_tensor(_Holder(), device=torch.device("cuda", device_index))
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    return t.view(shape)
 
 
 def version() -> str:

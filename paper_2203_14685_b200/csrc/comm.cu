@@ -13,19 +13,18 @@
 #include <cstring>
 #include <vector>
 
-#include "common.cuh"
+#include "comm.cuh"
 
 namespace moe {
 
 moe_status_t chunk_permute_launch(const void* src, void* dst, int N, int G, long long chunk_bytes,
                                   cudaStream_t stream);
+moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_off_rank,
+                            size_t bytes_per_peer, int nranks, int rank, cudaStream_t stream);
+moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out);
+void symm_release(moe_comm* c, SymmBuf& b);
 
 }  // namespace moe
-
-struct moe_comm {
-  ncclComm_t nccl;
-  int nranks, rank, device;
-};
 
 namespace moe {
 
@@ -147,13 +146,30 @@ moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, 
   ncclComm_t c;
   moe_status_t s = nccl_status(ncclCommInitRankConfig(&c, nranks, u, rank, &cfg), "moe_comm_init");
   if (s != MOE_OK) return s;
-  moe_comm_t* m = new moe_comm_t{c, nranks, rank, dev};
+  moe_comm_t* m = new moe_comm_t();
+  m->nccl = c;
+  m->nranks = nranks;
+  m->rank = rank;
+  m->device = dev;
+  m->sig = SymmBuf{};
+  // Signal words of the device-side barrier (one-sided NVLink path).  If the
+  // GPUs cannot map each other's memory, that path is reported unsupported;
+  // the NCCL path still works.  Every rank tries, so the collective
+  // handle exchange inside symm_alloc stays matched.
+  m->p2p_ok = false;
+  if (nranks <= kMaxRanks && env_int("MOE_DISABLE_P2P", 0) == 0) {
+    moe_status_t ss = symm_alloc(m, 4096, &m->sig);
+    m->p2p_ok = ss == MOE_OK;
+  }
   *out = m;
   return MOE_OK;
 }
 
 moe_status_t moe_comm_destroy(moe_comm_t* comm) {
   if (!comm) return MOE_OK;
+  cudaDeviceSynchronize();
+  for (SymmBuf& b : comm->symm) symm_release(comm, b);
+  if (comm->sig.base) symm_release(comm, comm->sig);
   moe_status_t s = nccl_status(ncclCommDestroy(comm->nccl), "moe_comm_destroy");
   delete comm;
   return s;
@@ -203,7 +219,7 @@ moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, co
     return MOE_ERR_INVALID_ARG;
   }
   const int P = comm->nranks, r = comm->rank;
-  if (algo != MOE_A2A_FLAT && algo != MOE_A2A_HIER_LEADER) {
+  if (algo != MOE_A2A_FLAT && algo != MOE_A2A_HIER_LEADER && algo != MOE_A2A_P2P) {
     set_error("moe_alltoall: invalid algo %d", algo);
     return MOE_ERR_INVALID_ARG;
   }
@@ -220,6 +236,29 @@ moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, co
   if (send == recv) {
     set_error("moe_alltoall: in-place (send == recv) is not supported for nranks > 1");
     return MOE_ERR_INVALID_ARG;
+  }
+  if (algo == MOE_A2A_P2P) {
+    if (!comm->p2p_ok) {
+      set_error("moe_alltoall(P2P): peer memory is not available between these GPUs");
+      return MOE_ERR_UNSUPPORTED;
+    }
+    if (bytes_per_peer % 16 != 0 || reinterpret_cast<uintptr_t>(send) % 16 ||
+        reinterpret_cast<uintptr_t>(recv) % 16) {
+      set_error("moe_alltoall(P2P): 16-byte aligned buffers and chunks required");
+      return MOE_ERR_ALIGNMENT;
+    }
+    const SymmBuf* sb = find_symm(comm, recv, (size_t)P * bytes_per_peer);
+    if (!sb) {
+      set_error("moe_alltoall(P2P): recv is not inside a symmetric buffer (moe_comm_symm_alloc)");
+      return MOE_ERR_INVALID_ARG;
+    }
+    PeerPtrs dst;
+    const size_t off = static_cast<const char*>(recv) - sb->base;
+    for (int q = 0; q < P; ++q) dst.p[q] = sb->peer.p[q] + off;
+    moe_status_t s = a2a_p2p_launch(static_cast<const char*>(send), dst, (size_t)r * bytes_per_peer,
+                                    bytes_per_peer, P, r, stream);
+    if (s != MOE_OK) return s;
+    return barrier_launch(comm->sig.peer, P, r, stream);
   }
   const bool hier = algo == MOE_A2A_HIER_LEADER;
   if (hier && r % group_size == 0) {

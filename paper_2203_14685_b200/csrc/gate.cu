@@ -31,6 +31,7 @@ constexpr int kGateThreads = 256;
 constexpr int kGateWarps = kGateThreads / 32;
 constexpr int kMaxTileItems = 2048;  // tile_tokens * k
 constexpr int kMaxCols = 2048;       // look-back columns: E or k*E
+constexpr int kLookWords = 8192;     // status words one look-back round reads
 
 struct GateCtrl {  // 64 bytes at the head of the workspace
   unsigned ticket, done, epoch, bad;
@@ -83,7 +84,7 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   p.bytes = p.totals_off + sizeof(int32_t) * (size_t)p.ncols;
   p.bytes = (p.bytes + 255) & ~(size_t)255;
   size_t items = (size_t)tt * d.k;
-  p.smem = sizeof(int) * (2 * items + (size_t)(kGateWarps + 2) * p.ncols);
+  p.smem = sizeof(int) * (2 * items + (size_t)(kGateWarps + 4) * p.ncols + kLookWords);
   return p;
 }
 
@@ -334,6 +335,9 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   int* s_hist = s_rank + items;               // [warps][ncols]
   int* s_excl = s_hist + kGateWarps * a.ncols;  // [ncols] tiles-before
   int* s_tot = s_excl + a.ncols;              // [ncols] aggregate, then inclusive
+  int* s_done = s_tot + a.ncols;              // [ncols] look-back finished
+  int* s_pin = s_done + a.ncols;              // [ncols] nearest inclusive tile
+  int* s_scr = s_pin + a.ncols;               // [kLookWords] status values
   __shared__ unsigned s_tile, s_epoch, s_bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -423,10 +427,13 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   __syncthreads();
 
   // ---------------- Phase B2: warp prefix, then a decoupled look-back per
-  // column.  Aggregates are published first (successors never wait on our
-  // look-back); then one warp per column scans 32 predecessor tiles at a time
-  // (status is column-major, so the 32 lanes read 256 contiguous bytes) and
-  // stops at the nearest tile that already carries an inclusive prefix.
+  // column, read by the whole CTA in parallel.  Aggregates are published
+  // first (successors never wait on our look-back).  Each round reads the
+  // status words of W predecessor tiles for every column at once (column-
+  // major, so consecutive threads read consecutive words), keeps, per
+  // column, everything after the nearest tile that already carries an
+  // inclusive prefix, and stops there; with W*ncols <= kLookWords one round
+  // covers all predecessors, so there is no sequential chain across tiles.
   const bool last_tile = tile == a.n_tiles - 1;
   for (int c = tid; c < a.ncols; c += kGateThreads) {
     int run = 0;
@@ -436,44 +443,59 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
       s_hist[w * a.ncols + c] = run;
       run += v;
     }
-    s_tot[c] = run;  // tile aggregate (overwritten by the inclusive total below)
+    s_tot[c] = run;  // tile aggregate (the inclusive total after the look-back)
+    s_excl[c] = 0;
+    s_done[c] = tile == 0;
+    s_pin[c] = -1;
     st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
                    (epoch << 34) | ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)run);
   }
   __syncthreads();
-  for (int c = warp; c < a.ncols; c += kGateWarps) {
-    const unsigned agg = (unsigned)s_tot[c];
-    unsigned excl = 0;
-    if (tile > 0) {
-      const unsigned long long* col = a.status + (size_t)c * a.n_tiles;
-      int hi = tile - 1;
-      while (true) {
-        const int p = hi - lane;  // lane 0 = nearest predecessor
-        unsigned flag = 2, val = 0;
-        if (p >= 0) {
+  if (tile > 0) {
+    const int W = max(1, min(tile, kLookWords / a.ncols));
+    int hi = tile - 1;
+    while (true) {
+      const int lo = max(0, hi - W + 1), Wn = hi - lo + 1, n = Wn * a.ncols;
+      for (int i = tid; i < n; i += kGateThreads) {
+        const int c = i / Wn, q = i - c * Wn, p = hi - q;
+        int v = 0;
+        if (!s_done[c]) {
+          const unsigned long long* wp = a.status + (size_t)c * a.n_tiles + p;
           unsigned long long w;
+          unsigned flag;
           do {
-            w = ld_relaxed_u64(col + p);
+            w = ld_relaxed_u64(wp);
             flag = (unsigned)(w >> 32) & 3u;
           } while ((w >> 34) != epoch || flag == 0);
-          val = (unsigned)w;
+          v = (int)(unsigned)w;
+          if (flag == 2) atomicMax(&s_pin[c], p);
         }
-        const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
-        const int first = incl ? __ffs(incl) - 1 : 31;
-        unsigned contrib = lane <= first ? val : 0u;
-#pragma unroll
-        for (int m = 16; m > 0; m >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, m);
-        excl += contrib;
-        if (incl) break;
-        hi -= 32;
+        s_scr[i] = v;
       }
-      if (lane == 0)
-        st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
-                       (epoch << 34) | (2ull << 32) | (excl + agg));
+      __syncthreads();
+      int pending = 0;
+      for (int c = warp; c < a.ncols; c += kGateWarps) {
+        if (s_done[c]) continue;
+        const int pin = s_pin[c];
+        const int qmax = pin >= 0 ? hi - pin : Wn - 1;  // keep p in [pin, hi]
+        int sum = 0;
+        for (int q = lane; q <= qmax; q += 32) sum += s_scr[c * Wn + q];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+        __syncwarp();
+        if (lane == 0) {
+          s_excl[c] += sum;
+          if (pin >= 0 || lo == 0) s_done[c] = 1; else pending = 1;
+          s_pin[c] = -1;
+        }
+      }
+      if (!__syncthreads_or(pending)) break;
+      hi = lo - 1;
     }
-    if (lane == 0) {
-      s_excl[c] = (int)excl;
-      s_tot[c] = (int)(excl + agg);
+    for (int c = tid; c < a.ncols; c += kGateThreads) {
+      const unsigned incl = (unsigned)(s_excl[c] + s_tot[c]);
+      st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile, (epoch << 34) | (2ull << 32) | incl);
+      s_tot[c] = (int)incl;
     }
   }
   __syncthreads();

@@ -15,7 +15,7 @@
 //    0, one RNE store; fully dropped tokens store zeros.
 #include <algorithm>
 
-#include "common.cuh"
+#include "comm.cuh"
 
 namespace moe {
 
@@ -32,7 +32,21 @@ struct RowArgs {
   int S, E, k, cap;
   int row_bytes;
   int d;
+  // layout destination: expert e lives on rank q = e / E_local and its rows
+  // go to dpeer.p[q] + ((rank*E_local + e mod E_local)*cap + s)*row.  Local
+  // moe_layout: dpeer.p[0] = dispatch, E_local = E, rank = 0.
+  PeerPtrs dpeer;
+  int E_local, rank;
+  int sys_fence;  // stores went to peers: fence.sys before the CTA exits
+  // reverse source: row (e, s) is read from speer.p[q] + ((rank*E_local +
+  // e mod E_local)*cap + s)*row (same mapping; local: speer.p[0] = back)
+  PeerPtrs speer;
 };
+
+__device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
+  const int q = e / a.E_local;
+  return a.speer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+}
 
 template <int VB>
 struct Vec;
@@ -113,7 +127,9 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
           const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
           if (s < 0) continue;
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
-          char* drow = a.dst + ((size_t)e * a.cap + s) * a.row_bytes;
+          const int q = e / a.E_local;
+          char* drow = a.dpeer.p[q] +
+                       ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -131,11 +147,14 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
       }
       const int e = lo;
       const int s = min(__ldg(a.load + e), a.cap) + (p - s_beg[e]);
-      char* drow = a.dst + ((size_t)e * a.cap + s) * a.row_bytes;
+      const int q = e / a.E_local;
+      char* drow = a.dpeer.p[q] +
+                   ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
       const typename V::T z = V::zero();
       for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
     }
   }
+  if (a.sys_fence) __threadfence_system();
 }
 
 // ------------------------------------------------------------ Reverse + combine
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         if (s0 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
           w0 = __ldg(a.weight + (size_t)t * a.k + j);
-          const char* b = a.src + ((size_t)e * a.cap + s0) * a.row_bytes;
+          const char* b = src_row(a, e, s0);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -205,7 +224,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         if (s1 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j + 1);
           w1 = __ldg(a.weight + (size_t)t * a.k + j + 1);
-          const char* b = a.src + ((size_t)e * a.cap + s1) * a.row_bytes;
+          const char* b = src_row(a, e, s1);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -251,7 +270,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
         if (s < 0) continue;
         const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
         const float w = __ldg(a.weight + (size_t)t * a.k + j);
-        const V4 v = ld_stream_v4(a.src + ((size_t)e * a.cap + s) * a.row_bytes + off);
+        const V4 v = ld_stream_v4(src_row(a, e, s) + off);
         if constexpr (DT == MOE_F32) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
@@ -332,11 +351,11 @@ static int row_grid(const void* kern) {
   return std::max(1, per_sm) * device_sm_count();
 }
 
-moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream) {
+moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
+                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
+                                 int rank, cudaStream_t stream) {
   RowArgs a{};
   a.src = static_cast<const char*>(x);
-  a.dst = static_cast<char*>(dispatch);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
   a.load = r.load;
@@ -346,6 +365,10 @@ moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, con
   a.cap = d.capacity;
   a.row_bytes = dtype_size * dcols;
   a.d = dcols;
+  a.dpeer = dst;
+  a.E_local = E_local;
+  a.rank = rank;
+  a.sys_fence = E_local != d.E;
   const void* kern;
   if (a.row_bytes % 32 == 0)
     kern = env_int("MOE_LAYOUT_U", 4) == 2 ? (const void*)k_layout<32, 2> : (const void*)k_layout<32, 4>;
@@ -359,10 +382,17 @@ moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, con
   return MOE_OK;
 }
 
-moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
-                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream) {
+moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
+                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream) {
+  PeerPtrs dst{};
+  dst.p[0] = static_cast<char*>(dispatch);
+  return layout_launch_peers(d, r, x, dtype_size, dcols, dst, d.E, 0, stream);
+}
+
+moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
+                                  const PeerPtrs& src, int E_local, int rank, int dtype,
+                                  int dtype_size, int dcols, void* y, cudaStream_t stream) {
   RowArgs a{};
-  a.src = static_cast<const char*>(back);
   a.dst = static_cast<char*>(y);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
@@ -373,6 +403,9 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
   a.cap = d.capacity;
   a.row_bytes = dtype_size * dcols;
   a.d = dcols;
+  a.speer = src;
+  a.E_local = E_local;
+  a.rank = rank;
   const void* kern;
   const int U = env_int("MOE_REVERSE_U", 1);
   if (a.row_bytes % 32 == 0) {
@@ -384,11 +417,18 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
     kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
   }
   void* args[] = {&a};
-  const int occ = env_int("MOE_REVERSE_CTAS_PER_SM", 0);
+  const int occ = env_int(E_local != d.E ? "MOE_COMBINE_CTAS_PER_SM" : "MOE_REVERSE_CTAS_PER_SM", 0);
   const int grid = occ > 0 ? occ * device_sm_count() : row_grid(kern);
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
   return MOE_OK;
+}
+
+moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
+                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream) {
+  PeerPtrs src{};
+  src.p[0] = const_cast<char*>(static_cast<const char*>(back));
+  return reverse_launch_peers(d, r, src, d.E, 0, dtype, dtype_size, dcols, y, stream);
 }
 
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,

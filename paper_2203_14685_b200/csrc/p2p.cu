@@ -1,0 +1,329 @@
+// p2p.cu -- the one-sided NVLink path: AllToAll steps
+// 3/5 of Algorithm 1 done with SM stores straight
+// into the owner rank's memory over NVLink 5 / NVSwitch, with the layout
+// transform of step 2 fused into the dispatch.
+//
+//  - symmetric buffers: cudaMalloc + CUDA IPC handles, exchanged over the
+//    library's own NCCL communicator (one ncclAllGather of 64-byte handles);
+//    every rank maps every peer's allocation;
+//  - device-side barrier: each rank bumps a local epoch, stores it (release,
+//    system scope) into every peer's flag slot for this rank, and spins
+//    (acquire, system scope) until all peers' flags reach it.  The epoch lives
+//    in device memory, so the barrier is CUDA-graph replay safe;
+//  - k_a2a_p2p: rank r copies its chunk q into rank q's receive buffer at
+//    chunk r; destinations are interleaved so all NVLink ports stay busy;
+//  - moe_dispatch_p2p: k_layout in peer mode stores every admitted row (and
+//    the zero padding rows) directly into recv[r][e mod E/P][slot] of the
+//    expert's owner.  Both end with the barrier, so when the call completes in
+//    stream order every rank's receive buffer is complete.
+#include <cstring>
+
+#include "comm.cuh"
+
+namespace moe {
+
+moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
+                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
+                                 int rank, cudaStream_t stream);
+moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
+                                  const PeerPtrs& src, int E_local, int rank, int dtype,
+                                  int dtype_size, int dcols, void* y, cudaStream_t stream);
+
+static moe_status_t nccl_st(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return MOE_OK;
+  set_error("%s: NCCL error %d (%s)", what, (int)r, ncclGetErrorString(r));
+  return MOE_ERR_NCCL;
+}
+
+// ------------------------------------------------------------ symmetric memory
+moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out) {
+  const int P = c->nranks, r = c->rank;
+  if (P > kMaxRanks) {
+    set_error("symmetric memory supports up to %d ranks (got %d)", kMaxRanks, P);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, bytes);
+  if (e != cudaSuccess) return cuda_status(e, "symmetric alloc: cudaMalloc");
+  e = cudaMemset(base, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, base);
+  char* d_h = nullptr;
+  cudaStream_t st = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&d_h, (size_t)P * sizeof h);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemcpy(d_h + (size_t)r * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    if (d_h) cudaFree(d_h);
+    if (st) cudaStreamDestroy(st);
+    return cuda_status(e, "symmetric alloc: IPC handle");
+  }
+  moe_status_t s = nccl_st(ncclAllGather(d_h + (size_t)r * sizeof h, d_h, sizeof h, ncclInt8,
+                                         c->nccl, st),
+                           "symmetric alloc: handle exchange");
+  std::vector<cudaIpcMemHandle_t> all(P);
+  if (s == MOE_OK) {
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpy(all.data(), d_h, (size_t)P * sizeof h, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) s = cuda_status(e, "symmetric alloc: handle exchange");
+  }
+  cudaFree(d_h);
+  cudaStreamDestroy(st);
+  if (s != MOE_OK) {
+    cudaFree(base);
+    return s;
+  }
+  SymmBuf b{};
+  b.base = base;
+  b.bytes = bytes;
+  for (int q = 0; q < P; ++q) {
+    if (q == r) {
+      b.peer.p[q] = base;
+      continue;
+    }
+    void* pp = nullptr;
+    e = cudaIpcOpenMemHandle(&pp, all[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int u = 0; u < q; ++u)
+        if (u != r) cudaIpcCloseMemHandle(b.peer.p[u]);
+      cudaFree(base);
+      return cuda_status(e, "symmetric alloc: cudaIpcOpenMemHandle (no peer access?)");
+    }
+    b.peer.p[q] = static_cast<char*>(pp);
+  }
+  *out = b;
+  return MOE_OK;
+}
+
+void symm_release(moe_comm* c, SymmBuf& b) {
+  for (int q = 0; q < c->nranks; ++q)
+    if (q != c->rank && b.peer.p[q]) cudaIpcCloseMemHandle(b.peer.p[q]);
+  if (b.base) cudaFree(b.base);
+  b.base = nullptr;
+}
+
+// A host-side rendezvous of all ranks (used around frees).
+static moe_status_t host_barrier(moe_comm* c) {
+  int* d = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_status(e, "barrier");
+  moe_status_t s = nccl_st(ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->nccl, st), "barrier");
+  if (s == MOE_OK) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) s = cuda_status(e, "barrier");
+  }
+  cudaFree(d);
+  cudaStreamDestroy(st);
+  return s;
+}
+
+// ------------------------------------------------------------ device barrier
+__global__ void k_barrier(PeerPtrs sig, int P, int rank) {
+  __shared__ unsigned long long s_e;
+  unsigned long long* mine = reinterpret_cast<unsigned long long*>(sig.p[rank]);
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    s_e = mine[kMaxRanks] + 1;
+    mine[kMaxRanks] = s_e;
+  }
+  __syncthreads();
+  const unsigned long long e = s_e;
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    unsigned long long* flag = reinterpret_cast<unsigned long long*>(sig.p[q]) + rank;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+  }
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + q) : "memory");
+    } while (v < e);
+  }
+}
+
+moe_status_t barrier_launch(const PeerPtrs& sig, int nranks, int rank, cudaStream_t stream) {
+  k_barrier<<<1, 32, 0, stream>>>(sig, nranks, rank);
+  MOE_CHECK_LAUNCH("moe_comm_barrier: launch");
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------ P2P AllToAll
+// Rank r: for every q, send[q] -> recv_q[r] (recv_q = rank q's buffer).
+// Work is cut into 64 KiB pieces, interleaved over destinations.
+__global__ void __launch_bounds__(256) k_a2a_p2p(const char* __restrict__ send, PeerPtrs recv,
+                                                 size_t off_rank, size_t b, int P, int rank) {
+  constexpr size_t kPiece = 64 * 1024;
+  constexpr int U = 4;
+  pdl_wait();
+  const size_t per = (b + kPiece - 1) / kPiece;
+  const size_t n = per * (size_t)P;
+  for (size_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const int q = (rank + 1 + (int)(j % P)) % P;
+    const size_t beg = (j / P) * kPiece;
+    const size_t len = (b - beg) < kPiece ? (b - beg) : kPiece;
+    const char* src = send + (size_t)q * b + beg;
+    char* dst = recv.p[q] + off_rank + beg;
+    for (size_t o = (size_t)threadIdx.x * 16; o < len; o += (size_t)blockDim.x * 16 * U) {
+      V4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t oo = o + (size_t)u * blockDim.x * 16;
+        if (oo < len) v[u] = ld_stream_v4(src + oo);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t oo = o + (size_t)u * blockDim.x * 16;
+        if (oo < len) st_v4(dst + oo, v[u]);
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_off_rank,
+                            size_t bytes_per_peer, int nranks, int rank, cudaStream_t stream) {
+  const size_t pieces = ((bytes_per_peer + 65535) / 65536) * nranks;
+  int grid = (int)std::min<size_t>(pieces, (size_t)device_sm_count() * 4);
+  if (grid < 1) grid = 1;
+  void* args[] = {(void*)&send, (void*)&recv, &recv_off_rank, &bytes_per_peer, &nranks, &rank};
+  cudaError_t e = launch_pdl((const void*)k_a2a_p2p, dim3(grid), dim3(256), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_alltoall(P2P): launch");
+  return MOE_OK;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+moe_status_t moe_comm_symm_alloc(moe_comm_t* comm, size_t bytes, void** out) {
+  if (!comm || !out || bytes == 0) {
+    set_error("moe_comm_symm_alloc: bad arguments");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!comm->p2p_ok) {
+    set_error("moe_comm_symm_alloc: peer memory is not available between these GPUs");
+    return MOE_ERR_UNSUPPORTED;
+  }
+  SymmBuf b;
+  moe_status_t s = symm_alloc(comm, bytes, &b);
+  if (s != MOE_OK) return s;
+  comm->symm.push_back(b);
+  *out = b.base;
+  return MOE_OK;
+}
+
+moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* p) {
+  if (!comm || !p) {
+    set_error("moe_comm_symm_free: bad arguments");
+    return MOE_ERR_INVALID_ARG;
+  }
+  for (size_t i = 0; i < comm->symm.size(); ++i) {
+    if (comm->symm[i].base == p) {
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) return cuda_status(e, "moe_comm_symm_free: sync");
+      moe_status_t s = host_barrier(comm);  // nobody still reads/writes it
+      if (s != MOE_OK) return s;
+      symm_release(comm, comm->symm[i]);
+      comm->symm.erase(comm->symm.begin() + i);
+      return host_barrier(comm);
+    }
+  }
+  set_error("moe_comm_symm_free: %p is not a symmetric buffer of this communicator", p);
+  return MOE_ERR_INVALID_ARG;
+}
+
+moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream) {
+  if (!comm) {
+    set_error("moe_comm_barrier: comm is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!comm->p2p_ok) {
+    set_error("moe_comm_barrier: peer memory is not available between these GPUs");
+    return MOE_ERR_UNSUPPORTED;
+  }
+  return barrier_launch(comm->sig.peer, comm->nranks, comm->rank,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Shared checks of the fused entry points; fills the peer pointers of `buf`.
+static moe_status_t p2p_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
+                             const moe_routing_t* routing, const void* a, const void* buf,
+                             int32_t d, int32_t dtype, PeerPtrs* peers, int* ds) {
+  if (!comm || !desc || !routing || !a || !buf || d < 1 || (dtype != MOE_F32 && dtype != MOE_BF16)) {
+    set_error("%s: bad arguments", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!comm->p2p_ok) {
+    set_error("%s: peer memory is not available between these GPUs", fn);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  const int P = comm->nranks;
+  if (desc->E % P != 0) {
+    set_error("%s: E=%d experts do not shard over %d ranks", fn, desc->E, P);
+    return MOE_ERR_INVALID_ARG;
+  }
+  *ds = dtype == MOE_F32 ? 4 : 2;
+  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
+      reinterpret_cast<uintptr_t>(buf) % 16) {
+    set_error("%s: rows and pointers must be 16-byte aligned", fn);
+    return MOE_ERR_ALIGNMENT;
+  }
+  const size_t bytes = (size_t)desc->E * desc->capacity * d * *ds;
+  const SymmBuf* b = find_symm(comm, buf, bytes);
+  if (!b) {
+    set_error("%s: the [E,cap,d] buffer (%zu bytes) is not inside a symmetric buffer "
+              "(moe_comm_symm_alloc)", fn, bytes);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const size_t off = static_cast<const char*>(buf) - b->base;
+  for (int q = 0; q < P; ++q) peers->p[q] = b->peer.p[q] + off;
+  return MOE_OK;
+}
+
+moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                             const moe_routing_t* routing, const void* expert_out, int32_t d,
+                             int32_t dtype, void* y, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = p2p_args("moe_combine_p2p", comm, desc, routing, y, expert_out, d, dtype, &src,
+                            &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight) {
+    set_error("moe_combine_p2p: routing.weight is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every expert is done
+  if (s != MOE_OK) return s;
+  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream);
+  if (s != MOE_OK) return s;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // nobody reads them any more
+}
+
+moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                              const moe_routing_t* routing, const void* x, int32_t d,
+                              int32_t dtype, void* recv, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs dst;
+  int ds = 0;
+  moe_status_t s0 = p2p_args("moe_dispatch_p2p", comm, desc, routing, x, recv, d, dtype, &dst, &ds);
+  if (s0 != MOE_OK) return s0;
+  if (!routing->load) {
+    set_error("moe_dispatch_p2p: routing.load is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  moe_status_t s = layout_launch_peers(*desc, *routing, x, ds, d, dst, desc->E / P, comm->rank,
+                                       stream);
+  if (s != MOE_OK) return s;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+}
+
+}  // extern "C"

@@ -33,11 +33,18 @@ class RoutePipeline:
         self.routing = Routing.empty(S, E, k, cap, self.device, self.gate.kind, self.gate.mode,
                                      self.gate.prio, slot_src)
         mk = lambda *shape: torch.empty(shape, dtype=dtype, device=self.device)
-        self.dispatch = mk(E, cap, d)
-        if self.P > 1:
+        if self.P > 1 and algo == "p2p":
+            # one-sided NVLink path: layout fused into the dispatch (rows are
+            # stored into the owner's symmetric recv), combine fused into the
+            # reverse (rows are read from the owner's recv); no staging buffers
+            self.recv = comm.symm_empty((E, cap, d), dtype)
+            self.dispatch = self.back = self.recv
+        elif self.P > 1:
+            self.dispatch = mk(E, cap, d)
             self.recv = mk(E, cap, d)
             self.back = mk(E, cap, d)
         else:
+            self.dispatch = mk(E, cap, d)
             self.recv = self.back = self.dispatch
         self.y = mk(S, d)
         self.ws = None
@@ -57,13 +64,23 @@ class RoutePipeline:
         mark = mark or (lambda name: None)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         mark("gate")
-        layout(x, r, out=self.dispatch)                                    # step 2
-        mark("layout")
-        self.alltoall(self.dispatch, self.recv)                            # step 3
-        mark("a2a_dispatch")
+        if self.P > 1 and self.algo == "p2p":                              # steps 2+3 fused
+            self.comm.dispatch_p2p(x, r, self.recv)
+            mark("layout")
+            mark("a2a_dispatch")
+        else:
+            layout(x, r, out=self.dispatch)                                # step 2
+            mark("layout")
+            self.alltoall(self.dispatch, self.recv)                        # step 3
+            mark("a2a_dispatch")
         if expert:                                                         # step 4 (stand-in)
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
             mark("expert")
+        if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
+            self.comm.combine_p2p(self.recv, r, self.y)
+            mark("a2a_combine")
+            mark("reverse")
+            return self.y
         self.alltoall(self.recv, self.back)                                # step 5
         mark("a2a_combine")
         reverse_layout(self.back, r, out=self.y)                           # step 6
@@ -97,16 +114,23 @@ class RoutePipeline:
                 graphs = g
             else:
                 r = self.routing
+                p2p = self.P > 1 and self.algo == "p2p"
                 fns = {
                     "gate": lambda: self.gate(logits, token_ids, table, out=r),
-                    "layout": lambda: layout(x, r, out=self.dispatch),
+                    "layout": (lambda: self.comm.dispatch_p2p(x, r, self.recv)) if p2p else
+                              (lambda: layout(x, r, out=self.dispatch)),
                     "a2a_dispatch": lambda: self.alltoall(self.dispatch, self.recv),
-                    "a2a_combine": lambda: self.alltoall(self.recv, self.back),
+                    "a2a_combine": (lambda: self.comm.combine_p2p(self.recv, r, self.y)) if p2p else
+                                   (lambda: self.alltoall(self.recv, self.back)),
                     "reverse": lambda: reverse_layout(self.back, r, out=self.y),
                 }
                 for name in self.STAGES:
-                    if self.P == 1 and name.startswith("a2a"):
-                        continue   # nothing to launch at P=1 (recv/back alias dispatch)
+                    if (self.P == 1 or p2p) and name == "a2a_dispatch":
+                        continue   # P=1: recv aliases dispatch; p2p: fused into "layout"
+                    if self.P == 1 and name == "a2a_combine":
+                        continue
+                    if p2p and name == "reverse":
+                        continue   # fused into "a2a_combine"
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(g, stream=s):
                         fns[name]()

@@ -57,12 +57,13 @@ def _run(world, algo, G, port):
     return out
 
 
-@pytest.mark.parametrize("world,algo,G", [(2, "flat", 1), (2, "hier", 2), (4, "flat", 1),
-                                          (4, "hier", 2), (4, "hier", 4)])
+@pytest.mark.parametrize("world,algo,G", [(2, "flat", 1), (2, "hier", 2), (2, "p2p", 1),
+                                          (4, "flat", 1), (4, "hier", 2), (4, "hier", 4),
+                                          (4, "p2p", 1)])
 def test_multi_gpu_route(orc, world, algo, G):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
-    out = _run(world, algo, G, 29600 + world * 10 + G + (3 if algo == "hier" else 0))
+    out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo])
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--min-mib", type=int, default=1)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default="")
+    ap.add_argument("--p2p", action="store_true", help="also time the one-sided NVLink AllToAll")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -54,21 +55,23 @@ def main():
         chunk_words = B // 4 // P
         send = torch.cat([pattern(r, q, chunk_words, dev) for q in range(P)])
         recv = torch.empty_like(send)
+        recv_sym = comm.symm_empty(send.shape, send.dtype) if a.p2p else None
         ws = torch.empty(comm.workspace_bytes("hier", G, B // P) if r % G == 0 else 0,
                          dtype=torch.uint8, device=dev)
         res = {"B_mib": mib, "P": P, "G": G, "per_peer_bytes": B // P}
-        for algo in ("flat", "hier"):
-            recv.fill_(-1)
-            comm.alltoall(send, recv, algo, G, ws)      # eager warm-up + check
+        for algo in ("flat", "hier") + (("p2p",) if a.p2p else ()):
+            rv = recv_sym if algo == "p2p" else recv
+            rv.fill_(-1)
+            comm.alltoall(send, rv, algo, G, ws)        # eager warm-up + check
             torch.cuda.synchronize()
             want = torch.cat([pattern(q, r, chunk_words, dev) for q in range(P)])
-            ok = torch.tensor([1 if torch.equal(recv, want) else 0], device=dev)
+            ok = torch.tensor([1 if torch.equal(rv, want) else 0], device=dev)
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
-                    comm.alltoall(send, recv, algo, G, ws)
+                    comm.alltoall(send, rv, algo, G, ws)
             torch.cuda.current_stream().wait_stream(s)
             ts = []
             for _ in range(a.reps):
@@ -79,10 +82,11 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            recv.fill_(-1)
+            rv.fill_(-1)
+            dist.barrier()
             g.replay()
             torch.cuda.synchronize()
-            ok &= torch.tensor([1 if torch.equal(recv, want) else 0], device=dev)
+            ok &= torch.tensor([1 if torch.equal(rv, want) else 0], device=dev)
             t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
@@ -91,10 +95,15 @@ def main():
                          "correct": bool(ok.item())}
             del g
         res["t_flat_over_t_hier"] = res["flat"]["ms"] / res["hier"]["ms"]
+        if a.p2p:
+            res["t_flat_over_t_p2p"] = res["flat"]["ms"] / res["p2p"]["ms"]
+            dist.barrier()
+            torch.cuda.synchronize()
+            comm.symm_free(recv_sym)
         rows.append(res)
         if r == 0:
             print(json.dumps(res), flush=True)
-        del send, recv, ws
+        del send, recv, ws, recv_sym
         torch.cuda.empty_cache()
         mib *= 2
     if r == 0 and a.out:
