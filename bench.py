@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
-    ap.add_argument("--algo", default="flat", choices=["flat", "hier"])
+    ap.add_argument("--algo", default="p2p", choices=["p2p", "flat", "hier"],
+                    help="AllToAll at N>1: p2p = fused one-sided NVLink path (falls back to "
+                         "flat if the GPUs cannot map each other's memory); flat/hier = NCCL")
     ap.add_argument("--group-size", type=int, default=0, help="hier group size (default N/2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -239,8 +241,17 @@ def main():
     cap = moe.capacity(S, w.E, w.k, w.C)
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
     row = w.d * (2 if w.dtype == "bf16" else 4)
-    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm,
-                             algo=a.algo if P > 1 else "flat", group_size=G, device=dev)
+    algo = a.algo if P > 1 else "flat"
+    try:
+        pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
+                                 group_size=G, device=dev)
+    except moe.MoeError as err:
+        if algo != "p2p":
+            raise
+        log("p2p unavailable (%s): NCCL flat AllToAll instead" % err)
+        algo = "flat"
+        pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
+                                 group_size=G, device=dev)
 
     lg, ids, table, x = synthgen.workload_inputs(w, rank)
 
@@ -404,33 +415,52 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(S * row),
                "ms_per_step": float(t_e2e[0])}
 
-    # ---- roofline of the dominant kernel (layout or reverse; HBM-bound)
+    # ---- roofline of the dominant kernel
     admitted = int((pipe.routing.slot_idx >= 0).sum().item())
     ab = algorithmic_bytes(w, S, cap, P, row)
     ab["reverse"] = admitted * row + S * row + 12 * S * w.k
-    dom = "layout" if stage_ms["layout"] >= stage_ms["reverse"] else "reverse"
     peak, peak_src = measured_peaks()
-    achieved = ab[dom] / (stage_ms[dom] / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("%s/%s" % (w.name, dom))
+            tr = json.load(f)
     except Exception:
-        pass
-    roof = {"bound": "hbm", "kernel": "k_" + dom, "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "algorithmic_bytes": ab[dom], "peak_source": peak_src,
-            "per_kernel_gbs": {
-                "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
-                "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
-                "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9}}
+        tr = {}
+    fused = P > 1 and algo == "p2p"
+    if not fused:
+        # N=1 (or NCCL AllToAll): layout / reverse are HBM-bound row movers
+        dom = "layout" if stage_ms["layout"] >= stage_ms["reverse"] else "reverse"
+        achieved = ab[dom] / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_" + dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": tr.get("%s/%s" % (w.name, dom)),
+                "algorithmic_bytes": ab[dom], "peak_source": peak_src}
+    else:
+        # fused one-sided path: the dispatch (k_layout in peer mode) and the
+        # combine (k_reverse in peer mode) are bound by the bytes that must
+        # cross NVLink, (P-1)/P of the [E,cap,d] buffer each way
+        dom = "layout" if stage_ms["layout"] >= stage_ms["a2a_combine"] else "a2a_combine"
+        t = stage_ms[dom] / 1e3
+        achieved = ab["a2a"] / t / 1e9
+        roof = {"bound": "nvlink", "kernel": "k_layout (peer dispatch)" if dom == "layout"
+                else "k_reverse (peer combine)", "achieved": achieved, "peak": NVLINK_GBS,
+                "unit": "GB/s", "frac": achieved / NVLINK_GBS, "traffic": None,
+                "algorithmic_bytes": ab["a2a"],
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md), 900 nominal"}
+    roof["per_kernel_gbs"] = {
+        "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+        "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
+        "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9 if stage_ms["reverse"] > 1e-3
+        else None}
     a2a = None
     if P > 1:
-        a2a = {"bytes_out_per_rank": ab["a2a"],
-               "busbw_gbs": {s: ab["a2a"] / (stage_ms[s] / 1e3) / 1e9
-                             for s in ("a2a_dispatch", "a2a_combine")},
-               "peak_gbs": NVLINK_GBS, "algo": a.algo, "group_size": G if a.algo == "hier" else None}
-        a2a["frac"] = min(a2a["busbw_gbs"].values()) / NVLINK_GBS
+        if fused:
+            bw = {"dispatch (fused with layout)": ab["a2a"] / (stage_ms["layout"] / 1e3) / 1e9,
+                  "combine (fused with reverse)": ab["a2a"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
+        else:
+            bw = {s_: ab["a2a"] / (stage_ms[s_] / 1e3) / 1e9 for s_ in ("a2a_dispatch", "a2a_combine")}
+        a2a = {"bytes_out_per_rank": ab["a2a"], "busbw_gbs": bw, "peak_gbs": NVLINK_GBS,
+               "algo": algo, "group_size": G if algo == "hier" else None}
+        a2a["frac"] = min(bw.values()) / NVLINK_GBS
 
     # ---- CPU baseline: the oracle, rank 0, N=1 only, bounded sample
     cpu = None
@@ -459,7 +489,8 @@ def main():
 
     # our kernels per step: gate (+ finalize for SLOT priority), layout, reverse,
     # and on hierarchical leaders one chunk permute per AllToAll
-    launches_per_step = 3 + (2 if (P > 1 and a.algo == "hier" and rank % G == 0) else 0)
+    launches_per_step = 3 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
+        (2 if (P > 1 and algo == "p2p") else 0)   # p2p: two k_barrier launches
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
@@ -468,7 +499,7 @@ def main():
             "data": "synthetic (synthgen: seeded N(0,1) logits/tokens, no near ties)",
             "config": {"workload": w.name, "desc": w.note, "S_per_rank": S, "d": w.d, "E": w.E,
                        "k": w.k, "gate": w.kind, "capacity_factor": w.C, "capacity": cap,
-                       "a2a": a.algo if P > 1 else None,
+                       "a2a": algo if P > 1 else None,
                        "parallelism": "ep%d (experts sharded, tokens data-parallel)" % P,
                        "l2": "flushed between timed steps (2x L2 memset, outside events)",
                        "expert": "identity in the timed step; s_e stand-in timed separately"},

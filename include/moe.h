@@ -77,7 +77,7 @@ typedef enum { MOE_PRIO_TOKEN = 0, MOE_PRIO_SLOT = 1 } moe_priority_t;
  *                 `group_size` consecutive ranks on one box (Fig. 6, R13)
  *   P2P         : one-sided: SM stores straight into the peers' receive
  *                 buffers over NVLink (recv must be a symmetric buffer,
- *                 moe_comm_symm_alloc), then a device-side barrier */
+ *                 moe_comm_symm_alloc), between two device-side barriers */
 typedef enum { MOE_A2A_FLAT = 0, MOE_A2A_HIER_LEADER = 1, MOE_A2A_P2P = 2 } moe_a2a_algo_t;
 
 /* Gate problem description.  Enums are carried as int32 for a fixed ABI. */
@@ -125,7 +125,8 @@ size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc);
  * selection (TOPK: Eq. 1 TopK on raw fp32 logits, R2; KTOP1: per-prototype
  * argmax; HASH: table lookup), weights (Eq. 1 softmax, R1) and capacity
  * slots (per-expert prefix sum in admission order, slot >= cap -> dropped).
- *   logits    [S,E] fp32 row-major (TOPK, KTOP1; ignored for HASH)
+ *   logits    [S,E] fp32 row-major, 16-byte aligned (TOPK, KTOP1; ignored
+ *             for HASH)
  *   token_ids [S] int32, table [vocab] int32 (HASH only; else may be NULL)
  *   out       routing arrays (see moe_routing_t); all written
  *   ws        workspace of >= moe_gate_workspace_bytes(desc) bytes
@@ -241,18 +242,26 @@ moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* local);
  * buffers) are visible to every rank after it. */
 moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream);
 
+/* Barrier flags of moe_dispatch_p2p / moe_combine_p2p (default 0: both).
+ * The entry barrier guarantees no rank writes into (dispatch) or reads from
+ * (combine) a peer's buffer before that peer's stream reached the call; the
+ * exit barrier that every store landed (dispatch) / every read finished
+ * (combine).  A caller that orders its steps itself may skip redundant ones,
+ * e.g. dispatch(NO_ENTRY) after a combine with its exit barrier. */
+enum { MOE_P2P_NO_ENTRY_BARRIER = 1, MOE_P2P_NO_EXIT_BARRIER = 2 };
+
 /* Steps 2+3 fused: for every admitted item (t,j) with
  * expert e and slot s, the row x[t] is stored into rank q = e/(E/P)'s
  * `recv` at [r][e mod E/P][s] (r = this rank); padding rows
- * [min(load[e],cap), cap) are zeroed there; then moe_comm_barrier.  The
- * resulting recv buffers are byte-identical to moe_layout followed by
- * moe_alltoall(FLAT).  recv: symmetric, [P][E/P][cap][d] of dtype. */
+ * [min(load[e],cap), cap) are zeroed there; bracketed by moe_comm_barrier
+ * (see flags).  The resulting recv buffers are byte-identical to moe_layout
+ * followed by moe_alltoall(FLAT).  recv: symmetric, [P][E/P][cap][d]. */
 moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                               const moe_routing_t* routing, const void* x, int32_t d,
-                              int32_t dtype, void* recv, moe_stream_t stream);
+                              int32_t dtype, void* recv, int32_t flags, moe_stream_t stream);
 
 /* Steps 5+6 fused: moe_comm_barrier (every rank's experts
- * are done), then y[t] = sum_j w[t,j] * expert_out_q[r][e mod E/P][s] with
+ * are done; see flags), then y[t] = sum_j w[t,j] * expert_out_q[r][e mod E/P][s] with
  * every admitted row read straight from its owner rank q's `expert_out` over
  * NVLink (fp32 accumulate in ascending j, one RNE store, 0 if all slots
  * dropped), then moe_comm_barrier (the buffers may be reused).  Same result
@@ -260,7 +269,7 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
  * [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
-                             int32_t dtype, void* y, moe_stream_t stream);
+                             int32_t dtype, void* y, int32_t flags, moe_stream_t stream);
 
 /* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
  * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,

@@ -56,9 +56,9 @@ SIGNATURES = [
     ("moe_comm_symm_free", ctypes.c_int, [vp, vp]),
     ("moe_comm_barrier", ctypes.c_int, [vp, vp]),
     ("moe_dispatch_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
-                                        i32, i32, vp, vp]),
+                                        i32, i32, vp, i32, vp]),
     ("moe_combine_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
-                                       i32, i32, vp, vp]),
+                                       i32, i32, vp, i32, vp]),
     ("moe_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("moe_last_error", ctypes.c_char_p, []),
     ("moe_version", ctypes.c_char_p, []),

@@ -263,19 +263,22 @@ class Comm:
         """Device-side barrier of all ranks on the current stream."""
         check(lib().moe_comm_barrier(self._h, _stream()), "moe_comm_barrier")
 
-    def dispatch_p2p(self, x: torch.Tensor, r: "Routing", recv: torch.Tensor) -> torch.Tensor:
+    NO_ENTRY_BARRIER, NO_EXIT_BARRIER = 1, 2
+
+    def dispatch_p2p(self, x: torch.Tensor, r: "Routing", recv: torch.Tensor,
+                     flags: int = 0) -> torch.Tensor:
         """Layout_Transform fused with the dispatch AllToAll over NVLink:
         rows land directly in the owner rank's symmetric `recv`."""
         _need_cuda(x, "x")
         d = x.shape[-1]
         desc, rc = r.desc(), r.c()
         check(lib().moe_dispatch_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(x), d,
-                                     _DT[x.dtype], _p(recv), _stream(x.device)),
+                                     _DT[x.dtype], _p(recv), flags, _stream(x.device)),
               "moe_dispatch_p2p")
         return recv
 
     def combine_p2p(self, expert_out: torch.Tensor, r: "Routing",
-                    y: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    y: Optional[torch.Tensor] = None, flags: int = 0) -> torch.Tensor:
         """AllToAll combine fused with Reverse_Layout_Transform over NVLink:
         every admitted row is read from its owner's symmetric `expert_out`."""
         d = expert_out.shape[-1]
@@ -283,7 +286,7 @@ class Comm:
             y = torch.empty((r.S, d), dtype=expert_out.dtype, device=expert_out.device)
         desc, rc = r.desc(), r.c()
         check(lib().moe_combine_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(expert_out),
-                                    d, _DT[expert_out.dtype], _p(y), _stream(y.device)),
+                                    d, _DT[expert_out.dtype], _p(y), flags, _stream(y.device)),
               "moe_combine_p2p")
         return y
 

@@ -97,9 +97,9 @@ static moe_status_t check_desc(const char* fn, const moe_gate_desc_t* d) {
     set_error("%s: E=%d > 256 is not supported", fn, d->E);
     return MOE_ERR_UNSUPPORTED;
   }
-  if ((long long)d->S * d->k >= (1ll << 31) || (long long)d->E * d->capacity >= (1ll << 31)) {
-    set_error("%s: S*k and E*capacity must be < 2^31 (S=%d k=%d E=%d capacity=%d)", fn, d->S, d->k,
-              d->E, d->capacity);
+  if ((long long)d->S * d->k >= (1ll << 30) || (long long)d->E * d->capacity >= (1ll << 31)) {
+    set_error("%s: need S*k < 2^30 and E*capacity < 2^31 (S=%d k=%d E=%d capacity=%d)", fn, d->S,
+              d->k, d->E, d->capacity);
     return MOE_ERR_UNSUPPORTED;
   }
   return MOE_OK;
@@ -174,8 +174,8 @@ moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const in
   } else if (!logits) {
     set_error("moe_gate: logits is NULL");
     return MOE_ERR_INVALID_ARG;
-  } else if (!aligned(logits, 4)) {
-    set_error("moe_gate: logits must be 4-byte aligned");
+  } else if (!aligned(logits, 16)) {
+    set_error("moe_gate: logits must be 16-byte aligned (TMA bulk copy source)");
     return MOE_ERR_ALIGNMENT;
   }
   const size_t need = gate_workspace_bytes(*desc);

@@ -255,6 +255,10 @@ moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, co
     PeerPtrs dst;
     const size_t off = static_cast<const char*>(recv) - sb->base;
     for (int q = 0; q < P; ++q) dst.p[q] = sb->peer.p[q] + off;
+    // entry barrier: no rank writes into a receive buffer before its owner's
+    // stream has reached this call (the receive semantics of the NCCL path)
+    moe_status_t s0 = barrier_launch(comm->sig.peer, P, r, stream);
+    if (s0 != MOE_OK) return s0;
     moe_status_t s = a2a_p2p_launch(static_cast<const char*>(send), dst, (size_t)r * bytes_per_peer,
                                     bytes_per_peer, P, r, stream);
     if (s != MOE_OK) return s;

@@ -32,6 +32,8 @@ constexpr int kGateWarps = kGateThreads / 32;
 constexpr int kMaxTileItems = 2048;  // tile_tokens * k
 constexpr int kMaxCols = 2048;       // look-back columns: E or k*E
 constexpr int kLookWords = 8192;     // status words one look-back round reads
+constexpr size_t kMaxTileLogitBytes = 64 * 1024;
+constexpr unsigned kValMask = (1u << 30) - 1;  // counts < 2^30 (S*k < 2^30, checked)
 
 struct GateCtrl {  // 64 bytes at the head of the workspace
   unsigned ticket, done, epoch, bad;
@@ -45,6 +47,7 @@ struct GateArgs {
   int vocab;
   int S, E, k, cap, mode, prio;
   int tile_tokens, n_tiles, ncols;
+  int lg_words;  // shared-memory words of the staged logits tile (16-byte multiple)
   int32_t* expert_idx;
   int32_t* slot_idx;
   float* weight;
@@ -57,7 +60,7 @@ struct GateArgs {
 
 // ------------------------------------------------------------ layout of ws
 struct GatePlan {
-  int L, K, tile_tokens, n_tiles, ncols;
+  int L, K, tile_tokens, n_tiles, ncols, lg_words;
   size_t status_off, totals_off, bytes, smem;
 };
 
@@ -76,6 +79,9 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   int tt = 256;
   while (tt > 32 && (d.S + tt - 1) / tt < 256) tt >>= 1;
   while (tt > 1 && tt * d.k > kMaxTileItems) tt >>= 1;
+  // the staged logits tile stays within kMaxTileLogitBytes of shared memory
+  if (d.kind != MOE_GATE_HASH)
+    while (tt > 1 && (size_t)tt * d.E * 4 > kMaxTileLogitBytes) tt >>= 1;
   p.tile_tokens = tt;
   p.n_tiles = (d.S + tt - 1) / tt;
   p.ncols = d.priority == MOE_PRIO_SLOT ? d.k * d.E : d.E;
@@ -84,7 +90,8 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   p.bytes = p.totals_off + sizeof(int32_t) * (size_t)p.ncols;
   p.bytes = (p.bytes + 255) & ~(size_t)255;
   size_t items = (size_t)tt * d.k;
-  p.smem = sizeof(int) * (2 * items + (size_t)(kGateWarps + 4) * p.ncols + kLookWords);
+  p.lg_words = d.kind == MOE_GATE_HASH ? 0 : ((tt * d.E + 3) & ~3);
+  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)(kGateWarps + 4) * p.ncols + kLookWords);
   return p;
 }
 
@@ -122,7 +129,8 @@ struct TopList {
   }
 };
 
-// Visit the E/L logits of lane `l` of token t: f(value, expert).
+// Visit the E/L logits of lane `l` of one token row (in shared memory):
+// f(value, expert).
 template <typename F>
 __device__ __forceinline__ void for_lane_logits(const float* row, int l, int epl, bool vec4,
                                                 F&& f) {
@@ -130,14 +138,14 @@ __device__ __forceinline__ void for_lane_logits(const float* row, int l, int epl
   if (vec4) {
     const float4* r4 = reinterpret_cast<const float4*>(row + base);
     for (int q = 0; q < epl / 4; ++q) {
-      float4 x = __ldg(r4 + q);
+      float4 x = r4[q];
       f(x.x, base + 4 * q);
       f(x.y, base + 4 * q + 1);
       f(x.z, base + 4 * q + 2);
       f(x.w, base + 4 * q + 3);
     }
   } else {
-    for (int q = 0; q < epl; ++q) f(__ldg(row + base + q), base + q);
+    for (int q = 0; q < epl; ++q) f(row[base + q], base + q);
   }
 }
 
@@ -156,11 +164,11 @@ __device__ __forceinline__ float group_max(float x) {
 
 // Top-k (Eq. 1), register path, K >= k.
 template <int L, int K>
-__device__ __forceinline__ void select_topk_reg(const GateArgs& a, int t, bool valid, int l,
-                                                int epl, bool vec4, int* s_sel /*[k]*/) {
+__device__ __forceinline__ void select_topk_reg(const GateArgs& a, const float* row, int t,
+                                                bool valid, int l, int epl, bool vec4,
+                                                int* s_sel /*[k]*/) {
   TopList<K> top;
   top.init();
-  const float* row = a.logits + (size_t)t * a.E;
   if (valid) for_lane_logits(row, l, epl, vec4, [&](float x, int e) { top.insert(x, e); });
 #pragma unroll
   for (int m = 1; m < L; m <<= 1) {
@@ -205,8 +213,9 @@ __device__ __forceinline__ void select_topk_reg(const GateArgs& a, int t, bool v
 
 // k-top-1 (R11), register path, K >= k prototypes.
 template <int L, int K>
-__device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, int t, bool valid, int l,
-                                                 int epl, bool vec4, int* s_sel) {
+__device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, const float* row, int t,
+                                                 bool valid, int l, int epl, bool vec4,
+                                                 int* s_sel) {
   const int n = a.E / a.k;
   float bv[K];
   int bi[K];
@@ -215,7 +224,6 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, int t, bool 
     bv[p] = -INFINITY;
     bi[p] = INT_MAX;
   }
-  const float* row = a.logits + (size_t)t * a.E;
   if (valid)
     for_lane_logits(row, l, epl, vec4, [&](float x, int e) {
       const int pe = e / n;
@@ -272,32 +280,31 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, int t, bool 
 // of elements of its segment that beat it, if that is < k (top-k: segment =
 // row; k-top-1: segment = its prototype slice, selected iff rank == 0).
 template <int L, bool KTOP1>
-__device__ __forceinline__ void select_rank(const GateArgs& a, int t, bool valid, int l, int epl,
-                                            int* s_sel) {
-  const float* row = a.logits + (size_t)t * a.E;
+__device__ __forceinline__ void select_rank(const GateArgs& a, const float* row, int t, bool valid,
+                                            int l, int epl, int* s_sel) {
   const int n = KTOP1 ? a.E / a.k : a.E;
   float lmax = -INFINITY;
   if (valid)
-    for (int q = 0; q < epl; ++q) lmax = fmaxf(lmax, __ldg(row + l * epl + q));
+    for (int q = 0; q < epl; ++q) lmax = fmaxf(lmax, row[l * epl + q]);
   const double mx = (double)group_max<L>(lmax);
   double part = 0.0;
   for (int q = 0; q < epl; ++q) {
     const int e = l * epl + q;
     if (!valid) break;
-    const float x = __ldg(row + e);
+    const float x = row[e];
     const int seg = KTOP1 ? (e / n) * n : 0;
     int rank = 0;
-    for (int u = seg; u < seg + n; ++u) rank += beats(__ldg(row + u), u, x, e) ? 1 : 0;
+    for (int u = seg; u < seg + n; ++u) rank += beats(row[u], u, x, e) ? 1 : 0;
     if (!KTOP1 && (a.mode == MOE_W_SOFTMAX || rank < a.k)) part += exp((double)x - mx);
   }
   const double den_topk = KTOP1 ? 1.0 : group_sum<L>(part);
   for (int q = 0; q < epl; ++q) {
     const int e = l * epl + q;
     if (!valid) break;
-    const float x = __ldg(row + e);
+    const float x = row[e];
     const int seg = KTOP1 ? (e / n) * n : 0;
     int rank = 0;
-    for (int u = seg; u < seg + n; ++u) rank += beats(__ldg(row + u), u, x, e) ? 1 : 0;
+    for (int u = seg; u < seg + n; ++u) rank += beats(row[u], u, x, e) ? 1 : 0;
     int j = -1;
     float w = 0.f;
     if (KTOP1) {
@@ -305,7 +312,7 @@ __device__ __forceinline__ void select_rank(const GateArgs& a, int t, bool valid
         j = e / n;
         if (a.mode == MOE_W_SOFTMAX) {
           double den = 0.0;
-          for (int u = seg; u < seg + n; ++u) den += exp((double)__ldg(row + u) - (double)x);
+          for (int u = seg; u < seg + n; ++u) den += exp((double)row[u] - (double)x);
           w = (float)(1.0 / den);
         } else {
           w = 1.0f;
@@ -328,9 +335,10 @@ enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2 };
 
 template <int KIND, int L, int K>
 __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
-  extern __shared__ int smem[];
+  extern __shared__ __align__(16) int smem[];
   const int items = a.tile_tokens * a.k;
-  int* s_exp = smem;                          // [items] expert of item tt*k+j
+  float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
+  int* s_exp = smem + a.lg_words;             // [items] expert of item tt*k+j
   int* s_rank = s_exp + items;                // [items] rank inside its warp
   int* s_hist = s_rank + items;               // [warps][ncols]
   int* s_excl = s_hist + kGateWarps * a.ncols;  // [ncols] tiles-before
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   int* s_pin = s_done + a.ncols;              // [ncols] nearest inclusive tile
   int* s_scr = s_pin + a.ncols;               // [kLookWords] status values
   __shared__ unsigned s_tile, s_epoch, s_bad;
+  __shared__ __align__(8) unsigned long long s_mbar;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();     // the producer of the logits / the previous step must be done
@@ -355,6 +364,37 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   const unsigned long long epoch = s_epoch;
   const int t0 = tile * a.tile_tokens;
   const int nt = min(a.tile_tokens, a.S - t0);
+  if constexpr (KIND != KIND_HASH) {
+    // Stage the tile's logits (nt*E contiguous floats) into shared memory
+    // with one TMA bulk copy (one DRAM latency for the whole tile); the
+    // sub-16-byte tail, if any, with plain loads.
+    const unsigned bytes = (unsigned)nt * a.E * 4u, bulk = bytes & ~15u;
+    const float* g = a.logits + (size_t)t0 * a.E;
+    const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bulk)
+                   : "memory");
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(s_lg);
+      for (unsigned o = 0; o < bulk; o += 65536u) {
+        const unsigned n = min(65536u, bulk - o);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst + o), "l"(reinterpret_cast<const char*>(g) + o), "r"(n), "r"(mbar)
+            : "memory");
+      }
+    }
+    for (unsigned i = bulk / 4 + tid; i < bytes / 4; i += kGateThreads) s_lg[i] = __ldg(g + i);
+    __syncthreads();  // mbarrier initialised before anyone waits on it
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(mbar)
+          : "memory");
+  }
 
   // ---------------- Phase A: selection + weights
   if constexpr (KIND == KIND_HASH) {
@@ -382,12 +422,13 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
       const bool valid = tt < nt;
       const int t = valid ? t0 + tt : 0;
       int* s_sel = s_exp + (size_t)tt * a.k;
+      const float* row = s_lg + (size_t)(valid ? tt : 0) * a.E;
       if constexpr (K == 0) {
-        select_rank<L, KIND == KIND_KTOP1>(a, t, valid, l, epl, s_sel);
+        select_rank<L, KIND == KIND_KTOP1>(a, row, t, valid, l, epl, s_sel);
       } else if constexpr (KIND == KIND_TOPK) {
-        select_topk_reg<L, K>(a, t, valid, l, epl, vec4, s_sel);
+        select_topk_reg<L, K>(a, row, t, valid, l, epl, vec4, s_sel);
       } else {
-        select_ktop1_reg<L, K>(a, t, valid, l, epl, vec4, s_sel);
+        select_ktop1_reg<L, K>(a, row, t, valid, l, epl, vec4, s_sel);
       }
     }
   }
@@ -456,21 +497,33 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
     int hi = tile - 1;
     while (true) {
       const int lo = max(0, hi - W + 1), Wn = hi - lo + 1, n = Wn * a.ncols;
+      // pass 1: issue every load of the round without waiting (one L2 round
+      // trip); entries are packed as flag << 30 | value, flag 0 = not ready
+#pragma unroll 4
       for (int i = tid; i < n; i += kGateThreads) {
-        const int c = i / Wn, q = i - c * Wn, p = hi - q;
-        int v = 0;
+        const int c = i / Wn, p = hi - (i - c * Wn);
+        unsigned code = 1u << 30;  // finished column: counts as 0
         if (!s_done[c]) {
+          const unsigned long long w = ld_relaxed_u64(a.status + (size_t)c * a.n_tiles + p);
+          code = (w >> 34) == epoch ? (((unsigned)(w >> 32) & 3u) << 30) | ((unsigned)w & kValMask)
+                                    : 0u;
+        }
+        s_scr[i] = (int)code;
+      }
+      // pass 2: poll only what was not published yet; note inclusive tiles
+      for (int i = tid; i < n; i += kGateThreads) {
+        const int c = i / Wn, p = hi - (i - c * Wn);
+        unsigned code = (unsigned)s_scr[i];
+        if ((code >> 30) == 0) {
           const unsigned long long* wp = a.status + (size_t)c * a.n_tiles + p;
           unsigned long long w;
-          unsigned flag;
           do {
             w = ld_relaxed_u64(wp);
-            flag = (unsigned)(w >> 32) & 3u;
-          } while ((w >> 34) != epoch || flag == 0);
-          v = (int)(unsigned)w;
-          if (flag == 2) atomicMax(&s_pin[c], p);
+          } while ((w >> 34) != epoch || ((w >> 32) & 3u) == 0);
+          code = (((unsigned)(w >> 32) & 3u) << 30) | ((unsigned)w & kValMask);
+          s_scr[i] = (int)code;
         }
-        s_scr[i] = v;
+        if ((code >> 30) == 2 && !s_done[c]) atomicMax(&s_pin[c], p);
       }
       __syncthreads();
       int pending = 0;
@@ -479,7 +532,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
         const int pin = s_pin[c];
         const int qmax = pin >= 0 ? hi - pin : Wn - 1;  // keep p in [pin, hi]
         int sum = 0;
-        for (int q = lane; q <= qmax; q += 32) sum += s_scr[c * Wn + q];
+        for (int q = lane; q <= qmax; q += 32) sum += s_scr[c * Wn + q] & (int)kValMask;
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
         __syncwarp();
@@ -635,6 +688,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
   a.tile_tokens = p.tile_tokens;
   a.n_tiles = p.n_tiles;
   a.ncols = p.ncols;
+  a.lg_words = p.lg_words;
   a.expert_idx = out.expert_idx;
   a.slot_idx = out.slot_idx;
   a.weight = out.weight;

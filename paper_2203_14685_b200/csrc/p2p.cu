@@ -288,7 +288,7 @@ static moe_status_t p2p_args(const char* fn, moe_comm_t* comm, const moe_gate_de
 
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
-                             int32_t dtype, void* y, moe_stream_t stream_) {
+                             int32_t dtype, void* y, int32_t flags, moe_stream_t stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   PeerPtrs src;
   int ds = 0;
@@ -300,16 +300,19 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     return MOE_ERR_INVALID_ARG;
   }
   const int P = comm->nranks;
-  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every expert is done
-  if (s != MOE_OK) return s;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // every rank's expert is done
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
   s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream);
   if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // nobody reads them any more
 }
 
 moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                               const moe_routing_t* routing, const void* x, int32_t d,
-                              int32_t dtype, void* recv, moe_stream_t stream_) {
+                              int32_t dtype, void* recv, int32_t flags, moe_stream_t stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   PeerPtrs dst;
   int ds = 0;
@@ -320,10 +323,15 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     return MOE_ERR_INVALID_ARG;
   }
   const int P = comm->nranks;
-  moe_status_t s = layout_launch_peers(*desc, *routing, x, ds, d, dst, desc->E / P, comm->rank,
-                                       stream);
+  moe_status_t s;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // every owner is ready to receive
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, desc->E / P, comm->rank, stream);
   if (s != MOE_OK) return s;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
 }
 
 }  // extern "C"

@@ -52,6 +52,14 @@ class RoutePipeline:
             nb = comm.workspace_bytes(algo, group_size, self.dispatch.nbytes // self.P)
             self.ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
 
+    def _first_flags(self):
+        # The very first dispatch needs its entry barrier (peers may not have
+        # allocated / zeroed recv yet); later ones follow a combine's exit one.
+        if not getattr(self, "_started", False):
+            self._started = True
+            return 0
+        return self.comm.NO_ENTRY_BARRIER
+
     def alltoall(self, send, recv):
         if self.P > 1:
             self.comm.alltoall(send, recv, self.algo, self.group_size, self.ws)
@@ -65,7 +73,8 @@ class RoutePipeline:
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         mark("gate")
         if self.P > 1 and self.algo == "p2p":                              # steps 2+3 fused
-            self.comm.dispatch_p2p(x, r, self.recv)
+            # no entry barrier: the previous step's combine ended with one
+            self.comm.dispatch_p2p(x, r, self.recv, flags=self._first_flags())
             mark("layout")
             mark("a2a_dispatch")
         else:
@@ -77,7 +86,10 @@ class RoutePipeline:
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
             mark("expert")
         if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
-            self.comm.combine_p2p(self.recv, r, self.y)
+            # entry barrier only if an expert wrote recv after the dispatch's
+            # exit barrier; the exit barrier frees recv for the next step
+            self.comm.combine_p2p(self.recv, r, self.y,
+                                  flags=0 if expert else self.comm.NO_ENTRY_BARRIER)
             mark("a2a_combine")
             mark("reverse")
             return self.y
@@ -117,10 +129,11 @@ class RoutePipeline:
                 p2p = self.P > 1 and self.algo == "p2p"
                 fns = {
                     "gate": lambda: self.gate(logits, token_ids, table, out=r),
-                    "layout": (lambda: self.comm.dispatch_p2p(x, r, self.recv)) if p2p else
+                    "layout": (lambda: self.comm.dispatch_p2p(x, r, self.recv, flags=1)) if p2p else
                               (lambda: layout(x, r, out=self.dispatch)),
                     "a2a_dispatch": lambda: self.alltoall(self.dispatch, self.recv),
-                    "a2a_combine": (lambda: self.comm.combine_p2p(self.recv, r, self.y)) if p2p else
+                    "a2a_combine": (lambda: self.comm.combine_p2p(self.recv, r, self.y, flags=1))
+                                   if p2p else
                                    (lambda: self.alltoall(self.recv, self.back)),
                     "reverse": lambda: reverse_layout(self.back, r, out=self.y),
                 }
