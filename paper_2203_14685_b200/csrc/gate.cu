@@ -497,18 +497,30 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
     int hi = tile - 1;
     while (true) {
       const int lo = max(0, hi - W + 1), Wn = hi - lo + 1, n = Wn * a.ncols;
-      // pass 1: issue every load of the round without waiting (one L2 round
-      // trip); entries are packed as flag << 30 | value, flag 0 = not ready
-#pragma unroll 4
-      for (int i = tid; i < n; i += kGateThreads) {
-        const int c = i / Wn, p = hi - (i - c * Wn);
-        unsigned code = 1u << 30;  // finished column: counts as 0
-        if (!s_done[c]) {
-          const unsigned long long w = ld_relaxed_u64(a.status + (size_t)c * a.n_tiles + p);
-          code = (w >> 34) == epoch ? (((unsigned)(w >> 32) & 3u) << 30) | ((unsigned)w & kValMask)
-                                    : 0u;
+      // pass 1: issue the loads of the round 16 at a time into registers
+      // before consuming any (one L2 round trip per 16 words per thread);
+      // entries are packed as flag << 30 | value, flag 0 = not ready
+      constexpr int B = 16;
+      for (int base = tid; base < n; base += kGateThreads * B) {
+        unsigned long long w[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int i = base + u * kGateThreads;
+          w[u] = 0;
+          if (i < n) {
+            const int c = i / Wn, p = hi - (i - c * Wn);
+            if (!s_done[c]) w[u] = ld_relaxed_u64(a.status + (size_t)c * a.n_tiles + p);
+            else w[u] = (epoch << 34) | (1ull << 32);  // finished column: counts as 0
+          }
         }
-        s_scr[i] = (int)code;
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int i = base + u * kGateThreads;
+          if (i < n)
+            s_scr[i] = (int)((w[u] >> 34) == epoch
+                                 ? (((unsigned)(w[u] >> 32) & 3u) << 30) | ((unsigned)w[u] & kValMask)
+                                 : 0u);
+        }
       }
       // pass 2: poll only what was not published yet; note inclusive tiles
       for (int i = tid; i < n; i += kGateThreads) {
