@@ -56,12 +56,28 @@ struct GateArgs {
   GateCtrl* ctrl;
   unsigned long long* status;  // [ncols][n_tiles] (column-major: warp look-back)
   int32_t* totals;             // [ncols] (SLOT priority)
+  unsigned long long* trace;   // [n_tiles][8] globaltimer stamps (MOE_GATE_TRACE builds)
 };
+
+#ifdef MOE_GATE_TRACE
+#define GATE_TRACE(k)                                                         \
+  do {                                                                        \
+    if (threadIdx.x == 0) {                                                   \
+      unsigned long long _t;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                  \
+      a.trace[(size_t)s_tile * 8 + (k)] = _t;                                 \
+    }                                                                         \
+  } while (0)
+#else
+#define GATE_TRACE(k) \
+  do {                \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------ layout of ws
 struct GatePlan {
   int L, K, tile_tokens, n_tiles, ncols, lg_words;
-  size_t status_off, totals_off, bytes, smem;
+  size_t status_off, totals_off, bytes, smem, trace_off;
 };
 
 static int choose_lanes(int E) {
@@ -89,6 +105,10 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   p.totals_off = p.status_off + sizeof(unsigned long long) * (size_t)p.n_tiles * p.ncols;
   p.bytes = p.totals_off + sizeof(int32_t) * (size_t)p.ncols;
   p.bytes = (p.bytes + 255) & ~(size_t)255;
+#ifdef MOE_GATE_TRACE
+  p.trace_off = p.bytes;
+  p.bytes += sizeof(unsigned long long) * 8 * (size_t)p.n_tiles;
+#endif
   size_t items = (size_t)tt * d.k;
   p.lg_words = d.kind == MOE_GATE_HASH ? 0 : ((tt * d.E + 3) & ~3);
   p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)(kGateWarps + 4) * p.ncols + kLookWords);
@@ -360,6 +380,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   for (int i = tid; i < items; i += kGateThreads) s_exp[i] = -1;
   for (int i = tid; i < kGateWarps * a.ncols; i += kGateThreads) s_hist[i] = 0;
   __syncthreads();
+  GATE_TRACE(0);
   const int tile = (int)s_tile;
   const unsigned long long epoch = s_epoch;
   const int t0 = tile * a.tile_tokens;
@@ -395,6 +416,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
           : "r"(mbar)
           : "memory");
   }
+  GATE_TRACE(1);
 
   // ---------------- Phase A: selection + weights
   if constexpr (KIND == KIND_HASH) {
@@ -434,6 +456,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   }
   __syncthreads();
 
+  GATE_TRACE(2);
   // ---------------- Phase B1: ranks inside the tile, per warp
   const bool slot_prio = a.prio == MOE_PRIO_SLOT;
   const int per = (items + kGateWarps - 1) / kGateWarps;
@@ -492,6 +515,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
                    (epoch << 34) | ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)run);
   }
   __syncthreads();
+  GATE_TRACE(3);
   if (tile > 0) {
     const int W = max(1, min(tile, kLookWords / a.ncols));
     int hi = tile - 1;
@@ -565,6 +589,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   }
   __syncthreads();
 
+  GATE_TRACE(4);
   // ---------------- Phase B3: final slots (coalesced over t*k+j)
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const int e = s_exp[i];
@@ -601,6 +626,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
 
   // ---------------- reset the control block for the next call
   __syncthreads();
+  GATE_TRACE(5);
   // Every CTA read the epoch before it incremented `done`, so the last one
   // may reset the block without a fence; the next launch sees it.
   if (tid == 0) {
@@ -710,6 +736,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
   a.ctrl = reinterpret_cast<GateCtrl*>(w);
   a.status = reinterpret_cast<unsigned long long*>(w + p.status_off);
   a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
+  a.trace = p.trace_off ? reinterpret_cast<unsigned long long*>(w + p.trace_off) : nullptr;
 
   GateKernel kern = d.kind == MOE_GATE_HASH    ? k_gate<KIND_HASH, 1, 1>
                     : d.kind == MOE_GATE_KTOP1 ? pick_l<KIND_KTOP1>(p.L, p.K)
