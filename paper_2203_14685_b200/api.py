@@ -114,7 +114,8 @@ class Gate:
             if tuple(logits.shape) != (self.S, self.E):
                 raise ValueError("logits shape %s != (S=%d, E=%d)" % (tuple(logits.shape),
                                                                      self.S, self.E))
-        d = out.desc()
+        out.kind, out.weight_mode, out.priority = self.kind, self.mode, self.prio
+        d = GateDesc(self.S, self.E, self.k, self.cap, self.kind, self.mode, self.prio)
         rc = out.c()
         check(lib().moe_gate(ctypes.byref(d), _p(logits), _p(token_ids), _p(table), vocab,
                              ctypes.byref(rc), _p(self.ws), self.ws.numel(),

@@ -31,7 +31,6 @@ constexpr int kGateThreads = 256;
 constexpr int kGateWarps = kGateThreads / 32;
 constexpr int kMaxTileItems = 2048;  // tile_tokens * k
 constexpr int kMaxCols = 2048;       // look-back columns: E or k*E
-constexpr int kLookWords = 8192;     // status words one look-back round reads
 constexpr size_t kMaxTileLogitBytes = 64 * 1024;
 constexpr unsigned kValMask = (1u << 30) - 1;  // counts < 2^30 (S*k < 2^30, checked)
 
@@ -111,7 +110,7 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
 #endif
   size_t items = (size_t)tt * d.k;
   p.lg_words = d.kind == MOE_GATE_HASH ? 0 : ((tt * d.E + 3) & ~3);
-  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)(kGateWarps + 4) * p.ncols + kLookWords);
+  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)(kGateWarps + 2) * p.ncols);
   return p;
 }
 
@@ -363,9 +362,6 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   int* s_hist = s_rank + items;               // [warps][ncols]
   int* s_excl = s_hist + kGateWarps * a.ncols;  // [ncols] tiles-before
   int* s_tot = s_excl + a.ncols;              // [ncols] aggregate, then inclusive
-  int* s_done = s_tot + a.ncols;              // [ncols] look-back finished
-  int* s_pin = s_done + a.ncols;              // [ncols] nearest inclusive tile
-  int* s_scr = s_pin + a.ncols;               // [kLookWords] status values
   __shared__ unsigned s_tile, s_epoch, s_bad;
   __shared__ __align__(8) unsigned long long s_mbar;
 
@@ -491,13 +487,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   __syncthreads();
 
   // ---------------- Phase B2: warp prefix, then a decoupled look-back per
-  // column, read by the whole CTA in parallel.  Aggregates are published
-  // first (successors never wait on our look-back).  Each round reads the
-  // status words of W predecessor tiles for every column at once (column-
-  // major, so consecutive threads read consecutive words), keeps, per
-  // column, everything after the nearest tile that already carries an
-  // inclusive prefix, and stops there; with W*ncols <= kLookWords one round
-  // covers all predecessors, so there is no sequential chain across tiles.
+  // column.  Aggregates are published first (successors never wait on our
+  // look-back); the look-back itself reads 256 predecessor tiles per round
+  // per column from registers and stops at the nearest tile that already
+  // carries an inclusive prefix, so there is no sequential chain across tiles.
   const bool last_tile = tile == a.n_tiles - 1;
   for (int c = tid; c < a.ncols; c += kGateThreads) {
     int run = 0;
@@ -509,86 +502,82 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
     }
     s_tot[c] = run;  // tile aggregate (the inclusive total after the look-back)
     s_excl[c] = 0;
-    s_done[c] = tile == 0;
-    s_pin[c] = -1;
     st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
                    (epoch << 34) | ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)run);
   }
   __syncthreads();
   GATE_TRACE(3);
   if (tile > 0) {
-    const int W = max(1, min(tile, kLookWords / a.ncols));
-    int hi = tile - 1;
-    while (true) {
-      const int lo = max(0, hi - W + 1), Wn = hi - lo + 1, n = Wn * a.ncols;
-      // pass 1: issue the loads of the round 16 at a time into registers
-      // before consuming any (one L2 round trip per 16 words per thread);
-      // entries are packed as flag << 30 | value, flag 0 = not ready
-      constexpr int B = 16;
-      for (int base = tid; base < n; base += kGateThreads * B) {
-        unsigned long long w[B];
+    // One warp per column: lane l holds the words of predecessors
+    // p = hi - l - 32*u (u < kLB), i.e. 32*kLB tiles per round, loaded
+    // before any is consumed; kCB columns are in flight per warp.  The
+    // nearest inclusive tile p* is a warp max-reduce; the exclusive prefix
+    // is the register sum of the words with p >= p*.  Rounds move to older
+    // tiles only while no inclusive word has been seen.
+    constexpr int kLB = 8, kCB = 4;
+    for (int c0 = warp * kCB; c0 < a.ncols; c0 += kGateWarps * kCB) {
+      int hi = tile - 1;
+      unsigned excl[kCB];
+      bool done[kCB];
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          const int i = base + u * kGateThreads;
-          w[u] = 0;
-          if (i < n) {
-            const int c = i / Wn, p = hi - (i - c * Wn);
-            if (!s_done[c]) w[u] = ld_relaxed_u64(a.status + (size_t)c * a.n_tiles + p);
-            else w[u] = (epoch << 34) | (1ull << 32);  // finished column: counts as 0
+      for (int cb = 0; cb < kCB; ++cb) {
+        excl[cb] = 0;
+        done[cb] = c0 + cb >= a.ncols;
+      }
+      while (true) {
+        unsigned long long w[kCB][kLB];
+#pragma unroll
+        for (int cb = 0; cb < kCB; ++cb)
+#pragma unroll
+          for (int u = 0; u < kLB; ++u) {
+            const int p = hi - lane - 32 * u;
+            w[cb][u] = (epoch << 34) | (2ull << 32);  // p < 0: virtual inclusive 0
+            if (p >= 0 && !done[cb])
+              w[cb][u] = ld_relaxed_u64(a.status + (size_t)(c0 + cb) * a.n_tiles + p);
           }
-        }
+        bool all_done = true;
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          const int i = base + u * kGateThreads;
-          if (i < n)
-            s_scr[i] = (int)((w[u] >> 34) == epoch
-                                 ? (((unsigned)(w[u] >> 32) & 3u) << 30) | ((unsigned)w[u] & kValMask)
-                                 : 0u);
-        }
-      }
-      // pass 2: poll only what was not published yet; note inclusive tiles
-      for (int i = tid; i < n; i += kGateThreads) {
-        const int c = i / Wn, p = hi - (i - c * Wn);
-        unsigned code = (unsigned)s_scr[i];
-        if ((code >> 30) == 0) {
-          const unsigned long long* wp = a.status + (size_t)c * a.n_tiles + p;
-          unsigned long long w;
-          do {
-            w = ld_relaxed_u64(wp);
-          } while ((w >> 34) != epoch || ((w >> 32) & 3u) == 0);
-          code = (((unsigned)(w >> 32) & 3u) << 30) | ((unsigned)w & kValMask);
-          s_scr[i] = (int)code;
-        }
-        if ((code >> 30) == 2 && !s_done[c]) atomicMax(&s_pin[c], p);
-      }
-      __syncthreads();
-      int pending = 0;
-      for (int c = warp; c < a.ncols; c += kGateWarps) {
-        if (s_done[c]) continue;
-        const int pin = s_pin[c];
-        const int qmax = pin >= 0 ? hi - pin : Wn - 1;  // keep p in [pin, hi]
-        int sum = 0;
-        for (int q = lane; q <= qmax; q += 32) sum += s_scr[c * Wn + q] & (int)kValMask;
+        for (int cb = 0; cb < kCB; ++cb) {
+          if (done[cb]) continue;  // warp-uniform
+          int pin = -1;            // nearest inclusive predecessor seen by this lane
 #pragma unroll
-        for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
-        __syncwarp();
-        if (lane == 0) {
-          s_excl[c] += sum;
-          if (pin >= 0 || lo == 0) s_done[c] = 1; else pending = 1;
-          s_pin[c] = -1;
+          for (int u = 0; u < kLB; ++u) {
+            const int p = hi - lane - 32 * u;
+            while ((w[cb][u] >> 34) != epoch || ((w[cb][u] >> 32) & 3u) == 0)  // rare
+              w[cb][u] = ld_relaxed_u64(a.status + (size_t)(c0 + cb) * a.n_tiles + p);
+            if (((w[cb][u] >> 32) & 3u) == 2u) pin = max(pin, p);
+          }
+#pragma unroll
+          for (int m = 16; m > 0; m >>= 1) pin = max(pin, __shfl_xor_sync(0xffffffffu, pin, m));
+          unsigned sum = 0;
+#pragma unroll
+          for (int u = 0; u < kLB; ++u) {
+            const int p = hi - lane - 32 * u;
+            if (p >= pin && p >= 0) sum += (unsigned)w[cb][u];
+          }
+#pragma unroll
+          for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+          excl[cb] += sum;
+          if (pin >= hi - 32 * kLB + 1 || hi - 32 * kLB + 1 <= 0) done[cb] = true;
+          else all_done = false;
         }
+        if (all_done) break;
+        hi -= 32 * kLB;
       }
-      if (!__syncthreads_or(pending)) break;
-      hi = lo - 1;
-    }
-    for (int c = tid; c < a.ncols; c += kGateThreads) {
-      const unsigned incl = (unsigned)(s_excl[c] + s_tot[c]);
-      st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile, (epoch << 34) | (2ull << 32) | incl);
-      s_tot[c] = (int)incl;
+      if (lane < kCB && c0 + lane < a.ncols) {
+        unsigned ex = 0;
+#pragma unroll
+        for (int cb = 0; cb < kCB; ++cb)
+          if (cb == lane) ex = excl[cb];
+        const int c = c0 + lane;
+        const unsigned incl = ex + (unsigned)s_tot[c];
+        st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile, (epoch << 34) | (2ull << 32) | incl);
+        s_excl[c] = (int)ex;
+        s_tot[c] = (int)incl;
+      }
     }
   }
   __syncthreads();
-
   GATE_TRACE(4);
   // ---------------- Phase B3: final slots (coalesced over t*k+j)
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
@@ -618,8 +607,8 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
     } else {
       for (int e = tid; e < a.E; e += kGateThreads) a.load[e] = s_tot[e];
       if (a.slot_src)
-        for (int e = 0; e < a.E; ++e)
-          for (int s = min(s_tot[e], a.cap) + tid; s < a.cap; s += kGateThreads)
+        for (int e = warp; e < a.E; e += kGateWarps)  // warp per expert, coalesced
+          for (int s = min(s_tot[e], a.cap) + lane; s < a.cap; s += 32)
             a.slot_src[(size_t)e * a.cap + s] = -1;
     }
   }
