@@ -114,11 +114,11 @@ typedef struct {
  * C <= 0 or the result does not fit in int32. */
 int32_t moe_capacity(int32_t S, int32_t E, int32_t k, double C);
 
-/* host.  Device workspace moe_gate needs for `desc` (0 if desc is invalid).
- * The workspace must be ZERO-FILLED before its first use; after that every
- * moe_gate call leaves it ready for the next one (it carries an epoch), so
- * it may be reused across calls and CUDA-graph replays on one stream.  Do
- * not use one workspace from two streams concurrently. */
+/* host.  Device workspace moe_gate needs for `desc` (0 if desc is invalid):
+ * per-tile, per-expert counts and the invalid-hash-id counter.  Zero-fill it
+ * once before first use (the counter); it may then be reused by any number of
+ * calls and CUDA-graph replays on one stream.  Do not use one workspace from
+ * two streams concurrently. */
 size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc);
 
 /* Step 1 of Algorithm 1 plus capacity:

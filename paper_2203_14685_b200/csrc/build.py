@@ -24,7 +24,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "moe_b200")
 SO = os.path.join(PKG, "libmoe_b200.so")
 # variants: extra -D flags, their own object dir and library name
-VARIANTS = {"": [], "trace": ["-DMOE_GATE_TRACE"]}
+VARIANTS = {"": []}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,25 +1,26 @@
 // gate.cu -- moe_gate: Step 1 of Algorithm 1 on given gate
-// logits, fused with capacity slot assignment.
+// logits, fused with capacity slot assignment.  Three kernels,
+// chained with programmatic dependent launch (each one's launch overlaps its
+// predecessor's tail), no spin-waits and no co-residency assumption:
 //
-// One CTA per tile of tokens; the tile id comes from an atomic ticket, so a
-// CTA only ever waits on tiles already claimed by running CTAs (look-back
-// always makes progress, whatever else occupies the SMs).
-//
-//   Phase A  selection + weights (Eq. 1, 123-124, 144-145)
-//            L lanes per token; each lane keeps a register top-K of its E/L
-//            logits, a shfl_xor butterfly merges the lists (comparator:
-//            larger raw fp32 logit, then lower index -- R2, R3).  k > 8 uses
-//            a rank-counting path.  Weights are evaluated in fp64 and rounded
-//            once to fp32 (R1).
-//   Phase B  capacity (R4-R6): in-tile ranks of each item among earlier
-//            items of the same expert column (__match_any_sync, 32 items at a
-//            time, per-warp histograms), then a decoupled look-back across
-//            tiles per column: 64-bit status words (epoch | flag | value)
-//            that carry their own payload, so relaxed gpu-scope stores and
-//            loads suffice (no fences on the critical path).  slot =
-//            tiles-before + warps-before + rank-in-warp; >= cap -> dropped.
-//            SLOT priority (j-major) runs the same scan per (j, e) column and
-//            k_gate_slot_finalize adds the totals of earlier j afterwards.
+//   k_gate_select  one CTA per tile of tokens.  The tile's logits come into
+//                  shared memory with one TMA bulk copy.  Selection + weights
+//                  (Eq. 1, 123-124, 144-145): L lanes per
+//                  token, each keeps a register top-K of its E/L logits, a
+//                  shfl_xor butterfly merges the lists (larger raw fp32
+//                  logit, then lower index -- R2, R3); k > 8 uses a rank-
+//                  counting path; weights in fp64, rounded once (R1).  Then
+//                  in-tile ranks per expert column (__match_any_sync over 32
+//                  items at a time in admission order, per-warp histograms):
+//                  provisional slot = warps-before + rank-in-warp, and the
+//                  tile's per-column aggregate.
+//   k_gate_scan    warp per column: exclusive scan of the tile aggregates
+//                  (8 tiles per lane per round, in registers); totals, load.
+//   k_gate_slots   slot = earlier tiles + provisional (SLOT priority: + the
+//                  items of earlier j); >= cap -> dropped, weight 0 (R4-R6);
+//                  slot_src and its empty entries.
+// Columns are experts (TOKEN priority, t-major admission) or (j, expert)
+// pairs (SLOT priority, j-major).  Traffic is O(tiles x columns).
 #include <cfloat>
 #include <climits>
 
@@ -35,8 +36,8 @@ constexpr size_t kMaxTileLogitBytes = 64 * 1024;
 constexpr unsigned kValMask = (1u << 30) - 1;  // counts < 2^30 (S*k < 2^30, checked)
 
 struct GateCtrl {  // 64 bytes at the head of the workspace
-  unsigned ticket, done, epoch, bad;
-  unsigned pad[12];
+  unsigned bad;     // invalid hash ids since the last moe_gate_check
+  unsigned pad[15];
 };
 
 struct GateArgs {
@@ -53,30 +54,16 @@ struct GateArgs {
   int32_t* load;
   int32_t* slot_src;
   GateCtrl* ctrl;
-  unsigned long long* status;  // [ncols][n_tiles] (column-major: warp look-back)
+  unsigned long long* status;  // [ncols][n_tiles] u32 tile aggregates, then prefixes
   int32_t* totals;             // [ncols] (SLOT priority)
-  unsigned long long* trace;   // [n_tiles][8] globaltimer stamps (MOE_GATE_TRACE builds)
 };
 
-#ifdef MOE_GATE_TRACE
-#define GATE_TRACE(k)                                                         \
-  do {                                                                        \
-    if (threadIdx.x == 0) {                                                   \
-      unsigned long long _t;                                                  \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                  \
-      a.trace[(size_t)s_tile * 8 + (k)] = _t;                                 \
-    }                                                                         \
-  } while (0)
-#else
-#define GATE_TRACE(k) \
-  do {                \
-  } while (0)
-#endif
+
 
 // ------------------------------------------------------------ layout of ws
 struct GatePlan {
   int L, K, tile_tokens, n_tiles, ncols, lg_words;
-  size_t status_off, totals_off, bytes, smem, trace_off;
+  size_t status_off, totals_off, bytes, smem;
 };
 
 static int choose_lanes(int E) {
@@ -101,16 +88,12 @@ static GatePlan gate_plan(const moe_gate_desc_t& d) {
   p.n_tiles = (d.S + tt - 1) / tt;
   p.ncols = d.priority == MOE_PRIO_SLOT ? d.k * d.E : d.E;
   p.status_off = sizeof(GateCtrl);
-  p.totals_off = p.status_off + sizeof(unsigned long long) * (size_t)p.n_tiles * p.ncols;
+  p.totals_off = p.status_off + sizeof(unsigned) * (size_t)p.n_tiles * p.ncols;
   p.bytes = p.totals_off + sizeof(int32_t) * (size_t)p.ncols;
   p.bytes = (p.bytes + 255) & ~(size_t)255;
-#ifdef MOE_GATE_TRACE
-  p.trace_off = p.bytes;
-  p.bytes += sizeof(unsigned long long) * 8 * (size_t)p.n_tiles;
-#endif
   size_t items = (size_t)tt * d.k;
   p.lg_words = d.kind == MOE_GATE_HASH ? 0 : ((tt * d.E + 3) & ~3);
-  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)(kGateWarps + 2) * p.ncols);
+  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)kGateWarps * p.ncols);
   return p;
 }
 
@@ -353,32 +336,24 @@ __device__ __forceinline__ void select_rank(const GateArgs& a, const float* row,
 enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2 };
 
 template <int KIND, int L, int K>
-__global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
+__global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   extern __shared__ __align__(16) int smem[];
   const int items = a.tile_tokens * a.k;
   float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
   int* s_exp = smem + a.lg_words;             // [items] expert of item tt*k+j
   int* s_rank = s_exp + items;                // [items] rank inside its warp
   int* s_hist = s_rank + items;               // [warps][ncols]
-  int* s_excl = s_hist + kGateWarps * a.ncols;  // [ncols] tiles-before
-  int* s_tot = s_excl + a.ncols;              // [ncols] aggregate, then inclusive
-  __shared__ unsigned s_tile, s_epoch, s_bad;
+  __shared__ unsigned s_bad;
   __shared__ __align__(8) unsigned long long s_mbar;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();     // the producer of the logits / the previous step must be done
-  pdl_trigger();  // moe_layout may launch now; it waits for our completion
-  if (tid == 0) {
-    s_tile = atomicAdd(&a.ctrl->ticket, 1u);
-    s_epoch = *((volatile unsigned*)&a.ctrl->epoch) & 0x3FFFFFFFu;
-    s_bad = 0;
-  }
+  pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
+  if (tid == 0) s_bad = 0;
   for (int i = tid; i < items; i += kGateThreads) s_exp[i] = -1;
   for (int i = tid; i < kGateWarps * a.ncols; i += kGateThreads) s_hist[i] = 0;
   __syncthreads();
-  GATE_TRACE(0);
-  const int tile = (int)s_tile;
-  const unsigned long long epoch = s_epoch;
+  const int tile = blockIdx.x;
   const int t0 = tile * a.tile_tokens;
   const int nt = min(a.tile_tokens, a.S - t0);
   if constexpr (KIND != KIND_HASH) {
@@ -412,7 +387,6 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
           : "r"(mbar)
           : "memory");
   }
-  GATE_TRACE(1);
 
   // ---------------- Phase A: selection + weights
   if constexpr (KIND == KIND_HASH) {
@@ -452,7 +426,6 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   }
   __syncthreads();
 
-  GATE_TRACE(2);
   // ---------------- Phase B1: ranks inside the tile, per warp
   const bool slot_prio = a.prio == MOE_PRIO_SLOT;
   const int per = (items + kGateWarps - 1) / kGateWarps;
@@ -486,114 +459,105 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
   }
   __syncthreads();
 
-  // ---------------- Phase B2: warp prefix, then a decoupled look-back per
-  // column.  Aggregates are published first (successors never wait on our
-  // look-back); the look-back itself reads 256 predecessor tiles per round
-  // per column from registers and stops at the nearest tile that already
-  // carries an inclusive prefix, so there is no sequential chain across tiles.
-  const bool last_tile = tile == a.n_tiles - 1;
+  // ---------------- Phase B2: per-column warp prefix and tile aggregate
+  unsigned* agg = reinterpret_cast<unsigned*>(a.status);  // [ncols][n_tiles]
   for (int c = tid; c < a.ncols; c += kGateThreads) {
-    int run = 0;
+    unsigned run = 0;
 #pragma unroll
     for (int w = 0; w < kGateWarps; ++w) {
-      const int v = s_hist[w * a.ncols + c];
-      s_hist[w * a.ncols + c] = run;
+      const unsigned v = (unsigned)s_hist[w * a.ncols + c];
+      s_hist[w * a.ncols + c] = (int)run;
       run += v;
     }
-    s_tot[c] = run;  // tile aggregate (the inclusive total after the look-back)
-    s_excl[c] = 0;
-    st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile,
-                   (epoch << 34) | ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)run);
+    agg[(size_t)c * a.n_tiles + tile] = run;
   }
   __syncthreads();
-  GATE_TRACE(3);
-  if (tile > 0) {
-    // One warp per column: lane l holds the words of predecessors
-    // p = hi - l - 32*u (u < kLB), i.e. 32*kLB tiles per round, loaded
-    // before any is consumed; kCB columns are in flight per warp.  The
-    // nearest inclusive tile p* is a warp max-reduce; the exclusive prefix
-    // is the register sum of the words with p >= p*.  Rounds move to older
-    // tiles only while no inclusive word has been seen.
-    constexpr int kLB = 8, kCB = 4;
-    for (int c0 = warp * kCB; c0 < a.ncols; c0 += kGateWarps * kCB) {
-      int hi = tile - 1;
-      unsigned excl[kCB];
-      bool done[kCB];
-#pragma unroll
-      for (int cb = 0; cb < kCB; ++cb) {
-        excl[cb] = 0;
-        done[cb] = c0 + cb >= a.ncols;
-      }
-      while (true) {
-        unsigned long long w[kCB][kLB];
-#pragma unroll
-        for (int cb = 0; cb < kCB; ++cb)
-#pragma unroll
-          for (int u = 0; u < kLB; ++u) {
-            const int p = hi - lane - 32 * u;
-            w[cb][u] = (epoch << 34) | (2ull << 32);  // p < 0: virtual inclusive 0
-            if (p >= 0 && !done[cb])
-              w[cb][u] = ld_relaxed_u64(a.status + (size_t)(c0 + cb) * a.n_tiles + p);
-          }
-        bool all_done = true;
-#pragma unroll
-        for (int cb = 0; cb < kCB; ++cb) {
-          if (done[cb]) continue;  // warp-uniform
-          int pin = -1;            // nearest inclusive predecessor seen by this lane
-#pragma unroll
-          for (int u = 0; u < kLB; ++u) {
-            const int p = hi - lane - 32 * u;
-            while ((w[cb][u] >> 34) != epoch || ((w[cb][u] >> 32) & 3u) == 0)  // rare
-              w[cb][u] = ld_relaxed_u64(a.status + (size_t)(c0 + cb) * a.n_tiles + p);
-            if (((w[cb][u] >> 32) & 3u) == 2u) pin = max(pin, p);
-          }
-#pragma unroll
-          for (int m = 16; m > 0; m >>= 1) pin = max(pin, __shfl_xor_sync(0xffffffffu, pin, m));
-          unsigned sum = 0;
-#pragma unroll
-          for (int u = 0; u < kLB; ++u) {
-            const int p = hi - lane - 32 * u;
-            if (p >= pin && p >= 0) sum += (unsigned)w[cb][u];
-          }
-#pragma unroll
-          for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
-          excl[cb] += sum;
-          if (pin >= hi - 32 * kLB + 1 || hi - 32 * kLB + 1 <= 0) done[cb] = true;
-          else all_done = false;
-        }
-        if (all_done) break;
-        hi -= 32 * kLB;
-      }
-      if (lane < kCB && c0 + lane < a.ncols) {
-        unsigned ex = 0;
-#pragma unroll
-        for (int cb = 0; cb < kCB; ++cb)
-          if (cb == lane) ex = excl[cb];
-        const int c = c0 + lane;
-        const unsigned incl = ex + (unsigned)s_tot[c];
-        st_relaxed_u64(a.status + (size_t)c * a.n_tiles + tile, (epoch << 34) | (2ull << 32) | incl);
-        s_excl[c] = (int)ex;
-        s_tot[c] = (int)incl;
-      }
-    }
-  }
-  __syncthreads();
-  GATE_TRACE(4);
-  // ---------------- Phase B3: final slots (coalesced over t*k+j)
+  // ---------------- provisional slots: rank inside the tile's column
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const int e = s_exp[i];
     const size_t gi = (size_t)t0 * a.k + i;
     if (e < 0) {
-      a.slot_idx[gi] = -1;
+      a.slot_idx[gi] = -1;  // invalid hash id: routed as dropped
       continue;
     }
     const int tt = i / a.k, j = i - tt * a.k;
     const int pos = slot_prio ? j * a.tile_tokens + tt : i;
     const int col = slot_prio ? j * a.E + e : e;
-    const int s = s_excl[col] + s_hist[(pos / per) * a.ncols + col] + s_rank[i];
+    a.slot_idx[gi] = s_hist[(pos / per) * a.ncols + col] + s_rank[i];
+  }
+  if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
+}
+
+// Exclusive scan of every column's tile aggregates (in place), warp per
+// column, 8 consecutive tiles per lane per round; totals[c] = column total.
+// TOKEN priority: the column is the expert, so load[e] = totals[e].
+__global__ void __launch_bounds__(kGateThreads) k_gate_scan(GateArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kGateWarps + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_trigger();
+  if (c >= a.ncols) return;
+  unsigned* col = reinterpret_cast<unsigned*>(a.status) + (size_t)c * a.n_tiles;
+  unsigned carry = 0;
+  for (int base = 0; base < a.n_tiles; base += 256) {
+    unsigned v[8], run = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + lane * 8 + u;
+      v[u] = i < a.n_tiles ? col[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned x = v[u];
+      v[u] = run;
+      run += x;
+    }
+    unsigned incl = run;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, incl, m);
+      if (lane >= m) incl += o;
+    }
+    const unsigned lane_excl = carry + incl - run;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + lane * 8 + u;
+      if (i < a.n_tiles) col[i] = lane_excl + v[u];
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    a.totals[c] = (int)carry;
+    if (a.prio != MOE_PRIO_SLOT) a.load[c] = (int)carry;
+  }
+}
+
+// Final slots: slot = (SLOT priority: items of earlier j of this expert) +
+// items of earlier tiles in the column + the provisional in-tile rank;
+// slot >= cap -> dropped (weight 0).  Then every CTA fills its share of the
+// empty slot_src entries [min(load,cap), cap) (warp per expert).
+__global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int t0 = tile * a.tile_tokens;
+  const int nt = min(a.tile_tokens, a.S - t0);
+  const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  pdl_wait();
+  pdl_trigger();
+  const unsigned* pre = reinterpret_cast<const unsigned*>(a.status);
+  for (int i = tid; i < nt * a.k; i += kGateThreads) {
+    const size_t gi = (size_t)t0 * a.k + i;
+    const int e = a.expert_idx[gi];
+    if (e < 0) continue;
+    const int j = i % a.k;
+    int s = a.slot_idx[gi];
     if (slot_prio) {
-      a.slot_idx[gi] = s;  // rank inside the j-stream; finalised by k_gate_slot_finalize
-    } else if (s < a.cap) {
+      for (int jj = 0; jj < j; ++jj) s += a.totals[jj * a.E + e];
+      s += (int)pre[(size_t)(j * a.E + e) * a.n_tiles + tile];
+    } else {
+      s += (int)pre[(size_t)e * a.n_tiles + tile];
+    }
+    if (s < a.cap) {
       a.slot_idx[gi] = s;
       if (a.slot_src) a.slot_src[(size_t)e * a.cap + s] = (int)gi;
     } else {
@@ -601,68 +565,16 @@ __global__ void __launch_bounds__(kGateThreads) k_gate(GateArgs a) {
       a.weight[gi] = 0.f;
     }
   }
-  if (last_tile) {
+  for (int e = tile * kGateWarps + warp; e < a.E; e += gridDim.x * kGateWarps) {
+    int ld = 0;
     if (slot_prio) {
-      for (int c = tid; c < a.ncols; c += kGateThreads) a.totals[c] = s_tot[c];
-    } else {
-      for (int e = tid; e < a.E; e += kGateThreads) a.load[e] = s_tot[e];
-      if (a.slot_src)
-        for (int e = warp; e < a.E; e += kGateWarps)  // warp per expert, coalesced
-          for (int s = min(s_tot[e], a.cap) + lane; s < a.cap; s += 32)
-            a.slot_src[(size_t)e * a.cap + s] = -1;
-    }
-  }
-
-  // ---------------- reset the control block for the next call
-  __syncthreads();
-  GATE_TRACE(5);
-  // Every CTA read the epoch before it incremented `done`, so the last one
-  // may reset the block without a fence; the next launch sees it.
-  if (tid == 0) {
-    if (s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-    const unsigned prev = atomicAdd(&a.ctrl->done, 1u);
-    if (prev == gridDim.x - 1) {
-      a.ctrl->ticket = 0;
-      a.ctrl->done = 0;
-      a.ctrl->epoch = (unsigned)((epoch + 1) & 0x3FFFFFFFu);
-    }
-  }
-}
-
-// SLOT priority: slot = (admitted items of earlier j for this expert) +
-// rank inside the j-stream; then capacity, load and slot_src.
-__global__ void k_gate_slot_finalize(GateArgs a) {
-  const size_t n = (size_t)a.S * a.k;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int e = a.expert_idx[i];
-    if (e < 0) continue;
-    const int j = (int)(i % a.k);
-    int base = 0;
-    for (int jj = 0; jj < j; ++jj) base += a.totals[jj * a.E + e];
-    const int s = base + a.slot_idx[i];
-    if (s < a.cap) {
-      a.slot_idx[i] = s;
-      if (a.slot_src) a.slot_src[(size_t)e * a.cap + s] = (int)i;
-    } else {
-      a.slot_idx[i] = -1;
-      a.weight[i] = 0.f;
-    }
-  }
-  const size_t nslots = (size_t)a.E * a.cap;
-  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < nslots || q < (size_t)a.E;
-       q += stride) {
-    if (q < (size_t)a.E) {
-      int ld = 0;
-      for (int jj = 0; jj < a.k; ++jj) ld += a.totals[jj * a.E + (int)q];
-      a.load[q] = ld;
-    }
-    if (a.slot_src && q < nslots) {
-      const int e = (int)(q / a.cap), s = (int)(q % a.cap);
-      int ld = 0;
       for (int jj = 0; jj < a.k; ++jj) ld += a.totals[jj * a.E + e];
-      if (s >= min(ld, a.cap)) a.slot_src[q] = -1;
+      if (lane == 0) a.load[e] = ld;
+    } else {
+      ld = a.totals[e];
     }
+    if (a.slot_src)
+      for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
   }
 }
 
@@ -672,11 +584,11 @@ using GateKernel = void (*)(GateArgs);
 template <int KIND, int L>
 static GateKernel pick_k(int K) {
   switch (K) {
-    case 1: return k_gate<KIND, L, 1>;
-    case 2: return k_gate<KIND, L, 2>;
-    case 4: return k_gate<KIND, L, 4>;
-    case 8: return k_gate<KIND, L, 8>;
-    default: return k_gate<KIND, L, 0>;
+    case 1: return k_gate_select<KIND, L, 1>;
+    case 2: return k_gate_select<KIND, L, 2>;
+    case 4: return k_gate_select<KIND, L, 4>;
+    case 8: return k_gate_select<KIND, L, 8>;
+    default: return k_gate_select<KIND, L, 0>;
   }
 }
 template <int KIND>
@@ -725,9 +637,8 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
   a.ctrl = reinterpret_cast<GateCtrl*>(w);
   a.status = reinterpret_cast<unsigned long long*>(w + p.status_off);
   a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
-  a.trace = p.trace_off ? reinterpret_cast<unsigned long long*>(w + p.trace_off) : nullptr;
 
-  GateKernel kern = d.kind == MOE_GATE_HASH    ? k_gate<KIND_HASH, 1, 1>
+  GateKernel kern = d.kind == MOE_GATE_HASH    ? k_gate_select<KIND_HASH, 1, 1>
                     : d.kind == MOE_GATE_KTOP1 ? pick_l<KIND_KTOP1>(p.L, p.K)
                                                : pick_l<KIND_TOPK>(p.L, p.K);
   if (p.smem > 48 * 1024) {
@@ -735,18 +646,15 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
                                          (int)p.smem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
   }
-  {
-    void* args[] = {&a};
-    cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
-                               stream, args);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate launch");
-  }
-  if (d.priority == MOE_PRIO_SLOT) {
-    const size_t n = std::max((size_t)d.S * d.k, (size_t)d.E * d.capacity);
-    int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)device_sm_count() * 8);
-    k_gate_slot_finalize<<<blocks, 256, 0, stream>>>(a);
-    MOE_CHECK_LAUNCH("moe_gate: k_gate_slot_finalize launch");
-  }
+  void* args[] = {&a};
+  cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
+                             stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
+  e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
+                 dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
+  e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
   return MOE_OK;
 }
 
