@@ -12,7 +12,8 @@ Layout_Transform -> AllToAll dispatch -> AllToAll combine ->
 Reverse_Layout_Transform.  The expert is the identity inside the timed step
 (routing isolated, north_star); the s_e stand-in is timed separately
 (`expert_ms`).  Inputs are synthetic (synthgen, seeded) and resident in HBM;
-the L2 is flushed (a 2x-L2 memset) between timed steps, outside the events.
+the L2 is flushed (a 2x-L2 memset, then a 2x-L2 read so no dirty line is left) between
+timed steps, outside the events.
 Each step is timed with CUDA events on the launching stream; the reported
 time is the max over ranks.  `value` = tokens of all ranks / time.
 
@@ -267,6 +268,16 @@ def main():
     d_in = {k: (None if v is None else v.to(dev)) for k, v in host.items()}
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros_like(flush)
+    flush_sink = torch.empty((), dtype=torch.int64, device=dev)
+
+    def flush_l2():
+        # write 2x L2 (evicts every line of the previous step), then read
+        # another 2x L2 so the write-back of those dirty lines happens HERE,
+        # outside the events, not inside the next timed step: L2 is left cold
+        # (no line of the step's data) and clean.
+        flush.zero_()
+        torch.sum(flush_rd.view(torch.int64), dim=0, out=flush_sink)
 
     def barrier():
         if P > 1:
@@ -302,7 +313,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         for i in range(K):
-            flush.zero_()                       # L2 flush, outside the events
+            flush_l2()                          # L2 flush, outside the events
             ev[i][0].record()
             g_step.replay()
             ev[i][1].record()
@@ -317,7 +328,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         for i in range(K):
-            flush.zero_()
+            flush_l2()
             g_timed.replay()
             torch.cuda.synchronize()
             for j in range(len(stages)):
@@ -331,7 +342,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         for i in range(K):
-            flush.zero_()
+            flush_l2()
             ev[i][0].record()
             step()
             ev[i][1].record()
@@ -373,7 +384,7 @@ def main():
 
     # expert stand-in, timed on its own (not part of the step)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    flush.zero_()
+    flush_l2()
     e0.record()
     moe.expert_scale(pipe.recv, P, w.E // P, rank * (w.E // P), out=pipe.recv)
     e1.record()
@@ -395,7 +406,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         for i in range(K2):
-            flush.zero_()
+            flush_l2()
             evs[i][0].record()
             pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
                            inputs=staging)
@@ -501,7 +512,7 @@ def main():
                        "k": w.k, "gate": w.kind, "capacity_factor": w.C, "capacity": cap,
                        "a2a": algo if P > 1 else None,
                        "parallelism": "ep%d (experts sharded, tokens data-parallel)" % P,
-                       "l2": "flushed between timed steps (2x L2 memset, outside events)",
+                       "l2": "flushed between timed steps (2x L2 memset + 2x L2 read, outside events)",
                        "expert": "identity in the timed step; s_e stand-in timed separately"},
             "stages_ms": stage_ms, "expert_ms": expert_ms, "min_ms_per_step": float(vals[-2]),
             "eager_ms_per_step": float(vals[-1]),

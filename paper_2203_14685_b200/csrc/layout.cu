@@ -157,6 +157,174 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   if (a.sys_fence) __threadfence_system();
 }
 
+// ------------------------------------------------------------ Layout_Transform, TMA
+// The same contract as k_layout, with the rows moved by the copy engine
+// instead of registers: every warp is an independent pipeline whose lane 0
+// bulk-loads x rows into a ring of NS shared-memory stages
+// (cp.async.bulk global->shared, mbarrier completion; SASS UBLKCP) and
+// bulk-stores each staged row to its <= k destinations (cp.async.bulk
+// shared->global, bulk groups).  A stage is reloaded once the stores issued
+// kTmaLag tasks ago have finished READING it, so NS - kTmaLag loads and
+// kTmaLag store groups are in flight per warp without a single register of
+// payload: bytes in flight per SM are set by shared memory, not by occupancy.
+// Each warp owns one contiguous range of the task list (x rows, then the
+// zero padding rows, which are bulk-stored from a zeroed shared row).  The
+// routing of 32 tasks is fetched at once (lane l: task base + l) and
+// broadcast with shuffles, so lane 0 never waits on an index load.
+constexpr int kTmaWarps = 4;
+constexpr int kTmaThreads = kTmaWarps * 32;
+constexpr int kTmaLag = 2;
+constexpr int kTmaMaxK = 4;  // destinations fetched per lane; larger k reads the rest inline
+
+struct TmaArgs {
+  RowArgs a;
+  int ns;  // stages per warp
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, unsigned src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ char* dst_row(const RowArgs& a, int e, int s) {
+  const int q = e / a.E_local;
+  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+}
+
+__global__ void __launch_bounds__(kTmaThreads) k_layout_tma(TmaArgs ta) {
+  const RowArgs& a = ta.a;
+  const int NS = ta.ns;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ int s_beg[257];
+  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps * 16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned rb = (unsigned)a.row_bytes;
+  char* zero_row = smem;  // [row], then [warps][NS][row] stages
+  char* stages = smem + rb;
+  for (unsigned o = threadIdx.x * 16; o < rb; o += kTmaThreads * 16)
+    *reinterpret_cast<uint4*>(zero_row + o) = make_uint4(0, 0, 0, 0);
+  if (lane == 0)
+    for (int s = 0; s < NS; ++s) mbar_init(smem_u32(&s_bar[warp * 16 + s]), 1);
+  // generic-proxy zeros and barrier inits must be visible to the async proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  pdl_wait();  // routing comes from moe_gate
+  pdl_trigger();
+  pad_prefix(a, s_beg);  // ends with __syncthreads (also publishes the above)
+
+  const long long n_tasks = (long long)a.S + s_beg[a.E];
+  const long long gw = (long long)blockIdx.x * kTmaWarps + warp, GW = (long long)gridDim.x * kTmaWarps;
+  const long long beg = n_tasks * gw / GW, end = n_tasks * (gw + 1) / GW;
+  const long long tok_end = min(end, (long long)a.S);
+  const int ntok = tok_end > beg ? (int)(tok_end - beg) : 0;  // x rows of this warp
+  const unsigned st0 = smem_u32(stages + (size_t)warp * NS * rb);
+  const unsigned bar0 = smem_u32(&s_bar[warp * 16]);
+
+  // prologue: the first NS x rows
+  if (lane == 0)
+    for (int o = 0; o < min(NS, ntok); ++o)
+      bulk_load(st0 + o * rb, a.src + (size_t)(beg + o) * rb, rb, bar0 + 8 * o);
+
+  int ord = 0;  // x-row ordinal of the store cursor
+  for (long long base = beg; base < end; base += 32) {
+    // routing of tasks base .. base+31, one task per lane
+    const long long my = base + lane;
+    char* dst[kTmaMaxK];
+#pragma unroll
+    for (int j = 0; j < kTmaMaxK; ++j) dst[j] = nullptr;
+    if (my < end) {
+      if (my < a.S) {
+        const int t = (int)my;
+#pragma unroll
+        for (int j = 0; j < kTmaMaxK; ++j) {
+          if (j < a.k) {
+            const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
+            if (s >= 0) dst[j] = dst_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
+          }
+        }
+      } else {
+        const int p = (int)(my - a.S);
+        int lo = 0, hi = a.E - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        dst[0] = dst_row(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
+      }
+    }
+    const int cnt = (int)min(32LL, end - base);
+    for (int u = 0; u < cnt; ++u) {
+      char* d[kTmaMaxK];
+#pragma unroll
+      for (int j = 0; j < kTmaMaxK; ++j)
+        d[j] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst[j]), u));
+      if (lane == 0) {
+        const long long task = base + u;
+        if (task < a.S) {
+          const int st = ord % NS;
+          mbar_wait(bar0 + 8 * st, (unsigned)(ord / NS) & 1u);
+          const unsigned src = st0 + st * rb;
+#pragma unroll
+          for (int j = 0; j < kTmaMaxK; ++j)
+            if (d[j]) bulk_store(d[j], src, rb);
+          for (int j = kTmaMaxK; j < a.k; ++j) {  // k > kTmaMaxK (rare)
+            const int t = (int)task;
+            const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
+            if (s >= 0) bulk_store(dst_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s), src, rb);
+          }
+          bulk_commit();
+          // the stage of ordinal ord - kTmaLag is free once its stores have read it
+          const int o2 = ord - kTmaLag;
+          if (o2 >= 0 && o2 + NS < ntok) {
+            bulk_wait_read<kTmaLag>();
+            const int st2 = o2 % NS;
+            bulk_load(st0 + st2 * rb, a.src + (size_t)(beg + o2 + NS) * rb, rb, bar0 + 8 * st2);
+          }
+          ++ord;
+        } else {
+          bulk_store(d[0], smem_u32(zero_row), rb);
+          bulk_commit();
+        }
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  if (a.sys_fence) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();
+  }
+}
+
 // ------------------------------------------------------------ Reverse + combine
 struct F32Acc {
   static constexpr int kPerVec = 8;  // fp32 per 32 bytes
@@ -246,6 +414,61 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
       for (int u = 0; u < U; ++u) {
         const int off = seg + (lane + 32 * u) * VB;
         if (off < a.row_bytes) st_v8(yrow + off, pack_vec<DT>(acc[u]));
+      }
+    }
+  }
+}
+
+// k <= 2 specialisation: every load of a U-vector segment of the KK rows is
+// issued before the first FMA (KK*U*32 bytes in flight per lane), and each
+// output vector is finished and stored straight away, so the accumulators
+// cost 16 registers instead of U*16.  For k = 1 (Switch), U = 4 moves a whole
+// 4 KiB row per warp per round.  Same arithmetic order as k_reverse: fp32
+// FMA from 0 in ascending j, one RNE store.
+template <int DT, int KK, int U>
+__global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
+  constexpr int VB = 32;
+  constexpr int NA = DT == MOE_F32 ? 8 : 16;
+  constexpr int SEG = 32 * U * VB;
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * kRowWarps;
+  pdl_wait();
+  pdl_trigger();
+  for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
+    char* yrow = a.dst + (size_t)t * a.row_bytes;
+    const char* b[KK];
+    float w[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      const int s = __ldg(a.slot_idx + (size_t)t * KK + j);
+      b[j] = nullptr;
+      w[j] = 0.f;
+      if (s >= 0) {
+        b[j] = src_row(a, __ldg(a.expert_idx + (size_t)t * KK + j), s);
+        w[j] = __ldg(a.weight + (size_t)t * KK + j);
+      }
+    }
+    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
+      V8 r[KK][U];
+#pragma unroll
+      for (int j = 0; j < KK; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (b[j] && off < a.row_bytes) r[j][u] = ld_stream_v8(b[j] + off);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int off = seg + (lane + 32 * u) * VB;
+        if (off < a.row_bytes) {
+          float acc[NA];
+#pragma unroll
+          for (int q = 0; q < NA; ++q) acc[q] = 0.f;
+#pragma unroll
+          for (int j = 0; j < KK; ++j)
+            if (b[j]) fma_vec<DT>(acc, w[j], r[j][u]);
+          st_v8(yrow + off, pack_vec<DT>(acc));
+        }
       }
     }
   }
@@ -369,6 +592,26 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.E_local = E_local;
   a.rank = rank;
   a.sys_fence = E_local != d.E;
+  // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
+  // ~100 KB per-CTA budget (two CTAs per SM)
+  const int tma_env = env_int(a.sys_fence ? "MOE_P2P_LAYOUT_TMA" : "MOE_LAYOUT_TMA", 0);
+  const int budget = env_int("MOE_LAYOUT_TMA_SMEM", 100 * 1024);
+  const int ns = std::min(16, (budget - a.row_bytes) / (kTmaWarps * std::max(1, a.row_bytes)));
+  if (tma_env && a.row_bytes % 16 == 0 && ns >= 2) {
+    TmaArgs ta{a, ns};
+    const size_t smem = (size_t)a.row_bytes * (1 + kTmaWarps * ns);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_layout_tma,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "moe_layout: smem attribute");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_layout_tma, kTmaThreads, smem);
+    const int occ = env_int("MOE_LAYOUT_CTAS_PER_SM", 0);
+    const int grid = (occ > 0 ? occ : std::max(1, per_sm)) * device_sm_count();
+    void* args[] = {&ta};
+    e = launch_pdl((const void*)k_layout_tma, dim3(grid), dim3(kTmaThreads), smem, stream, args);
+    if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout_tma launch");
+    return MOE_OK;
+  }
   const void* kern;
   if (a.row_bytes % 32 == 0)
     kern = env_int("MOE_LAYOUT_U", 4) == 2 ? (const void*)k_layout<32, 2> : (const void*)k_layout<32, 4>;
@@ -408,7 +651,17 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   a.rank = rank;
   const void* kern;
   const int U = env_int("MOE_REVERSE_U", 1);
-  if (a.row_bytes % 32 == 0) {
+  const int KU = env_int("MOE_REVERSE_KU", 4);  // k <= 2 path: vectors per lane per round (x k rows)
+  const bool kspec = env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
+  if (kspec) {
+    const bool f = dtype == MOE_F32;
+    if (a.k == 1)
+      kern = KU >= 4 ? (f ? (const void*)k_reverse_k<MOE_F32, 1, 4> : (const void*)k_reverse_k<MOE_BF16, 1, 4>)
+                     : (f ? (const void*)k_reverse_k<MOE_F32, 1, 2> : (const void*)k_reverse_k<MOE_BF16, 1, 2>);
+    else
+      kern = KU >= 4 ? (f ? (const void*)k_reverse_k<MOE_F32, 2, 2> : (const void*)k_reverse_k<MOE_BF16, 2, 2>)
+                     : (f ? (const void*)k_reverse_k<MOE_F32, 2, 1> : (const void*)k_reverse_k<MOE_BF16, 2, 1>);
+  } else if (a.row_bytes % 32 == 0) {
     if (U == 1)
       kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
     else
