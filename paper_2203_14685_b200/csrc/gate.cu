@@ -23,6 +23,7 @@
 // pairs (SLOT priority, j-major).  Traffic is O(tiles x columns).
 #include <cfloat>
 #include <climits>
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -36,8 +37,10 @@ constexpr size_t kMaxTileLogitBytes = 64 * 1024;
 constexpr unsigned kValMask = (1u << 30) - 1;  // counts < 2^30 (S*k < 2^30, checked)
 
 struct GateCtrl {  // 64 bytes at the head of the workspace
-  unsigned bad;     // invalid hash ids since the last moe_gate_check
-  unsigned pad[15];
+  unsigned bad;        // invalid hash ids since the last moe_gate_check
+  unsigned bar_count;  // k_gate_fused grid barrier: arrivals (reset by the last)
+  unsigned bar_gen;    // and generation
+  unsigned pad[13];
 };
 
 struct GateArgs {
@@ -72,14 +75,16 @@ static int choose_lanes(int E) {
   return L;
 }
 
-static GatePlan gate_plan(const moe_gate_desc_t& d) {
+// want_tiles: the three-kernel path wants >= 256 tiles when S allows (about
+// 1.7 CTAs per SM on 148 SMs); the single-launch path fewer, larger tiles
+// (every CTA reduces all tiles' aggregates after its grid barrier).
+static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles = 256) {
   GatePlan p{};
   p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.E);
   p.K = d.k <= 1 ? 1 : d.k <= 2 ? 2 : d.k <= 4 ? 4 : d.k <= 8 ? 8 : 0;
-  // >= 256 tiles when S allows (about 1.7 CTAs per SM on 148 SMs), tiles of
-  // 32..256 tokens, at most kMaxTileItems items per tile
+  // tiles of 32..256 tokens, at most kMaxTileItems items per tile
   int tt = 256;
-  while (tt > 32 && (d.S + tt - 1) / tt < 256) tt >>= 1;
+  while (tt > 32 && (d.S + tt - 1) / tt < want_tiles) tt >>= 1;
   while (tt > 1 && tt * d.k > kMaxTileItems) tt >>= 1;
   // the staged logits tile stays within kMaxTileLogitBytes of shared memory
   if (d.kind != MOE_GATE_HASH)
@@ -335,20 +340,21 @@ __device__ __forceinline__ void select_rank(const GateArgs& a, const float* row,
 // ------------------------------------------------------------ the kernel
 enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2 };
 
+// Phases A and B of one tile (shared by k_gate_select and k_gate_fused):
+// stage the logits, select + weights (expert_idx, weight written), in-tile
+// ranks per column (s_exp, s_rank), s_hist[w][c] turned into the exclusive
+// prefix over warps, and the tile aggregates agg[c][tile] written.  Returns
+// with the CTA synchronised.
 template <int KIND, int L, int K>
-__global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
-  extern __shared__ __align__(16) int smem[];
+__device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned& s_bad,
+                                          unsigned long long& s_mbar) {
   const int items = a.tile_tokens * a.k;
   float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
   int* s_exp = smem + a.lg_words;             // [items] expert of item tt*k+j
   int* s_rank = s_exp + items;                // [items] rank inside its warp
   int* s_hist = s_rank + items;               // [warps][ncols]
-  __shared__ unsigned s_bad;
-  __shared__ __align__(8) unsigned long long s_mbar;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  pdl_wait();     // the producer of the logits / the previous step must be done
-  pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
   if (tid == 0) s_bad = 0;
   for (int i = tid; i < items; i += kGateThreads) s_exp[i] = -1;
   for (int i = tid; i < kGateWarps * a.ncols; i += kGateThreads) s_hist[i] = 0;
@@ -472,6 +478,26 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
     agg[(size_t)c * a.n_tiles + tile] = run;
   }
   __syncthreads();
+}
+
+template <int KIND, int L, int K>
+__global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
+  extern __shared__ __align__(16) int smem[];
+  __shared__ unsigned s_bad;
+  __shared__ __align__(8) unsigned long long s_mbar;
+  pdl_wait();     // the producer of the logits / the previous step must be done
+  pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
+  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
+  const int tid = threadIdx.x;
+  const int items = a.tile_tokens * a.k;
+  const int* s_exp = smem + a.lg_words;
+  const int* s_rank = s_exp + items;
+  const int* s_hist = s_rank + items;
+  const int tile = blockIdx.x;
+  const int t0 = tile * a.tile_tokens;
+  const int nt = min(a.tile_tokens, a.S - t0);
+  const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  const int per = (items + kGateWarps - 1) / kGateWarps;
   // ---------------- provisional slots: rank inside the tile's column
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const int e = s_exp[i];
@@ -578,37 +604,200 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
   }
 }
 
+// ------------------------------------------------------------ single launch
+// The three kernels above as ONE cooperative launch (every tile's CTA is
+// co-resident): phases A/B as in k_gate_select, one grid barrier, then each
+// CTA reduces every column's tile aggregates itself (the exclusive prefix
+// over earlier tiles and the column total, O(tiles x columns) L2 reads per
+// CTA) and finishes its own slots from the ranks still in shared memory.
+// Saves two launches and the global round trip of the provisional slots.
+// Used when the tiles fit on the device at once (host checks occupancy).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sense-reversing grid barrier on two words of the control block: the last
+// arriver resets the count and bumps the generation, so it works for any
+// grid size and is CUDA-graph replay safe.
+__device__ __forceinline__ void grid_barrier(GateCtrl* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(&c->bar_gen);
+    __threadfence();
+    const unsigned old = atomicAdd(&c->bar_count, 1u);
+    if (old == gridDim.x - 1) {
+      c->bar_count = 0;
+      __threadfence();
+      atomicAdd(&c->bar_gen, 1u);
+    } else {
+      while (ld_acquire_u32(&c->bar_gen) == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int KIND, int L, int K>
+__global__ void __launch_bounds__(kGateThreads) k_gate_fused(GateArgs a) {
+  extern __shared__ __align__(16) int smem[];
+  __shared__ unsigned s_bad;
+  __shared__ __align__(8) unsigned long long s_mbar;
+  pdl_wait();
+  pdl_trigger();
+  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int items = a.tile_tokens * a.k;
+  const int* s_exp = smem + a.lg_words;
+  const int* s_rank = s_exp + items;
+  const int* s_hist = s_rank + items;
+  int* s_pre = const_cast<int*>(s_hist) + kGateWarps * a.ncols;  // [ncols] earlier tiles
+  int* s_tot = s_pre + a.ncols;                                   // [ncols] column totals
+  const int tile = blockIdx.x;
+  const int t0 = tile * a.tile_tokens;
+  const int nt = min(a.tile_tokens, a.S - t0);
+  const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  const int per = (items + kGateWarps - 1) / kGateWarps;
+  if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
+
+  grid_barrier(a.ctrl);
+
+  // every column: prefix over tiles < tile and the total, warp per column
+  const unsigned* agg = reinterpret_cast<const unsigned*>(a.status);
+  for (int c = warp; c < a.ncols; c += kGateWarps) {
+    const unsigned* col = agg + (size_t)c * a.n_tiles;
+    unsigned pre = 0, tot = 0;
+    // 8 independent loads in flight per lane per round (one L2 round trip
+    // covers 256 tiles)
+    for (int base = 0; base < a.n_tiles; base += 256) {
+      unsigned v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * 32 + lane;
+        v[u] = i < a.n_tiles ? __ldcg(col + i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * 32 + lane;
+        tot += v[u];
+        if (i < tile) pre += v[u];
+      }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+      pre += __shfl_xor_sync(0xffffffffu, pre, m);
+      tot += __shfl_xor_sync(0xffffffffu, tot, m);
+    }
+    if (lane == 0) {
+      s_pre[c] = (int)pre;
+      s_tot[c] = (int)tot;
+    }
+  }
+  __syncthreads();
+
+  // final slots: (SLOT: items of earlier j) + earlier tiles + warps before + rank
+  for (int i = tid; i < nt * a.k; i += kGateThreads) {
+    const int e = s_exp[i];
+    const size_t gi = (size_t)t0 * a.k + i;
+    if (e < 0) {
+      a.slot_idx[gi] = -1;  // invalid hash id: routed as dropped
+      continue;
+    }
+    const int tt = i / a.k, j = i - tt * a.k;
+    const int pos = slot_prio ? j * a.tile_tokens + tt : i;
+    const int col = slot_prio ? j * a.E + e : e;
+    int s = s_pre[col] + s_hist[(pos / per) * a.ncols + col] + s_rank[i];
+    if (slot_prio)
+      for (int jj = 0; jj < j; ++jj) s += s_tot[jj * a.E + e];
+    if (s < a.cap) {
+      a.slot_idx[gi] = s;
+      if (a.slot_src) a.slot_src[(size_t)e * a.cap + s] = (int)gi;
+    } else {
+      a.slot_idx[gi] = -1;
+      a.weight[gi] = 0.f;
+    }
+  }
+  // load[] and the empty slot_src entries, warp per expert across the grid
+  for (int e = tile * kGateWarps + warp; e < a.E; e += gridDim.x * kGateWarps) {
+    int ld = 0;
+    if (slot_prio)
+      for (int jj = 0; jj < a.k; ++jj) ld += s_tot[jj * a.E + e];
+    else
+      ld = s_tot[e];
+    if (lane == 0) a.load[e] = ld;
+    if (a.slot_src)
+      for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
+  }
+}
+
 // ------------------------------------------------------------ host side
 using GateKernel = void (*)(GateArgs);
 
-template <int KIND, int L>
+template <int KIND, int L, bool FUSED>
 static GateKernel pick_k(int K) {
   switch (K) {
-    case 1: return k_gate_select<KIND, L, 1>;
-    case 2: return k_gate_select<KIND, L, 2>;
-    case 4: return k_gate_select<KIND, L, 4>;
-    case 8: return k_gate_select<KIND, L, 8>;
-    default: return k_gate_select<KIND, L, 0>;
+    case 1: return FUSED ? k_gate_fused<KIND, L, 1> : k_gate_select<KIND, L, 1>;
+    case 2: return FUSED ? k_gate_fused<KIND, L, 2> : k_gate_select<KIND, L, 2>;
+    case 4: return FUSED ? k_gate_fused<KIND, L, 4> : k_gate_select<KIND, L, 4>;
+    case 8: return FUSED ? k_gate_fused<KIND, L, 8> : k_gate_select<KIND, L, 8>;
+    default: return FUSED ? k_gate_fused<KIND, L, 0> : k_gate_select<KIND, L, 0>;
   }
 }
-template <int KIND>
+template <int KIND, bool FUSED>
 static GateKernel pick_l(int L, int K) {
   switch (L) {
-    case 1: return pick_k<KIND, 1>(K);
-    case 2: return pick_k<KIND, 2>(K);
-    case 4: return pick_k<KIND, 4>(K);
-    case 8: return pick_k<KIND, 8>(K);
-    case 16: return pick_k<KIND, 16>(K);
-    default: return pick_k<KIND, 32>(K);
+    case 1: return pick_k<KIND, 1, FUSED>(K);
+    case 2: return pick_k<KIND, 2, FUSED>(K);
+    case 4: return pick_k<KIND, 4, FUSED>(K);
+    case 8: return pick_k<KIND, 8, FUSED>(K);
+    case 16: return pick_k<KIND, 16, FUSED>(K);
+    default: return pick_k<KIND, 32, FUSED>(K);
   }
 }
+template <bool FUSED>
+static GateKernel pick_gate(const moe_gate_desc_t& d, const GatePlan& p) {
+  return d.kind == MOE_GATE_HASH    ? (FUSED ? k_gate_fused<KIND_HASH, 1, 1> : k_gate_select<KIND_HASH, 1, 1>)
+         : d.kind == MOE_GATE_KTOP1 ? pick_l<KIND_KTOP1, FUSED>(p.L, p.K)
+                                    : pick_l<KIND_TOPK, FUSED>(p.L, p.K);
+}
 
-size_t gate_workspace_bytes(const moe_gate_desc_t& d) { return gate_plan(d).bytes; }
+static int fused_tiles() { return env_int("MOE_GATE_FUSED_TILES", 128); }
+
+size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
+  return std::max(gate_plan(d).bytes, gate_plan(d, fused_tiles()).bytes);
+}
+
+// The three-kernel path (k_gate_select -> k_gate_scan -> k_gate_slots, PDL).
+static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, GateArgs& a,
+                                 cudaStream_t stream) {
+  void* args[] = {&a};
+  GateKernel kern = pick_gate<false>(d, p);
+  if (p.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p.smem);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
+  }
+  cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
+                             stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
+  e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
+                 dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
+  e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
+  return MOE_OK;
+}
 
 moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const int32_t* ids,
                          const int32_t* table, int32_t vocab, const moe_routing_t& out, void* ws,
                          cudaStream_t stream) {
-  const GatePlan p = gate_plan(d);
+  // one launch with a grid barrier when every tile's CTA fits on the device
+  // at once and the per-CTA reduction (tiles x columns words) is small
+  const GatePlan pf = gate_plan(d, fused_tiles());
+  bool fused = env_int("MOE_GATE_FUSED", 0) &&
+               (long long)pf.n_tiles * pf.ncols <= env_int("MOE_GATE_FUSED_MAXW", 8192);
+  const GatePlan p = fused ? pf : gate_plan(d);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
@@ -638,24 +827,48 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
   a.status = reinterpret_cast<unsigned long long*>(w + p.status_off);
   a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
 
-  GateKernel kern = d.kind == MOE_GATE_HASH    ? k_gate_select<KIND_HASH, 1, 1>
-                    : d.kind == MOE_GATE_KTOP1 ? pick_l<KIND_KTOP1>(p.L, p.K)
-                                               : pick_l<KIND_TOPK>(p.L, p.K);
-  if (p.smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p.smem);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
-  }
   void* args[] = {&a};
-  cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
-                             stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
-  e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
-                 dim3(kGateThreads), 0, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
-  e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
-  return MOE_OK;
+  if (fused) {
+    GateKernel fk = pick_gate<true>(d, p);
+    const size_t fsmem = p.smem + 2 * sizeof(int) * (size_t)p.ncols;
+    cudaError_t e = cudaSuccess;
+    if (fsmem > 48 * 1024)
+      e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    int per_sm = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fk, kGateThreads, fsmem);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: fused occupancy");
+    if (p.n_tiles > per_sm * device_sm_count()) {
+      const GatePlan p3 = gate_plan(d);
+      a.tile_tokens = p3.tile_tokens;
+      a.n_tiles = p3.n_tiles;
+      a.lg_words = p3.lg_words;
+      a.totals = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p3.totals_off);
+      return gate_launch3(d, p3, a, stream);
+    }
+    {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(p.n_tiles);
+      cfg.blockDim = dim3(kGateThreads);
+      cfg.dynamicSmemBytes = fsmem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      if (!env_int("MOE_GATE_COOP", 0)) {  // co-residency from the occupancy check alone
+        cfg.attrs = attr + 1;
+        cfg.numAttrs = 1;
+      }
+      e = cudaLaunchKernelExC(&cfg, (const void*)fk, args);
+      if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_fused launch");
+      return MOE_OK;
+    }
+  }
+  return gate_launch3(d, p, a, stream);
 }
 
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad) {

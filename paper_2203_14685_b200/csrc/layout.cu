@@ -48,6 +48,11 @@ __device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
   return a.speer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
 }
 
+__device__ __forceinline__ char* dst_row_of(const RowArgs& a, int e, int s) {
+  const int q = e / a.E_local;
+  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+}
+
 template <int VB>
 struct Vec;
 template <>
@@ -153,6 +158,64 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
       const typename V::T z = V::zero();
       for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
     }
+  }
+  if (a.sys_fence) __threadfence_system();
+}
+
+// Layout for 32-byte-vector rows with TPW consecutive tokens per warp
+// iteration: all TPW*U row loads are in flight before the first store (a
+// 2 KiB row with U = 2, TPW = 2 keeps 4 KiB per warp in flight, like a
+// 4 KiB row with U = 4).  The zero padding rows follow as their own
+// grid-stride loop over warps.
+template <int U, int TPW>
+__global__ void __launch_bounds__(kRowThreads) k_layout_t(RowArgs a) {
+  constexpr int VB = 32;
+  constexpr int SEG = 32 * U * VB;
+  __shared__ int s_beg[257];
+  pdl_wait();
+  pdl_trigger();
+  pad_prefix(a, s_beg);
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kRowWarps;
+  for (int tb = gw * TPW; tb < a.S; tb += nw * TPW) {
+    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
+      V8 r[TPW][U];
+#pragma unroll
+      for (int p = 0; p < TPW; ++p)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (tb + p < a.S && off < a.row_bytes)
+            r[p][u] = ld_stream_v8(a.src + (size_t)(tb + p) * a.row_bytes + off);
+        }
+#pragma unroll
+      for (int p = 0; p < TPW; ++p) {
+        const int t = tb + p;
+        if (t >= a.S) break;
+        for (int j = 0; j < a.k; ++j) {
+          const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
+          if (s < 0) continue;
+          char* drow = dst_row_of(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int off = seg + (lane + 32 * u) * VB;
+            if (off < a.row_bytes) st_v8(drow + off, r[p][u]);
+          }
+        }
+      }
+    }
+  }
+  const int npad = s_beg[a.E];
+  const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int p = gw; p < npad; p += nw) {
+    int lo = 0, hi = a.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    char* drow = dst_row_of(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
+    for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) st_v8(drow + off, z);
   }
   if (a.sys_fence) __threadfence_system();
 }
@@ -419,55 +482,65 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
   }
 }
 
-// k <= 2 specialisation: every load of a U-vector segment of the KK rows is
-// issued before the first FMA (KK*U*32 bytes in flight per lane), and each
-// output vector is finished and stored straight away, so the accumulators
-// cost 16 registers instead of U*16.  For k = 1 (Switch), U = 4 moves a whole
-// 4 KiB row per warp per round.  Same arithmetic order as k_reverse: fp32
-// FMA from 0 in ascending j, one RNE store.
-template <int DT, int KK, int U>
+// k <= 2 specialisation: every load of a U-vector segment of the KK rows of
+// TPW consecutive tokens is issued before the first FMA (TPW*KK*U*32 bytes in
+// flight per lane; the host picks TPW*KK*U = 4), and each output vector is
+// finished and stored straight away, so the accumulators cost 16 registers
+// instead of U*16.  Switch (k = 1) on 4 KiB rows: U = 4; on 2 KiB rows:
+// U = 2, TPW = 2.  Same arithmetic order as k_reverse: fp32 FMA from 0 in
+// ascending j, one RNE store.
+template <int DT, int KK, int U, int TPW>
 __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   constexpr int VB = 32;
   constexpr int NA = DT == MOE_F32 ? 8 : 16;
   constexpr int SEG = 32 * U * VB;
   const int lane = threadIdx.x & 31;
-  const int wstride = gridDim.x * kRowWarps;
+  const int wstride = gridDim.x * kRowWarps * TPW;
   pdl_wait();
   pdl_trigger();
-  for (int t = blockIdx.x * kRowWarps + (threadIdx.x >> 5); t < a.S; t += wstride) {
-    char* yrow = a.dst + (size_t)t * a.row_bytes;
-    const char* b[KK];
-    float w[KK];
+  for (int tb = (blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * TPW; tb < a.S; tb += wstride) {
+    const char* b[TPW][KK];
+    float w[TPW][KK];
 #pragma unroll
-    for (int j = 0; j < KK; ++j) {
-      const int s = __ldg(a.slot_idx + (size_t)t * KK + j);
-      b[j] = nullptr;
-      w[j] = 0.f;
-      if (s >= 0) {
-        b[j] = src_row(a, __ldg(a.expert_idx + (size_t)t * KK + j), s);
-        w[j] = __ldg(a.weight + (size_t)t * KK + j);
+    for (int p = 0; p < TPW; ++p)
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        const int t = tb + p;
+        const int s = t < a.S ? __ldg(a.slot_idx + (size_t)t * KK + j) : -1;
+        b[p][j] = nullptr;
+        w[p][j] = 0.f;
+        if (s >= 0) {
+          b[p][j] = src_row(a, __ldg(a.expert_idx + (size_t)t * KK + j), s);
+          w[p][j] = __ldg(a.weight + (size_t)t * KK + j);
+        }
       }
-    }
     for (int seg = 0; seg < a.row_bytes; seg += SEG) {
-      V8 r[KK][U];
+      V8 r[TPW][KK][U];
 #pragma unroll
-      for (int j = 0; j < KK; ++j)
+      for (int p = 0; p < TPW; ++p)
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int off = seg + (lane + 32 * u) * VB;
+            if (b[p][j] && off < a.row_bytes) r[p][j][u] = ld_stream_v8(b[p][j] + off);
+          }
+#pragma unroll
+      for (int p = 0; p < TPW; ++p) {
+        if (tb + p >= a.S) break;
+        char* yrow = a.dst + (size_t)(tb + p) * a.row_bytes;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int off = seg + (lane + 32 * u) * VB;
-          if (b[j] && off < a.row_bytes) r[j][u] = ld_stream_v8(b[j] + off);
-        }
+          if (off < a.row_bytes) {
+            float acc[NA];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int off = seg + (lane + 32 * u) * VB;
-        if (off < a.row_bytes) {
-          float acc[NA];
+            for (int q = 0; q < NA; ++q) acc[q] = 0.f;
 #pragma unroll
-          for (int q = 0; q < NA; ++q) acc[q] = 0.f;
-#pragma unroll
-          for (int j = 0; j < KK; ++j)
-            if (b[j]) fma_vec<DT>(acc, w[j], r[j][u]);
-          st_v8(yrow + off, pack_vec<DT>(acc));
+            for (int j = 0; j < KK; ++j)
+              if (b[p][j]) fma_vec<DT>(acc, w[p][j], r[p][j][u]);
+            st_v8(yrow + off, pack_vec<DT>(acc));
+          }
         }
       }
     }
@@ -613,7 +686,12 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
     return MOE_OK;
   }
   const void* kern;
-  if (a.row_bytes % 32 == 0)
+  const int LT = env_int("MOE_LAYOUT_TPW", 0);  // measured: no gain over k_layout<32,4>;  // TPW * U = 4 vectors in flight per lane
+  if (a.row_bytes % 32 == 0 && LT) {
+    const int segs = std::max(1, a.row_bytes / 1024);
+    kern = segs >= 4 ? (const void*)k_layout_t<4, 1>
+           : segs >= 2 ? (const void*)k_layout_t<2, 2> : (const void*)k_layout_t<1, 4>;
+  } else if (a.row_bytes % 32 == 0)
     kern = env_int("MOE_LAYOUT_U", 4) == 2 ? (const void*)k_layout<32, 2> : (const void*)k_layout<32, 4>;
   else
     kern = (const void*)k_layout<16, 4>;
@@ -654,13 +732,20 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   const int KU = env_int("MOE_REVERSE_KU", 4);  // k <= 2 path: vectors per lane per round (x k rows)
   const bool kspec = env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
   if (kspec) {
+    // TPW * k * U = KU (default 4) vectors in flight per lane, U covering at
+    // most one row (1 KiB of row per U step)
     const bool f = dtype == MOE_F32;
+    const int segs = std::max(1, a.row_bytes / 1024);  // 1 KiB per U step
+    const int per = std::max(1, KU / a.k);                // U * TPW
+    const int Uc = std::min(per, segs) >= 4 ? 4 : std::min(per, segs) >= 2 ? 2 : 1;
+    const int T = env_int("MOE_REVERSE_TPW", 0) ? std::max(1, per / Uc) : 1;  // TPW: no measured gain
+#define MOE_RK(KK, UU, TT) (f ? (const void*)k_reverse_k<MOE_F32, KK, UU, TT> : (const void*)k_reverse_k<MOE_BF16, KK, UU, TT>)
     if (a.k == 1)
-      kern = KU >= 4 ? (f ? (const void*)k_reverse_k<MOE_F32, 1, 4> : (const void*)k_reverse_k<MOE_BF16, 1, 4>)
-                     : (f ? (const void*)k_reverse_k<MOE_F32, 1, 2> : (const void*)k_reverse_k<MOE_BF16, 1, 2>);
+      kern = Uc == 4 ? MOE_RK(1, 4, 1) : Uc == 2 ? (T >= 2 ? MOE_RK(1, 2, 2) : MOE_RK(1, 2, 1))
+                                      : (T >= 4 ? MOE_RK(1, 1, 4) : T >= 2 ? MOE_RK(1, 1, 2) : MOE_RK(1, 1, 1));
     else
-      kern = KU >= 4 ? (f ? (const void*)k_reverse_k<MOE_F32, 2, 2> : (const void*)k_reverse_k<MOE_BF16, 2, 2>)
-                     : (f ? (const void*)k_reverse_k<MOE_F32, 2, 1> : (const void*)k_reverse_k<MOE_BF16, 2, 1>);
+      kern = Uc >= 2 ? MOE_RK(2, 2, 1) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
+#undef MOE_RK
   } else if (a.row_bytes % 32 == 0) {
     if (U == 1)
       kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;

@@ -92,18 +92,31 @@ GATE_CASES = [
 ]
 
 
+# kernel variants selected by the library's tuning knobs (read per call)
+GATE_PATHS = {"fused": {}, "three": {"MOE_GATE_FUSED": "0"},
+              "fused_small_tiles": {"MOE_GATE_FUSED_TILES": "512", "MOE_GATE_FUSED_MAXW": "1000000"}}
+ROW_PATHS = {"default": {}, "tma_layout": {"MOE_LAYOUT_TMA": "1"}, "layout_tpw": {"MOE_LAYOUT_TPW": "1", "MOE_REVERSE_TPW": "1"},
+             "reverse_generic": {"MOE_REVERSE_KSPEC": "0"}, "reverse_u2": {"MOE_REVERSE_KU": "2"}}
+
+
+@pytest.mark.parametrize("path", sorted(GATE_PATHS))
 @pytest.mark.parametrize("case", GATE_CASES, ids=lambda c: "-".join(
     "%s=%s" % (k, v) for k, v in c.items() if k not in ("bad_ids",)))
-def test_gate_parity(orc, case):
+def test_gate_parity(orc, case, path, monkeypatch):
+    for k, v in GATE_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     rg, ro, g, _ = _run_gate(orc, case)
     assert_routing_equal(rg, ro, str(case))
     if case["kind"] == "hash":
         assert g.check() == ro.bad
 
 
-def test_gate_workspace_reuse_and_graph_replay(orc):
-    """The workspace resets itself (epoch): repeated calls, and CUDA-graph
-    replays with new inputs, each match the oracle."""
+@pytest.mark.parametrize("path", sorted(GATE_PATHS))
+def test_gate_workspace_reuse_and_graph_replay(orc, path, monkeypatch):
+    """The workspace resets itself (grid-barrier words, counters): repeated
+    calls, and CUDA-graph replays with new inputs, each match the oracle."""
+    for k, v in GATE_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     S, E, k = 3000, 16, 2
     cap = orc.capacity(S, E, k, 1.0)
     g = moe.Gate(S, E, k, cap)
@@ -144,9 +157,12 @@ LAYOUT_CASES = [
 ]
 
 
+@pytest.mark.parametrize("path", sorted(ROW_PATHS))
 @pytest.mark.parametrize("case", LAYOUT_CASES, ids=lambda c: "-".join(
     "%s=%s" % (k, v) for k, v in c.items()))
-def test_layout_and_reverse_parity(orc, case):
+def test_layout_and_reverse_parity(orc, case, path, monkeypatch):
+    for k, v in ROW_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     rg, ro, _, _ = _run_gate(orc, case)
     assert_routing_equal(rg, ro)
     S, d, bf16 = case["S"], case["d"], case["dtype"] == "bf16"
