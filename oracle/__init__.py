@@ -83,6 +83,13 @@ def lib():
         L.orc_alltoall_hier.restype = ctypes.c_int
         L.orc_alltoall_flat_stats.argtypes = [i32, i32, i64, ctypes.POINTER(_Stats)]
         L.orc_alltoall_flat_stats.restype = None
+        L.orc_reverse_layout_bwd.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P, P,
+                                             P, P, P, P]
+        L.orc_reverse_layout_bwd.restype = None
+        L.orc_layout_bwd.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P, P, P]
+        L.orc_layout_bwd.restype = None
+        L.orc_gate_bwd.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, P, P, P, P, P]
+        L.orc_gate_bwd.restype = ctypes.c_int
         L.orc_bf16_to_f64.argtypes = [ctypes.c_uint16]
         L.orc_bf16_to_f64.restype = ctypes.c_double
         L.orc_f64_to_bf16.argtypes = [ctypes.c_double]
@@ -177,6 +184,46 @@ def expert_scale(buf: np.ndarray, e_base: int) -> np.ndarray:
     nsrc, El, cap, d = buf.shape
     out = np.empty_like(buf)
     lib().orc_expert_scale(_dt(buf), nsrc, El, e_base, cap, d, _ptr(buf), _ptr(out))
+    return out
+
+
+def reverse_layout_bwd(dy: np.ndarray, back: np.ndarray, r: Routing):
+    """Adjoint of the combine: (d_back [E,cap,d], d_weight [S,k] float32)."""
+    dy = np.ascontiguousarray(dy)
+    back = np.ascontiguousarray(back)
+    E, cap, d = back.shape
+    assert E == r.E and cap == r.cap and dy.shape == (r.S, d) and dy.dtype == back.dtype
+    d_back = np.empty_like(back)
+    d_w = np.empty((r.S, r.k), np.float32)
+    lib().orc_reverse_layout_bwd(_dt(back), r.S, r.E, r.k, r.cap, d, _ptr(r.expert_idx),
+                                 _ptr(r.slot_idx), _ptr(r.weight), _ptr(dy), _ptr(back),
+                                 _ptr(d_back), _ptr(d_w))
+    return d_back, d_w
+
+
+def layout_bwd(d_dispatch: np.ndarray, r: Routing) -> np.ndarray:
+    """Adjoint of Layout_Transform: [E,cap,d] -> dx [S,d]."""
+    g = np.ascontiguousarray(d_dispatch)
+    E, cap, d = g.shape
+    assert E == r.E and cap == r.cap
+    dx = np.empty((r.S, d), g.dtype)
+    lib().orc_layout_bwd(_dt(g), r.S, r.E, r.k, r.cap, d, _ptr(r.expert_idx), _ptr(r.slot_idx),
+                         _ptr(g), _ptr(dx))
+    return dx
+
+
+def gate_bwd(logits: np.ndarray, r: Routing, d_weight: np.ndarray, *, kind="topk",
+             weight_mode="renorm") -> np.ndarray:
+    """Adjoint of Eq. 1's weights w.r.t. the logits (selection fixed)."""
+    logits = _c(logits, np.float32)
+    d_weight = _c(d_weight, np.float32)
+    S, E = logits.shape
+    assert d_weight.shape == (S, r.k)
+    out = np.empty((S, E), np.float32)
+    rc = lib().orc_gate_bwd(KINDS[kind], MODES[weight_mode], S, E, r.k, _ptr(logits),
+                            _ptr(r.expert_idx), _ptr(r.slot_idx), _ptr(d_weight), _ptr(out))
+    if rc != 0:
+        raise ValueError("orc_gate_bwd rejected its arguments")
     return out
 
 

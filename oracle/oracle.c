@@ -353,3 +353,109 @@ int orc_alltoall_hier(int32_t P, int32_t G, int64_t bytes_per_peer,
   if (st) *st = s;
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Backward of the routing path.       */
+/* ------------------------------------------------------------------------ */
+
+/* Adjoint of the combine y_i += w_(i,idx) * e_idx(x_i). */
+void orc_reverse_layout_bwd(int dtype, int32_t S, int32_t E, int32_t k, int32_t cap,
+                            int32_t d, const int32_t* expert_idx,
+                            const int32_t* slot_idx, const float* weight,
+                            const void* dy, const void* back, void* d_back,
+                            float* d_weight) {
+  /* every slot starts at 0: empty slots and padding get no gradient */
+  for (int64_t i = 0; i < (int64_t)E * cap * d; ++i) store_elem(dtype, d_back, i, 0.0);
+  for (int32_t t = 0; t < S; ++t)
+    for (int32_t j = 0; j < k; ++j) {
+      int64_t i = (int64_t)t * k + j;
+      if (slot_idx[i] < 0) { d_weight[i] = 0.0f; continue; }
+      int64_t row = (int64_t)expert_idx[i] * cap + slot_idx[i];
+      double dot = 0.0;
+      for (int32_t c = 0; c < d; ++c) {
+        double g = load_elem(dtype, dy, (int64_t)t * d + c);
+        /* dy/d(back[row][c]) = w_(t,j)                                   */
+        store_elem(dtype, d_back, row * d + c, (double)weight[i] * g);
+        /* dy/d(w_(t,j)) = back[row][c]                                   */
+        dot += g * load_elem(dtype, back, row * d + c);
+      }
+      d_weight[i] = (float)dot;
+    }
+}
+
+/* Adjoint of Layout_Transform: a gather-sum. */
+void orc_layout_bwd(int dtype, int32_t S, int32_t E, int32_t k, int32_t cap, int32_t d,
+                    const int32_t* expert_idx, const int32_t* slot_idx,
+                    const void* d_dispatch, void* dx) {
+  (void)E;
+  for (int32_t t = 0; t < S; ++t)
+    for (int32_t c = 0; c < d; ++c) {
+      double acc = 0.0;
+      for (int32_t j = 0; j < k; ++j) {
+        int64_t i = (int64_t)t * k + j;
+        if (slot_idx[i] < 0) continue;
+        int64_t row = (int64_t)expert_idx[i] * cap + slot_idx[i];
+        acc += load_elem(dtype, d_dispatch, row * d + c);
+      }
+      store_elem(dtype, dx, (int64_t)t * d + c, acc);
+    }
+}
+
+/* Softmax probabilities over the domain dom[0..n) of one row, in double:
+ * p[q] = exp(l_dom[q] - m) / sum exp(l - m), m = max over the domain. */
+static void softmax_dom(const float* row, const int32_t* dom, int32_t n, double* p) {
+  double m = (double)row[dom[0]];
+  for (int32_t q = 1; q < n; ++q)
+    if ((double)row[dom[q]] > m) m = (double)row[dom[q]];
+  double den = 0.0;
+  for (int32_t q = 0; q < n; ++q) den += exp((double)row[dom[q]] - m);
+  for (int32_t q = 0; q < n; ++q) p[q] = exp((double)row[dom[q]] - m) / den;
+}
+
+/* Adjoint of Eq. 1's softmax w.r.t. the logits. */
+int orc_gate_bwd(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
+                 const float* logits, const int32_t* expert_idx, const int32_t* slot_idx,
+                 const float* d_weight, float* d_logits) {
+  if (S < 1 || E < 1 || k < 1 || k > E || !logits) return -1;
+  if (kind != ORC_TOPK && kind != ORC_KTOP1) return -1;
+  if (kind == ORC_KTOP1 && E % k != 0) return -1;
+  int32_t* dom = (int32_t*)malloc(sizeof(int32_t) * (size_t)E);
+  double* p = (double*)malloc(sizeof(double) * (size_t)E);
+  double* grad = (double*)malloc(sizeof(double) * (size_t)E);
+  for (int32_t t = 0; t < S; ++t) {
+    const float* row = logits + (int64_t)t * E;
+    const int32_t* sel = expert_idx + (int64_t)t * k;
+    for (int32_t e = 0; e < E; ++e) grad[e] = 0.0;
+    for (int32_t j = 0; j < k; ++j) {
+      int64_t i = (int64_t)t * k + j;
+      double gj = slot_idx[i] >= 0 ? (double)d_weight[i] : 0.0;  /* m_j * g_j */
+      int32_t n;
+      if (kind == ORC_TOPK && weight_mode == ORC_RENORM) {        /* the k selected */
+        n = k;
+        for (int32_t q = 0; q < k; ++q) dom[q] = sel[q];
+      } else if (kind == ORC_TOPK) {                              /* the whole row */
+        n = E;
+        for (int32_t q = 0; q < E; ++q) dom[q] = q;
+      } else if (weight_mode == ORC_SOFTMAX) {                    /* prototype slice j */
+        n = E / k;
+        for (int32_t q = 0; q < n; ++q) dom[q] = j * n + q;
+      } else {
+        continue;                                                 /* w = 1: constant */
+      }
+      softmax_dom(row, dom, n, p);
+      double pj = 0.0;
+      for (int32_t q = 0; q < n; ++q)
+        if (dom[q] == sel[j]) pj = p[q];
+      /* dp_j/dl_e = p_j * (delta(e, e_j) - p_e) for e in the domain */
+      for (int32_t q = 0; q < n; ++q) {
+        double delta = (dom[q] == sel[j]) ? 1.0 : 0.0;
+        grad[dom[q]] += gj * pj * (delta - p[q]);
+      }
+    }
+    for (int32_t e = 0; e < E; ++e) d_logits[(int64_t)t * E + e] = (float)grad[e];
+  }
+  free(dom);
+  free(p);
+  free(grad);
+  return 0;
+}

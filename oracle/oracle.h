@@ -107,6 +107,45 @@ int orc_alltoall_hier(int32_t P, int32_t G, int64_t bytes_per_peer,
 void orc_alltoall_flat_stats(int32_t P, int32_t G, int64_t bytes_per_peer,
                              orc_a2a_stats_t* stats);
 
+/* ---- Backward of the routing path: Algorithm 1 is a
+ * training process, so each forward step has an
+ * adjoint.  Routing (expert_idx, slot_idx, weight) is the forward's output and
+ * is held fixed (selection and capacity are piecewise constant in the
+ * inputs). */
+
+/* Adjoint of step 6 + the combine, y[t] =
+ * sum_j w[t,j] * back[e_j][s_j]:
+ *   d_back[e][s]  = w[t,j] * dy[t]             for the admitted (t,j) at (e,s),
+ *                   0 for every empty slot      (double product, one rounding)
+ *   d_weight[t,j] = sum_c dy[t][c] * back[e_j][s_j][c]   (double, one rounding;
+ *                   0 for a dropped slot: its weight is the constant 0, R6) */
+void orc_reverse_layout_bwd(int dtype, int32_t S, int32_t E, int32_t k, int32_t cap,
+                            int32_t d, const int32_t* expert_idx,
+                            const int32_t* slot_idx, const float* weight,
+                            const void* dy, const void* back, void* d_back,
+                            float* d_weight);
+
+/* Adjoint of step 2, dispatch[e_j][s_j] = x[t]:
+ *   dx[t] = sum_{j ascending, admitted} d_dispatch[e_j][s_j]  (double, one
+ *   rounding); 0 for a fully dropped token. */
+void orc_layout_bwd(int dtype, int32_t S, int32_t E, int32_t k, int32_t cap, int32_t d,
+                    const int32_t* expert_idx, const int32_t* slot_idx,
+                    const void* d_dispatch, void* dx);
+
+/* Adjoint of the gate weights (Eq. 1; R1, R6, R11) w.r.t. the
+ * logits, selection fixed.  The combine uses w'_j = m_j * p_j with m_j = 1
+ * for an admitted slot, 0 for a dropped one, and p_j the Eq. 1 probability;
+ * so with g_j = d_weight[t,j]:
+ *   d_logits[t][e] = sum_j m_j * g_j * dp_j/dl_e
+ * where dp_j/dl_e = p_j * (delta(e, e_j) - p_e) over the softmax's domain
+ * (RENORM: the k selected logits; SOFTMAX: the row; k-top-1 SOFTMAX: the
+ * prototype slice) and 0 outside it.  k-top-1 RENORM weights are the constant
+ * 1: zero gradient.  Written out as the Jacobian sum, in double, one
+ * rounding.  Returns 0, or -1 for invalid arguments (HASH has no logits). */
+int orc_gate_bwd(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
+                 const float* logits, const int32_t* expert_idx, const int32_t* slot_idx,
+                 const float* d_weight, float* d_logits);
+
 /* bf16 helpers of the oracle's own (R14): exact widening, and a single
  * round-to-nearest-even narrowing from double. */
 double   orc_bf16_to_f64(uint16_t h);
