@@ -181,6 +181,51 @@ moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E
                               int32_t e_base, int32_t cap, int32_t d, int32_t dtype,
                               moe_stream_t stream);
 
+/* ---------------------------------------------------------------- backward
+ * SURVEY §8(f) NEXT-1.  Algorithm 1 is a training process (PAPER.md:26-28,
+ * 41-68); these are the adjoints of its routing steps, with the routing of
+ * the forward (expert_idx, slot_idx, weight, load) held fixed.  The AllToAll
+ * steps are their own adjoints with the direction swapped (moe_alltoall with
+ * the roles of send/recv exchanged), so a backward pass is
+ *   moe_reverse_layout_backward -> moe_alltoall -> (expert backward) ->
+ *   moe_alltoall -> moe_layout_backward, plus moe_gate_backward. */
+
+/* Adjoint of step 6 + the combine, given dy [S,d]
+ * and the expert outputs back [E,cap,d] of the forward:
+ *   d_back[e][s][:] = weight[t*k+j] * dy[t][:]   for the admitted (t,j) at
+ *                     (e,s): the product rounded once to dtype (RNE) --
+ *                     bit-identical to an exact product rounded once;
+ *   d_back[e][s][:] = 0                          for s in [min(load,cap), cap);
+ *   d_weight[t*k+j] = sum_c dy[t][c] * back[e][s][c]  (fp32 accumulate; 0 for
+ *                     a dropped slot, whose weight is the constant 0, R6).
+ * dy, back, d_back of `dtype`; d_weight [S*k] fp32.  Uses expert_idx,
+ * slot_idx, weight, load.  Errors: as moe_layout. */
+moe_status_t moe_reverse_layout_backward(const moe_gate_desc_t* desc,
+                                         const moe_routing_t* routing, const void* dy,
+                                         const void* back, int32_t d, int32_t dtype,
+                                         void* d_back, float* d_weight, moe_stream_t stream);
+
+/* Adjoint of step 2, Layout_Transform:
+ *   dx[t][:] = sum_{j ascending, slot_idx >= 0} d_dispatch[e][s][:]
+ * fp32 accumulate from 0, one RNE store; 0 for a fully dropped token.
+ * d_dispatch [E,cap,d], dx [S,d] of dtype.  Errors: as moe_layout. */
+moe_status_t moe_layout_backward(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                 const void* d_dispatch, int32_t d, int32_t dtype, void* dx,
+                                 moe_stream_t stream);
+
+/* Adjoint of the gate weights (Eq. 1; R1, R6, R11) w.r.t. the
+ * logits [S,E] fp32, selection fixed: with p the Eq. 1 probabilities over the
+ * softmax's domain (RENORM top-k: the k selected; SOFTMAX top-k: the row;
+ * SOFTMAX k-top-1: the prototype slice) and g_j = d_weight[t*k+j] for an
+ * admitted slot, 0 for a dropped one:
+ *   d_logits[t][e] = sum_j g_j p_j (delta(e, e_j) - p_e)  on the domain, 0
+ *   elsewhere; k-top-1 RENORM weights are constant: d_logits = 0.
+ * Evaluated in fp64, rounded once to fp32.  Errors: INVALID_ARG (HASH has no
+ * logits; NULL pointers), as moe_gate's description checks. */
+moe_status_t moe_gate_backward(const moe_gate_desc_t* desc, const float* logits,
+                               const moe_routing_t* routing, const float* d_weight,
+                               float* d_logits, moe_stream_t stream);
+
 /* ---------------------------------------------------------------- AllToAll */
 
 typedef struct moe_comm moe_comm_t;
@@ -270,6 +315,30 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
                              int32_t dtype, void* y, int32_t flags, moe_stream_t stream);
+
+/* Backward of the fused steps over NVLink (adjoints of moe_combine_p2p and
+ * moe_dispatch_p2p, same barrier flags).
+ * moe_combine_backward_p2p: entry barrier; for every admitted item (t,j) at
+ * expert e (owner q) and slot s, reads expert_out_q[r][e mod E/P][s] for
+ * d_weight and stores weight * dy[t] into d_expert_out_q[r][e mod E/P][s],
+ * zero-fills the padding rows there; exit barrier.  Equals
+ * moe_alltoall(FLAT) of expert_out + moe_reverse_layout_backward +
+ * moe_alltoall(FLAT) of d_back.  expert_out, d_expert_out: symmetric
+ * [P][E/P][cap][d]; d_weight [S*k] fp32 local. */
+moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                      const moe_routing_t* routing, const void* dy,
+                                      const void* expert_out, int32_t d, int32_t dtype,
+                                      void* d_expert_out, float* d_weight, int32_t flags,
+                                      moe_stream_t stream);
+
+/* moe_dispatch_backward_p2p: entry barrier; dx[t] = sum_j d_recv_q[r][e mod
+ * E/P][s] read from each owner q over NVLink (fp32 accumulate, one RNE
+ * store); exit barrier.  Equals moe_alltoall(FLAT) + moe_layout_backward.
+ * d_recv: symmetric [P][E/P][cap][d]. */
+moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                       const moe_routing_t* routing, const void* d_recv,
+                                       int32_t d, int32_t dtype, void* dx, int32_t flags,
+                                       moe_stream_t stream);
 
 /* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
  * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,

@@ -46,6 +46,19 @@ SIGNATURES = [
     ("moe_reverse_layout", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
                                           i32, i32, vp, vp]),
     ("moe_expert_scale", ctypes.c_int, [vp, vp, i32, i32, i32, i32, i32, i32, vp]),
+    ("moe_reverse_layout_backward", ctypes.c_int, [ctypes.POINTER(GateDesc),
+                                                   ctypes.POINTER(RoutingC), vp, vp, i32, i32,
+                                                   vp, vp, vp]),
+    ("moe_layout_backward", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
+                                           i32, i32, vp, vp]),
+    ("moe_gate_backward", ctypes.c_int, [ctypes.POINTER(GateDesc), vp, ctypes.POINTER(RoutingC),
+                                         vp, vp, vp]),
+    ("moe_combine_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                                ctypes.POINTER(RoutingC), vp, vp, i32, i32, vp,
+                                                vp, i32, vp]),
+    ("moe_dispatch_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                                 ctypes.POINTER(RoutingC), vp, i32, i32, vp, i32,
+                                                 vp]),
     ("moe_comm_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("moe_comm_init", ctypes.c_int, [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]),
     ("moe_comm_destroy", ctypes.c_int, [vp]),

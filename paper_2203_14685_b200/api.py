@@ -182,6 +182,66 @@ def reverse_layout(back: torch.Tensor, r: Routing,
     return out
 
 
+def reverse_layout_backward(dy: torch.Tensor, back: torch.Tensor, r: Routing,
+                            d_back: Optional[torch.Tensor] = None,
+                            d_weight: Optional[torch.Tensor] = None):
+    """Adjoint of the combine (NEXT-1): d_back [E,cap,d] = w * dy scattered to
+    the slots (padding rows 0), d_weight [S,k] = <dy[t], back[e][s]>."""
+    _need_cuda(dy, "dy")
+    _need_cuda(back, "back", dy.dtype)
+    if dy.dtype not in _DT:
+        raise TypeError("dy must be float32 or bfloat16")
+    S, d = dy.shape
+    if S != r.S or back.numel() != r.E * r.cap * d:
+        raise ValueError("dy must be [S=%d, d], back [E=%d, cap=%d, d]" % (r.S, r.E, r.cap))
+    if d_back is None:
+        d_back = torch.empty((r.E, r.cap, d), dtype=dy.dtype, device=dy.device)
+    if d_weight is None:
+        d_weight = torch.empty((r.S, r.k), dtype=torch.float32, device=dy.device)
+    _need_cuda(d_back, "d_back", dy.dtype)
+    _need_cuda(d_weight, "d_weight", torch.float32)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_reverse_layout_backward(ctypes.byref(desc), ctypes.byref(rc), _p(dy), _p(back),
+                                            d, _DT[dy.dtype], _p(d_back), _p(d_weight),
+                                            _stream(dy.device)), "moe_reverse_layout_backward")
+    return d_back, d_weight
+
+
+def layout_backward(d_dispatch: torch.Tensor, r: Routing,
+                    out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Adjoint of Layout_Transform (NEXT-1): dx[t] = sum_j d_dispatch[e_j][s_j]."""
+    _need_cuda(d_dispatch, "d_dispatch")
+    if d_dispatch.dtype not in _DT:
+        raise TypeError("d_dispatch must be float32 or bfloat16")
+    d = d_dispatch.shape[-1]
+    if d_dispatch.numel() != r.E * r.cap * d:
+        raise ValueError("d_dispatch must hold [E=%d, cap=%d, d] rows" % (r.E, r.cap))
+    if out is None:
+        out = torch.empty((r.S, d), dtype=d_dispatch.dtype, device=d_dispatch.device)
+    _need_cuda(out, "dx", d_dispatch.dtype)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_layout_backward(ctypes.byref(desc), ctypes.byref(rc), _p(d_dispatch), d,
+                                    _DT[d_dispatch.dtype], _p(out), _stream(d_dispatch.device)),
+          "moe_layout_backward")
+    return out
+
+
+def gate_backward(logits: torch.Tensor, r: Routing, d_weight: torch.Tensor,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Adjoint of Eq. 1's weights w.r.t. the logits (NEXT-1), selection fixed."""
+    _need_cuda(logits, "logits", torch.float32)
+    _need_cuda(d_weight, "d_weight", torch.float32)
+    if tuple(logits.shape) != (r.S, r.E) or d_weight.numel() != r.S * r.k:
+        raise ValueError("logits must be [S=%d, E=%d], d_weight [S, k=%d]" % (r.S, r.E, r.k))
+    if out is None:
+        out = torch.empty_like(logits)
+    _need_cuda(out, "d_logits", torch.float32)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_gate_backward(ctypes.byref(desc), _p(logits), ctypes.byref(rc), _p(d_weight),
+                                  _p(out), _stream(logits.device)), "moe_gate_backward")
+    return out
+
+
 def expert_scale(buf: torch.Tensor, nsrc: int, E_local: int, e_base: int,
                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Bench stand-in expert (R16): s_e * buf over [nsrc][E_local][cap][d]."""
@@ -290,6 +350,34 @@ class Comm:
                                     d, _DT[expert_out.dtype], _p(y), flags, _stream(y.device)),
               "moe_combine_p2p")
         return y
+
+    def combine_backward_p2p(self, dy: torch.Tensor, expert_out: torch.Tensor, r: "Routing",
+                             d_expert_out: torch.Tensor, d_weight: Optional[torch.Tensor] = None,
+                             flags: int = 0):
+        """Adjoint of combine_p2p: w*dy stored into the owners' symmetric
+        d_expert_out over NVLink, d_weight from the owners' expert_out."""
+        _need_cuda(dy, "dy")
+        d = dy.shape[-1]
+        if d_weight is None:
+            d_weight = torch.empty((r.S, r.k), dtype=torch.float32, device=dy.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_combine_backward_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(dy),
+                                             _p(expert_out), d, _DT[dy.dtype], _p(d_expert_out),
+                                             _p(d_weight), flags, _stream(dy.device)),
+              "moe_combine_backward_p2p")
+        return d_expert_out, d_weight
+
+    def dispatch_backward_p2p(self, d_recv: torch.Tensor, r: "Routing",
+                              dx: Optional[torch.Tensor] = None, flags: int = 0) -> torch.Tensor:
+        """Adjoint of dispatch_p2p: dx[t] = sum_j of the owners' d_recv rows."""
+        d = d_recv.shape[-1]
+        if dx is None:
+            dx = torch.empty((r.S, d), dtype=d_recv.dtype, device=d_recv.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_dispatch_backward_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                              _p(d_recv), d, _DT[d_recv.dtype], _p(dx), flags,
+                                              _stream(dx.device)), "moe_dispatch_backward_p2p")
+        return dx
 
     def destroy(self):
         if getattr(self, "_h", None):

@@ -9,7 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "common.cuh"
+#include "comm.cuh"
 
 namespace moe {
 
@@ -20,6 +20,12 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);
 moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                            int dtype_size, int dcols, void* dispatch, cudaStream_t stream);
+moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
+                                const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
+                                int rank, int dtype, int dtype_size, int dcols, float* d_weight,
+                                cudaStream_t stream);
+moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, const moe_routing_t& r,
+                             const float* d_weight, float* d_logits, cudaStream_t stream);
 moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
                             int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream);
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
@@ -216,6 +222,53 @@ moe_status_t moe_reverse_layout(const moe_gate_desc_t* desc, const moe_routing_t
   if (s != MOE_OK) return s;
   return reverse_launch(*desc, *routing, back, dtype, dtype_size(dtype), d, y,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_reverse_layout_backward(const moe_gate_desc_t* desc,
+                                         const moe_routing_t* routing, const void* dy,
+                                         const void* back, int32_t d, int32_t dtype,
+                                         void* d_back, float* d_weight, moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_reverse_layout_backward", desc, routing, dy, "dy", back, "back",
+                              d, dtype, true, true);
+  if (s != MOE_OK) return s;
+  if (!d_back || !d_weight || !aligned(d_back, 16)) {
+    set_error("moe_reverse_layout_backward: d_back (16-byte aligned) and d_weight are required");
+    return d_back && d_weight ? MOE_ERR_ALIGNMENT : MOE_ERR_INVALID_ARG;
+  }
+  PeerPtrs b{}, g{};
+  b.p[0] = const_cast<char*>(static_cast<const char*>(back));
+  g.p[0] = static_cast<char*>(d_back);
+  return combine_bwd_launch(*desc, *routing, dy, b, g, desc->E, 0, dtype, dtype_size(dtype), d,
+                            d_weight, reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_layout_backward(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                 const void* d_dispatch, int32_t d, int32_t dtype, void* dx,
+                                 moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_layout_backward", desc, routing, d_dispatch, "d_dispatch", dx,
+                              "dx", d, dtype, false, false);
+  if (s != MOE_OK) return s;
+  moe_routing_t unit = *routing;
+  unit.weight = nullptr;  // the adjoint of the copy is the combine with w = 1
+  return reverse_launch(*desc, unit, d_dispatch, dtype, dtype_size(dtype), d, dx,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_gate_backward(const moe_gate_desc_t* desc, const float* logits,
+                               const moe_routing_t* routing, const float* d_weight,
+                               float* d_logits, moe_stream_t stream) {
+  moe_status_t s = check_desc("moe_gate_backward", desc);
+  if (s != MOE_OK) return s;
+  if (desc->kind == MOE_GATE_HASH) {
+    set_error("moe_gate_backward: the hash gate has no logits (no gradient)");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!logits || !routing || !routing->expert_idx || !routing->slot_idx || !d_weight || !d_logits) {
+    set_error("moe_gate_backward: logits, routing.expert_idx/slot_idx, d_weight, d_logits required");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return gate_bwd_launch(*desc, logits, *routing, d_weight, d_logits,
+                         reinterpret_cast<cudaStream_t>(stream));
 }
 
 moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E_local,

@@ -15,94 +15,9 @@
 //    0, one RNE store; fully dropped tokens store zeros.
 #include <algorithm>
 
-#include "comm.cuh"
+#include "rows.cuh"
 
 namespace moe {
-
-constexpr int kRowThreads = 256;
-constexpr int kRowWarps = kRowThreads / 32;
-
-struct RowArgs {
-  const char* src;
-  char* dst;
-  const int32_t* expert_idx;
-  const int32_t* slot_idx;
-  const float* weight;
-  const int32_t* load;
-  int S, E, k, cap;
-  int row_bytes;
-  int d;
-  // layout destination: expert e lives on rank q = e / E_local and its rows
-  // go to dpeer.p[q] + ((rank*E_local + e mod E_local)*cap + s)*row.  Local
-  // moe_layout: dpeer.p[0] = dispatch, E_local = E, rank = 0.
-  PeerPtrs dpeer;
-  int E_local, rank;
-  int sys_fence;  // stores went to peers: fence.sys before the CTA exits
-  // reverse source: row (e, s) is read from speer.p[q] + ((rank*E_local +
-  // e mod E_local)*cap + s)*row (same mapping; local: speer.p[0] = back)
-  PeerPtrs speer;
-};
-
-__device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
-  const int q = e / a.E_local;
-  return a.speer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
-}
-
-__device__ __forceinline__ char* dst_row_of(const RowArgs& a, int e, int s) {
-  const int q = e / a.E_local;
-  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
-}
-
-template <int VB>
-struct Vec;
-template <>
-struct Vec<32> {
-  using T = V8;
-  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v8(p); }
-  static __device__ __forceinline__ T ld(const void* p) { return ld_v8(p); }
-  static __device__ __forceinline__ void st(void* p, const T& v) { st_v8(p, v); }
-  static __device__ __forceinline__ T zero() { return V8{{0, 0, 0, 0, 0, 0, 0, 0}}; }
-};
-template <>
-struct Vec<16> {
-  using T = V4;
-  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v4(p); }
-  static __device__ __forceinline__ T ld(const void* p) {
-    V4 r;
-    asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
-                 : "l"(p));
-    return r;
-  }
-  static __device__ __forceinline__ void st(void* p, const T& v) { st_v4(p, v); }
-  static __device__ __forceinline__ T zero() { return V4{{0, 0, 0, 0}}; }
-};
-
-// Exclusive prefix of the padding-row counts cap - min(load[e], cap) into
-// s_beg[0..E] (E <= 256), computed by every CTA (tiny).
-__device__ __forceinline__ void pad_prefix(const RowArgs& a, int* s_beg) {
-  __shared__ int s_cnt[257];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < a.E; e += blockDim.x) s_cnt[e] = a.cap - min(__ldg(a.load + e), a.cap);
-  __syncthreads();
-  if (tid < 32) {
-    int carry = 0;
-    for (int base = 0; base < a.E; base += 32) {
-      const int e = base + tid;
-      int v = e < a.E ? s_cnt[e] : 0;
-      int incl = v;
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, incl, m);
-        if (tid >= m) incl += o;
-      }
-      if (e < a.E) s_beg[e] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (tid == 0) s_beg[a.E] = carry;
-  }
-  __syncthreads();
-}
 
 // ------------------------------------------------------------ Layout_Transform
 template <int VB, int U>
@@ -389,36 +304,6 @@ __global__ void __launch_bounds__(kTmaThreads) k_layout_tma(TmaArgs ta) {
 }
 
 // ------------------------------------------------------------ Reverse + combine
-struct F32Acc {
-  static constexpr int kPerVec = 8;  // fp32 per 32 bytes
-};
-
-template <int DT>  // MOE_F32 or MOE_BF16; 32-byte vectors
-__device__ __forceinline__ void fma_vec(float* acc, float w, const V8& v) {
-  if constexpr (DT == MOE_F32) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      acc[2 * q] = fmaf(w, bf16lo(v.w[q]), acc[2 * q]);
-      acc[2 * q + 1] = fmaf(w, bf16hi(v.w[q]), acc[2 * q + 1]);
-    }
-  }
-}
-template <int DT>
-__device__ __forceinline__ V8 pack_vec(const float* acc) {
-  V8 o;
-  if constexpr (DT == MOE_F32) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) o.w[q] = __float_as_uint(acc[q]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) o.w[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
-  }
-  return o;
-}
-
 template <int DT, int U>
 __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
   constexpr int VB = 32;
@@ -444,7 +329,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         float w0 = 0.f, w1 = 0.f;
         if (s0 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
-          w0 = __ldg(a.weight + (size_t)t * a.k + j);
+          w0 = row_weight(a, (size_t)t * a.k + j);
           const char* b = src_row(a, e, s0);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -454,7 +339,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         }
         if (s1 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j + 1);
-          w1 = __ldg(a.weight + (size_t)t * a.k + j + 1);
+          w1 = row_weight(a, (size_t)t * a.k + j + 1);
           const char* b = src_row(a, e, s1);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -511,7 +396,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
         w[p][j] = 0.f;
         if (s >= 0) {
           b[p][j] = src_row(a, __ldg(a.expert_idx + (size_t)t * KK + j), s);
-          w[p][j] = __ldg(a.weight + (size_t)t * KK + j);
+          w[p][j] = row_weight(a, (size_t)t * KK + j);
         }
       }
     for (int seg = 0; seg < a.row_bytes; seg += SEG) {
@@ -565,7 +450,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
         const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
         if (s < 0) continue;
         const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
-        const float w = __ldg(a.weight + (size_t)t * a.k + j);
+        const float w = row_weight(a, (size_t)t * a.k + j);
         const V4 v = ld_stream_v4(src_row(a, e, s) + off);
         if constexpr (DT == MOE_F32) {
 #pragma unroll
@@ -641,11 +526,6 @@ __global__ void __launch_bounds__(kRowThreads) k_chunk_permute(const char* src, 
 }
 
 // ------------------------------------------------------------ host side
-static int row_grid(const void* kern) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);
-  return std::max(1, per_sm) * device_sm_count();
-}
 
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,

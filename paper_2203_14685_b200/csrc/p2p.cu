@@ -29,6 +29,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream);
 
+moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
+                                const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
+                                int rank, int dtype, int dtype_size, int dcols, float* d_weight,
+                                cudaStream_t stream);
+
 static moe_status_t nccl_st(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return MOE_OK;
   set_error("%s: NCCL error %d (%s)", what, (int)r, ncclGetErrorString(r));
@@ -332,6 +337,59 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
+}
+
+moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                      const moe_routing_t* routing, const void* dy,
+                                      const void* expert_out, int32_t d, int32_t dtype,
+                                      void* d_expert_out, float* d_weight, int32_t flags,
+                                      moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs src, dst;
+  int ds = 0;
+  moe_status_t s = p2p_args("moe_combine_backward_p2p", comm, desc, routing, dy, expert_out, d,
+                            dtype, &src, &ds);
+  if (s != MOE_OK) return s;
+  s = p2p_args("moe_combine_backward_p2p", comm, desc, routing, dy, d_expert_out, d, dtype, &dst,
+               &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight || !routing->load || !d_weight) {
+    set_error("moe_combine_backward_p2p: routing.weight, routing.load and d_weight are required");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  s = combine_bwd_launch(*desc, *routing, dy, src, dst, desc->E / P, comm->rank, dtype, ds, d,
+                         d_weight, stream);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+}
+
+moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                       const moe_routing_t* routing, const void* d_recv,
+                                       int32_t d, int32_t dtype, void* dx, int32_t flags,
+                                       moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = p2p_args("moe_dispatch_backward_p2p", comm, desc, routing, dx, d_recv, d, dtype,
+                            &src, &ds);
+  if (s != MOE_OK) return s;
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  moe_routing_t unit = *routing;
+  unit.weight = nullptr;  // adjoint of the dispatch copy: unit-weight combine
+  s = reverse_launch_peers(*desc, unit, src, desc->E / P, comm->rank, dtype, ds, d, dx, stream);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
 }
 
 }  // extern "C"

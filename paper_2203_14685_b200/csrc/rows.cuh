@@ -1,0 +1,139 @@
+// rows.cuh -- shared pieces of the row-moving kernels (layout.cu,
+// backward.cu): the argument block with its peer-pointer row mapping, the
+// padding-row prefix, 32-byte vector FMA/pack helpers and the grid size.
+#pragma once
+#include <algorithm>
+
+#include "comm.cuh"
+
+namespace moe {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+
+struct RowArgs {
+  const char* src;
+  char* dst;
+  const int32_t* expert_idx;
+  const int32_t* slot_idx;
+  const float* weight;
+  const int32_t* load;
+  int S, E, k, cap;
+  int row_bytes;
+  int d;
+  // layout destination: expert e lives on rank q = e / E_local and its rows
+  // go to dpeer.p[q] + ((rank*E_local + e mod E_local)*cap + s)*row.  Local
+  // moe_layout: dpeer.p[0] = dispatch, E_local = E, rank = 0.
+  PeerPtrs dpeer;
+  int E_local, rank;
+  int sys_fence;  // stores went to peers: fence.sys before the CTA exits
+  // reverse source: row (e, s) is read from speer.p[q] + ((rank*E_local +
+  // e mod E_local)*cap + s)*row (same mapping; local: speer.p[0] = back)
+  PeerPtrs speer;
+};
+
+__device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
+  const int q = e / a.E_local;
+  return a.speer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+}
+
+__device__ __forceinline__ char* dst_row_of(const RowArgs& a, int e, int s) {
+  const int q = e / a.E_local;
+  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+}
+
+template <int VB>
+struct Vec;
+template <>
+struct Vec<32> {
+  using T = V8;
+  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v8(p); }
+  static __device__ __forceinline__ T ld(const void* p) { return ld_v8(p); }
+  static __device__ __forceinline__ void st(void* p, const T& v) { st_v8(p, v); }
+  static __device__ __forceinline__ T zero() { return V8{{0, 0, 0, 0, 0, 0, 0, 0}}; }
+};
+template <>
+struct Vec<16> {
+  using T = V4;
+  static __device__ __forceinline__ T ld_stream(const void* p) { return ld_stream_v4(p); }
+  static __device__ __forceinline__ T ld(const void* p) {
+    V4 r;
+    asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "l"(p));
+    return r;
+  }
+  static __device__ __forceinline__ void st(void* p, const T& v) { st_v4(p, v); }
+  static __device__ __forceinline__ T zero() { return V4{{0, 0, 0, 0}}; }
+};
+
+// Exclusive prefix of the padding-row counts cap - min(load[e], cap) into
+// s_beg[0..E] (E <= 256), computed by every CTA (tiny).
+__device__ __forceinline__ void pad_prefix(const RowArgs& a, int* s_beg) {
+  __shared__ int s_cnt[257];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < a.E; e += blockDim.x) s_cnt[e] = a.cap - min(__ldg(a.load + e), a.cap);
+  __syncthreads();
+  if (tid < 32) {
+    int carry = 0;
+    for (int base = 0; base < a.E; base += 32) {
+      const int e = base + tid;
+      int v = e < a.E ? s_cnt[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (tid >= m) incl += o;
+      }
+      if (e < a.E) s_beg[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) s_beg[a.E] = carry;
+  }
+  __syncthreads();
+}
+
+struct F32Acc {
+  static constexpr int kPerVec = 8;  // fp32 per 32 bytes
+};
+
+template <int DT>  // MOE_F32 or MOE_BF16; 32-byte vectors
+__device__ __forceinline__ void fma_vec(float* acc, float w, const V8& v) {
+  if constexpr (DT == MOE_F32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc[2 * q] = fmaf(w, bf16lo(v.w[q]), acc[2 * q]);
+      acc[2 * q + 1] = fmaf(w, bf16hi(v.w[q]), acc[2 * q + 1]);
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ V8 pack_vec(const float* acc) {
+  V8 o;
+  if constexpr (DT == MOE_F32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o.w[q] = __float_as_uint(acc[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o.w[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
+  }
+  return o;
+}
+
+// Combine weight of item i; a NULL weight array means unit weights (the
+// adjoint of Layout_Transform is the combine with w = 1).
+__device__ __forceinline__ float row_weight(const RowArgs& a, size_t i) {
+  return a.weight ? __ldg(a.weight + i) : 1.f;
+}
+
+// Persistent grid: SMs x resident CTAs of `kern` at kRowThreads threads.
+inline int row_grid(const void* kern) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);
+  return std::max(1, per_sm) * device_sm_count();
+}
+
+}  // namespace moe

@@ -80,3 +80,78 @@ def test_multi_gpu_route(orc, world, algo, G):
                                                    q * (E // world)).reshape(E, cap, D)
                                   for q in range(world)])[r]
         assert_y_close(y, ys[r], combine_bound(as_f64(back), routings[r]), True)
+
+
+def _bwd_rank_main(rank, world, port, q):
+    """Backward over NVLink: combine_backward_p2p + dispatch_backward_p2p."""
+    import torch.distributed as dist
+    import paper_2203_14685_b200 as moe
+    from gpu_util import dev, host
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = moe.Comm.from_process_group()
+    lg = synthgen.logits(synthgen.seed_for(9, rank, 5), S, E, K, skew=0.5)
+    cap = moe.capacity(S, E, K, 0.8)
+    r = moe.Gate(S, E, K, cap)(dev(lg))
+    eo = synthgen.tokens(synthgen.seed_for(9, rank, 6), E * cap, D, "bf16").reshape(E, cap, D)
+    dr = synthgen.tokens(synthgen.seed_for(9, rank, 7), E * cap, D, "bf16").reshape(E, cap, D)
+    dy = synthgen.tokens(synthgen.seed_for(9, rank, 8), S, D, "bf16")
+    expert_out = comm.symm_empty((E, cap, D), torch.bfloat16)
+    d_expert_out = comm.symm_empty((E, cap, D), torch.bfloat16)
+    d_recv = comm.symm_empty((E, cap, D), torch.bfloat16)
+    expert_out.copy_(dev(eo))
+    d_recv.copy_(dev(dr))
+    d_expert_out.fill_(7.0)  # every row must be overwritten (admitted or padding)
+    torch.cuda.synchronize()
+    _, dw = comm.combine_backward_p2p(dev(dy), expert_out, r, d_expert_out)
+    dx = comm.dispatch_backward_p2p(d_recv, r)
+    torch.cuda.synchronize()
+    q.put((rank, lg, eo, dr, dy, host(d_expert_out).copy(), host(dw).copy(), host(dx).copy()))
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_backward_p2p(orc, world):
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs %d GPUs" % world)
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = 29700 + world
+    ps = [ctx.Process(target=_bwd_rank_main, args=(r, world, port, qu)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = {}
+    for _ in range(world):
+        v = qu.get(timeout=300)
+        out[v[0]] = v[1:]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    from gpu_util import as_f64, assert_y_close, combine_bound
+    cap = orc.capacity(S, E, K, 0.8)
+    ros = [orc.gate(out[r][0], E=E, k=K, cap=cap) for r in range(world)]
+    backs = orc.alltoall_flat([out[q][1] for q in range(world)])      # rows each rank combines
+    d_backs, dws = [], []
+    for r in range(world):
+        db, dw = orc.reverse_layout_bwd(out[r][3], backs[r], ros[r])
+        d_backs.append(db)
+        dws.append(dw)
+    d_eo = orc.alltoall_flat(d_backs)                                   # lands at the owners
+    d_disp = orc.alltoall_flat([out[q][2] for q in range(world)])
+    for r in range(world):
+        assert out[r][4].tobytes() == d_eo[r].tobytes()
+        dwb = np.abs(out[r][5].astype(np.float64) - dws[r].astype(np.float64))
+        rows = as_f64(backs[r])
+        bound = np.zeros_like(dwb)
+        for j in range(K):
+            ok = ros[r].slot_idx[:, j] >= 0
+            bound[ok, j] = np.abs(as_f64(out[r][3])[ok] *
+                                  rows[ros[r].expert_idx[ok, j], ros[r].slot_idx[ok, j]]).sum(1)
+        assert (dwb <= (D / 32 + 6) * 2.0 ** -24 * bound + 1e-30).all()
+        dx_o = orc.layout_bwd(d_disp[r], ros[r])
+        unit = type(ros[r])(**{**ros[r].__dict__,
+                               "weight": (ros[r].slot_idx >= 0).astype(np.float32)})
+        assert_y_close(out[r][6], dx_o, combine_bound(as_f64(d_disp[r]), unit), True, "dx")
