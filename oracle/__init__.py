@@ -83,6 +83,12 @@ def lib():
         L.orc_alltoall_hier.restype = ctypes.c_int
         L.orc_alltoall_flat_stats.argtypes = [i32, i32, i64, ctypes.POINTER(_Stats)]
         L.orc_alltoall_flat_stats.restype = None
+        L.orc_gate_sam.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, i32, i32, P, P,
+                                   P, P, P, P, P]
+        L.orc_gate_sam.restype = i64
+        L.orc_gate_d2s.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, ctypes.c_double,
+                                   ctypes.c_double, P, P, P, P, P, P, P]
+        L.orc_gate_d2s.restype = i64
         L.orc_reverse_layout_bwd.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P, P,
                                              P, P, P, P]
         L.orc_reverse_layout_bwd.restype = None
@@ -148,6 +154,38 @@ def gate(logits=None, *, S=None, E, k, cap, kind="topk", weight_mode="renorm",
     if bad < 0:
         raise ValueError("orc_gate rejected its arguments")
     return Routing(ei, si, w, load, ss, S, E, k, cap, int(bad))
+
+
+def gate_sam(group_logits, logits, *, E, k, cap, n_groups, weight_mode="renorm",
+             priority="token") -> Routing:
+    """Hierarchical top-k (SAM; R17)."""
+    gl = _c(group_logits, np.float32)
+    lg = _c(logits, np.float32)
+    S = lg.shape[0]
+    assert lg.shape == (S, E) and gl.shape == (S, n_groups)
+    ei, si = np.empty((S, k), np.int32), np.empty((S, k), np.int32)
+    w, load, ss = np.empty((S, k), np.float32), np.empty((E,), np.int32), np.empty((E * cap,), np.int32)
+    rc = lib().orc_gate_sam(MODES[weight_mode], PRIOS[priority], S, E, k, cap, n_groups, _ptr(gl),
+                            _ptr(lg), _ptr(ei), _ptr(si), _ptr(w), _ptr(load), _ptr(ss))
+    if rc < 0:
+        raise ValueError("orc_gate_sam rejected its arguments")
+    return Routing(ei, si, w, load, ss, S, E, k, cap, 0)
+
+
+def gate_d2s(logits, *, cap, tau, eps=1e-3, uniforms=None, weight_mode="renorm",
+             priority="token") -> Routing:
+    """Dense-to-Sparse (R18): k = E slots, pruned slots -1."""
+    lg = _c(logits, np.float32)
+    S, E = lg.shape
+    u = _c(uniforms, np.float32)
+    assert u is None or u.shape == (S, E)
+    ei, si = np.empty((S, E), np.int32), np.empty((S, E), np.int32)
+    w, load, ss = np.empty((S, E), np.float32), np.empty((E,), np.int32), np.empty((E * cap,), np.int32)
+    rc = lib().orc_gate_d2s(MODES[weight_mode], PRIOS[priority], S, E, cap, float(tau), float(eps),
+                            _ptr(lg), _ptr(u), _ptr(ei), _ptr(si), _ptr(w), _ptr(load), _ptr(ss))
+    if rc < 0:
+        raise ValueError("orc_gate_d2s rejected its arguments")
+    return Routing(ei, si, w, load, ss, S, E, E, cap, 0)
 
 
 def layout(x: np.ndarray, r: Routing) -> np.ndarray:

@@ -136,6 +136,10 @@ static void ktop1_row(const float* row, int32_t E, int32_t k, int mode,
   }
 }
 
+static void capacity_replay(int priority, int32_t S, int32_t E, int32_t k, int32_t cap,
+                            const int32_t* expert_idx, int32_t* slot_idx, float* weight,
+                            int32_t* load, int32_t* slot_src);
+
 int64_t orc_gate(int kind, int weight_mode, int priority,
                  int32_t S, int32_t E, int32_t k, int32_t cap,
                  const float* logits, const int32_t* token_ids,
@@ -171,9 +175,18 @@ int64_t orc_gate(int kind, int weight_mode, int priority,
   }
   free(order);
 
-  /* 2. capacity replay (R4, R5, R6): walk the items in
-   * admission order; slot = number of earlier items with the same expert;
-   * slot >= cap -> dropped, weight 0. */
+  capacity_replay(priority, S, E, k, cap, expert_idx, slot_idx, weight, load, slot_src);
+  return bad;
+}
+
+/* Capacity (R4, R5, R6): walk the items in admission order;
+ * slot = number of earlier items with the same expert; slot >= cap ->
+ * dropped, weight 0.  Items with expert -1 (an invalid hash id, a pruned
+ * Dense-to-Sparse slot) are not admitted and not counted. */
+static void capacity_replay(int priority, int32_t S, int32_t E, int32_t k, int32_t cap,
+                            const int32_t* expert_idx, int32_t* slot_idx, float* weight,
+                            int32_t* load, int32_t* slot_src) {
+  /* 2. capacity replay */
   int32_t* cnt = (int32_t*)calloc((size_t)E, sizeof(int32_t));
   int64_t n_items = (int64_t)S * k;
   for (int64_t it = 0; it < n_items; ++it) {
@@ -201,7 +214,6 @@ int64_t orc_gate(int kind, int weight_mode, int priority,
       if (slot_idx[i] >= 0)
         slot_src[(int64_t)expert_idx[i] * cap + slot_idx[i]] = (int32_t)i;
   }
-  return bad;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -457,5 +469,114 @@ int orc_gate_bwd(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
   free(dom);
   free(p);
   free(grad);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Hierarchical top-k, SAM ("the Switch Router first        */
+/* selects one group and then the Mixture Router selects multiple experts in */
+/* the same group"; R17).                                                    */
+/* ------------------------------------------------------------------------ */
+int64_t orc_gate_sam(int weight_mode, int priority, int32_t S, int32_t E, int32_t k,
+                     int32_t cap, int32_t n_groups, const float* group_logits,
+                     const float* logits, int32_t* expert_idx, int32_t* slot_idx,
+                     float* weight, int32_t* load, int32_t* slot_src) {
+  if (S < 1 || E < 1 || k < 1 || cap < 1 || n_groups < 1 || E % n_groups != 0) return -1;
+  const int32_t n = E / n_groups;  /* experts per group, contiguous (R10, R17) */
+  if (k > n || !group_logits || !logits) return -1;
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  for (int32_t t = 0; t < S; ++t) {
+    const float* gl = group_logits + (int64_t)t * n_groups;
+    const float* row = logits + (int64_t)t * E;
+    /* Switch Router: the group of largest logit (= largest softmax
+     * probability), strict '>' scanning upward: lowest index on ties (R3) */
+    int32_t g = 0;
+    for (int32_t h = 1; h < n_groups; ++h)
+      if (gl[h] > gl[g]) g = h;
+    /* Mixture Router: top-k of the expert logits inside group g (R2, R3) */
+    int32_t* sel = expert_idx + (int64_t)t * k;
+    topk_row(row + (int64_t)g * n, n, k, order, sel);
+    for (int32_t j = 0; j < k; ++j) sel[j] += g * n;
+    /* weights, in double, rounded once (R17):
+     *   RENORM : softmax over the k selected logits (group probability x
+     *            within-group softmax, renormalised to sum 1);
+     *   SOFTMAX: P(g) * P(e | g), P(g) = softmax over the group logits,
+     *            P(e | g) = softmax over the n logits of group g. */
+    double m = (double)row[sel[0]], den = 0.0, pg = 1.0;
+    if (weight_mode == ORC_RENORM) {
+      for (int32_t j = 0; j < k; ++j) den += exp((double)row[sel[j]] - m);
+    } else {
+      for (int32_t e = g * n; e < (g + 1) * n; ++e) den += exp((double)row[e] - m);
+      double gden = 0.0;
+      for (int32_t h = 0; h < n_groups; ++h) gden += exp((double)gl[h] - (double)gl[g]);
+      pg = 1.0 / gden;
+    }
+    for (int32_t j = 0; j < k; ++j)
+      weight[(int64_t)t * k + j] = (float)(pg * (exp((double)row[sel[j]] - m) / den));
+  }
+  free(order);
+  capacity_replay(priority, S, E, k, cap, expert_idx, slot_idx, weight, load, slot_src);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Dense-to-Sparse ("utilizes the Gumbel Softmax and decreases  */
+/* the temperature during training"; R18).                                  */
+/* ------------------------------------------------------------------------ */
+int64_t orc_gate_d2s(int weight_mode, int priority, int32_t S, int32_t E, int32_t cap,
+                     double tau, double eps, const float* logits, const float* uniforms,
+                     int32_t* expert_idx, int32_t* slot_idx, float* weight, int32_t* load,
+                     int32_t* slot_src) {
+  if (S < 1 || E < 1 || cap < 1 || !(tau > 0.0) || !(eps >= 0.0) || !logits) return -1;
+  const int32_t k = E;  /* every expert is a candidate slot */
+  double* z = (double*)malloc(sizeof(double) * (size_t)E);
+  double* p = (double*)malloc(sizeof(double) * (size_t)E);
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)E);
+  for (int32_t t = 0; t < S; ++t) {
+    const float* row = logits + (int64_t)t * E;
+    /* z_e = (l_e + G_e) / tau, G_e = -log(-log(u_e)) a Gumbel(0,1) draw
+     * (train), 0 (eval) */
+    for (int32_t e = 0; e < E; ++e) {
+      double g = 0.0;
+      if (uniforms) g = -log(-log((double)uniforms[(int64_t)t * E + e]));
+      z[e] = ((double)row[e] + g) / tau;
+    }
+    /* p = softmax(z) over all E experts (the dense gate) */
+    double m = z[0];
+    for (int32_t e = 1; e < E; ++e)
+      if (z[e] > m) m = z[e];
+    double den = 0.0;
+    for (int32_t e = 0; e < E; ++e) den += exp(z[e] - m);
+    for (int32_t e = 0; e < E; ++e) p[e] = exp(z[e] - m) / den;
+    /* survivors p_e >= eps, in descending z (ties: lower index): insertion
+     * sort of the survivors */
+    int32_t ns = 0;
+    double psum = 0.0;
+    for (int32_t e = 0; e < E; ++e) {
+      if (!(p[e] >= eps)) continue;
+      psum += p[e];
+      int32_t q = ns++;
+      while (q > 0 && (z[e] > z[order[q - 1]] || (z[e] == z[order[q - 1]] && e < order[q - 1]))) {
+        order[q] = order[q - 1];
+        --q;
+      }
+      order[q] = e;
+    }
+    for (int32_t j = 0; j < k; ++j) {
+      int64_t i = (int64_t)t * k + j;
+      if (j < ns) {
+        expert_idx[i] = order[j];
+        /* RENORM: survivors renormalised to sum 1; SOFTMAX: p unchanged */
+        weight[i] = (float)(weight_mode == ORC_RENORM ? p[order[j]] / psum : p[order[j]]);
+      } else {
+        expert_idx[i] = -1;  /* pruned */
+        weight[i] = 0.0f;
+      }
+    }
+  }
+  free(z);
+  free(p);
+  free(order);
+  capacity_replay(priority, S, E, k, cap, expert_idx, slot_idx, weight, load, slot_src);
   return 0;
 }

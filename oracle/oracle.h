@@ -57,6 +57,31 @@ int64_t orc_gate(int kind, int weight_mode, int priority,
                  int32_t* expert_idx, int32_t* slot_idx, float* weight,
                  int32_t* load, int32_t* slot_src);
 
+/* Hierarchical top-k / SAM (R17): experts in n_groups
+ * contiguous groups of n = E/n_groups; group g = argmax of the group logits
+ * [S,n_groups] (the Switch Router), then the top-k (k <= n) of the expert
+ * logits inside group g (the Mixture Router).  Weights: RENORM = softmax
+ * over the k selected logits; SOFTMAX = P(g) * P(e | g) (group softmax times
+ * the within-group softmax, not renormalised).  Capacity as orc_gate.
+ * Returns 0, or -1 for invalid arguments. */
+int64_t orc_gate_sam(int weight_mode, int priority, int32_t S, int32_t E, int32_t k,
+                     int32_t cap, int32_t n_groups, const float* group_logits,
+                     const float* logits, int32_t* expert_idx, int32_t* slot_idx,
+                     float* weight, int32_t* load, int32_t* slot_src);
+
+/* Dense-to-Sparse (R18): k = E candidate slots per token.
+ * z_e = (l_e + G_e)/tau with G_e = -log(-log(u_e)) (train: uniforms [S,E]
+ * in (0,1)) or 0 (eval: uniforms NULL); p = softmax(z) over all E; experts
+ * with p_e < eps are pruned; survivors fill slots 0..k'-1 in descending z
+ * (ties: lower index), weight p_e / sum_survivors p (RENORM) or p_e
+ * (SOFTMAX); pruned slots j >= k' get expert -1, slot -1, weight 0.
+ * Capacity as orc_gate over the survivors.  Returns 0, or -1 for invalid
+ * arguments. */
+int64_t orc_gate_d2s(int weight_mode, int priority, int32_t S, int32_t E, int32_t cap,
+                     double tau, double eps, const float* logits, const float* uniforms,
+                     int32_t* expert_idx, int32_t* slot_idx, float* weight, int32_t* load,
+                     int32_t* slot_src);
+
 /* Step 2: dispatch[e][s][:] = x[t][:] for every
  * admitted (t,j), padded layout [E][cap][row] with zeroed padding (R9).
  * Byte copy: dtype agnostic. */

@@ -127,6 +127,39 @@ def logits(seed: int, S: int, E: int, k: int = 1, kind: str = "topk", gap: float
     return out
 
 
+def group_logits_and_logits(seed: int, S: int, E: int, k: int, n_groups: int,
+                            gap: float = 1e-4):
+    """Hierarchical-gate inputs: group logits [S, n_groups] (top 2 of every
+    row >= gap apart) and expert logits [S, E] with the top k+1 of EVERY
+    group's slice >= gap apart, so no near ties are generated whichever
+    group wins (i.i.d. N(0,1); rows re-drawn like logits())."""
+    gl = logits(seed, S, n_groups, 1, "topk", gap)
+    n = E // n_groups
+    out = normal(seed + 7, 0, S * E).astype(np.float32).reshape(S, E)
+    pos = S * E
+
+    def close(rows):
+        m = min(k + 1, n)
+        if m < 2:
+            return np.zeros(rows.shape[0], bool)
+        top = -np.sort(-rows.reshape(-1, n_groups, n), axis=2)[:, :, :m]
+        return (np.diff(-top, axis=2) < gap).any(axis=(1, 2))
+    bad = np.nonzero(close(out))[0]
+    while bad.size:
+        fresh = normal(seed + 7, pos, bad.size * E).astype(np.float32).reshape(-1, E)
+        pos += bad.size * E
+        out[bad] = fresh
+        bad = bad[close(out[bad])]
+    return gl, out
+
+
+def uniforms_f32(seed: int, S: int, E: int) -> np.ndarray:
+    """Uniform draws [S, E] float32 in the open interval (0, 1), for the
+    Dense-to-Sparse gate's Gumbel noise: ((x >> 40) + 0.5) * 2^-24."""
+    x = splitmix64(seed, 0, S * E) >> np.uint64(40)
+    return ((x.astype(np.float64) + 0.5) * 2.0 ** -24).astype(np.float32).reshape(S, E)
+
+
 def tokens(seed: int, S: int, d: int, dtype: str = "bf16") -> np.ndarray:
     """Token batch x_S [S, d], i.i.d. N(0,1): float32, or uint16
     bf16 bit patterns when dtype == 'bf16'."""
