@@ -58,7 +58,13 @@ typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype_t;
  *   KTOP1 : M6-T k-top-1, k prototypes of E/k contiguous experts each, top-1
  *           inside every prototype, outputs summed (R11)
  *   HASH  : Hash layer, expert = table[token_id], k = 1 */
-typedef enum { MOE_GATE_TOPK = 0, MOE_GATE_KTOP1 = 1, MOE_GATE_HASH = 2 } moe_gate_kind_t;
+typedef enum {
+  MOE_GATE_TOPK = 0,
+  MOE_GATE_KTOP1 = 1,
+  MOE_GATE_HASH = 2,
+  MOE_GATE_SAM = 3, /* hierarchical top-k (SAM): moe_gate_ex  */
+  MOE_GATE_D2S = 4  /* Dense-to-Sparse, k == E: moe_gate_ex    */
+} moe_gate_kind_t;
 
 /* Combine weights (R1):
  *   RENORM  : Eq. 1 literally, g = softmax over the k selected logits
@@ -141,6 +147,39 @@ moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits,
                       const int32_t* token_ids, const int32_t* table, int32_t vocab,
                       const moe_routing_t* out, void* ws, size_t ws_bytes,
                       moe_stream_t stream);
+
+/* Inputs of every gate kind, for moe_gate_ex. */
+typedef struct {
+  const float* logits;       /* [S,E] fp32, 16-byte aligned (all but HASH)         */
+  const int32_t* token_ids;  /* [S] (HASH)                                          */
+  const int32_t* table;      /* [vocab] (HASH)                                      */
+  int32_t vocab;             /* (HASH)                                              */
+  const float* group_logits; /* [S,n_groups] fp32 (SAM): the Switch Router's scores */
+  int32_t n_groups;          /* SAM: experts in n_groups contiguous groups of E/n   */
+  const float* uniforms;     /* [S,E] fp32 in (0,1) (D2S train: Gumbel draws); NULL
+                                = eval (no noise).  Random numbers are inputs: the
+                                caller owns the generator.                          */
+  double tau;                /* D2S temperature > 0                                 */
+  double eps;                /* D2S prune threshold >= 0 (SPEC: 1e-3)               */
+} moe_gate_inputs_t;
+
+/* moe_gate for every gate kind (the same routing outputs and workspace).
+ * SAM (R17): group g = argmax of group_logits[t] (lowest index on ties),
+ *   then the top-k (k <= E/n_groups, k <= 8) of the logits of experts
+ *   [g*E/n, (g+1)*E/n); weights: RENORM = softmax over the k selected;
+ *   SOFTMAX = P(g) * P(e | g) (group softmax x within-group softmax).
+ * D2S (R18): desc->k must equal E.  z_e = (l_e + G_e)/tau, G_e =
+ *   -log(-log(u_e)) (0 without uniforms), p = softmax(z) over all E; experts
+ *   with p_e < eps are pruned; survivors fill slots 0..k'-1 in descending z
+ *   (ties: lower index) with weight p_e / sum_survivors p (RENORM) or p_e
+ *   (SOFTMAX); pruned slots get expert_idx = slot_idx = -1, weight 0.  All in
+ *   fp64, one rounding; then capacity over the survivors as for every gate.
+ * Errors: as moe_gate; INVALID_ARG for SAM without group_logits or with
+ *   E % n_groups != 0 or k > E/n_groups, D2S with k != E, tau <= 0, eps < 0;
+ *   UNSUPPORTED for SAM with k > 8. */
+moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                         const moe_routing_t* out, void* ws, size_t ws_bytes,
+                         moe_stream_t stream);
 
 /* host, SYNCHRONISES `stream`.  Number of invalid hash tokens seen since the
  * last check (the counter is reset to 0). */

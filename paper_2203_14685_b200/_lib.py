@@ -28,6 +28,13 @@ class RoutingC(ctypes.Structure):
                 ("slot_src", vp)]
 
 
+class GateInputs(ctypes.Structure):
+    """moe_gate_inputs_t"""
+    _fields_ = [("logits", vp), ("token_ids", vp), ("table", vp), ("vocab", i32),
+                ("group_logits", vp), ("n_groups", i32), ("uniforms", vp),
+                ("tau", ctypes.c_double), ("eps", ctypes.c_double)]
+
+
 class A2AOp(ctypes.Structure):
     """moe_a2a_op_t"""
     _fields_ = [("phase", i32), ("op", i32), ("peer", i32), ("src_buf", i32), ("dst_buf", i32),
@@ -40,6 +47,8 @@ SIGNATURES = [
     ("moe_gate_workspace_bytes", sz, [ctypes.POINTER(GateDesc)]),
     ("moe_gate", ctypes.c_int, [ctypes.POINTER(GateDesc), vp, vp, vp, i32,
                                 ctypes.POINTER(RoutingC), vp, sz, vp]),
+    ("moe_gate_ex", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),
+                                   ctypes.POINTER(RoutingC), vp, sz, vp]),
     ("moe_gate_check", ctypes.c_int, [vp, vp, ctypes.POINTER(i32)]),
     ("moe_layout", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp, i32,
                                   i32, vp, vp]),

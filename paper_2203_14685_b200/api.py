@@ -14,9 +14,9 @@ from typing import Optional
 
 import torch
 
-from ._lib import A2AOp, GateDesc, RoutingC, check, lib
+from ._lib import A2AOp, GateDesc, GateInputs, RoutingC, check, lib
 
-KINDS = {"topk": 0, "ktop1": 1, "hash": 2}
+KINDS = {"topk": 0, "ktop1": 1, "hash": 2, "sam": 3, "d2s": 4}
 MODES = {"renorm": 0, "softmax": 1}
 PRIOS = {"token": 0, "slot": 1}
 ALGOS = {"flat": 0, "hier": 1, "p2p": 2}
@@ -87,8 +87,13 @@ class Gate:
     """moe_gate with its persistent (self-resetting) workspace."""
 
     def __init__(self, S: int, E: int, k: int, capacity: int, kind: str = "topk",
-                 weight_mode: str = "renorm", priority: str = "token", device=None):
+                 weight_mode: str = "renorm", priority: str = "token", device=None,
+                 n_groups: int = 1, tau: float = 1.0, eps: float = 1e-3):
+        """kind: topk | ktop1 | hash | sam (n_groups: the Switch Router's
+        groups) | d2s (k must equal E; tau, eps: temperature and prune
+        threshold -- the caller owns the schedule)."""
         self.S, self.E, self.k, self.cap = S, E, k, capacity
+        self.n_groups, self.tau, self.eps = n_groups, tau, eps
         self.kind, self.mode, self.prio = KINDS[kind], MODES[weight_mode], PRIOS[priority]
         self.device = torch.device("cuda") if device is None else torch.device(device)
         d = GateDesc(S, E, k, capacity, self.kind, self.mode, self.prio)
@@ -100,7 +105,11 @@ class Gate:
         self.ws = torch.zeros(nb, dtype=torch.uint8, device=self.device)
 
     def __call__(self, logits: Optional[torch.Tensor] = None, token_ids=None, table=None,
-                 out: Optional[Routing] = None, slot_src: bool = True) -> Routing:
+                 out: Optional[Routing] = None, slot_src: bool = True,
+                 group_logits: Optional[torch.Tensor] = None,
+                 uniforms: Optional[torch.Tensor] = None) -> Routing:
+        """uniforms (d2s, train mode): [S,E] float32 draws in (0,1) for the
+        Gumbel noise; None = eval (no noise)."""
         if out is None:
             out = Routing.empty(self.S, self.E, self.k, self.cap, self.device, self.kind,
                                 self.mode, self.prio, slot_src)
@@ -114,12 +123,21 @@ class Gate:
             if tuple(logits.shape) != (self.S, self.E):
                 raise ValueError("logits shape %s != (S=%d, E=%d)" % (tuple(logits.shape),
                                                                      self.S, self.E))
+        if self.kind == KINDS["sam"]:
+            _need_cuda(group_logits, "group_logits", torch.float32)
+            if tuple(group_logits.shape) != (self.S, self.n_groups):
+                raise ValueError("group_logits must be [S=%d, n_groups=%d]" % (self.S, self.n_groups))
+        if uniforms is not None:
+            _need_cuda(uniforms, "uniforms", torch.float32)
+            if tuple(uniforms.shape) != (self.S, self.E):
+                raise ValueError("uniforms must be [S=%d, E=%d]" % (self.S, self.E))
         out.kind, out.weight_mode, out.priority = self.kind, self.mode, self.prio
         d = GateDesc(self.S, self.E, self.k, self.cap, self.kind, self.mode, self.prio)
+        inp = GateInputs(_p(logits), _p(token_ids), _p(table), vocab, _p(group_logits),
+                         self.n_groups, _p(uniforms), float(self.tau), float(self.eps))
         rc = out.c()
-        check(lib().moe_gate(ctypes.byref(d), _p(logits), _p(token_ids), _p(table), vocab,
-                             ctypes.byref(rc), _p(self.ws), self.ws.numel(),
-                             _stream(self.device)), "moe_gate")
+        check(lib().moe_gate_ex(ctypes.byref(d), ctypes.byref(inp), ctypes.byref(rc), _p(self.ws),
+                                self.ws.numel(), _stream(self.device)), "moe_gate")
         return out
 
     def check(self) -> int:

@@ -14,9 +14,8 @@
 namespace moe {
 
 size_t gate_workspace_bytes(const moe_gate_desc_t& d);
-moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const int32_t* ids,
-                         const int32_t* table, int32_t vocab, const moe_routing_t& out, void* ws,
-                         cudaStream_t stream);
+moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                         const moe_routing_t& out, void* ws, cudaStream_t stream);
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);
 moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                            int dtype_size, int dcols, void* dispatch, cudaStream_t stream);
@@ -79,7 +78,7 @@ static moe_status_t check_desc(const char* fn, const moe_gate_desc_t* d) {
               d->E, d->k, d->capacity);
     return MOE_ERR_INVALID_ARG;
   }
-  if (d->kind < MOE_GATE_TOPK || d->kind > MOE_GATE_HASH) {
+  if (d->kind < MOE_GATE_TOPK || d->kind > MOE_GATE_D2S) {
     set_error("%s: invalid gate kind %d", fn, d->kind);
     return MOE_ERR_INVALID_ARG;
   }
@@ -93,6 +92,11 @@ static moe_status_t check_desc(const char* fn, const moe_gate_desc_t* d) {
   }
   if (d->kind == MOE_GATE_KTOP1 && d->E % d->k != 0) {
     set_error("%s: k-top-1 needs E %% k == 0 (E=%d, k=%d prototypes)", fn, d->E, d->k);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (d->kind == MOE_GATE_D2S && d->k != d->E) {
+    set_error("%s: Dense-to-Sparse needs k == E (every expert is a candidate slot; k=%d, E=%d)",
+              fn, d->k, d->E);
     return MOE_ERR_INVALID_ARG;
   }
   if (d->kind == MOE_GATE_HASH && d->k != 1) {
@@ -163,26 +167,47 @@ size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc) {
   return gate_workspace_bytes(*desc);
 }
 
-moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const int32_t* token_ids,
-                      const int32_t* table, int32_t vocab, const moe_routing_t* out, void* ws,
-                      size_t ws_bytes, moe_stream_t stream) {
+moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                         const moe_routing_t* out, void* ws, size_t ws_bytes,
+                         moe_stream_t stream) {
   moe_status_t s = check_desc("moe_gate", desc);
   if (s != MOE_OK) return s;
+  if (!in) {
+    set_error("moe_gate: inputs are NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
   if (!out || !out->expert_idx || !out->slot_idx || !out->weight || !out->load) {
     set_error("moe_gate: out or one of expert_idx/slot_idx/weight/load is NULL");
     return MOE_ERR_INVALID_ARG;
   }
   if (desc->kind == MOE_GATE_HASH) {
-    if (!token_ids || !table || vocab < 1) {
-      set_error("moe_gate: hash gate needs token_ids, table and vocab >= 1 (vocab=%d)", vocab);
+    if (!in->token_ids || !in->table || in->vocab < 1) {
+      set_error("moe_gate: hash gate needs token_ids, table and vocab >= 1 (vocab=%d)", in->vocab);
       return MOE_ERR_INVALID_ARG;
     }
-  } else if (!logits) {
+  } else if (!in->logits) {
     set_error("moe_gate: logits is NULL");
     return MOE_ERR_INVALID_ARG;
-  } else if (!aligned(logits, 16)) {
+  } else if (!aligned(in->logits, 16)) {
     set_error("moe_gate: logits must be 16-byte aligned (TMA bulk copy source)");
     return MOE_ERR_ALIGNMENT;
+  }
+  if (desc->kind == MOE_GATE_SAM) {
+    const int G = in->n_groups;
+    if (!in->group_logits || G < 1 || desc->E % G != 0 || desc->k > desc->E / G) {
+      set_error("moe_gate: SAM needs group_logits and n_groups dividing E with k <= E/n_groups "
+                "(n_groups=%d E=%d k=%d)", G, desc->E, desc->k);
+      return MOE_ERR_INVALID_ARG;
+    }
+    if (desc->k > 8) {
+      set_error("moe_gate: SAM supports k <= 8 experts per group (k=%d)", desc->k);
+      return MOE_ERR_UNSUPPORTED;
+    }
+  }
+  if (desc->kind == MOE_GATE_D2S && (!(in->tau > 0.0) || !(in->eps >= 0.0))) {
+    set_error("moe_gate: Dense-to-Sparse needs tau > 0 and eps >= 0 (tau=%g eps=%g)", in->tau,
+              in->eps);
+    return MOE_ERR_INVALID_ARG;
   }
   const size_t need = gate_workspace_bytes(*desc);
   if (!ws || ws_bytes < need) {
@@ -193,8 +218,22 @@ moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const in
     set_error("moe_gate: workspace must be 16-byte aligned");
     return MOE_ERR_ALIGNMENT;
   }
-  return gate_launch(*desc, logits, token_ids, table, vocab, *out, ws,
-                     reinterpret_cast<cudaStream_t>(stream));
+  return gate_launch(*desc, *in, *out, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const int32_t* token_ids,
+                      const int32_t* table, int32_t vocab, const moe_routing_t* out, void* ws,
+                      size_t ws_bytes, moe_stream_t stream) {
+  if (desc && (desc->kind == MOE_GATE_SAM || desc->kind == MOE_GATE_D2S)) {
+    set_error("moe_gate: SAM and Dense-to-Sparse gates take extra inputs: use moe_gate_ex");
+    return MOE_ERR_INVALID_ARG;
+  }
+  moe_gate_inputs_t in{};
+  in.logits = logits;
+  in.token_ids = token_ids;
+  in.table = table;
+  in.vocab = vocab;
+  return moe_gate_ex(desc, &in, out, ws, ws_bytes, stream);
 }
 
 moe_status_t moe_gate_check(void* ws, moe_stream_t stream, int32_t* bad_count) {

@@ -51,6 +51,13 @@ struct GateArgs {
   int S, E, k, cap, mode, prio;
   int tile_tokens, n_tiles, ncols;
   int lg_words;  // shared-memory words of the staged logits tile (16-byte multiple)
+  int z_words;   // D2S: shared-memory words of the per-tile z = (l + G)/tau doubles
+  // SAM (R17): group logits [S, ngroups], experts in contiguous groups
+  const float* glogits;
+  int ngroups;
+  // Dense-to-Sparse (R18): uniforms [S, E] in (0,1) (NULL = eval), tau, eps
+  const float* uniforms;
+  double tau, eps;
   int32_t* expert_idx;
   int32_t* slot_idx;
   float* weight;
@@ -65,7 +72,7 @@ struct GateArgs {
 
 // ------------------------------------------------------------ layout of ws
 struct GatePlan {
-  int L, K, tile_tokens, n_tiles, ncols, lg_words;
+  int L, K, tile_tokens, n_tiles, ncols, lg_words, z_words;
   size_t status_off, totals_off, bytes, smem;
 };
 
@@ -78,9 +85,9 @@ static int choose_lanes(int E) {
 // want_tiles: the three-kernel path wants >= 256 tiles when S allows (about
 // 1.7 CTAs per SM on 148 SMs); the single-launch path fewer, larger tiles
 // (every CTA reduces all tiles' aggregates after its grid barrier).
-static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles = 256) {
+static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles = 256, int ngroups = 1) {
   GatePlan p{};
-  p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.E);
+  p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.kind == MOE_GATE_SAM ? d.E / std::max(1, ngroups) : d.E);
   p.K = d.k <= 1 ? 1 : d.k <= 2 ? 2 : d.k <= 4 ? 4 : d.k <= 8 ? 8 : 0;
   // tiles of 32..256 tokens, at most kMaxTileItems items per tile
   int tt = 256;
@@ -98,7 +105,8 @@ static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles = 256) {
   p.bytes = (p.bytes + 255) & ~(size_t)255;
   size_t items = (size_t)tt * d.k;
   p.lg_words = d.kind == MOE_GATE_HASH ? 0 : ((tt * d.E + 3) & ~3);
-  p.smem = sizeof(int) * (p.lg_words + 2 * items + (size_t)kGateWarps * p.ncols);
+  p.z_words = d.kind == MOE_GATE_D2S ? 2 * tt * d.E : 0;
+  p.smem = sizeof(int) * (p.lg_words + p.z_words + 2 * items + (size_t)kGateWarps * p.ncols);
   return p;
 }
 
@@ -170,10 +178,14 @@ __device__ __forceinline__ float group_max(float x) {
 }
 
 // Top-k (Eq. 1), register path, K >= k.
+// `row` is the softmax/selection domain (the whole row, or SAM's group
+// slice starting at expert `ebase`); SAM SOFTMAX multiplies by `scale` =
+// P(group).
 template <int L, int K>
 __device__ __forceinline__ void select_topk_reg(const GateArgs& a, const float* row, int t,
                                                 bool valid, int l, int epl, bool vec4,
-                                                int* s_sel /*[k]*/) {
+                                                int* s_sel /*[k]*/, int ebase = 0,
+                                                double scale = 1.0) {
   TopList<K> top;
   top.init();
   if (valid) for_lane_logits(row, l, epl, vec4, [&](float x, int e) { top.insert(x, e); });
@@ -210,9 +222,9 @@ __device__ __forceinline__ void select_topk_reg(const GateArgs& a, const float* 
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       if (p < a.k) {
-        a.expert_idx[o + p] = top.i[p];
-        a.weight[o + p] = (float)(ex[p] / den);
-        s_sel[p] = top.i[p];
+        a.expert_idx[o + p] = ebase + top.i[p];
+        a.weight[o + p] = (float)(scale * (ex[p] / den));
+        s_sel[p] = ebase + top.i[p];
       }
     }
   }
@@ -337,8 +349,122 @@ __device__ __forceinline__ void select_rank(const GateArgs& a, const float* row,
   }
 }
 
+// Hierarchical top-k / SAM (R17), K >= k: the Switch
+// Router picks group g = argmax of the group logits (lowest index on ties;
+// the L lanes of the token scan strided and merge with a butterfly), then the
+// Mixture Router is the top-k register path on the group's n logits.
+// SOFTMAX: weight = P(g) * within-group softmax, P(g) in fp64.
+template <int L, int K>
+__device__ __forceinline__ void select_sam_reg(const GateArgs& a, const float* row, int t,
+                                               bool valid, int l, int* s_sel) {
+  const int n = a.E / a.ngroups;
+  const float* gl = a.glogits + (size_t)t * a.ngroups;
+  float bv = -INFINITY;
+  int bi = INT_MAX;
+  if (valid)
+    for (int h = l; h < a.ngroups; h += L) {
+      const float x = __ldg(gl + h);
+      if (beats(x, h, bv, bi)) {
+        bv = x;
+        bi = h;
+      }
+    }
+#pragma unroll
+  for (int m = 1; m < L; m <<= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, m);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+    if (beats(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  const int g = valid ? bi : 0;
+  double pg = 1.0;
+  if (a.mode == MOE_W_SOFTMAX) {
+    double part = 0.0;
+    if (valid)
+      for (int h = l; h < a.ngroups; h += L) part += exp((double)__ldg(gl + h) - (double)bv);
+    pg = 1.0 / group_sum<L>(part);
+  }
+  const int epl = n / L;
+  const bool vec4 = (n % 4 == 0) && (epl % 4 == 0);
+  select_topk_reg<L, K>(a, row + (size_t)g * n, t, valid, l, epl, vec4, s_sel, g * n, pg);
+}
+
+template <int L>
+__device__ __forceinline__ double group_max_d(double x) {
+#pragma unroll
+  for (int m = 1; m < L; m <<= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, m));
+  return x;
+}
+
+// Dense-to-Sparse (R18), k = E slots: z_e = (l_e + G_e)/tau
+// in fp64 with G_e = -log(-log(u_e)) (train) or 0 (eval); p = softmax(z);
+// survivors p_e >= eps fill slots 0..k'-1 in descending z (ties: lower
+// index): each lane ranks its survivors against the token's z row in shared
+// memory (pruned entries set to -inf first).  Pruned slots: expert -1,
+// weight 0 (not admitted by the capacity pass).
+template <int L>
+__device__ __forceinline__ void select_d2s(const GateArgs& a, const float* row, double* zrow,
+                                           int t, bool valid, int l, int* s_sel) {
+  const int E = a.E, epl = E / L;
+  const float* u = a.uniforms ? a.uniforms + (size_t)t * E : nullptr;
+  double mx = -INFINITY;
+  for (int q = 0; q < epl && valid; ++q) {
+    const int e = l * epl + q;
+    const double g = u ? -log(-log((double)__ldg(u + e))) : 0.0;
+    const double z = ((double)row[e] + g) / a.tau;
+    zrow[e] = z;
+    mx = fmax(mx, z);
+  }
+  mx = group_max_d<L>(mx);
+  double part = 0.0;
+  for (int q = 0; q < epl && valid; ++q) part += exp(zrow[l * epl + q] - mx);
+  const double den = group_sum<L>(part);
+  double psum = 0.0;
+  int ns = 0;
+  for (int q = 0; q < epl && valid; ++q) {
+    const int e = l * epl + q;
+    const double p = exp(zrow[e] - mx) / den;
+    if (p >= a.eps) {
+      psum += p;
+      ++ns;
+    }
+  }
+  psum = group_sum<L>(psum);
+#pragma unroll
+  for (int m = 1; m < L; m <<= 1) ns += __shfl_xor_sync(0xffffffffu, ns, m);
+  // survivors keep z, pruned -> -inf (each lane only rewrites its own
+  // entries, which no other lane has read yet), then rank against the row
+  for (int q = 0; q < epl && valid; ++q) {
+    const int e = l * epl + q;
+    if (!(exp(zrow[e] - mx) / den >= a.eps)) zrow[e] = -INFINITY;
+  }
+  __syncwarp();
+  if (!valid) return;
+  const size_t o = (size_t)t * E;
+  for (int q = 0; q < epl; ++q) {
+    const int e = l * epl + q;
+    const double z = zrow[e];
+    if (z == -INFINITY) continue;
+    int r = 0;
+    for (int e2 = 0; e2 < E; ++e2) {
+      const double z2 = zrow[e2];
+      r += (z2 > z || (z2 == z && e2 < e)) ? 1 : 0;
+    }
+    const double p = exp(z - mx) / den;
+    a.expert_idx[o + r] = e;
+    a.weight[o + r] = (float)(a.mode == MOE_W_RENORM ? p / psum : p);
+    s_sel[r] = e;
+  }
+  for (int j = ns + l; j < E; j += L) {
+    a.expert_idx[o + j] = -1;
+    a.weight[o + j] = 0.f;
+  }
+}
+
 // ------------------------------------------------------------ the kernel
-enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2 };
+enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2, KIND_SAM = 3, KIND_D2S = 4 };
 
 // Phases A and B of one tile (shared by k_gate_select and k_gate_fused):
 // stage the logits, select + weights (expert_idx, weight written), in-tile
@@ -350,7 +476,8 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
                                           unsigned long long& s_mbar) {
   const int items = a.tile_tokens * a.k;
   float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
-  int* s_exp = smem + a.lg_words;             // [items] expert of item tt*k+j
+  double* s_z = reinterpret_cast<double*>(smem + a.lg_words);  // D2S: [tile_tokens][E]
+  int* s_exp = smem + a.lg_words + a.z_words;  // [items] expert of item tt*k+j
   int* s_rank = s_exp + items;                // [items] rank inside its warp
   int* s_hist = s_rank + items;               // [warps][ncols]
 
@@ -421,7 +548,11 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
       const int t = valid ? t0 + tt : 0;
       int* s_sel = s_exp + (size_t)tt * a.k;
       const float* row = s_lg + (size_t)(valid ? tt : 0) * a.E;
-      if constexpr (K == 0) {
+      if constexpr (KIND == KIND_D2S) {
+        select_d2s<L>(a, row, s_z + (size_t)(valid ? tt : 0) * a.E, t, valid, l, s_sel);
+      } else if constexpr (KIND == KIND_SAM) {
+        select_sam_reg<L, K>(a, row, t, valid, l, s_sel);
+      } else if constexpr (K == 0) {
         select_rank<L, KIND == KIND_KTOP1>(a, row, t, valid, l, epl, s_sel);
       } else if constexpr (KIND == KIND_TOPK) {
         select_topk_reg<L, K>(a, row, t, valid, l, epl, vec4, s_sel);
@@ -490,7 +621,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
   const int tid = threadIdx.x;
   const int items = a.tile_tokens * a.k;
-  const int* s_exp = smem + a.lg_words;
+  const int* s_exp = smem + a.lg_words + a.z_words;
   const int* s_rank = s_exp + items;
   const int* s_hist = s_rank + items;
   const int tile = blockIdx.x;
@@ -649,7 +780,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_fused(GateArgs a) {
   gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int items = a.tile_tokens * a.k;
-  const int* s_exp = smem + a.lg_words;
+  const int* s_exp = smem + a.lg_words + a.z_words;
   const int* s_rank = s_exp + items;
   const int* s_hist = s_rank + items;
   int* s_pre = const_cast<int*>(s_hist) + kGateWarps * a.ncols;  // [ncols] earlier tiles
@@ -755,8 +886,39 @@ static GateKernel pick_l(int L, int K) {
     default: return pick_k<KIND, 32, FUSED>(K);
   }
 }
+template <int L>
+static GateKernel pick_sam_k(int K) {
+  switch (K) {
+    case 1: return k_gate_select<KIND_SAM, L, 1>;
+    case 2: return k_gate_select<KIND_SAM, L, 2>;
+    case 4: return k_gate_select<KIND_SAM, L, 4>;
+    default: return k_gate_select<KIND_SAM, L, 8>;
+  }
+}
+static GateKernel pick_sam(int L, int K) {
+  switch (L) {
+    case 1: return pick_sam_k<1>(K);
+    case 2: return pick_sam_k<2>(K);
+    case 4: return pick_sam_k<4>(K);
+    case 8: return pick_sam_k<8>(K);
+    case 16: return pick_sam_k<16>(K);
+    default: return pick_sam_k<32>(K);
+  }
+}
+static GateKernel pick_d2s(int L) {
+  switch (L) {
+    case 1: return k_gate_select<KIND_D2S, 1, 1>;
+    case 2: return k_gate_select<KIND_D2S, 2, 1>;
+    case 4: return k_gate_select<KIND_D2S, 4, 1>;
+    case 8: return k_gate_select<KIND_D2S, 8, 1>;
+    case 16: return k_gate_select<KIND_D2S, 16, 1>;
+    default: return k_gate_select<KIND_D2S, 32, 1>;
+  }
+}
 template <bool FUSED>
 static GateKernel pick_gate(const moe_gate_desc_t& d, const GatePlan& p) {
+  if (!FUSED && d.kind == MOE_GATE_SAM) return pick_sam(p.L, p.K);
+  if (!FUSED && d.kind == MOE_GATE_D2S) return pick_d2s(p.L);
   return d.kind == MOE_GATE_HASH    ? (FUSED ? k_gate_fused<KIND_HASH, 1, 1> : k_gate_select<KIND_HASH, 1, 1>)
          : d.kind == MOE_GATE_KTOP1 ? pick_l<KIND_KTOP1, FUSED>(p.L, p.K)
                                     : pick_l<KIND_TOPK, FUSED>(p.L, p.K);
@@ -773,7 +935,7 @@ static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, Ga
                                  cudaStream_t stream) {
   void* args[] = {&a};
   GateKernel kern = pick_gate<false>(d, p);
-  if (p.smem > 48 * 1024) {
+  if (p.smem > 40 * 1024) {  // + static shared memory
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)p.smem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
@@ -789,24 +951,30 @@ static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, Ga
   return MOE_OK;
 }
 
-moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const int32_t* ids,
-                         const int32_t* table, int32_t vocab, const moe_routing_t& out, void* ws,
-                         cudaStream_t stream) {
+moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                         const moe_routing_t& out, void* ws, cudaStream_t stream) {
   // one launch with a grid barrier when every tile's CTA fits on the device
   // at once and the per-CTA reduction (tiles x columns words) is small
-  const GatePlan pf = gate_plan(d, fused_tiles());
-  bool fused = env_int("MOE_GATE_FUSED", 0) &&
+  const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
+  const GatePlan pf = gate_plan(d, fused_tiles(), ng);
+  bool fused = env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH &&
                (long long)pf.n_tiles * pf.ncols <= env_int("MOE_GATE_FUSED_MAXW", 8192);
-  const GatePlan p = fused ? pf : gate_plan(d);
+  const GatePlan p = fused ? pf : gate_plan(d, 256, ng);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
   }
   GateArgs a{};
-  a.logits = logits;
-  a.ids = ids;
-  a.table = table;
-  a.vocab = vocab;
+  a.logits = in.logits;
+  a.ids = in.token_ids;
+  a.table = in.table;
+  a.vocab = in.vocab;
+  a.glogits = in.group_logits;
+  a.ngroups = ng;
+  a.uniforms = in.uniforms;
+  a.tau = in.tau;
+  a.eps = in.eps;
+  a.z_words = p.z_words;
   a.S = d.S;
   a.E = d.E;
   a.k = d.k;
@@ -832,14 +1000,14 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const float* logits, const in
     GateKernel fk = pick_gate<true>(d, p);
     const size_t fsmem = p.smem + 2 * sizeof(int) * (size_t)p.ncols;
     cudaError_t e = cudaSuccess;
-    if (fsmem > 48 * 1024)
+    if (fsmem > 40 * 1024)
       e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     int per_sm = 0;
     if (e == cudaSuccess)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fk, kGateThreads, fsmem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: fused occupancy");
     if (p.n_tiles > per_sm * device_sm_count()) {
-      const GatePlan p3 = gate_plan(d);
+      const GatePlan p3 = gate_plan(d, 256, ng);
       a.tile_tokens = p3.tile_tokens;
       a.n_tiles = p3.n_tiles;
       a.lg_words = p3.lg_words;

@@ -79,7 +79,8 @@ def _gate(desc, logits=FAKE, ids=None, table=None, vocab=0, routing="ok", ws=FAK
 
 @pytest.mark.parametrize("fields,status", [
     (dict(S=0), INVALID), (dict(E=0), INVALID), (dict(k=0), INVALID), (dict(k=9), INVALID),
-    (dict(capacity=0), INVALID), (dict(kind=3), INVALID), (dict(weight_mode=2), INVALID),
+    (dict(capacity=0), INVALID), (dict(kind=5), INVALID), (dict(weight_mode=2), INVALID),
+    (dict(kind=4, k=2), INVALID),                                # Dense-to-Sparse needs k == E
     (dict(priority=5), INVALID), (dict(kind=1, k=3), INVALID),   # E % k != 0
     (dict(kind=2, k=2), INVALID),                                # hash needs k == 1
     (dict(E=257, k=1), UNSUPPORTED),
@@ -94,6 +95,32 @@ def test_gate_rejects_invalid_desc(fields, status):
         assert ws_need == 0
     assert _gate(d) == status
     assert lib().moe_last_error().decode().startswith("moe_gate")
+
+
+def test_gate_ex_kinds_need_their_inputs():
+    """SAM / D2S go through moe_gate_ex; their extra inputs are checked on the
+    host before anything is enqueued."""
+    from paper_2203_14685_b200._lib import GateInputs
+    L = lib()
+    r = RoutingC(FAKE, FAKE, FAKE, FAKE, None)
+    sam = GateDesc(64, 8, 2, 16, 3, 0, 0)
+    assert _gate(sam) == INVALID and "moe_gate_ex" in L.moe_last_error().decode()
+    need = L.moe_gate_workspace_bytes(ctypes.byref(sam))
+    assert need > 0
+
+    def ex(d, **kw):
+        base = dict(logits=FAKE, token_ids=None, table=None, vocab=0, group_logits=FAKE,
+                    n_groups=2, uniforms=None, tau=1.0, eps=1e-3)
+        base.update(kw)
+        return L.moe_gate_ex(ctypes.byref(d), ctypes.byref(GateInputs(**base)), ctypes.byref(r),
+                             FAKE, need, None)
+    assert ex(sam, group_logits=None) == INVALID
+    assert ex(sam, n_groups=3) == INVALID                # 3 does not divide E = 8
+    assert ex(sam, n_groups=8) == INVALID                # k = 2 > E/n_groups = 1
+    assert ex(GateDesc(64, 64, 9, 16, 3, 0, 0), n_groups=4) == UNSUPPORTED  # k > 8
+    d2s = GateDesc(64, 8, 8, 16, 4, 0, 0)
+    assert ex(d2s, tau=0.0) == INVALID
+    assert ex(d2s, eps=-1.0) == INVALID
 
 
 def test_gate_rejects_missing_buffers():
