@@ -89,6 +89,15 @@ def lib():
         L.orc_gate_d2s.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, ctypes.c_double,
                                    ctypes.c_double, P, P, P, P, P, P, P]
         L.orc_gate_d2s.restype = i64
+        L.orc_expert_offsets.argtypes = [i32, i32, P, P]
+        L.orc_expert_offsets.restype = None
+        L.orc_layout_packed.argtypes = [i32, i32, i32, i64, P, P, P, P, P]
+        L.orc_layout_packed.restype = None
+        L.orc_reverse_layout_packed.argtypes = [ctypes.c_int, i32, i32, i32, i32, P, P, P, P, P,
+                                                P]
+        L.orc_reverse_layout_packed.restype = None
+        L.orc_alltoallv.argtypes = [i32, i64, P, ctypes.POINTER(P), ctypes.POINTER(P)]
+        L.orc_alltoallv.restype = None
         L.orc_reverse_layout_bwd.argtypes = [ctypes.c_int, i32, i32, i32, i32, i32, P, P, P,
                                              P, P, P, P]
         L.orc_reverse_layout_bwd.restype = None
@@ -223,6 +232,48 @@ def expert_scale(buf: np.ndarray, e_base: int) -> np.ndarray:
     out = np.empty_like(buf)
     lib().orc_expert_scale(_dt(buf), nsrc, El, e_base, cap, d, _ptr(buf), _ptr(out))
     return out
+
+
+def expert_offsets(r: Routing) -> np.ndarray:
+    """SPEC's Permutation.expert_offsets [E+1] of the admitted slots."""
+    out = np.empty((r.E + 1,), np.int32)
+    lib().orc_expert_offsets(r.E, r.cap, _ptr(np.ascontiguousarray(r.load, np.int32)), _ptr(out))
+    return out
+
+
+def layout_packed(x: np.ndarray, r: Routing, offsets: np.ndarray) -> np.ndarray:
+    """Dropless packed layout: [offsets[E], d] rows, expert-major."""
+    x = np.ascontiguousarray(x)
+    S, d = x.shape
+    offsets = np.ascontiguousarray(offsets, np.int32)
+    out = np.empty((int(offsets[-1]), d), x.dtype)
+    lib().orc_layout_packed(S, r.E, r.k, d * x.itemsize, _ptr(r.expert_idx), _ptr(r.slot_idx),
+                            _ptr(offsets), _ptr(x), _ptr(out))
+    return out
+
+
+def reverse_layout_packed(back: np.ndarray, r: Routing, offsets: np.ndarray) -> np.ndarray:
+    back = np.ascontiguousarray(back)
+    d = back.shape[-1]
+    offsets = np.ascontiguousarray(offsets, np.int32)
+    y = np.empty((r.S, d), back.dtype)
+    lib().orc_reverse_layout_packed(_dt(back), r.S, r.E, r.k, d, _ptr(r.expert_idx),
+                                    _ptr(r.slot_idx), _ptr(r.weight), _ptr(offsets), _ptr(back),
+                                    _ptr(y))
+    return y
+
+
+def alltoallv(sends, counts):
+    """sends[q]: [rows_q, ...] arrays of one row size; counts [P, P]: rows q
+    sends to r.  Returns recv[r] (segments in ascending source rank)."""
+    P = len(sends)
+    sends = [np.ascontiguousarray(s) for s in sends]
+    counts = np.ascontiguousarray(counts, np.int64)
+    row_shape = sends[0].shape[1:]
+    row_bytes = int(np.prod(row_shape, dtype=np.int64)) * sends[0].itemsize
+    recvs = [np.empty((int(counts[:, r].sum()),) + row_shape, sends[0].dtype) for r in range(P)]
+    lib().orc_alltoallv(P, row_bytes, _ptr(counts), _ptrs(sends), _ptrs(recvs))
+    return recvs
 
 
 def reverse_layout_bwd(dy: np.ndarray, back: np.ndarray, r: Routing):

@@ -580,3 +580,59 @@ int64_t orc_gate_d2s(int weight_mode, int priority, int32_t S, int32_t E, int32_
   capacity_replay(priority, S, E, k, cap, expert_idx, slot_idx, weight, load, slot_src);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Dropless packed layout.            */
+/* ------------------------------------------------------------------------ */
+void orc_expert_offsets(int32_t E, int32_t cap, const int32_t* load, int32_t* offsets) {
+  offsets[0] = 0;
+  for (int32_t e = 0; e < E; ++e)
+    offsets[e + 1] = offsets[e] + (load[e] < cap ? load[e] : cap);
+}
+
+void orc_layout_packed(int32_t S, int32_t E, int32_t k, int64_t row_bytes,
+                       const int32_t* expert_idx, const int32_t* slot_idx,
+                       const int32_t* offsets, const void* x, void* packed) {
+  (void)E;
+  for (int32_t t = 0; t < S; ++t)
+    for (int32_t j = 0; j < k; ++j) {
+      int64_t i = (int64_t)t * k + j;
+      if (slot_idx[i] < 0) continue;
+      int64_t row = (int64_t)offsets[expert_idx[i]] + slot_idx[i];
+      memcpy((char*)packed + row * row_bytes, (const char*)x + (int64_t)t * row_bytes,
+             (size_t)row_bytes);
+    }
+}
+
+void orc_reverse_layout_packed(int dtype, int32_t S, int32_t E, int32_t k, int32_t d,
+                               const int32_t* expert_idx, const int32_t* slot_idx,
+                               const float* weight, const int32_t* offsets,
+                               const void* back, void* y) {
+  (void)E;
+  for (int32_t t = 0; t < S; ++t)
+    for (int32_t c = 0; c < d; ++c) {
+      double acc = 0.0;
+      for (int32_t j = 0; j < k; ++j) {
+        int64_t i = (int64_t)t * k + j;
+        if (slot_idx[i] < 0) continue;
+        int64_t row = (int64_t)offsets[expert_idx[i]] + slot_idx[i];
+        acc += (double)weight[i] * load_elem(dtype, back, row * d + c);
+      }
+      store_elem(dtype, y, (int64_t)t * d + c, acc);
+    }
+}
+
+void orc_alltoallv(int32_t P, int64_t row_bytes, const int64_t* counts,
+                   const void* const* send, void* const* recv) {
+  for (int32_t r = 0; r < P; ++r) {
+    int64_t at = 0;  /* rows already placed in recv[r] */
+    for (int32_t q = 0; q < P; ++q) {
+      int64_t from = 0;  /* rows of send[q] before its segment for r */
+      for (int32_t rr = 0; rr < r; ++rr) from += counts[(int64_t)q * P + rr];
+      int64_t n = counts[(int64_t)q * P + r];
+      memcpy((char*)recv[r] + at * row_bytes, (const char*)send[q] + from * row_bytes,
+             (size_t)(n * row_bytes));
+      at += n;
+    }
+  }
+}

@@ -132,6 +132,33 @@ int orc_alltoall_hier(int32_t P, int32_t G, int64_t bytes_per_peer,
 void orc_alltoall_flat_stats(int32_t P, int32_t G, int64_t bytes_per_peer,
                              orc_a2a_stats_t* stats);
 
+/* ---- Dropless packed layout (SPEC.md:241-256
+ * "Permutation": rows grouped by expert ascending, within an expert in
+ * admission order -- a stable counting sort; no padding rows). */
+
+/* offsets[e] = sum_{e' < e} min(load[e'], cap), e = 0..E (offsets[E] = R,
+ * the number of admitted slots). */
+void orc_expert_offsets(int32_t E, int32_t cap, const int32_t* load, int32_t* offsets);
+
+/* packed[offsets[e] + s][:] = x[t][:] for every admitted (t,j) at (e,s);
+ * [offsets[E]][row] bytes.  Byte copy. */
+void orc_layout_packed(int32_t S, int32_t E, int32_t k, int64_t row_bytes,
+                       const int32_t* expert_idx, const int32_t* slot_idx,
+                       const int32_t* offsets, const void* x, void* packed);
+
+/* y[t] = sum_{j ascending, admitted} w[t,j] * back[offsets[e] + s] (double,
+ * one rounding); 0 for a fully dropped token. */
+void orc_reverse_layout_packed(int dtype, int32_t S, int32_t E, int32_t k, int32_t d,
+                               const int32_t* expert_idx, const int32_t* slot_idx,
+                               const float* weight, const int32_t* offsets,
+                               const void* back, void* y);
+
+/* Variable-size AllToAll (the dropless exchange): rank q sends rows
+ * counts[q*P + r] to rank r, taken consecutively from send[q] in ascending
+ * r; recv[r] = the segments of every q in ascending q.  Rows of row_bytes. */
+void orc_alltoallv(int32_t P, int64_t row_bytes, const int64_t* counts,
+                   const void* const* send, void* const* recv);
+
 /* ---- Backward of the routing path: Algorithm 1 is a
  * training process, so each forward step has an
  * adjoint.  Routing (expert_idx, slot_idx, weight) is the forward's output and
