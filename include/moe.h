@@ -220,6 +220,32 @@ moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E
                               int32_t e_base, int32_t cap, int32_t d, int32_t dtype,
                               moe_stream_t stream);
 
+/* ---------------------------------------------------------------- dropless packed form
+ * SURVEY §8(f) NEXT-4.  SPEC's Permutation: the admitted
+ * rows grouped by expert ascending, within an expert in admission order
+ * (slot), no padding.  With capacity >= every load (e.g. S*k) nothing is
+ * dropped: exact hash-gate semantics without a padding tax. */
+
+/* offsets[e] = sum_{e' < e} min(load[e'], capacity), e = 0..E; offsets[E]
+ * = R, the admitted rows.  One tiny kernel (E <= 256).  offsets: [E+1]
+ * int32 device. */
+moe_status_t moe_expert_offsets(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                int32_t* offsets, moe_stream_t stream);
+
+/* packed[offsets[e] + s][:] = x[t][:] for every admitted (t,j) at (e,s).
+ * packed: [>= offsets[E], d] of dtype (size it for the worst case S*k rows
+ * to avoid reading offsets[E] on the host).  Errors: as moe_layout. */
+moe_status_t moe_layout_packed(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                               const int32_t* offsets, const void* x, int32_t d, int32_t dtype,
+                               void* packed, moe_stream_t stream);
+
+/* y[t] = sum_{j ascending, admitted} weight[t*k+j] * back[offsets[e] + s]
+ * (fp32 accumulate, one RNE store; 0 if every slot was dropped). */
+moe_status_t moe_reverse_layout_packed(const moe_gate_desc_t* desc,
+                                       const moe_routing_t* routing, const int32_t* offsets,
+                                       const void* back, int32_t d, int32_t dtype, void* y,
+                                       moe_stream_t stream);
+
 /* ---------------------------------------------------------------- backward
  * SURVEY §8(f) NEXT-1.  Algorithm 1 is a training process (PAPER.md:26-28,
  * 41-68); these are the adjoints of its routing steps, with the routing of
@@ -378,6 +404,48 @@ moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* 
                                        const moe_routing_t* routing, const void* d_recv,
                                        int32_t d, int32_t dtype, void* dx, int32_t flags,
                                        moe_stream_t stream);
+
+/* Variable-size AllToAll (the NCCL dropless exchange): rank r sends
+ * send_rows[q] rows of row_bytes to every rank q, taken consecutively from
+ * `send` in ascending q, and receives recv_rows[q] rows from every q into
+ * `recv`, consecutively in ascending q (SPEC's alltoallv).  send_rows /
+ * recv_rows are HOST arrays [nranks] (exchange the per-expert counts first,
+ * e.g. moe_alltoall(FLAT) of an int32 [P][E/P] count table, and read them on
+ * the host).  Collective.  Errors: INVALID_ARG, NCCL. */
+moe_status_t moe_alltoallv(moe_comm_t* comm, const void* send, const int64_t* send_rows,
+                           void* recv, const int64_t* recv_rows, size_t row_bytes,
+                           moe_stream_t stream);
+
+/* Dropless dispatch over NVLink, no host synchronisation: the count
+ * exchange and the offsets are computed on the device.
+ *  1. (entry barrier) rank r stores its per-expert admitted counts for rank
+ *     q's experts into q's symmetric `counts` [P][E/P] int32 at row r;
+ *     barrier;
+ *  2. peer_base[q] = rows earlier ranks put into q's recv (read from q's
+ *     counts); recv_offsets[src*E/P + le] = where rank src's rows of local
+ *     expert le start in this rank's recv (prefix over `counts`), [E+1];
+ *  3. every admitted row x[t] of (e,s) is stored into q = e/(E/P)'s `recv`
+ *     at row peer_base[q] + offsets[e] - offsets[q*E/P] + s; (exit barrier).
+ * recv layout: source-rank major, then local expert, then slot -- equal to
+ * moe_alltoallv of moe_layout_packed.  recv: symmetric, recv_cap_rows rows,
+ * which must be >= nranks*S*k (the worst case: everything to one rank).
+ * offsets: this rank's moe_expert_offsets; peer_base [P], recv_offsets
+ * [E+1] int32 device outputs (keep them for the combine). */
+moe_status_t moe_dispatch_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                     const moe_routing_t* routing, const int32_t* offsets,
+                                     int32_t* counts, int32_t* peer_base, int32_t* recv_offsets,
+                                     const void* x, int32_t d, int32_t dtype, void* recv,
+                                     int64_t recv_cap_rows, int32_t flags, moe_stream_t stream);
+
+/* Dropless combine over NVLink: (entry barrier) y[t] = sum_j w[t,j] *
+ * expert_out_q[peer_base[q] + offsets[e] - offsets[q*E/P] + s] read from
+ * each owner q (fp32 accumulate, one RNE store); (exit barrier).
+ * expert_out: symmetric, recv layout of moe_dispatch_packed_p2p. */
+moe_status_t moe_combine_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                    const moe_routing_t* routing, const int32_t* offsets,
+                                    const int32_t* peer_base, const void* expert_out, int32_t d,
+                                    int32_t dtype, int64_t expert_out_rows, void* y,
+                                    int32_t flags, moe_stream_t stream);
 
 /* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
  * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,

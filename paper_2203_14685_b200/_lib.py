@@ -55,6 +55,20 @@ SIGNATURES = [
     ("moe_reverse_layout", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
                                           i32, i32, vp, vp]),
     ("moe_expert_scale", ctypes.c_int, [vp, vp, i32, i32, i32, i32, i32, i32, vp]),
+    ("moe_expert_offsets", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
+                                          vp]),
+    ("moe_layout_packed", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
+                                         vp, i32, i32, vp, vp]),
+    ("moe_reverse_layout_packed", ctypes.c_int, [ctypes.POINTER(GateDesc),
+                                                 ctypes.POINTER(RoutingC), vp, vp, i32, i32, vp,
+                                                 vp]),
+    ("moe_alltoallv", ctypes.c_int, [vp, vp, ctypes.POINTER(i64), vp, ctypes.POINTER(i64), sz, vp]),
+    ("moe_dispatch_packed_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                               ctypes.POINTER(RoutingC), vp, vp, vp, vp, vp, i32,
+                                               i32, vp, i64, i32, vp]),
+    ("moe_combine_packed_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                              ctypes.POINTER(RoutingC), vp, vp, vp, i32, i32, i64,
+                                              vp, i32, vp]),
     ("moe_reverse_layout_backward", ctypes.c_int, [ctypes.POINTER(GateDesc),
                                                    ctypes.POINTER(RoutingC), vp, vp, i32, i32,
                                                    vp, vp, vp]),

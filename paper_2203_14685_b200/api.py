@@ -200,6 +200,48 @@ def reverse_layout(back: torch.Tensor, r: Routing,
     return out
 
 
+def expert_offsets(r: Routing, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """[E+1] int32: offsets[e] = sum_{e'<e} min(load[e'], cap) (NEXT-4,
+    SPEC's Permutation.expert_offsets), computed on the device."""
+    if out is None:
+        out = torch.empty((r.E + 1,), dtype=torch.int32, device=r.load.device)
+    _need_cuda(out, "offsets", torch.int32)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_expert_offsets(ctypes.byref(desc), ctypes.byref(rc), _p(out),
+                                   _stream(out.device)), "moe_expert_offsets")
+    return out
+
+
+def layout_packed(x: torch.Tensor, r: Routing, offsets: torch.Tensor,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Dropless Layout_Transform: admitted rows expert-major, no padding.
+    `out` defaults to the worst case [S*k, d] (rows >= offsets[E] unused)."""
+    _need_cuda(x, "x")
+    _need_cuda(offsets, "offsets", torch.int32)
+    S, d = x.shape
+    if out is None:
+        out = torch.empty((r.S * r.k, d), dtype=x.dtype, device=x.device)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_layout_packed(ctypes.byref(desc), ctypes.byref(rc), _p(offsets), _p(x), d,
+                                  _DT[x.dtype], _p(out), _stream(x.device)), "moe_layout_packed")
+    return out
+
+
+def reverse_layout_packed(back: torch.Tensor, r: Routing, offsets: torch.Tensor,
+                          out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Dropless weighted Reverse_Layout_Transform from the packed rows."""
+    _need_cuda(back, "back")
+    _need_cuda(offsets, "offsets", torch.int32)
+    d = back.shape[-1]
+    if out is None:
+        out = torch.empty((r.S, d), dtype=back.dtype, device=back.device)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_reverse_layout_packed(ctypes.byref(desc), ctypes.byref(rc), _p(offsets),
+                                          _p(back), d, _DT[back.dtype], _p(out),
+                                          _stream(back.device)), "moe_reverse_layout_packed")
+    return out
+
+
 def reverse_layout_backward(dy: torch.Tensor, back: torch.Tensor, r: Routing,
                             d_back: Optional[torch.Tensor] = None,
                             d_weight: Optional[torch.Tensor] = None):
@@ -367,6 +409,53 @@ class Comm:
         check(lib().moe_combine_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc), _p(expert_out),
                                     d, _DT[expert_out.dtype], _p(y), flags, _stream(y.device)),
               "moe_combine_p2p")
+        return y
+
+    def alltoallv(self, send: torch.Tensor, send_rows, recv: torch.Tensor, recv_rows) -> torch.Tensor:
+        """Variable-size AllToAll (NCCL): send_rows / recv_rows are host
+        sequences [nranks] of rows of send's row size."""
+        _need_cuda(send, "send")
+        _need_cuda(recv, "recv", send.dtype)
+        row_bytes = send[0].numel() * send.element_size() if send.dim() > 1 else send.element_size()
+        sr = (ctypes.c_int64 * self.nranks)(*[int(v) for v in send_rows])
+        rr = (ctypes.c_int64 * self.nranks)(*[int(v) for v in recv_rows])
+        check(lib().moe_alltoallv(self._h, _p(send), sr, _p(recv), rr, row_bytes,
+                                  _stream(send.device)), "moe_alltoallv")
+        return recv
+
+    def dispatch_packed_p2p(self, x: torch.Tensor, r: "Routing", offsets: torch.Tensor,
+                            counts: torch.Tensor, recv: torch.Tensor, peer_base=None,
+                            recv_offsets=None, flags: int = 0):
+        """Dropless dispatch over NVLink with the count exchange on the
+        device.  counts: symmetric int32 [E]; recv: symmetric [rows, d] with
+        rows >= nranks*S*k.  Returns (peer_base [P], recv_offsets [E+1])."""
+        _need_cuda(x, "x")
+        d = x.shape[-1]
+        if peer_base is None:
+            peer_base = torch.empty((self.nranks,), dtype=torch.int32, device=x.device)
+        if recv_offsets is None:
+            recv_offsets = torch.empty((r.E + 1,), dtype=torch.int32, device=x.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_dispatch_packed_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                            _p(offsets), _p(counts), _p(peer_base),
+                                            _p(recv_offsets), _p(x), d, _DT[x.dtype], _p(recv),
+                                            recv.shape[0], flags, _stream(x.device)),
+              "moe_dispatch_packed_p2p")
+        return peer_base, recv_offsets
+
+    def combine_packed_p2p(self, expert_out: torch.Tensor, r: "Routing", offsets: torch.Tensor,
+                           peer_base: torch.Tensor, y: Optional[torch.Tensor] = None,
+                           flags: int = 0) -> torch.Tensor:
+        """Dropless combine over NVLink from the owners' symmetric expert_out
+        (recv layout of dispatch_packed_p2p)."""
+        d = expert_out.shape[-1]
+        if y is None:
+            y = torch.empty((r.S, d), dtype=expert_out.dtype, device=expert_out.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_combine_packed_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                           _p(offsets), _p(peer_base), _p(expert_out), d,
+                                           _DT[expert_out.dtype], expert_out.shape[0], _p(y),
+                                           flags, _stream(y.device)), "moe_combine_packed_p2p")
         return y
 
     def combine_backward_p2p(self, dy: torch.Tensor, expert_out: torch.Tensor, r: "Routing",

@@ -9,27 +9,9 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "comm.cuh"
+#include "launch.cuh"
 
 namespace moe {
-
-size_t gate_workspace_bytes(const moe_gate_desc_t& d);
-moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
-                         const moe_routing_t& out, void* ws, cudaStream_t stream);
-moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);
-moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream);
-moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
-                                const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
-                                int rank, int dtype, int dtype_size, int dcols, float* d_weight,
-                                cudaStream_t stream);
-moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, const moe_routing_t& r,
-                             const float* d_weight, float* d_logits, cudaStream_t stream);
-moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
-                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream);
-moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
-                                 int cap, int dcols, int dtype, int dtype_size,
-                                 cudaStream_t stream);
 
 static thread_local char g_err[512] = "";
 
@@ -261,6 +243,47 @@ moe_status_t moe_reverse_layout(const moe_gate_desc_t* desc, const moe_routing_t
   if (s != MOE_OK) return s;
   return reverse_launch(*desc, *routing, back, dtype, dtype_size(dtype), d, y,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_expert_offsets(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                                int32_t* offsets, moe_stream_t stream) {
+  moe_status_t s = check_desc("moe_expert_offsets", desc);
+  if (s != MOE_OK) return s;
+  if (!routing || !routing->load || !offsets) {
+    set_error("moe_expert_offsets: routing.load and offsets are required");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return expert_offsets_launch(routing->load, desc->E, desc->capacity, offsets,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_layout_packed(const moe_gate_desc_t* desc, const moe_routing_t* routing,
+                               const int32_t* offsets, const void* x, int32_t d, int32_t dtype,
+                               void* packed, moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_layout_packed", desc, routing, x, "x", packed, "packed", d,
+                              dtype, false, true);
+  if (s != MOE_OK) return s;
+  if (!offsets) {
+    set_error("moe_layout_packed: offsets is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return layout_launch(*desc, *routing, x, dtype_size(dtype), d, packed,
+                       reinterpret_cast<cudaStream_t>(stream), offsets);
+}
+
+moe_status_t moe_reverse_layout_packed(const moe_gate_desc_t* desc,
+                                       const moe_routing_t* routing, const int32_t* offsets,
+                                       const void* back, int32_t d, int32_t dtype, void* y,
+                                       moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_reverse_layout_packed", desc, routing, back, "back", y, "y", d,
+                              dtype, true, false);
+  if (s != MOE_OK) return s;
+  if (!offsets) {
+    set_error("moe_reverse_layout_packed: offsets is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return reverse_launch(*desc, *routing, back, dtype, dtype_size(dtype), d, y,
+                        reinterpret_cast<cudaStream_t>(stream), offsets);
 }
 
 moe_status_t moe_reverse_layout_backward(const moe_gate_desc_t* desc,

@@ -210,6 +210,48 @@ moe_status_t moe_alltoall_plan(int32_t nranks, int32_t rank, int32_t algo, int32
   return MOE_OK;
 }
 
+moe_status_t moe_alltoallv(moe_comm_t* comm, const void* send, const int64_t* send_rows,
+                           void* recv, const int64_t* recv_rows, size_t row_bytes,
+                           moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (!comm || !send_rows || !recv_rows || row_bytes == 0) {
+    set_error("moe_alltoallv: NULL comm/send_rows/recv_rows or row_bytes == 0");
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  int64_t ns = 0, nr = 0;
+  for (int q = 0; q < P; ++q) {
+    if (send_rows[q] < 0 || recv_rows[q] < 0) {
+      set_error("moe_alltoallv: negative row count for rank %d", q);
+      return MOE_ERR_INVALID_ARG;
+    }
+    ns += send_rows[q];
+    nr += recv_rows[q];
+  }
+  if ((ns && !send) || (nr && !recv)) {
+    set_error("moe_alltoallv: NULL send/recv with rows to move");
+    return MOE_ERR_INVALID_ARG;
+  }
+  moe_status_t s = nccl_status(ncclGroupStart(), "moe_alltoallv: ncclGroupStart");
+  if (s != MOE_OK) return s;
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < P; ++q) {
+    ncclResult_t a = ncclSend(static_cast<const char*>(send) + so * row_bytes,
+                              (size_t)send_rows[q] * row_bytes, ncclInt8, q, comm->nccl, stream);
+    ncclResult_t b = a == ncclSuccess
+                         ? ncclRecv(static_cast<char*>(recv) + ro * row_bytes,
+                                    (size_t)recv_rows[q] * row_bytes, ncclInt8, q, comm->nccl, stream)
+                         : a;
+    if (b != ncclSuccess) {
+      ncclGroupEnd();
+      return nccl_status(b, "moe_alltoallv: send/recv");
+    }
+    so += send_rows[q];
+    ro += recv_rows[q];
+  }
+  return nccl_status(ncclGroupEnd(), "moe_alltoallv: ncclGroupEnd");
+}
+
 moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, const void* send,
                           void* recv, size_t bytes_per_peer, void* ws, size_t ws_bytes,
                           moe_stream_t stream_) {

@@ -46,10 +46,7 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
         for (int j = 0; j < a.k; ++j) {
           const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
           if (s < 0) continue;
-          const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
-          const int q = e / a.E_local;
-          char* drow = a.dpeer.p[q] +
-                       ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+          char* drow = dst_row_of(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -65,11 +62,7 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
         const int mid = (lo + hi + 1) >> 1;
         if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
       }
-      const int e = lo;
-      const int s = min(__ldg(a.load + e), a.cap) + (p - s_beg[e]);
-      const int q = e / a.E_local;
-      char* drow = a.dpeer.p[q] +
-                   ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+      char* drow = dst_row_of(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
       const typename V::T z = V::zero();
       for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
     }
@@ -194,10 +187,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ char* dst_row(const RowArgs& a, int e, int s) {
-  const int q = e / a.E_local;
-  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
-}
+__device__ __forceinline__ char* dst_row(const RowArgs& a, int e, int s) { return dst_row_of(a, e, s); }
 
 __global__ void __launch_bounds__(kTmaThreads) k_layout_tma(TmaArgs ta) {
   const RowArgs& a = ta.a;
@@ -525,12 +515,47 @@ __global__ void __launch_bounds__(kRowThreads) k_chunk_permute(const char* src, 
   }
 }
 
+// ------------------------------------------------------------ expert offsets
+// Dropless packed form (NEXT-4; SPEC.md:241-245 Permutation.expert_offsets):
+// offsets[e] = sum_{e' < e} min(load[e'], cap), one CTA, warp scan (E <= 256).
+__global__ void __launch_bounds__(32) k_expert_offsets(const int32_t* load, int E, int cap,
+                                                       int32_t* offsets) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x;
+  int carry = 0;
+  if (lane == 0) offsets[0] = 0;
+  for (int base = 0; base < E; base += 32) {
+    const int e = base + lane;
+    const int v = e < E ? min(__ldg(load + e), cap) : 0;
+    int incl = v;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, m);
+      if (lane >= m) incl += o;
+    }
+    if (e < E) offsets[e + 1] = carry + incl;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t* offsets,
+                                   cudaStream_t stream) {
+  void* args[] = {(void*)&load, &E, &cap, &offsets};
+  cudaError_t e = launch_pdl((const void*)k_expert_offsets, dim3(1), dim3(32), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_expert_offsets: launch");
+  return MOE_OK;
+}
+
 // ------------------------------------------------------------ host side
 
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
-                                 int rank, cudaStream_t stream) {
+                                 int rank, cudaStream_t stream, const int32_t* offsets,
+                                 const int32_t* peer_base) {
   RowArgs a{};
+  a.offsets = offsets;
+  a.peer_base = peer_base;
   a.src = static_cast<const char*>(x);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
@@ -584,16 +609,20 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
 }
 
 moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream) {
+                           int dtype_size, int dcols, void* dispatch, cudaStream_t stream,
+                           const int32_t* offsets) {
   PeerPtrs dst{};
   dst.p[0] = static_cast<char*>(dispatch);
-  return layout_launch_peers(d, r, x, dtype_size, dcols, dst, d.E, 0, stream);
+  return layout_launch_peers(d, r, x, dtype_size, dcols, dst, d.E, 0, stream, offsets, nullptr);
 }
 
 moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
-                                  int dtype_size, int dcols, void* y, cudaStream_t stream) {
+                                  int dtype_size, int dcols, void* y, cudaStream_t stream,
+                                  const int32_t* offsets, const int32_t* peer_base) {
   RowArgs a{};
+  a.offsets = offsets;
+  a.peer_base = peer_base;
   a.dst = static_cast<char*>(y);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
@@ -643,10 +672,12 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
 }
 
 moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,
-                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream) {
+                            int dtype, int dtype_size, int dcols, void* y, cudaStream_t stream,
+                            const int32_t* offsets) {
   PeerPtrs src{};
   src.p[0] = const_cast<char*>(static_cast<const char*>(back));
-  return reverse_launch_peers(d, r, src, d.E, 0, dtype, dtype_size, dcols, y, stream);
+  return reverse_launch_peers(d, r, src, d.E, 0, dtype, dtype_size, dcols, y, stream, offsets,
+                              nullptr);
 }
 
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,

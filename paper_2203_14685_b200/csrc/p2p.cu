@@ -18,21 +18,9 @@
 //    stream order every rank's receive buffer is complete.
 #include <cstring>
 
-#include "comm.cuh"
+#include "launch.cuh"
 
 namespace moe {
-
-moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
-                                 int rank, cudaStream_t stream);
-moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
-                                  const PeerPtrs& src, int E_local, int rank, int dtype,
-                                  int dtype_size, int dcols, void* y, cudaStream_t stream);
-
-moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
-                                const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
-                                int rank, int dtype, int dtype_size, int dcols, float* d_weight,
-                                cudaStream_t stream);
 
 static moe_status_t nccl_st(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return MOE_OK;
@@ -198,6 +186,52 @@ moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_
   cudaError_t e = launch_pdl((const void*)k_a2a_p2p, dim3(grid), dim3(256), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_alltoall(P2P): launch");
   return MOE_OK;
+}
+
+// ------------------------------------------------------------ dropless exchange
+// counts_q[r][le] = admitted rows of this rank r for q's local expert le
+// (stores into every owner's symmetric count table).
+__global__ void k_a2av_counts(const int32_t* offsets, PeerPtrs counts, int E, int El, int rank) {
+  pdl_wait();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int q = e / El, le = e - q * El;
+    reinterpret_cast<int32_t*>(counts.p[q])[rank * El + le] = __ldg(offsets + e + 1) - __ldg(offsets + e);
+  }
+  __threadfence_system();
+}
+
+// peer_base[q] = rows ranks < r put into q's recv (read from q's table);
+// recv_offsets = exclusive prefix of this rank's own table [src][le].
+__global__ void __launch_bounds__(256) k_a2av_plan(PeerPtrs counts, int P, int El, int rank,
+                                                   int32_t* peer_base, int32_t* recv_offsets) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = warp; q < P; q += blockDim.x / 32) {
+    const volatile int32_t* c = reinterpret_cast<const volatile int32_t*>(counts.p[q]);
+    int sum = 0;
+    for (int i = lane; i < rank * El; i += 32) sum += c[i];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+    if (lane == 0) peer_base[q] = sum;
+  }
+  if (warp == 0) {
+    const volatile int32_t* c = reinterpret_cast<const volatile int32_t*>(counts.p[rank]);
+    const int n = P * El;
+    int carry = 0;
+    if (lane == 0) recv_offsets[0] = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int v = i < n ? c[i] : 0;
+      int incl = v;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += o;
+      }
+      if (i < n) recv_offsets[i + 1] = carry + incl;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
 }
 
 }  // namespace moe
@@ -387,6 +421,116 @@ moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* 
   moe_routing_t unit = *routing;
   unit.weight = nullptr;  // adjoint of the dispatch copy: unit-weight combine
   s = reverse_launch_peers(*desc, unit, src, desc->E / P, comm->rank, dtype, ds, d, dx, stream);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+}
+
+// The symmetric buffer of `bytes` at p, with its per-rank mappings.
+static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
+                               PeerPtrs* out) {
+  const SymmBuf* b = find_symm(comm, p, bytes);
+  if (!b) {
+    set_error("%s: a buffer of %zu bytes is not inside a symmetric buffer (moe_comm_symm_alloc)",
+              fn, bytes);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const size_t off = static_cast<const char*>(p) - b->base;
+  for (int q = 0; q < comm->nranks; ++q) out->p[q] = b->peer.p[q] + off;
+  return MOE_OK;
+}
+
+static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                const moe_routing_t* routing, const int32_t* offsets,
+                                const void* a, const void* buf, int64_t rows, int32_t d,
+                                int32_t dtype, PeerPtrs* peers, int* ds) {
+  if (!comm || !desc || !routing || !routing->expert_idx || !routing->slot_idx || !offsets ||
+      !a || !buf || d < 1 || (dtype != MOE_F32 && dtype != MOE_BF16)) {
+    set_error("%s: bad arguments", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!comm->p2p_ok) {
+    set_error("%s: peer memory is not available between these GPUs", fn);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  const int P = comm->nranks;
+  if (desc->E % P != 0 || desc->E > 256) {
+    set_error("%s: E=%d experts must shard over %d ranks (E <= 256)", fn, desc->E, P);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if ((int64_t)P * desc->S * desc->k > rows) {
+    set_error("%s: buffer of %lld rows < nranks*S*k = %lld (the worst case)", fn, (long long)rows,
+              (long long)P * desc->S * desc->k);
+    return MOE_ERR_INVALID_ARG;
+  }
+  *ds = dtype == MOE_F32 ? 4 : 2;
+  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
+      reinterpret_cast<uintptr_t>(buf) % 16) {
+    set_error("%s: rows and pointers must be 16-byte aligned", fn);
+    return MOE_ERR_ALIGNMENT;
+  }
+  return symm_peers(fn, comm, buf, (size_t)rows * d * *ds, peers);
+}
+
+moe_status_t moe_dispatch_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                     const moe_routing_t* routing, const int32_t* offsets,
+                                     int32_t* counts, int32_t* peer_base, int32_t* recv_offsets,
+                                     const void* x, int32_t d, int32_t dtype, void* recv,
+                                     int64_t recv_cap_rows, int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_dispatch_packed_p2p";
+  PeerPtrs dst, cnt;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, x, recv, recv_cap_rows, d, dtype,
+                               &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!counts || !peer_base || !recv_offsets) {
+    set_error("%s: counts, peer_base and recv_offsets are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  s = symm_peers(fn, comm, counts, sizeof(int32_t) * (size_t)desc->E, &cnt);
+  if (s != MOE_OK) return s;
+  const int P = comm->nranks, El = desc->E / P;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // owners done with the previous step's tables
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  k_a2av_counts<<<1, 256, 0, stream>>>(offsets, cnt, desc->E, El, comm->rank);
+  MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: counts launch");
+  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every table complete
+  if (s != MOE_OK) return s;
+  k_a2av_plan<<<1, 256, 0, stream>>>(cnt, P, El, comm->rank, peer_base, recv_offsets);
+  MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: plan launch");
+  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, offsets,
+                          peer_base);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
+}
+
+moe_status_t moe_combine_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                    const moe_routing_t* routing, const int32_t* offsets,
+                                    const int32_t* peer_base, const void* expert_out, int32_t d,
+                                    int32_t dtype, int64_t expert_out_rows, void* y,
+                                    int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_combine_packed_p2p";
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, y, expert_out, expert_out_rows, d,
+                               dtype, &src, &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight || !peer_base) {
+    set_error("%s: routing.weight and peer_base are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream,
+                           offsets, peer_base);
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);

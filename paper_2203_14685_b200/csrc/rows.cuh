@@ -30,16 +30,30 @@ struct RowArgs {
   // reverse source: row (e, s) is read from speer.p[q] + ((rank*E_local +
   // e mod E_local)*cap + s)*row (same mapping; local: speer.p[0] = back)
   PeerPtrs speer;
+  // dropless packed form (NEXT-4): when `offsets` ([E+1] expert offsets of
+  // the sender) is set, row (e, s) is row base_q + offsets[e] -
+  // offsets[q*E_local] + s of rank q's buffer, base_q = peer_base[q] (the
+  // rows earlier source ranks put there; 0 locally); no padding rows.
+  const int32_t* offsets;
+  const int32_t* peer_base;
 };
+
+__device__ __forceinline__ size_t row_index(const RowArgs& a, int q, int e, int s) {
+  if (a.offsets) {
+    const int base = a.peer_base ? __ldg(a.peer_base + q) : 0;
+    return (size_t)(base + __ldg(a.offsets + e) - __ldg(a.offsets + q * a.E_local) + s);
+  }
+  return (size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s;
+}
 
 __device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
   const int q = e / a.E_local;
-  return a.speer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+  return a.speer.p[q] + row_index(a, q, e, s) * a.row_bytes;
 }
 
 __device__ __forceinline__ char* dst_row_of(const RowArgs& a, int e, int s) {
   const int q = e / a.E_local;
-  return a.dpeer.p[q] + ((size_t)(a.rank * a.E_local + (e - q * a.E_local)) * a.cap + s) * a.row_bytes;
+  return a.dpeer.p[q] + row_index(a, q, e, s) * a.row_bytes;
 }
 
 template <int VB>
@@ -72,7 +86,8 @@ struct Vec<16> {
 __device__ __forceinline__ void pad_prefix(const RowArgs& a, int* s_beg) {
   __shared__ int s_cnt[257];
   const int tid = threadIdx.x;
-  for (int e = tid; e < a.E; e += blockDim.x) s_cnt[e] = a.cap - min(__ldg(a.load + e), a.cap);
+  for (int e = tid; e < a.E; e += blockDim.x)
+    s_cnt[e] = a.offsets ? 0 : a.cap - min(__ldg(a.load + e), a.cap);  // packed: no padding
   __syncthreads();
   if (tid < 32) {
     int carry = 0;

@@ -155,3 +155,91 @@ def test_multi_gpu_backward_p2p(orc, world):
         unit = type(ros[r])(**{**ros[r].__dict__,
                                "weight": (ros[r].slot_idx >= 0).astype(np.float32)})
         assert_y_close(out[r][6], dx_o, combine_bound(as_f64(d_disp[r]), unit), True, "dx")
+
+
+def _packed_rank_main(rank, world, port, q):
+    """Dropless exchange: device-side (NVLink) and NCCL alltoallv."""
+    import torch.distributed as dist
+    import paper_2203_14685_b200 as moe
+    from gpu_util import dev, host
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = moe.Comm.from_process_group()
+    lg = synthgen.logits(synthgen.seed_for(9, rank, 11), S, E, K, skew=1.0 + rank)
+    x = synthgen.tokens(synthgen.seed_for(9, rank, 12), S, D, "bf16")
+    r = moe.Gate(S, E, K, S * K)(dev(lg), slot_src=False)            # dropless
+    off = moe.expert_offsets(r)
+    rows = world * S * K
+    counts = comm.symm_empty((E,), torch.int32)
+    recv = comm.symm_empty((rows, D), torch.bfloat16)
+    eo = comm.symm_empty((rows, D), torch.bfloat16)
+    pb, roff = comm.dispatch_packed_p2p(dev(x), r, off, counts, recv)
+    torch.cuda.synchronize()
+    R_in = int(host(roff)[-1])
+    recv_h = host(recv)[:R_in].copy()
+    # expert stand-in: an independent synthetic output per received row
+    out_h = synthgen.tokens(synthgen.seed_for(9, rank, 13), R_in, D, "bf16")
+    eo[:R_in].copy_(dev(out_h))
+    torch.cuda.synchronize()
+    y = host(comm.combine_packed_p2p(eo, r, off, pb)).copy()
+    # NCCL path: count table exchange, host counts, alltoallv of the packed rows
+    El = E // world
+    off_h = host(off)
+    send_cnt = np.diff(off_h).astype(np.int32)                     # [E] = [world][El]
+    cnt_recv = torch.empty((E,), dtype=torch.int32, device="cuda")
+    comm.alltoall(dev(send_cnt), cnt_recv)
+    rc = host(cnt_recv).reshape(world, El).sum(1)
+    sc = send_cnt.reshape(world, El).sum(1)
+    packed = moe.layout_packed(dev(x), r, off)
+    recv2 = torch.empty((int(rc.sum()), D), dtype=torch.bfloat16, device="cuda")
+    comm.alltoallv(packed, sc, recv2, rc)
+    torch.cuda.synchronize()
+    q.put((rank, lg, x, host(roff).copy(), recv_h, out_h, y, host(recv2).copy()))
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_dropless(orc, world):
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs %d GPUs" % world)
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = 29750 + world
+    ps = [ctx.Process(target=_packed_rank_main, args=(r, world, port, qu)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = {}
+    for _ in range(world):
+        v = qu.get(timeout=300)
+        out[v[0]] = v[1:]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    from gpu_util import as_f64, assert_y_close
+    El = E // world
+    ros = [orc.gate(out[r][0], E=E, k=K, cap=S * K) for r in range(world)]
+    offs = [orc.expert_offsets(ro) for ro in ros]
+    packs = [orc.layout_packed(out[r][1], ros[r], offs[r]) for r in range(world)]
+    counts = np.array([[offs[q][(r + 1) * El] - offs[q][r * El] for r in range(world)]
+                       for q in range(world)])
+    recvs = orc.alltoallv(packs, counts)
+    outs = [out[r][4] for r in range(world)]
+    backs = orc.alltoallv(outs, counts.T)
+    for r in range(world):
+        roff, recv_h, _, y, recv2 = out[r][2], out[r][3], out[r][4], out[r][5], out[r][6]
+        table = np.array([[offs[q][r * El + le + 1] - offs[q][r * El + le] for le in range(El)]
+                          for q in range(world)]).reshape(-1)
+        assert roff.tolist() == np.concatenate([[0], np.cumsum(table)]).tolist()
+        assert recv_h.tobytes() == recvs[r].tobytes()         # device-side exchange
+        assert recv2.tobytes() == recvs[r].tobytes()          # NCCL alltoallv
+        y_o = orc.reverse_layout_packed(backs[r], ros[r], offs[r])
+        b64 = as_f64(backs[r])
+        bound = np.zeros((S, D))
+        for j in range(K):
+            ok = ros[r].slot_idx[:, j] >= 0
+            rows = offs[r][ros[r].expert_idx[ok, j]] + ros[r].slot_idx[ok, j]
+            bound[ok] += np.abs(ros[r].weight[ok, j].astype(np.float64)[:, None] * b64[rows])
+        assert_y_close(y, y_o, bound, True, "y")
