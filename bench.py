@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verbose", action="store_true", help="progress on stderr")
     return ap.parse_args()
@@ -391,6 +392,56 @@ def main():
     torch.cuda.synchronize()
     expert_ms = e0.elapsed_time(e1)
 
+    # ---- backward of the routing path (NEXT-1), informational: the adjoint
+    # kernels of the same step (combine -> AllToAll x2 -> layout, + gate),
+    # one CUDA graph, L2 flushed between replays, max over ranks
+    bwd = None
+    if not a.no_backward:
+        dy = torch.from_numpy(synthgen.tokens(synthgen.seed_for(w.index, rank, 9), S, w.d,
+                                              w.dtype))
+        if w.dtype == "bf16":
+            dy = dy.view(torch.int16).view(torch.bfloat16)
+        dy = dy.to(dev)
+        step()
+        for _ in range(2):
+            pipe.backward(dy, d_in["logits"])
+        torch.cuda.synchronize()
+        sb = torch.cuda.Stream(dev)
+        sb.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(sb):
+            g_bwd = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_bwd, stream=sb):
+                pipe.backward(dy, d_in["logits"])
+        torch.cuda.current_stream(dev).wait_stream(sb)
+        g_bwd.replay()
+        torch.cuda.synchronize()
+        Kb = max(3, a.steps // 2)
+        evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(Kb)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(Kb):
+            flush_l2()
+            evb[i][0].record()
+            g_bwd.replay()
+            evb[i][1].record()
+        torch.cuda.synchronize()
+        barrier()
+        tb = torch.tensor([statistics.mean(s_.elapsed_time(e_) for s_, e_ in evb)],
+                          dtype=torch.float64)
+        if P > 1:
+            tbd = tb.to(dev)
+            dist.all_reduce(tbd, op=dist.ReduceOp.MAX)
+            tb = tbd.cpu()
+        bms = float(tb[0])
+        bwd = {"ms_per_step": bms, "train_value": P * S / ((ms + bms) / 1e3), "unit": UNIT,
+               "what": "adjoints of the routing step with an identity expert: "
+                       "reverse_layout_backward (d_back scatter + d_weight) -> AllToAll x2 -> "
+                       "layout_backward (dx) + gate_backward (d_logits); train_value = tokens / "
+                       "(forward + backward)"}
+        del g_bwd
+        log("backward timing done")
+
     # ---- end to end through the public API from pinned host buffers
     e2e = None
     if not a.no_e2e:
@@ -498,10 +549,11 @@ def main():
                          "%d of %d tokens of %s, single thread pinned to one core; %d host cores "
                          "present" % (n, S_s, w.S, w.name, os.cpu_count())}
 
-    # our kernels per step: gate (+ finalize for SLOT priority), layout, reverse,
-    # and on hierarchical leaders one chunk permute per AllToAll
-    launches_per_step = 3 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
-        (2 if (P > 1 and algo == "p2p") else 0)   # p2p: two k_barrier launches
+    # our kernels per step: gate (k_gate_select, k_gate_scan, k_gate_slots),
+    # layout, reverse, on hierarchical leaders one chunk permute per AllToAll,
+    # and on the one-sided path the dispatch's and the combine's exit barriers
+    launches_per_step = 5 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
+        (2 if (P > 1 and algo == "p2p") else 0)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
@@ -520,6 +572,7 @@ def main():
                       "from event-record nodes inside the step graph",
             "admitted_slots": admitted, "roofline": roof, "alltoall": a2a, "clocks": clocks,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches_per_step * a.steps,
+            "backward": bwd,
             "library": moe.version(),
         }
         print(json.dumps(out), flush=True)

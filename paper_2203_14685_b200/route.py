@@ -12,7 +12,8 @@ from typing import Optional
 
 import torch
 
-from .api import Comm, Gate, Routing, expert_scale, layout, reverse_layout
+from .api import (Comm, Gate, Routing, expert_scale, gate_backward, layout, layout_backward,
+                  reverse_layout, reverse_layout_backward)
 
 
 class RoutePipeline:
@@ -98,6 +99,40 @@ class RoutePipeline:
         reverse_layout(self.back, r, out=self.y)                           # step 6
         mark("reverse")
         return self.y
+
+    def backward(self, dy: torch.Tensor, logits: Optional[torch.Tensor] = None):
+        """Backward of the last step (NEXT-1) with the routing held fixed and
+        an identity expert: the adjoints in reverse order -- combine
+        (d_back, d_weight) -> AllToAll -> AllToAll -> layout (dx), plus the
+        gate (d_logits, when the gate has logits).  Returns (dx, d_logits)."""
+        r = self.routing
+        if not hasattr(self, "d_weight"):
+            mk = lambda *shape: torch.empty(shape, dtype=self.y.dtype, device=self.device)
+            self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32, device=self.device)
+            self.dx = mk(self.S, self.d)
+            self.d_logits = torch.empty((self.S, self.E), dtype=torch.float32, device=self.device)
+            if self.P > 1 and self.algo == "p2p":
+                self.d_recv = self.comm.symm_empty((self.E, self.cap, self.d), self.y.dtype)
+            elif self.P > 1:
+                self.d_back, self.d_recv, self.d_disp = (mk(self.E, self.cap, self.d)
+                                                         for _ in range(3))
+            else:
+                self.d_back = self.d_recv = self.d_disp = mk(self.E, self.cap, self.d)
+        if self.P > 1 and self.algo == "p2p":
+            # d_back rows are stored straight into the owners' d_recv, then
+            # every dx row gathers its gradient rows back over NVLink
+            self.comm.combine_backward_p2p(dy, self.recv, r, self.d_recv, self.d_weight)
+            self.comm.dispatch_backward_p2p(self.d_recv, r, self.dx,
+                                            flags=self.comm.NO_ENTRY_BARRIER)
+        else:
+            reverse_layout_backward(dy, self.back, r, self.d_back, self.d_weight)
+            self.alltoall(self.d_back, self.d_recv)        # adjoint of step 5
+            self.alltoall(self.d_recv, self.d_disp)        # adjoint of step 3 (identity expert)
+            layout_backward(self.d_disp, r, out=self.dx)
+        dl = None
+        if logits is not None and self.gate.kind != 2:
+            dl = gate_backward(logits, r, self.d_weight, out=self.d_logits)
+        return self.dx, dl
 
     STAGES = ("gate", "layout", "a2a_dispatch", "a2a_combine", "reverse")
 
