@@ -21,6 +21,25 @@
 
 namespace moe {
 
+// RNE of the EXACT product w * v to bf16, in fp32/integer arithmetic: hi =
+// RN_fp32(w*v), lo = the exact remainder (FMA).  RN to fp32 is monotone and
+// every bf16 midpoint is an fp32 number, so RNE(hi) is the correct rounding
+// unless hi sits exactly on a midpoint (low half 0x8000); then the sign of lo
+// decides, and only an exact tie (lo == 0) goes to even.  Bit-identical to
+// rounding the exact (fp64) product once.
+__device__ __forceinline__ uint32_t mul_rne_bf16(float w, float v) {
+  const float hi = __fmul_rn(w, v);
+  const float lo = fmaf(w, v, -hi);
+  const uint32_t b = __float_as_uint(hi);
+  const uint32_t r = b & 0xFFFFu;
+  uint32_t up;
+  if (r == 0x8000u && lo != 0.f)
+    up = ((lo > 0.f) == (hi > 0.f)) ? 1u : 0u;  // exact magnitude above the midpoint
+  else
+    up = (r > 0x8000u || (r == 0x8000u && (b & 0x10000u))) ? 1u : 0u;
+  return (b >> 16) + up;
+}
+
 template <int DT>
 __device__ __forceinline__ V8 scale_vec(float w, const V8& v) {
   V8 o;
@@ -29,12 +48,8 @@ __device__ __forceinline__ V8 scale_vec(float w, const V8& v) {
     for (int q = 0; q < 8; ++q) o.w[q] = __float_as_uint(__fmul_rn(w, __uint_as_float(v.w[q])));
   } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      // w (24 bits) x bf16 (8 bits) is exact in fp64; one RNE to bf16
-      const __nv_bfloat16 lo = __double2bfloat16((double)w * (double)bf16lo(v.w[q]));
-      const __nv_bfloat16 hi = __double2bfloat16((double)w * (double)bf16hi(v.w[q]));
-      o.w[q] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
-    }
+    for (int q = 0; q < 8; ++q)
+      o.w[q] = mul_rne_bf16(w, bf16lo(v.w[q])) | (mul_rne_bf16(w, bf16hi(v.w[q])) << 16);
   }
   return o;
 }
@@ -105,6 +120,86 @@ __global__ void __launch_bounds__(kRowThreads) k_combine_bwd(RowArgs a, float* d
     }
   }
   // zero gradient for the padding (empty) slots
+  const int npad = s_beg[a.E];
+  const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int p = gw; p < npad; p += nw) {
+    int lo = 0, hi = a.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    char* drow = dst_row_of(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
+    for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) st_v8(drow + off, z);
+  }
+  if (a.sys_fence) __threadfence_system();
+}
+
+// k <= 2 specialisation: dy and both expert rows of a segment are loaded
+// before any arithmetic ((1 + KK) * U vectors in flight per lane), then each
+// slot's scaled row is stored and its dot accumulated.  Same arithmetic
+// order as k_combine_bwd (column order per lane, then the warp tree).
+template <int DT, int KK, int U>
+__global__ void __launch_bounds__(kRowThreads) k_combine_bwd_k(RowArgs a, float* d_weight) {
+  constexpr int VB = 32, SEG = 32 * U * VB;
+  __shared__ int s_beg[257];
+  pdl_wait();
+  pdl_trigger();
+  pad_prefix(a, s_beg);
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kRowWarps;
+  for (int t = gw; t < a.S; t += nw) {
+    const char* dyrow = a.src + (size_t)t * a.row_bytes;
+    const char* brow[KK];
+    char* drow[KK];
+    float w[KK], dot[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      const size_t i = (size_t)t * KK + j;
+      const int s = __ldg(a.slot_idx + i);
+      brow[j] = nullptr;
+      drow[j] = nullptr;
+      w[j] = 0.f;
+      dot[j] = 0.f;
+      if (s >= 0) {
+        const int e = __ldg(a.expert_idx + i);
+        w[j] = __ldg(a.weight + i);
+        brow[j] = src_row(a, e, s);
+        drow[j] = dst_row_of(a, e, s);
+      }
+    }
+    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
+      V8 g[U], b[KK][U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int off = seg + (lane + 32 * u) * VB;
+        if (off < a.row_bytes) g[u] = ld_stream_v8(dyrow + off);
+      }
+#pragma unroll
+      for (int j = 0; j < KK; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (brow[j] && off < a.row_bytes) b[j][u] = ld_stream_v8(brow[j] + off);
+        }
+#pragma unroll
+      for (int j = 0; j < KK; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (brow[j] && off < a.row_bytes) {
+            st_v8(drow[j] + off, scale_vec<DT>(w[j], g[u]));
+            dot[j] = dot_vec<DT>(g[u], b[j][u], dot[j]);
+          }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) dot[j] += __shfl_xor_sync(0xffffffffu, dot[j], m);
+      if (lane == 0) d_weight[(size_t)t * KK + j] = brow[j] ? dot[j] : 0.f;
+    }
+  }
   const int npad = s_beg[a.E];
   const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
   for (int p = gw; p < npad; p += nw) {
@@ -201,9 +296,14 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
   a.sys_fence = E_local != d.E;
   const bool f = dtype == MOE_F32;
   const void* kern;
-  if (a.row_bytes % 32 == 0)
+  const int U2 = a.row_bytes >= 2048 ? 2 : 1;
+#define MOE_CBK(KK, UU) (f ? (const void*)k_combine_bwd_k<MOE_F32, KK, UU> : (const void*)k_combine_bwd_k<MOE_BF16, KK, UU>)
+  if (a.row_bytes % 32 == 0 && a.k <= 2 && env_int("MOE_COMBINE_BWD_KSPEC", 1))
+    kern = a.k == 1 ? (U2 == 2 ? MOE_CBK(1, 2) : MOE_CBK(1, 1)) : (U2 == 2 ? MOE_CBK(2, 2) : MOE_CBK(2, 1));
+  else if (a.row_bytes % 32 == 0)
     kern = a.row_bytes >= 2048 ? (f ? (const void*)k_combine_bwd<MOE_F32, 2> : (const void*)k_combine_bwd<MOE_BF16, 2>)
                                : (f ? (const void*)k_combine_bwd<MOE_F32, 1> : (const void*)k_combine_bwd<MOE_BF16, 1>);
+#undef MOE_CBK
   else
     kern = f ? (const void*)k_combine_bwd16<MOE_F32> : (const void*)k_combine_bwd16<MOE_BF16>;
   void* args[] = {&a, &d_weight};
@@ -213,13 +313,16 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
 }
 
 // ------------------------------------------------------------ gate adjoint
-// One warp per token.  With G_e = m_j g_j at e = e_j (0 elsewhere) and p the
-// Eq. 1 probabilities over the softmax's domain:
+// L lanes per token (32/L tokens per warp in flight), each lane owning the
+// experts e = l, l+L, ... (coalesced stores of the d_logits row).  With G_e =
+// m_j g_j at e = e_j (0 elsewhere) and p the Eq. 1 probabilities over the
+// softmax's domain:
 //   d_logits[e] = p_e * (G_e - sum_{j in the domain} G_{e_j} p_{e_j}),
 // i.e. sum_j m_j g_j p_j (delta(e, e_j) - p_e) (orc_gate_bwd's Jacobian sum
 // regrouped); 0 outside the domain.  Domains: RENORM top-k = the k selected
 // (max = l[e_0]); SOFTMAX top-k = the row (max = l[e_0]); SOFTMAX k-top-1 =
-// prototype slice j (max = l[e_j]).  k-top-1 RENORM: zero.
+// prototype slice j (max = l[e_j]).  k-top-1 RENORM: zero.  fp64, one
+// rounding.
 struct GateBwdArgs {
   const float* logits;
   const int32_t* expert_idx;
@@ -229,81 +332,93 @@ struct GateBwdArgs {
   int S, E, k, kind, mode;
 };
 
-constexpr int kGateBwdWarps = 4;
+constexpr int kGateBwdThreads = 256;
 
-__device__ __forceinline__ double warp_sum_d(double x) {
+template <int L>
+__device__ __forceinline__ double lanes_sum(double x) {
 #pragma unroll
-  for (int m = 16; m > 0; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+  for (int m = 1; m < L; m <<= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
   return x;
 }
 
-__global__ void __launch_bounds__(kGateBwdWarps * 32) k_gate_bwd(GateBwdArgs a) {
-  __shared__ double s_G[kGateBwdWarps][256];  // G_e of this warp's token
-  __shared__ double s_c[kGateBwdWarps][512];  // k-top-1: per slice (z_j, G_{e_j} p_{e_j})
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// G_e: the (masked) weight gradient of expert e if selected, else 0
+__device__ __forceinline__ double g_of(const GateBwdArgs& a, size_t t, int e) {
+  const int32_t* sel = a.expert_idx + t * a.k;
+  for (int j = 0; j < a.k; ++j)
+    if (__ldg(sel + j) == e)
+      return __ldg(a.slot_idx + t * a.k + j) >= 0 ? (double)__ldg(a.d_weight + t * a.k + j) : 0.0;
+  return 0.0;
+}
+
+template <int L>
+__global__ void __launch_bounds__(kGateBwdThreads) k_gate_bwd(GateBwdArgs a) {
+  const int l = threadIdx.x % L;
+  const int groups = gridDim.x * (kGateBwdThreads / L);
   pdl_wait();
   pdl_trigger();
-  double* G = s_G[warp];
-  double* C = s_c[warp];
-  for (int t = blockIdx.x * kGateBwdWarps + warp; t < a.S; t += gridDim.x * kGateBwdWarps) {
-    const float* row = a.logits + (size_t)t * a.E;
-    float* out = a.d_logits + (size_t)t * a.E;
-    const int32_t* sel = a.expert_idx + (size_t)t * a.k;
+  for (int base = blockIdx.x * (kGateBwdThreads / L); base < a.S; base += groups) {
+    const int tt = base + threadIdx.x / L;
+    const bool valid = tt < a.S;
+    const size_t t = valid ? (size_t)tt : 0;
+    const float* row = a.logits + t * a.E;
+    float* out = a.d_logits + t * a.E;
+    const int32_t* sel = a.expert_idx + t * a.k;
+    const double mx0 = (double)__ldg(row + __ldg(sel));
     if (a.kind == MOE_GATE_KTOP1 && a.mode == MOE_W_RENORM) {
-      for (int e = lane; e < a.E; e += 32) out[e] = 0.f;
-      continue;
-    }
-    for (int e = lane; e < a.E; e += 32) G[e] = 0.0;
-    __syncwarp();
-    for (int j = lane; j < a.k; j += 32) {
-      const size_t i = (size_t)t * a.k + j;
-      G[sel[j]] = __ldg(a.slot_idx + i) >= 0 ? (double)__ldg(a.d_weight + i) : 0.0;
-    }
-    __syncwarp();
-    if (a.kind == MOE_GATE_TOPK && a.mode == MOE_W_RENORM) {
-      const double mx = (double)__ldg(row + sel[0]);
-      double z = 0.0;
-      for (int j = lane; j < a.k; j += 32) z += exp((double)__ldg(row + sel[j]) - mx);
-      z = warp_sum_d(z);
-      double c = 0.0;
-      for (int j = lane; j < a.k; j += 32) c += G[sel[j]] * (exp((double)__ldg(row + sel[j]) - mx) / z);
-      c = warp_sum_d(c);
-      for (int e = lane; e < a.E; e += 32) out[e] = 0.f;
-      __syncwarp();
-      for (int j = lane; j < a.k; j += 32) {
-        const int e = sel[j];
-        const double p = exp((double)__ldg(row + e) - mx) / z;
-        out[e] = (float)(p * (G[e] - c));
+      if (valid)
+        for (int e = l; e < a.E; e += L) out[e] = 0.f;
+    } else if (a.kind == MOE_GATE_TOPK && a.mode == MOE_W_RENORM) {
+      // domain = the k selected: every lane evaluates the k terms itself
+      double z = 0.0, c = 0.0;
+      for (int j = 0; j < a.k; ++j) z += exp((double)__ldg(row + __ldg(sel + j)) - mx0);
+      for (int j = 0; j < a.k; ++j) {
+        const size_t i = t * a.k + j;
+        const double gj = __ldg(a.slot_idx + i) >= 0 ? (double)__ldg(a.d_weight + i) : 0.0;
+        c += gj * (exp((double)__ldg(row + __ldg(sel + j)) - mx0) / z);
       }
+      if (valid)
+        for (int e = l; e < a.E; e += L) {
+          double v = 0.0;
+          for (int j = 0; j < a.k; ++j)
+            if (__ldg(sel + j) == e) {
+              const size_t i = t * a.k + j;
+              const double gj = __ldg(a.slot_idx + i) >= 0 ? (double)__ldg(a.d_weight + i) : 0.0;
+              v = (exp((double)__ldg(row + e) - mx0) / z) * (gj - c);
+            }
+          out[e] = (float)v;
+        }
     } else if (a.kind == MOE_GATE_TOPK) {
-      const double mx = (double)__ldg(row + sel[0]);
-      double z = 0.0;
-      for (int e = lane; e < a.E; e += 32) z += exp((double)__ldg(row + e) - mx);
-      z = warp_sum_d(z);
+      // domain = the row: the L lanes share the partition sum
+      double part = 0.0;
+      if (valid)
+        for (int e = l; e < a.E; e += L) part += exp((double)__ldg(row + e) - mx0);
+      const double z = lanes_sum<L>(part);
       double c = 0.0;
-      for (int j = lane; j < a.k; j += 32) c += G[sel[j]] * (exp((double)__ldg(row + sel[j]) - mx) / z);
-      c = warp_sum_d(c);
-      for (int e = lane; e < a.E; e += 32) {
-        const double p = exp((double)__ldg(row + e) - mx) / z;
-        out[e] = (float)(p * (G[e] - c));
+      for (int j = 0; j < a.k; ++j) {
+        const size_t i = t * a.k + j;
+        const double gj = __ldg(a.slot_idx + i) >= 0 ? (double)__ldg(a.d_weight + i) : 0.0;
+        c += gj * (exp((double)__ldg(row + __ldg(sel + j)) - mx0) / z);
       }
-    } else {  // k-top-1 SOFTMAX: slice j = experts [j*n, (j+1)*n), max = l[e_j]
+      if (valid)
+        for (int e = l; e < a.E; e += L) {
+          const double p = exp((double)__ldg(row + e) - mx0) / z;
+          out[e] = (float)(p * (g_of(a, t, e) - c));
+        }
+    } else {  // k-top-1 SOFTMAX: slice j = [j*n, (j+1)*n), max = l[e_j]
       const int n = a.E / a.k;
-      for (int j = lane; j < a.k; j += 32) {
-        const double mx = (double)__ldg(row + sel[j]);
-        double z = 0.0;
-        for (int e = j * n; e < (j + 1) * n; ++e) z += exp((double)__ldg(row + e) - mx);
-        C[2 * j] = z;
-        C[2 * j + 1] = G[sel[j]] * (1.0 / z);  // G_{e_j} p_{e_j}: p at the slice max = 1/z
-      }
-      __syncwarp();
-      for (int e = lane; e < a.E; e += 32) {
-        const int j = e / n;
-        const double p = exp((double)__ldg(row + e) - (double)__ldg(row + sel[j])) / C[2 * j];
-        out[e] = (float)(p * (G[e] - C[2 * j + 1]));
-      }
+      if (valid)
+        for (int e = l; e < a.E; e += L) {
+          const int j = e / n;
+          const size_t i = t * a.k + j;
+          const double mj = (double)__ldg(row + __ldg(sel + j));
+          double z = 0.0;
+          for (int e2 = j * n; e2 < (j + 1) * n; ++e2) z += exp((double)__ldg(row + e2) - mj);
+          const double gj = __ldg(a.slot_idx + i) >= 0 ? (double)__ldg(a.d_weight + i) : 0.0;
+          const double p = exp((double)__ldg(row + e) - mj) / z;
+          const double G = (__ldg(sel + j) == e) ? gj : 0.0;
+          out[e] = (float)(p * (G - gj * (1.0 / z)));  // p_{e_j} = 1/z at the slice max
+        }
     }
-    __syncwarp();
   }
 }
 
@@ -311,14 +426,19 @@ moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, cons
                              const float* d_weight, float* d_logits, cudaStream_t stream) {
   GateBwdArgs a{logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
                 d.weight_mode};
+  // lanes per token: ~8 experts per lane, 1..32
+  int L = 1;
+  while (L < 32 && d.E / (L * 2) >= 8) L *= 2;
+  const void* kern = L == 1 ? (const void*)k_gate_bwd<1> : L == 2 ? (const void*)k_gate_bwd<2>
+                     : L == 4 ? (const void*)k_gate_bwd<4> : L == 8 ? (const void*)k_gate_bwd<8>
+                     : L == 16 ? (const void*)k_gate_bwd<16> : (const void*)k_gate_bwd<32>;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_gate_bwd,
-                                                kGateBwdWarps * 32, 0);
-  const int need = (d.S + kGateBwdWarps - 1) / kGateBwdWarps;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGateBwdThreads, 0);
+  const int tokens_per_cta = kGateBwdThreads / L;
+  const int need = (d.S + tokens_per_cta - 1) / tokens_per_cta;
   const int grid = std::min(need, std::max(1, per_sm) * device_sm_count());
   void* args[] = {&a};
-  cudaError_t e = launch_pdl((const void*)k_gate_bwd, dim3(grid), dim3(kGateBwdWarps * 32), 0,
-                             stream, args);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kGateBwdThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate_backward: launch");
   return MOE_OK;
 }
