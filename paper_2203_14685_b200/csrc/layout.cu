@@ -24,6 +24,7 @@ template <int VB, int U>
 __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   using V = Vec<VB>;
   __shared__ int s_beg[257];
+  if (a.prefetch) prefetch_share_l2(a.src, (size_t)a.S * a.row_bytes);
   pdl_wait();     // routing comes from moe_gate
   pdl_trigger();
   pad_prefix(a, s_beg);
@@ -570,6 +571,7 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.E_local = E_local;
   a.rank = rank;
   a.sys_fence = E_local != d.E;
+  a.prefetch = env_int("MOE_LAYOUT_PREFETCH", 1);
   // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
   // ~100 KB per-CTA budget (two CTAs per SM)
   const int tma_env = env_int(a.sys_fence ? "MOE_P2P_LAYOUT_TMA" : "MOE_LAYOUT_TMA", 0);

@@ -36,7 +36,31 @@ struct RowArgs {
   // rows earlier source ranks put there; 0 locally); no padding rows.
   const int32_t* offsets;
   const int32_t* peer_base;
+  // layout only: before waiting on the gate (PDL), the CTAs spread bulk L2
+  // prefetches of x (the rows do not depend on the routing), so x streams
+  // in from HBM while the latency-bound gate runs
+  int prefetch;
 };
+
+// Bulk-prefetch this CTA's 1/gridDim share of [p, p + bytes) into L2 with an
+// evict-last policy (cp.async.bulk.prefetch.L2; 16 KiB pieces, one per
+// thread).  Fire and forget: no shared memory, no completion to wait for.
+__device__ __forceinline__ void prefetch_share_l2(const char* p, size_t bytes) {
+  const size_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
+  const size_t beg = (size_t)blockIdx.x * per;
+  const size_t end = beg + per < bytes ? beg + per : bytes;
+  constexpr size_t kPiece = 16384;
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  for (size_t o = beg + (size_t)threadIdx.x * kPiece; o < end; o += (size_t)blockDim.x * kPiece) {
+    const size_t n = (end - o) < kPiece ? (end - o) : kPiece;
+    const unsigned nb = (unsigned)(n & ~(size_t)15);
+    if (nb)
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p + o),
+                   "r"(nb), "l"(pol)
+                   : "memory");
+  }
+}
 
 __device__ __forceinline__ size_t row_index(const RowArgs& a, int q, int e, int s) {
   if (a.offsets) {
