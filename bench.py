@@ -586,5 +586,16 @@ def main():
         dist.destroy_process_group()
 
 
+def _json_stdout():
+    """Keep stdout for the ONE JSON line: native libraries (NCCL's version
+    banner, ...) print to fd 1, so fd 1 is pointed at stderr and the JSON is
+    written to a saved duplicate of the original stdout."""
+    sys.stdout.flush()
+    real = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(real, "w")
+
+
 if __name__ == "__main__":
+    _json_stdout()
     main()
