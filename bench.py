@@ -284,6 +284,19 @@ def main():
         if P > 1:
             dist.barrier()
 
+    # Per-step alignment of the ranks' streams, OUTSIDE the events: without
+    # it, host-side launch skew between ranks shows up as device time inside
+    # the step (the first exchange waits for the latest rank).  A device-side
+    # barrier (moe_comm_barrier over NVLink) when peer memory is available.
+    can_align = P > 1 and comm is not None
+    def align():
+        nonlocal can_align
+        if can_align:
+            try:
+                comm.barrier()
+            except moe.MoeError:
+                can_align = False
+
     def step(mark=None):
         return pipe.step(d_in["logits"], d_in["x"], d_in["token_ids"], d_in["table"],
                          expert=False, mark=mark)
@@ -315,6 +328,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(K):
             flush_l2()                          # L2 flush, outside the events
+            align()
             ev[i][0].record()
             g_step.replay()
             ev[i][1].record()
@@ -330,6 +344,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(K):
             flush_l2()
+            align()
             g_timed.replay()
             torch.cuda.synchronize()
             for j in range(len(stages)):
@@ -344,6 +359,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(K):
             flush_l2()
+            align()
             ev[i][0].record()
             step()
             ev[i][1].record()
@@ -422,6 +438,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(Kb):
             flush_l2()
+            align()
             evb[i][0].record()
             g_bwd.replay()
             evb[i][1].record()
@@ -458,6 +475,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(K2):
             flush_l2()
+            align()
             evs[i][0].record()
             pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
                            inputs=staging)

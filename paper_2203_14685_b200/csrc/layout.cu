@@ -571,10 +571,12 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.E_local = E_local;
   a.rank = rank;
   a.sys_fence = E_local != d.E;
-  a.prefetch = env_int("MOE_LAYOUT_PREFETCH", 1);
+  a.prefetch = env_int("MOE_LAYOUT_PREFETCH", 0);  // measured slower (C2 +3 us, C3 +11 us): off
   // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
   // ~100 KB per-CTA budget (two CTAs per SM)
-  const int tma_env = env_int(a.sys_fence ? "MOE_P2P_LAYOUT_TMA" : "MOE_LAYOUT_TMA", 0);
+  // TMA bulk stores: slower than the register path into local HBM, faster
+  // into peers' memory over NVLink (C3 at P=2: 122 vs 132 us)
+  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", 1) : env_int("MOE_LAYOUT_TMA", 0);
   const int budget = env_int("MOE_LAYOUT_TMA_SMEM", 100 * 1024);
   const int ns = std::min(16, (budget - a.row_bytes) / (kTmaWarps * std::max(1, a.row_bytes)));
   if (tma_env && a.row_bytes % 16 == 0 && ns >= 2) {
@@ -652,10 +654,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     const int T = env_int("MOE_REVERSE_TPW", 0) ? std::max(1, per / Uc) : 1;  // TPW: no measured gain
 #define MOE_RK(KK, UU, TT) (f ? (const void*)k_reverse_k<MOE_F32, KK, UU, TT> : (const void*)k_reverse_k<MOE_BF16, KK, UU, TT>)
     if (a.k == 1)
-      kern = Uc == 4 ? MOE_RK(1, 4, 1) : Uc == 2 ? (T >= 2 ? MOE_RK(1, 2, 2) : MOE_RK(1, 2, 1))
-                                      : (T >= 4 ? MOE_RK(1, 1, 4) : T >= 2 ? MOE_RK(1, 1, 2) : MOE_RK(1, 1, 1));
+      kern = Uc == 4 ? (T >= 2 ? MOE_RK(1, 4, 2) : MOE_RK(1, 4, 1))
+             : Uc == 2 ? (T >= 4 ? MOE_RK(1, 2, 4) : T >= 2 ? MOE_RK(1, 2, 2) : MOE_RK(1, 2, 1))
+                       : (T >= 4 ? MOE_RK(1, 1, 4) : T >= 2 ? MOE_RK(1, 1, 2) : MOE_RK(1, 1, 1));
     else
-      kern = Uc >= 2 ? MOE_RK(2, 2, 1) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
+      kern = Uc >= 2 ? (T >= 2 ? MOE_RK(2, 2, 2) : MOE_RK(2, 2, 1)) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
 #undef MOE_RK
   } else if (a.row_bytes % 32 == 0) {
     if (U == 1)
