@@ -735,6 +735,77 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
   }
 }
 
+// Two-kernel variant of scan + slots: every CTA reduces the column
+// aggregates itself (prefix over earlier tiles and the total, warp per
+// column, 8 loads in flight per lane; O(tiles x columns) L2 words per CTA),
+// then finishes its slots like k_gate_slots.  One launch and one dependency
+// fewer than select -> scan -> slots.
+__global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
+  __shared__ int s_pre[kMaxCols], s_tot[kMaxCols];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int t0 = tile * a.tile_tokens;
+  const int nt = min(a.tile_tokens, a.S - t0);
+  const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  pdl_wait();
+  pdl_trigger();
+  const unsigned* agg = reinterpret_cast<const unsigned*>(a.status);
+  for (int c = warp; c < a.ncols; c += kGateWarps) {
+    const unsigned* col = agg + (size_t)c * a.n_tiles;
+    unsigned pre = 0, tot = 0;
+    for (int base = 0; base < a.n_tiles; base += 256) {
+      unsigned v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * 32 + lane;
+        v[u] = i < a.n_tiles ? __ldcg(col + i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        tot += v[u];
+        if (base + u * 32 + lane < tile) pre += v[u];
+      }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+      pre += __shfl_xor_sync(0xffffffffu, pre, m);
+      tot += __shfl_xor_sync(0xffffffffu, tot, m);
+    }
+    if (lane == 0) {
+      s_pre[c] = (int)pre;
+      s_tot[c] = (int)tot;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nt * a.k; i += kGateThreads) {
+    const size_t gi = (size_t)t0 * a.k + i;
+    const int e = a.expert_idx[gi];
+    if (e < 0) continue;
+    const int j = i % a.k;
+    const int col = slot_prio ? j * a.E + e : e;
+    int s = a.slot_idx[gi] + s_pre[col];
+    if (slot_prio)
+      for (int jj = 0; jj < j; ++jj) s += s_tot[jj * a.E + e];
+    if (s < a.cap) {
+      a.slot_idx[gi] = s;
+      if (a.slot_src) a.slot_src[(size_t)e * a.cap + s] = (int)gi;
+    } else {
+      a.slot_idx[gi] = -1;
+      a.weight[gi] = 0.f;
+    }
+  }
+  for (int e = tile * kGateWarps + warp; e < a.E; e += gridDim.x * kGateWarps) {
+    int ld = 0;
+    if (slot_prio)
+      for (int jj = 0; jj < a.k; ++jj) ld += s_tot[jj * a.E + e];
+    else
+      ld = s_tot[e];
+    if (lane == 0) a.load[e] = ld;
+    if (a.slot_src)
+      for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
+  }
+}
+
 // ------------------------------------------------------------ single launch
 // The three kernels above as ONE cooperative launch (every tile's CTA is
 // co-resident): phases A/B as in k_gate_select, one grid barrier, then each
@@ -943,6 +1014,13 @@ static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, Ga
   cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
                              stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
+  // two kernels (select -> slots2) when the per-CTA column reduction is small
+  if ((long long)p.n_tiles * p.ncols <= env_int("MOE_GATE_TWO_MAXW", 4096)) {
+    e = launch_pdl((const void*)k_gate_slots2, dim3(p.n_tiles), dim3(kGateThreads), 0, stream,
+                   args);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots2 launch");
+    return MOE_OK;
+  }
   e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
                  dim3(kGateThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");

@@ -423,6 +423,125 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   }
 }
 
+// ------------------------------------------------------------ Reverse, TMA
+// The combine with the k admitted rows of a token brought into shared memory
+// by the copy engine: each warp is an independent pipeline over a contiguous
+// token range.  Lane 0 bulk-loads the token's rows (cp.async.bulk, one
+// mbarrier per stage with the summed expect_tx) up to NS tokens ahead; the
+// whole warp then accumulates from shared memory in fp32 (ascending j from
+// 0, the same order as k_reverse) and stores y with 32-byte vectors.  The
+// routing of 32 tokens is fetched at once (lane l: token base + l) and
+// handed to lane 0 by shuffles.  Meant for the NVLink combine, where the
+// rows come from peers' memory: bytes in flight are set by shared memory.
+constexpr int kRevTmaMaxK = 4;
+
+template <int DT>
+__global__ void __launch_bounds__(kTmaThreads) k_reverse_tma(TmaArgs ta) {
+  const RowArgs& a = ta.a;
+  const int NS = ta.ns;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps * 16];
+  __shared__ float s_w[kTmaWarps][16][kRevTmaMaxK];  // per stage: weights (0 = no row)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned rb = (unsigned)a.row_bytes, sb = rb * a.k;  // stage bytes
+  if (lane == 0)
+    for (int s = 0; s < NS; ++s) mbar_init(smem_u32(&s_bar[warp * 16 + s]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  pdl_wait();
+  pdl_trigger();
+  const long long gw = (long long)blockIdx.x * kTmaWarps + warp, GW = (long long)gridDim.x * kTmaWarps;
+  const int beg = (int)((long long)a.S * gw / GW), end = (int)((long long)a.S * (gw + 1) / GW);
+  const int ntok = end - beg;
+  char* stages = smem + (size_t)warp * NS * sb;
+  const unsigned st0 = smem_u32(stages), bar0 = smem_u32(&s_bar[warp * 16]);
+  constexpr int NA = DT == MOE_F32 ? 8 : 16;
+
+  // routing of the current issue batch: lane l holds token (ibase + l)
+  const char* src[kRevTmaMaxK];
+  float wt[kRevTmaMaxK];
+  int ibase = -32;
+  int issued = 0;
+  for (int o = 0; o < ntok; ++o) {
+    // keep up to NS tokens issued ahead of the consumer
+    while (issued < ntok && issued < o + NS) {
+      if (issued >= ibase + 32) {  // next routing batch (warp-uniform)
+        ibase = issued;
+        const int t = beg + ibase + lane;
+#pragma unroll
+        for (int j = 0; j < kRevTmaMaxK; ++j) {
+          src[j] = nullptr;
+          wt[j] = 0.f;
+          if (j < a.k && t < end) {
+            const int sl = __ldg(a.slot_idx + (size_t)t * a.k + j);
+            if (sl >= 0) {
+              src[j] = src_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), sl);
+              wt[j] = row_weight(a, (size_t)t * a.k + j);
+            }
+          }
+        }
+      }
+      const int from = issued - ibase;
+      const int st = issued % NS;
+      unsigned nrows = 0;
+      const char* ps[kRevTmaMaxK];
+#pragma unroll
+      for (int j = 0; j < kRevTmaMaxK; ++j) {
+        ps[j] = reinterpret_cast<const char*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src[j]), from));
+        const float w = __shfl_sync(0xffffffffu, wt[j], from);
+        if (lane == 0) s_w[warp][st][j] = ps[j] ? w : 0.f;
+        nrows += ps[j] ? 1u : 0u;
+      }
+      if (lane == 0) {
+        const unsigned bar = bar0 + 8 * st;
+        if (nrows == 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+        } else {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"(nrows * rb)
+                       : "memory");
+#pragma unroll
+          for (int j = 0; j < kRevTmaMaxK; ++j)
+            if (ps[j])
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  ::"r"(st0 + st * sb + j * rb), "l"(ps[j]), "r"(rb), "r"(bar)
+                  : "memory");
+        }
+      }
+      ++issued;
+    }
+    __syncwarp();
+    const int st = o % NS;
+    mbar_wait(bar0 + 8 * st, (unsigned)(o / NS) & 1u);
+    const char* stage = stages + (size_t)st * sb;
+    char* yrow = a.dst + (size_t)(beg + o) * rb;
+    for (unsigned off = lane * 32u; off < rb; off += 32u * 32u) {
+      float acc[NA];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) acc[q] = 0.f;
+      for (int j = 0; j < a.k; ++j) {
+        const float w = s_w[warp][st][j];
+        // a dropped slot has no row; a zero weight adds an exact +0 (acc
+        // starts at +0), so skipping it leaves the same bits
+        if (w == 0.f) continue;
+        const V4* v4 = reinterpret_cast<const V4*>(stage + j * rb + off);
+        V8 v;
+        const V4 lo = v4[0], hi = v4[1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v.w[q] = lo.w[q];
+          v.w[q + 4] = hi.w[q];
+        }
+        fma_vec<DT>(acc, w, v);
+      }
+      st_v8(yrow + off, pack_vec<DT>(acc));
+    }
+    __syncwarp();  // every lane done with the stage before lane 0 refills it
+  }
+}
+
 // 16-byte fallback of the combine for rows that are not a multiple of 32 B.
 template <int DT>
 __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
@@ -640,6 +759,28 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   a.speer = src;
   a.E_local = E_local;
   a.rank = rank;
+  // TMA-staged combine (peer mode by default: rows come over NVLink)
+  {
+    const bool peer = E_local != d.E;
+    const int tma = peer ? env_int("MOE_P2P_REVERSE_TMA", 0) : env_int("MOE_REVERSE_TMA", 0);
+    const int budget = env_int("MOE_REVERSE_TMA_SMEM", 100 * 1024);
+    const int ns = std::min(16, budget / (kTmaWarps * std::max(1, a.row_bytes * a.k)));
+    if (tma && a.row_bytes % 32 == 0 && a.k <= kRevTmaMaxK && ns >= 2) {
+      TmaArgs ta{a, ns};
+      const size_t smem = (size_t)a.row_bytes * a.k * kTmaWarps * ns;
+      const void* kt = dtype == MOE_F32 ? (const void*)k_reverse_tma<MOE_F32>
+                                        : (const void*)k_reverse_tma<MOE_BF16>;
+      cudaError_t e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: smem attribute");
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, kTmaThreads, smem);
+      const int grid = std::max(1, per_sm) * device_sm_count();
+      void* args[] = {&ta};
+      e = launch_pdl(kt, dim3(grid), dim3(kTmaThreads), smem, stream, args);
+      if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: k_reverse_tma launch");
+      return MOE_OK;
+    }
+  }
   const void* kern;
   const int U = env_int("MOE_REVERSE_U", 1);
   const int KU = env_int("MOE_REVERSE_KU", 4);  // k <= 2 path: vectors per lane per round (x k rows)
