@@ -182,3 +182,40 @@ def test_alltoall_and_plan_validation():
     assert L.moe_expert_scale(FAKE, FAKE, 0, 1, 0, 1, 8, 1, None) == INVALID
     for s in range(7):
         assert L.moe_status_str(s).decode().startswith("MOE_")
+
+
+def test_backward_and_packed_entry_points_validate_on_host():
+    """The NEXT-1 / NEXT-4 entry points reject bad arguments before anything
+    is enqueued (no GPU needed: validation fails first)."""
+    from paper_2203_14685_b200._lib import i64
+    L = lib()
+    d = GateDesc(64, 8, 2, 16, 0, 0, 0)
+    r = RoutingC(FAKE, FAKE, FAKE, FAKE, None)
+    rd, dr = ctypes.byref(d), ctypes.byref(r)
+    # combine adjoint: d_back / d_weight required, alignment, dtype
+    assert L.moe_reverse_layout_backward(rd, dr, FAKE, FAKE, 64, 1, None, FAKE, None) == INVALID
+    assert L.moe_reverse_layout_backward(rd, dr, FAKE, FAKE, 64, 1, FAKE + 8, FAKE, None) == ALIGN
+    assert L.moe_reverse_layout_backward(rd, dr, FAKE, FAKE, 64, 7, FAKE, FAKE, None) == INVALID
+    assert L.moe_reverse_layout_backward(rd, dr, FAKE, FAKE, 3, 1, FAKE, FAKE, None) == ALIGN
+    # layout adjoint
+    assert L.moe_layout_backward(rd, dr, None, 64, 1, FAKE, None) == INVALID
+    assert L.moe_layout_backward(rd, dr, FAKE, 64, 1, FAKE + 4, None) == ALIGN
+    # gate adjoint: the hash gate has no logits
+    h = GateDesc(64, 8, 1, 16, 2, 0, 0)
+    assert L.moe_gate_backward(ctypes.byref(h), FAKE, dr, FAKE, FAKE, None) == INVALID
+    assert "hash" in L.moe_last_error().decode()
+    assert L.moe_gate_backward(rd, FAKE, dr, None, FAKE, None) == INVALID
+    # packed form
+    assert L.moe_expert_offsets(rd, dr, None, None) == INVALID
+    assert L.moe_layout_packed(rd, dr, None, FAKE, 64, 1, FAKE, None) == INVALID
+    assert L.moe_reverse_layout_packed(rd, dr, None, FAKE, 64, 1, FAKE, None) == INVALID
+    assert L.moe_layout_packed(rd, dr, FAKE, FAKE, 3, 1, FAKE, None) == ALIGN
+    # alltoallv and the device-side exchanges need a communicator
+    rows = (i64 * 1)(0)
+    assert L.moe_alltoallv(None, FAKE, rows, FAKE, rows, 64, None) == INVALID
+    assert L.moe_dispatch_packed_p2p(None, rd, dr, FAKE, FAKE, FAKE, FAKE, FAKE, 64, 1, FAKE,
+                                     1 << 20, 0, None) == INVALID
+    assert L.moe_combine_packed_p2p(None, rd, dr, FAKE, FAKE, FAKE, 64, 1, 1 << 20, FAKE, 0,
+                                    None) == INVALID
+    assert L.moe_combine_backward_p2p(None, rd, dr, FAKE, FAKE, 64, 1, FAKE, FAKE, 0, None) == INVALID
+    assert L.moe_dispatch_backward_p2p(None, rd, dr, FAKE, 64, 1, FAKE, 0, None) == INVALID
