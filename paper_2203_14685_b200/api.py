@@ -242,6 +242,27 @@ def reverse_layout_packed(back: torch.Tensor, r: Routing, offsets: torch.Tensor,
     return out
 
 
+def alltoallv_plan(offsets, recv_counts, nranks: int):
+    """Host plan of the NCCL dropless exchange (NEXT-4): from this rank's
+    expert offsets [E+1] (moe_expert_offsets) and the per-expert counts it
+    receives, recv_counts[src*E/P + le] (an AllToAll of the count table),
+    return (send_rows[P], recv_rows[P], recv_offsets[E+1]) for moe_alltoallv.
+    Experts are contiguous blocks of E/P per rank (R10); the receive buffer
+    is source-rank major, then local expert (R20).  Pure host arithmetic."""
+    offsets = [int(v) for v in offsets]
+    recv_counts = [int(v) for v in recv_counts]
+    E = len(offsets) - 1
+    if E % nranks or len(recv_counts) != E:
+        raise ValueError("need E %% nranks == 0 and E recv counts (E=%d, P=%d)" % (E, nranks))
+    El = E // nranks
+    send_rows = [offsets[(q + 1) * El] - offsets[q * El] for q in range(nranks)]
+    recv_rows = [sum(recv_counts[q * El:(q + 1) * El]) for q in range(nranks)]
+    recv_offsets = [0]
+    for c in recv_counts:
+        recv_offsets.append(recv_offsets[-1] + c)
+    return send_rows, recv_rows, recv_offsets
+
+
 def reverse_layout_backward(dy: torch.Tensor, back: torch.Tensor, r: Routing,
                             d_back: Optional[torch.Tensor] = None,
                             d_weight: Optional[torch.Tensor] = None):
