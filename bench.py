@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
+    ap.add_argument("--dropless", action="store_true",
+                    help="NEXT-4: packed dropless layout (capacity = S*k), device-side exchange")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verbose", action="store_true", help="progress on stderr")
     return ap.parse_args()
@@ -244,9 +246,13 @@ def main():
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
     row = w.d * (2 if w.dtype == "bf16" else 4)
     algo = a.algo if P > 1 else "flat"
+    if a.dropless:
+        cap = S * w.k     # nothing is dropped; the packed form has no padding (NEXT-4)
+        if P > 1:
+            algo = "p2p"
     try:
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
-                                 group_size=G, device=dev)
+                                 group_size=G, device=dev, dropless=a.dropless)
     except moe.MoeError as err:
         if algo != "p2p":
             raise
@@ -403,16 +409,17 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush_l2()
     e0.record()
-    moe.expert_scale(pipe.recv, P, w.E // P, rank * (w.E // P), out=pipe.recv)
+    if not a.dropless:
+        moe.expert_scale(pipe.recv, P, w.E // P, rank * (w.E // P), out=pipe.recv)
     e1.record()
     torch.cuda.synchronize()
-    expert_ms = e0.elapsed_time(e1)
+    expert_ms = None if a.dropless else e0.elapsed_time(e1)
 
     # ---- backward of the routing path (NEXT-1), informational: the adjoint
     # kernels of the same step (combine -> AllToAll x2 -> layout, + gate),
     # one CUDA graph, L2 flushed between replays, max over ranks
     bwd = None
-    if not a.no_backward:
+    if not a.no_backward and not a.dropless:
         dy = torch.from_numpy(synthgen.tokens(synthgen.seed_for(w.index, rank, 9), S, w.d,
                                               w.dtype))
         if w.dtype == "bf16":
@@ -499,6 +506,17 @@ def main():
     admitted = int((pipe.routing.slot_idx >= 0).sum().item())
     ab = algorithmic_bytes(w, S, cap, P, row)
     ab["reverse"] = admitted * row + S * row + 12 * S * w.k
+    if a.dropless:
+        # packed: no padding rows; the rows leaving this rank are the admitted
+        # rows of other ranks' experts
+        ab["layout"] = S * row + admitted * row + 8 * S * w.k
+        ab["gate"] = S * (4 * w.E if w.kind != "hash" else 8) + 12 * S * w.k + 8 * w.E
+        if P > 1:
+            El = w.E // P
+            ex = pipe.routing.expert_idx
+            out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) &
+                            ((ex // El) != rank)).sum().item())
+            ab["a2a"] = out_rows * row
     peak, peak_src = measured_peaks()
     traffic = None
     try:
@@ -570,8 +588,16 @@ def main():
     # our kernels per step: gate (k_gate_select, k_gate_scan, k_gate_slots),
     # layout, reverse, on hierarchical leaders one chunk permute per AllToAll,
     # and on the one-sided path the dispatch's and the combine's exit barriers
-    launches_per_step = 5 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
-        (2 if (P > 1 and algo == "p2p") else 0)
+    import ctypes
+    from paper_2203_14685_b200._lib import lib as _moelib
+    gate_k = _moelib().moe_gate_kernel_count(ctypes.byref(pipe.routing.desc()), 1)
+    if a.dropless:
+        # gate + expert offsets + (P=1: packed layout, packed reverse;
+        # P>1: counts, barrier, plan, layout, exit barrier, reverse, exit barrier)
+        launches_per_step = gate_k + 1 + (7 if P > 1 else 2)
+    else:
+        launches_per_step = gate_k + 2 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
+            (2 if (P > 1 and algo == "p2p") else 0)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
@@ -581,6 +607,7 @@ def main():
             "config": {"workload": w.name, "desc": w.note, "S_per_rank": S, "d": w.d, "E": w.E,
                        "k": w.k, "gate": w.kind, "capacity_factor": w.C, "capacity": cap,
                        "a2a": algo if P > 1 else None,
+                       "layout_form": "packed dropless (NEXT-4)" if a.dropless else "padded [E,cap,d]",
                        "parallelism": "ep%d (experts sharded, tokens data-parallel)" % P,
                        "l2": "flushed between timed steps (2x L2 memset + 2x L2 read, outside events)",
                        "expert": "identity in the timed step; s_e stand-in timed separately"},

@@ -127,6 +127,11 @@ int32_t moe_capacity(int32_t S, int32_t E, int32_t k, double C);
  * two streams concurrently. */
 size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc);
 
+/* host.  How many kernels one moe_gate / moe_gate_ex call enqueues for
+ * `desc` with the default tuning (2 or 3; -1 if desc is invalid or the
+ * count is decided at launch).  For launch accounting (bench.py). */
+int32_t moe_gate_kernel_count(const moe_gate_desc_t* desc, int32_t n_groups);
+
 /* Step 1 of Algorithm 1 plus capacity:
  * selection (TOPK: Eq. 1 TopK on raw fp32 logits, R2; KTOP1: per-prototype
  * argmax; HASH: table lookup), weights (Eq. 1 softmax, R1) and capacity

@@ -45,6 +45,7 @@ class A2AOp(ctypes.Structure):
 SIGNATURES = [
     ("moe_capacity", i32, [i32, i32, i32, ctypes.c_double]),
     ("moe_gate_workspace_bytes", sz, [ctypes.POINTER(GateDesc)]),
+    ("moe_gate_kernel_count", i32, [ctypes.POINTER(GateDesc), i32]),
     ("moe_gate", ctypes.c_int, [ctypes.POINTER(GateDesc), vp, vp, vp, i32,
                                 ctypes.POINTER(RoutingC), vp, sz, vp]),
     ("moe_gate_ex", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),

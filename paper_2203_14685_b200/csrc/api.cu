@@ -3,6 +3,7 @@
 // the kernels of gate.cu / layout.cu.  moe_alltoall lives in comm.cu.
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -142,6 +143,11 @@ int32_t moe_capacity(int32_t S, int32_t E, int32_t k, double C) {
   const double c = std::ceil(C * (double)S * (double)k / (double)E);
   if (!(c >= 1.0) || c > 2147483647.0) return -1;
   return (int32_t)c;
+}
+
+int32_t moe_gate_kernel_count(const moe_gate_desc_t* desc, int32_t n_groups) {
+  if (check_desc("moe_gate_kernel_count", desc) != MOE_OK) return -1;
+  return gate_kernel_count(*desc, desc->kind == MOE_GATE_SAM ? std::max(1, n_groups) : 1);
 }
 
 size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc) {

@@ -40,6 +40,19 @@ __device__ __forceinline__ uint32_t mul_rne_bf16(float w, float v) {
   return (b >> 16) + up;
 }
 
+// Two lanes of a bf16x2 word: the common case is one hardware RNE convert of
+// hi = RN_fp32(w*v) (cvt.rn.bf16x2.f32); only when either hi sits exactly on
+// a bf16 midpoint (low half 0x8000, ~2^-16 of values) is the exact
+// remainder consulted (mul_rne_bf16).  Same bits as mul_rne_bf16 on both.
+__device__ __forceinline__ uint32_t mul2_rne_bf16(float w, uint32_t v2) {
+  const float a = bf16lo(v2), b = bf16hi(v2);
+  const float ha = __fmul_rn(w, a), hb = __fmul_rn(w, b);
+  const uint32_t ba = __float_as_uint(ha), bb = __float_as_uint(hb);
+  if (((ba & 0xFFFFu) == 0x8000u) | ((bb & 0xFFFFu) == 0x8000u))
+    return mul_rne_bf16(w, a) | (mul_rne_bf16(w, b) << 16);
+  return pack_bf16x2(ha, hb);
+}
+
 template <int DT>
 __device__ __forceinline__ V8 scale_vec(float w, const V8& v) {
   V8 o;
@@ -48,8 +61,7 @@ __device__ __forceinline__ V8 scale_vec(float w, const V8& v) {
     for (int q = 0; q < 8; ++q) o.w[q] = __float_as_uint(__fmul_rn(w, __uint_as_float(v.w[q])));
   } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      o.w[q] = mul_rne_bf16(w, bf16lo(v.w[q])) | (mul_rne_bf16(w, bf16hi(v.w[q])) << 16);
+    for (int q = 0; q < 8; ++q) o.w[q] = mul2_rne_bf16(w, v.w[q]);
   }
   return o;
 }
@@ -139,7 +151,7 @@ __global__ void __launch_bounds__(kRowThreads) k_combine_bwd(RowArgs a, float* d
 // slot's scaled row is stored and its dot accumulated.  Same arithmetic
 // order as k_combine_bwd (column order per lane, then the warp tree).
 template <int DT, int KK, int U>
-__global__ void __launch_bounds__(kRowThreads) k_combine_bwd_k(RowArgs a, float* d_weight) {
+__global__ void __launch_bounds__(kRowThreads, 3) k_combine_bwd_k(RowArgs a, float* d_weight) {
   constexpr int VB = 32, SEG = 32 * U * VB;
   __shared__ int s_beg[257];
   pdl_wait();
@@ -426,9 +438,13 @@ moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, cons
                              const float* d_weight, float* d_logits, cudaStream_t stream) {
   GateBwdArgs a{logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
                 d.weight_mode};
-  // lanes per token: ~8 experts per lane, 1..32
-  int L = 1;
-  while (L < 32 && d.E / (L * 2) >= 8) L *= 2;
+  // lanes per token: one expert per lane up to 32 lanes (the per-token work
+  // is a short dependent chain; more lanes = more tokens' chains in flight)
+  int L = env_int("MOE_GATE_BWD_LANES", 0);
+  if (L <= 0) {
+    L = 1;
+    while (L < 32 && L * 2 <= d.E) L *= 2;
+  }
   const void* kern = L == 1 ? (const void*)k_gate_bwd<1> : L == 2 ? (const void*)k_gate_bwd<2>
                      : L == 4 ? (const void*)k_gate_bwd<4> : L == 8 ? (const void*)k_gate_bwd<8>
                      : L == 16 ? (const void*)k_gate_bwd<16> : (const void*)k_gate_bwd<32>;

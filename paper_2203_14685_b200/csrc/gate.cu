@@ -997,6 +997,14 @@ static GateKernel pick_gate(const moe_gate_desc_t& d, const GatePlan& p) {
 
 static int fused_tiles() { return env_int("MOE_GATE_FUSED_TILES", 128); }
 
+// Kernels one moe_gate call enqueues for `d` with the default knobs (the
+// fused single launch is off by default): 2 (select -> slots2) or 3.
+int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
+  if (env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH) return -1;  // decided at launch
+  const GatePlan p = gate_plan(d, 256, ngroups);
+  return (long long)p.n_tiles * p.ncols <= env_int("MOE_GATE_TWO_MAXW", 4096) ? 2 : 3;
+}
+
 size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
   return std::max(gate_plan(d).bytes, gate_plan(d, fused_tiles()).bytes);
 }

@@ -6,6 +6,7 @@
 namespace moe {
 
 size_t gate_workspace_bytes(const moe_gate_desc_t& d);
+int gate_kernel_count(const moe_gate_desc_t& d, int ngroups);
 moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
                          const moe_routing_t& out, void* ws, cudaStream_t stream);
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);

@@ -12,16 +12,25 @@ from typing import Optional
 
 import torch
 
-from .api import (Comm, Gate, Routing, expert_scale, gate_backward, layout, layout_backward,
-                  reverse_layout, reverse_layout_backward)
+from .api import (Comm, Gate, Routing, expert_offsets, expert_scale, gate_backward, layout,
+                  layout_backward, layout_packed, reverse_layout, reverse_layout_backward,
+                  reverse_layout_packed)
 
 
 class RoutePipeline:
     def __init__(self, S: int, d: int, E: int, k: int, cap: int, dtype=torch.bfloat16,
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
-                 device=None, slot_src: bool = True):
+                 device=None, slot_src: bool = True, dropless: bool = False):
+        """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
+        dropped) and the packed layout is used -- locally moe_layout_packed /
+        moe_reverse_layout_packed, across ranks the device-side NVLink
+        exchange (algo "p2p" only).  The expert stand-in is the identity."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.dropless = dropless
+        if dropless:
+            cap = S * k
+            slot_src = False
         self.comm = comm
         self.P = comm.nranks if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
@@ -34,7 +43,21 @@ class RoutePipeline:
         self.routing = Routing.empty(S, E, k, cap, self.device, self.gate.kind, self.gate.mode,
                                      self.gate.prio, slot_src)
         mk = lambda *shape: torch.empty(shape, dtype=dtype, device=self.device)
-        if self.P > 1 and algo == "p2p":
+        if dropless:
+            if self.P > 1 and algo != "p2p":
+                raise ValueError("dropless across ranks uses the device-side NVLink exchange "
+                                 "(algo='p2p'); see moe_alltoallv for the NCCL form")
+            self.offsets = torch.empty((E + 1,), dtype=torch.int32, device=self.device)
+            if self.P > 1:
+                rows = self.P * S * k   # worst case: every row to one rank
+                self.counts = comm.symm_empty((E,), torch.int32)
+                self.recv = comm.symm_empty((rows, d), dtype)
+                self.peer_base = torch.empty((self.P,), dtype=torch.int32, device=self.device)
+                self.recv_offsets = torch.empty((E + 1,), dtype=torch.int32, device=self.device)
+            else:
+                self.recv = mk(S * k, d)
+            self.dispatch = self.back = self.recv
+        elif self.P > 1 and algo == "p2p":
             # one-sided NVLink path: layout fused into the dispatch (rows are
             # stored into the owner's symmetric recv), combine fused into the
             # reverse (rows are read from the owner's recv); no staging buffers
@@ -72,6 +95,8 @@ class RoutePipeline:
         bench records a CUDA event there)."""
         mark = mark or (lambda name: None)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
+        if self.dropless:
+            return self._step_dropless(r, x, mark)
         mark("gate")
         if self.P > 1 and self.algo == "p2p":                              # steps 2+3 fused
             # no entry barrier: the previous step's combine ended with one
@@ -100,12 +125,37 @@ class RoutePipeline:
         mark("reverse")
         return self.y
 
+    def _step_dropless(self, r, x, mark):
+        expert_offsets(r, out=self.offsets)
+        mark("gate")
+        if self.P > 1:
+            self.comm.dispatch_packed_p2p(x, r, self.offsets, self.counts, self.recv,
+                                          self.peer_base, self.recv_offsets,
+                                          flags=self._first_flags())
+            mark("layout")
+            mark("a2a_dispatch")
+            self.comm.combine_packed_p2p(self.recv, r, self.offsets, self.peer_base, self.y,
+                                         flags=self.comm.NO_ENTRY_BARRIER)
+            mark("a2a_combine")
+            mark("reverse")
+            return self.y
+        layout_packed(x, r, self.offsets, out=self.recv)
+        mark("layout")
+        mark("a2a_dispatch")
+        mark("a2a_combine")
+        reverse_layout_packed(self.recv, r, self.offsets, out=self.y)
+        mark("reverse")
+        return self.y
+
     def backward(self, dy: torch.Tensor, logits: Optional[torch.Tensor] = None):
         """Backward of the last step (NEXT-1) with the routing held fixed and
         an identity expert: the adjoints in reverse order -- combine
         (d_back, d_weight) -> AllToAll -> AllToAll -> layout (dx), plus the
         gate (d_logits, when the gate has logits).  Returns (dx, d_logits)."""
         r = self.routing
+        if self.dropless:
+            raise NotImplementedError("backward of the dropless packed form is not built "
+                                      "(use the padded form)")
         if not hasattr(self, "d_weight"):
             mk = lambda *shape: torch.empty(shape, dtype=self.y.dtype, device=self.device)
             self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32, device=self.device)
