@@ -530,7 +530,9 @@ def main():
         dom = "layout" if stage_ms["layout"] >= stage_ms["reverse"] else "reverse"
         achieved = ab[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": "k_" + dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": tr.get("%s/%s" % (w.name, dom)),
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": tr.get("%s/%s" % (w.name, dom + ("_k" if dom == "reverse" and w.k <= 2 else "")),
+                                  tr.get("%s/%s" % (w.name, dom))),
                 "algorithmic_bytes": ab[dom], "peak_source": peak_src}
     else:
         # fused one-sided path: the dispatch (k_layout in peer mode) and the

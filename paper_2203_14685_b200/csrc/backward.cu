@@ -438,12 +438,11 @@ moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, cons
                              const float* d_weight, float* d_logits, cudaStream_t stream) {
   GateBwdArgs a{logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
                 d.weight_mode};
-  // lanes per token: one expert per lane up to 32 lanes (the per-token work
-  // is a short dependent chain; more lanes = more tokens' chains in flight)
+  // lanes per token (MOE_GATE_BWD_LANES overrides)
   int L = env_int("MOE_GATE_BWD_LANES", 0);
   if (L <= 0) {
-    L = 1;
-    while (L < 32 && L * 2 <= d.E) L *= 2;
+    L = 1;  // ~8 experts per lane (one per lane measured slower at E = 8)
+    while (L < 32 && d.E / (L * 2) >= 8) L *= 2;
   }
   const void* kern = L == 1 ? (const void*)k_gate_bwd<1> : L == 2 ? (const void*)k_gate_bwd<2>
                      : L == 4 ? (const void*)k_gate_bwd<4> : L == 8 ? (const void*)k_gate_bwd<8>
