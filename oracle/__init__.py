@@ -105,6 +105,9 @@ def lib():
         L.orc_layout_bwd.restype = None
         L.orc_gate_bwd.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, P, P, P, P, P]
         L.orc_gate_bwd.restype = ctypes.c_int
+        L.orc_gate_bwd_ex.argtypes = [ctypes.c_int, ctypes.c_int, i32, i32, i32, P, P, i32, P,
+                                      ctypes.c_double, P, P, P, P, P]
+        L.orc_gate_bwd_ex.restype = ctypes.c_int
         L.orc_bf16_to_f64.argtypes = [ctypes.c_uint16]
         L.orc_bf16_to_f64.restype = ctypes.c_double
         L.orc_f64_to_bf16.argtypes = [ctypes.c_double]
@@ -314,6 +317,26 @@ def gate_bwd(logits: np.ndarray, r: Routing, d_weight: np.ndarray, *, kind="topk
     if rc != 0:
         raise ValueError("orc_gate_bwd rejected its arguments")
     return out
+
+
+def gate_bwd_ex(logits, r: Routing, d_weight, *, kind, weight_mode="renorm", group_logits=None,
+                n_groups=1, uniforms=None, tau=1.0):
+    """Adjoint of the SAM / Dense-to-Sparse weights (selection fixed).
+    Returns (d_logits [S,E], d_group_logits [S,n_groups] or None)."""
+    K = {"topk": TOPK, "ktop1": KTOP1, "hash": HASH, "sam": 3, "d2s": 4}[kind]
+    lg = _c(logits, np.float32)
+    S, E = lg.shape
+    gl = _c(group_logits, np.float32)
+    u = _c(uniforms, np.float32)
+    dw = _c(d_weight, np.float32)
+    out = np.empty((S, E), np.float32)
+    dg = np.empty((S, n_groups), np.float32) if kind == "sam" else None
+    rc = lib().orc_gate_bwd_ex(K, MODES[weight_mode], S, E, r.k, _ptr(lg), _ptr(gl), n_groups,
+                               _ptr(u), float(tau), _ptr(r.expert_idx), _ptr(r.slot_idx),
+                               _ptr(dw), _ptr(out), _ptr(dg))
+    if rc != 0:
+        raise ValueError("orc_gate_bwd_ex rejected its arguments")
+    return out, dg
 
 
 def _ptrs(bufs):

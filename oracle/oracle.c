@@ -636,3 +636,94 @@ void orc_alltoallv(int32_t P, int64_t row_bytes, const int64_t* counts,
     }
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Adjoints of the SAM and Dense-to-Sparse weights (R17, R18, R19).          */
+/* ------------------------------------------------------------------------ */
+int orc_gate_bwd_ex(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
+                    const float* logits, const float* group_logits, int32_t n_groups,
+                    const float* uniforms, double tau, const int32_t* expert_idx,
+                    const int32_t* slot_idx, const float* d_weight, float* d_logits,
+                    float* d_group_logits) {
+  enum { SAM = 3, D2S = 4 };
+  if (kind != SAM && kind != D2S)
+    return orc_gate_bwd(kind, weight_mode, S, E, k, logits, expert_idx, slot_idx, d_weight,
+                        d_logits);
+  if (S < 1 || E < 1 || k < 1 || !logits) return -1;
+  if (kind == SAM && (n_groups < 1 || E % n_groups != 0 || !group_logits)) return -1;
+  if (kind == D2S && (k != E || !(tau > 0.0))) return -1;
+  if (kind == SAM && weight_mode == ORC_RENORM) {
+    /* RENORM SAM weights are Eq. 1 on the k selected expert logits */
+    int rc = orc_gate_bwd(ORC_TOPK, ORC_RENORM, S, E, k, logits, expert_idx, slot_idx,
+                          d_weight, d_logits);
+    if (rc == 0 && d_group_logits)
+      for (int64_t i = 0; i < (int64_t)S * n_groups; ++i) d_group_logits[i] = 0.0f;
+    return rc;
+  }
+  double* grad = (double*)malloc(sizeof(double) * (size_t)E);
+  double* q = (double*)malloc(sizeof(double) * (size_t)E);    /* softmax over the domain */
+  double* z = (double*)malloc(sizeof(double) * (size_t)E);
+  int32_t* in_dom = (int32_t*)malloc(sizeof(int32_t) * (size_t)E);
+  double* gg = kind == SAM ? (double*)malloc(sizeof(double) * (size_t)n_groups) : NULL;
+  for (int32_t t = 0; t < S; ++t) {
+    const float* row = logits + (int64_t)t * E;
+    const int32_t* sel = expert_idx + (int64_t)t * k;
+    for (int32_t e = 0; e < E; ++e) grad[e] = 0.0;
+    double scale = 1.0;
+    int32_t g = 0;
+    if (kind == SAM) {
+      /* domain = the group of the selected experts; z = the raw logits */
+      const int32_t n = E / n_groups;
+      g = sel[0] / n;
+      for (int32_t e = 0; e < E; ++e) { in_dom[e] = (e / n == g); z[e] = (double)row[e]; }
+    } else {
+      /* z = (l + G)/tau; domain = the survivors (RENORM) or the row (SOFTMAX) */
+      for (int32_t e = 0; e < E; ++e) {
+        double gn = uniforms ? -log(-log((double)uniforms[(int64_t)t * E + e])) : 0.0;
+        z[e] = ((double)row[e] + gn) / tau;
+        in_dom[e] = (weight_mode == ORC_SOFTMAX);
+      }
+      if (weight_mode == ORC_RENORM)
+        for (int32_t j = 0; j < k; ++j)
+          if (sel[j] >= 0) in_dom[sel[j]] = 1;
+      scale = 1.0 / tau;
+    }
+    double m = -INFINITY, den = 0.0;
+    for (int32_t e = 0; e < E; ++e)
+      if (in_dom[e] && z[e] > m) m = z[e];
+    for (int32_t e = 0; e < E; ++e) den += in_dom[e] ? exp(z[e] - m) : 0.0;
+    for (int32_t e = 0; e < E; ++e) q[e] = in_dom[e] ? exp(z[e] - m) / den : 0.0;
+    double pg = 1.0;
+    if (kind == SAM) {
+      const float* gl = group_logits + (int64_t)t * n_groups;
+      double gden = 0.0;
+      for (int32_t h = 0; h < n_groups; ++h) gden += exp((double)gl[h] - (double)gl[g]);
+      pg = 1.0 / gden;
+      for (int32_t h = 0; h < n_groups; ++h) gg[h] = 0.0;
+    }
+    for (int32_t j = 0; j < k; ++j) {
+      int64_t i = (int64_t)t * k + j;
+      if (sel[j] < 0 || slot_idx[i] < 0) continue;               /* m_j = 0 */
+      double gj = (double)d_weight[i];
+      double wj = pg * q[sel[j]];                                 /* the weight */
+      /* dw_j/dz_e = w_j (delta(e, e_j) - q_e) on the domain; dz/dl = scale */
+      for (int32_t e = 0; e < E; ++e)
+        if (in_dom[e]) grad[e] += gj * scale * wj * ((e == sel[j] ? 1.0 : 0.0) - q[e]);
+      if (kind == SAM) {
+        /* dw_j/dgl_h = w_j (delta(h, g) - P(h)) */
+        const float* gl = group_logits + (int64_t)t * n_groups;
+        for (int32_t h = 0; h < n_groups; ++h) {
+          double ph = exp((double)gl[h] - (double)gl[g]) * pg;
+          gg[h] += gj * wj * ((h == g ? 1.0 : 0.0) - ph);
+        }
+      }
+    }
+    for (int32_t e = 0; e < E; ++e) d_logits[(int64_t)t * E + e] = (float)grad[e];
+    if (kind == SAM && d_group_logits)
+      for (int32_t h = 0; h < n_groups; ++h)
+        d_group_logits[(int64_t)t * n_groups + h] = (float)gg[h];
+  }
+  free(grad); free(q); free(z); free(in_dom);
+  if (gg) free(gg);
+  return 0;
+}

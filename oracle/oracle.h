@@ -198,6 +198,26 @@ int orc_gate_bwd(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
                  const float* logits, const int32_t* expert_idx, const int32_t* slot_idx,
                  const float* d_weight, float* d_logits);
 
+/* orc_gate_bwd for the NEXT-3 gates (R17, R18, R19), selection fixed:
+ *  SAM RENORM : the top-k RENORM adjoint on the expert logits (the k
+ *               selected are the domain); no group-logit gradient.
+ *  SAM SOFTMAX: w_j = P(g) P(e_j | g):
+ *               d_logits[e]       = sum_j m_j g_j w_j (delta(e, e_j) - P(e | g)),
+ *                                   e in group g (0 elsewhere);
+ *               d_group_logits[h] = sum_j m_j g_j w_j (delta(h, g) - P(h)).
+ *  D2S        : over the survivors (RENORM: w = softmax of z over the
+ *               survivors) or the row (SOFTMAX: w = softmax of z), z = (l+G)/tau:
+ *               d_logits[e] = (1/tau) sum_j m_j g_j w_j (delta(e, e_j) - q_e), q
+ *               the same softmax; pruned experts (RENORM) get 0.
+ * Jacobian sums in double, one rounding.  group_logits / d_group_logits are
+ * used for SAM only, uniforms / tau for D2S only (uniforms NULL = eval).
+ * Returns 0, or -1 for invalid arguments. */
+int orc_gate_bwd_ex(int kind, int weight_mode, int32_t S, int32_t E, int32_t k,
+                    const float* logits, const float* group_logits, int32_t n_groups,
+                    const float* uniforms, double tau, const int32_t* expert_idx,
+                    const int32_t* slot_idx, const float* d_weight, float* d_logits,
+                    float* d_group_logits);
+
 /* bf16 helpers of the oracle's own (R14): exact widening, and a single
  * round-to-nearest-even narrowing from double. */
 double   orc_bf16_to_f64(uint16_t h);

@@ -212,3 +212,84 @@ def test_gate_bwd_rejects_hash(orc):
     r = orc.gate(None, E=E, k=1, cap=S, kind="hash", token_ids=ids, table=table)
     with pytest.raises(ValueError):
         orc.gate_bwd(np.zeros((S, E), np.float32), r, np.zeros((S, 1), np.float32), kind="hash")
+
+
+# ------------------------------------------------------------ SAM / Dense-to-Sparse adjoints
+def _sam_weights(gl, lg, r, G, mode):
+    S, E = lg.shape
+    n = E // G
+    w = np.zeros((S, r.k))
+    for t in range(S):
+        sel = r.expert_idx[t]
+        g = sel[0] // n
+        if mode == "renorm":
+            w[t] = softmax(lg[t, sel])
+        else:
+            w[t] = softmax(gl[t])[g] * softmax(lg[t, g * n:(g + 1) * n])[sel - g * n]
+    return w * (r.slot_idx >= 0)
+
+
+@pytest.mark.parametrize("mode,G,k", [("softmax", 4, 2), ("renorm", 4, 2), ("softmax", 2, 3)])
+def test_sam_bwd_central_difference(orc, mode, G, k):
+    S, E = 16, 16
+    gl, lg = synthgen.group_logits_and_logits(51 + G, S, E, k, G)
+    cap = orc.capacity(S, E, k, 0.9)
+    r = orc.gate_sam(gl, lg, E=E, k=k, cap=cap, n_groups=G, weight_mode=mode)
+    g = np.random.default_rng(52).standard_normal((S, k)).astype(np.float32)
+    dl, dgl = orc.gate_bwd_ex(lg, r, g, kind="sam", weight_mode=mode, group_logits=gl,
+                              n_groups=G)
+    x, y = lg.astype(np.float64), gl.astype(np.float64)
+    h = 1e-6
+    for t in range(S):
+        for e in range(E):
+            xp, xm = x.copy(), x.copy()
+            xp[t, e] += h
+            xm[t, e] -= h
+            fd = ((_sam_weights(y, xp, r, G, mode)[t] - _sam_weights(y, xm, r, G, mode)[t])
+                  * g[t]).sum() / (2 * h)
+            assert abs(dl[t, e] - fd) <= 1e-7 + 1e-6 * abs(fd), (t, e, dl[t, e], fd)
+        for hh in range(G):
+            yp, ym = y.copy(), y.copy()
+            yp[t, hh] += h
+            ym[t, hh] -= h
+            fd = ((_sam_weights(yp, x, r, G, mode)[t] - _sam_weights(ym, x, r, G, mode)[t])
+                  * g[t]).sum() / (2 * h)
+            assert abs(dgl[t, hh] - fd) <= 1e-7 + 1e-6 * abs(fd), (t, hh, dgl[t, hh], fd)
+
+
+def _d2s_weights(lg, u, r, tau, mode):
+    S, E = lg.shape
+    G = -np.log(-np.log(u.astype(np.float64)))
+    z = (lg + G) / tau
+    w = np.zeros((S, E))
+    for t in range(S):
+        live = r.expert_idx[t] >= 0
+        sel = r.expert_idx[t, live]
+        if mode == "renorm":
+            w[t, :live.sum()] = softmax(z[t, sel])
+        else:
+            w[t, :live.sum()] = softmax(z[t])[sel]
+    return w * (r.slot_idx >= 0)
+
+
+@pytest.mark.parametrize("mode,tau", [("renorm", 0.7), ("softmax", 0.7), ("renorm", 2.0)])
+def test_d2s_bwd_central_difference(orc, mode, tau):
+    S, E = 16, 8
+    lg = synthgen.logits(53, S, E)
+    u = synthgen.uniforms_f32(54, S, E)
+    cap = 9
+    r = orc.gate_d2s(lg, cap=cap, tau=tau, eps=2e-2, uniforms=u, weight_mode=mode)
+    assert (r.slot_idx < 0).any() and (r.expert_idx < 0).any()     # drops and prunes
+    g = np.random.default_rng(55).standard_normal((S, E)).astype(np.float32)
+    dl, dgl = orc.gate_bwd_ex(lg, r, g, kind="d2s", weight_mode=mode, uniforms=u, tau=tau)
+    assert dgl is None
+    x = lg.astype(np.float64)
+    h = 1e-6
+    for t in range(S):
+        for e in range(E):
+            xp, xm = x.copy(), x.copy()
+            xp[t, e] += h
+            xm[t, e] -= h
+            fd = ((_d2s_weights(xp, u, r, tau, mode)[t] - _d2s_weights(xm, u, r, tau, mode)[t])
+                  * g[t]).sum() / (2 * h)
+            assert abs(dl[t, e] - fd) <= 1e-7 + 1e-6 * abs(fd), (t, e, dl[t, e], fd)
