@@ -296,6 +296,21 @@ moe_status_t moe_gate_backward(const moe_gate_desc_t* desc, const float* logits,
                                const moe_routing_t* routing, const float* d_weight,
                                float* d_logits, moe_stream_t stream);
 
+/* moe_gate_backward for every gate with logits, the NEXT-3 gates included
+ * (R17-R19), selection fixed; inputs as given to moe_gate_ex:
+ *  SAM RENORM : as top-k RENORM; d_group_logits = 0.
+ *  SAM SOFTMAX: w_j = P(g) q(e_j), q = softmax over group g:
+ *               d_logits[e] = sum_j g_j w_j (delta(e, e_j) - q_e) on group g,
+ *               d_group_logits[h] = sum_j g_j w_j (delta(h, g) - P(h)).
+ *  D2S        : z = (l + G)/tau; q = softmax of z over the survivors (RENORM)
+ *               or the row (SOFTMAX): d_logits[e] = (1/tau) sum_j g_j w_j
+ *               (delta(e, e_j) - q_e) on that domain, 0 for pruned experts.
+ * g_j = d_weight for an admitted slot, 0 otherwise.  fp64, one rounding.
+ * d_group_logits [S, n_groups] fp32 (SAM only; else ignored). */
+moe_status_t moe_gate_backward_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                                  const moe_routing_t* routing, const float* d_weight,
+                                  float* d_logits, float* d_group_logits, moe_stream_t stream);
+
 /* ---------------------------------------------------------------- AllToAll */
 
 typedef struct moe_comm moe_comm_t;

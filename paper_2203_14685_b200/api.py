@@ -308,8 +308,11 @@ def layout_backward(d_dispatch: torch.Tensor, r: Routing,
 
 
 def gate_backward(logits: torch.Tensor, r: Routing, d_weight: torch.Tensor,
-                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """Adjoint of Eq. 1's weights w.r.t. the logits (NEXT-1), selection fixed."""
+                  out: Optional[torch.Tensor] = None, *, group_logits=None, n_groups: int = 1,
+                  d_group_logits=None, uniforms=None, tau: float = 1.0):
+    """Adjoint of the gate weights w.r.t. the logits (NEXT-1), selection
+    fixed.  SAM: also returns d_group_logits (pass group_logits, n_groups);
+    D2S: pass the same uniforms and tau as the forward."""
     _need_cuda(logits, "logits", torch.float32)
     _need_cuda(d_weight, "d_weight", torch.float32)
     if tuple(logits.shape) != (r.S, r.E) or d_weight.numel() != r.S * r.k:
@@ -317,10 +320,16 @@ def gate_backward(logits: torch.Tensor, r: Routing, d_weight: torch.Tensor,
     if out is None:
         out = torch.empty_like(logits)
     _need_cuda(out, "d_logits", torch.float32)
+    sam = r.kind == KINDS["sam"]
+    if sam and d_group_logits is None:
+        d_group_logits = torch.empty((r.S, n_groups), dtype=torch.float32, device=logits.device)
     desc, rc = r.desc(), r.c()
-    check(lib().moe_gate_backward(ctypes.byref(desc), _p(logits), ctypes.byref(rc), _p(d_weight),
-                                  _p(out), _stream(logits.device)), "moe_gate_backward")
-    return out
+    inp = GateInputs(_p(logits), None, None, 0, _p(group_logits), n_groups, _p(uniforms),
+                     float(tau), 0.0)
+    check(lib().moe_gate_backward_ex(ctypes.byref(desc), ctypes.byref(inp), ctypes.byref(rc),
+                                     _p(d_weight), _p(out), _p(d_group_logits),
+                                     _stream(logits.device)), "moe_gate_backward")
+    return (out, d_group_logits) if sam else out
 
 
 def expert_scale(buf: torch.Tensor, nsrc: int, E_local: int, e_base: int,

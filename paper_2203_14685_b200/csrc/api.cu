@@ -322,21 +322,45 @@ moe_status_t moe_layout_backward(const moe_gate_desc_t* desc, const moe_routing_
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
-moe_status_t moe_gate_backward(const moe_gate_desc_t* desc, const float* logits,
-                               const moe_routing_t* routing, const float* d_weight,
-                               float* d_logits, moe_stream_t stream) {
+moe_status_t moe_gate_backward_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                                  const moe_routing_t* routing, const float* d_weight,
+                                  float* d_logits, float* d_group_logits, moe_stream_t stream) {
   moe_status_t s = check_desc("moe_gate_backward", desc);
   if (s != MOE_OK) return s;
   if (desc->kind == MOE_GATE_HASH) {
     set_error("moe_gate_backward: the hash gate has no logits (no gradient)");
     return MOE_ERR_INVALID_ARG;
   }
-  if (!logits || !routing || !routing->expert_idx || !routing->slot_idx || !d_weight || !d_logits) {
+  if (!in || !in->logits || !routing || !routing->expert_idx || !routing->slot_idx ||
+      !d_weight || !d_logits) {
     set_error("moe_gate_backward: logits, routing.expert_idx/slot_idx, d_weight, d_logits required");
     return MOE_ERR_INVALID_ARG;
   }
-  return gate_bwd_launch(*desc, logits, *routing, d_weight, d_logits,
+  if (desc->kind == MOE_GATE_SAM) {
+    const int G = in->n_groups;
+    if (!in->group_logits || !d_group_logits || G < 1 || desc->E % G != 0) {
+      set_error("moe_gate_backward: SAM needs group_logits, d_group_logits and n_groups | E");
+      return MOE_ERR_INVALID_ARG;
+    }
+  }
+  if (desc->kind == MOE_GATE_D2S && !(in->tau > 0.0)) {
+    set_error("moe_gate_backward: Dense-to-Sparse needs tau > 0");
+    return MOE_ERR_INVALID_ARG;
+  }
+  return gate_bwd_launch(*desc, *in, *routing, d_weight, d_logits, d_group_logits,
                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_gate_backward(const moe_gate_desc_t* desc, const float* logits,
+                               const moe_routing_t* routing, const float* d_weight,
+                               float* d_logits, moe_stream_t stream) {
+  if (desc && (desc->kind == MOE_GATE_SAM || desc->kind == MOE_GATE_D2S)) {
+    set_error("moe_gate_backward: SAM and Dense-to-Sparse need moe_gate_backward_ex");
+    return MOE_ERR_INVALID_ARG;
+  }
+  moe_gate_inputs_t in{};
+  in.logits = logits;
+  return moe_gate_backward_ex(desc, &in, routing, d_weight, d_logits, nullptr, stream);
 }
 
 moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E_local,

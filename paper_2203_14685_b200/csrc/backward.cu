@@ -342,6 +342,13 @@ struct GateBwdArgs {
   const float* d_weight;
   float* d_logits;
   int S, E, k, kind, mode;
+  // SAM (R17): group logits [S, ngroups] and their gradient; D2S (R18):
+  // uniforms [S, E] (NULL = eval) and the temperature
+  const float* glogits;
+  int ngroups;
+  float* d_glogits;
+  const float* uniforms;
+  double tau;
 };
 
 constexpr int kGateBwdThreads = 256;
@@ -376,10 +383,83 @@ __global__ void __launch_bounds__(kGateBwdThreads) k_gate_bwd(GateBwdArgs a) {
     float* out = a.d_logits + t * a.E;
     const int32_t* sel = a.expert_idx + t * a.k;
     const double mx0 = (double)__ldg(row + __ldg(sel));
-    if (a.kind == MOE_GATE_KTOP1 && a.mode == MOE_W_RENORM) {
+    if (a.kind == MOE_GATE_SAM && a.mode == MOE_W_SOFTMAX) {
+      // w_j = P(g) q_{e_j}, q = softmax over group g's logits (max = l[e_0]),
+      // c = sum_j G_j w_j: d_l[e] = G_e w_e - q_e c on the group;
+      // d_gl[h] = c (delta(h, g) - P(h))
+      const int n = a.E / a.ngroups;
+      const int g = valid ? __ldg(sel) / n : 0;
+      const float* gl = a.glogits + t * a.ngroups;
+      const double glg = (double)__ldg(gl + g);
+      double pz = 0.0, pgz = 0.0;
+      if (valid) {
+        for (int e = g * n + l; e < (g + 1) * n; e += L) pz += exp((double)__ldg(row + e) - mx0);
+        for (int h = l; h < a.ngroups; h += L) pgz += exp((double)__ldg(gl + h) - glg);
+      }
+      const double z = lanes_sum<L>(pz), pg = 1.0 / lanes_sum<L>(pgz);
+      double c = 0.0;
+      for (int j = 0; j < a.k; ++j)
+        c += g_of(a, t, __ldg(sel + j)) * pg * (exp((double)__ldg(row + __ldg(sel + j)) - mx0) / z);
+      if (valid) {
+        for (int e = l; e < a.E; e += L) {
+          double v = 0.0;
+          if (e / n == g) {
+            const double q = exp((double)__ldg(row + e) - mx0) / z;
+            v = g_of(a, t, e) * pg * q - q * c;
+          }
+          out[e] = (float)v;
+        }
+        for (int h = l; h < a.ngroups; h += L) {
+          const double ph = exp((double)__ldg(gl + h) - glg) * pg;
+          a.d_glogits[t * a.ngroups + h] = (float)(c * ((h == g ? 1.0 : 0.0) - ph));
+        }
+      }
+    } else if (a.kind == MOE_GATE_D2S) {
+      // z = (l + G)/tau; domain: survivors (RENORM) or the row (SOFTMAX);
+      // max over either = z of slot 0; d_l[e] = (1/tau)(G_e q_e - q_e c)
+      const float* u = a.uniforms ? a.uniforms + t * a.E : nullptr;
+      auto zf = [&](int e) {
+        const double gn = u ? -log(-log((double)__ldg(u + e))) : 0.0;
+        return ((double)__ldg(row + e) + gn) / a.tau;
+      };
+      const double zm = zf(valid ? __ldg(sel) : 0);
+      auto in_dom = [&](int e) {
+        if (a.mode == MOE_W_SOFTMAX) return true;
+        for (int j = 0; j < a.k; ++j) {
+          const int ej = __ldg(sel + j);
+          if (ej < 0) return false;  // survivors are a prefix of the slots
+          if (ej == e) return true;
+        }
+        return false;
+      };
+      double pz = 0.0;
+      if (valid)
+        for (int e = l; e < a.E; e += L)
+          if (in_dom(e)) pz += exp(zf(e) - zm);
+      const double z = lanes_sum<L>(pz);
+      double c = 0.0;
+      if (valid)
+        for (int e = l; e < a.E; e += L) {
+          const double ge = g_of(a, t, e);
+          if (ge != 0.0) c += ge * (exp(zf(e) - zm) / z);
+        }
+      c = lanes_sum<L>(c);
+      if (valid)
+        for (int e = l; e < a.E; e += L) {
+          double v = 0.0;
+          if (in_dom(e)) {
+            const double q = exp(zf(e) - zm) / z;
+            v = (g_of(a, t, e) * q - q * c) / a.tau;
+          }
+          out[e] = (float)v;
+        }
+    } else if (a.kind == MOE_GATE_KTOP1 && a.mode == MOE_W_RENORM) {
       if (valid)
         for (int e = l; e < a.E; e += L) out[e] = 0.f;
-    } else if (a.kind == MOE_GATE_TOPK && a.mode == MOE_W_RENORM) {
+    } else if (a.mode == MOE_W_RENORM && (a.kind == MOE_GATE_TOPK || a.kind == MOE_GATE_SAM)) {
+      // (SAM RENORM: Eq. 1 on the k selected expert logits; no group gradient)
+      if (a.kind == MOE_GATE_SAM && valid)
+        for (int h = l; h < a.ngroups; h += L) a.d_glogits[t * a.ngroups + h] = 0.f;
       // domain = the k selected: every lane evaluates the k terms itself
       double z = 0.0, c = 0.0;
       for (int j = 0; j < a.k; ++j) z += exp((double)__ldg(row + __ldg(sel + j)) - mx0);
@@ -434,10 +514,12 @@ __global__ void __launch_bounds__(kGateBwdThreads) k_gate_bwd(GateBwdArgs a) {
   }
 }
 
-moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, const moe_routing_t& r,
-                             const float* d_weight, float* d_logits, cudaStream_t stream) {
-  GateBwdArgs a{logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
-                d.weight_mode};
+moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                             const moe_routing_t& r, const float* d_weight, float* d_logits,
+                             float* d_group_logits, cudaStream_t stream) {
+  GateBwdArgs a{in.logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
+                d.weight_mode, in.group_logits, d.kind == MOE_GATE_SAM ? in.n_groups : 1,
+                d_group_logits, in.uniforms, in.tau};
   // lanes per token (MOE_GATE_BWD_LANES overrides)
   int L = env_int("MOE_GATE_BWD_LANES", 0);
   if (L <= 0) {

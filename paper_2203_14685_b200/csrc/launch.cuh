@@ -10,8 +10,9 @@ int gate_kernel_count(const moe_gate_desc_t& d, int ngroups);
 moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
                          const moe_routing_t& out, void* ws, cudaStream_t stream);
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad);
-moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const float* logits, const moe_routing_t& r,
-                             const float* d_weight, float* d_logits, cudaStream_t stream);
+moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                             const moe_routing_t& r, const float* d_weight, float* d_logits,
+                             float* d_group_logits, cudaStream_t stream);
 
 // offsets != NULL: the dropless packed form ([offsets[E]][row], no padding)
 moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,

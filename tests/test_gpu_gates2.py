@@ -99,3 +99,46 @@ def test_d2s_layout_and_reverse(orc):
     back = synthgen.tokens(64, E * cap, d, "bf16").reshape(E, cap, d)
     y = host(moe.reverse_layout(dev(back), rg))
     assert_y_close(y, orc.reverse_layout(back, ro), combine_bound(as_f64(back), ro), True)
+
+
+def _bwd_close(got, ref, g, ro, scale=1.0):
+    gs = np.abs(g.astype(np.float64) * (ro.slot_idx >= 0)).sum(1, keepdims=True)
+    tol = 2.4e-7 * np.abs(ref.astype(np.float64)) + 1e-12 * scale * gs
+    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    assert (err <= tol).all(), "%d bad, worst %.3g" % ((err > tol).sum(), (err - tol).max())
+
+
+@pytest.mark.parametrize("mode", ["renorm", "softmax"])
+@pytest.mark.parametrize("E,G,k", [(64, 8, 2), (24, 8, 3), (256, 32, 4)])
+def test_sam_backward_parity(orc, mode, E, G, k):
+    S = 2049
+    gl, lg = synthgen.group_logits_and_logits(S + E + G + 1, S, E, k, G)
+    cap = orc.capacity(S, E, k, 0.8)
+    ro = orc.gate_sam(gl, lg, E=E, k=k, cap=cap, n_groups=G, weight_mode=mode)
+    rg = moe.Gate(S, E, k, cap, "sam", mode, n_groups=G)(dev(lg), group_logits=dev(gl))
+    torch.cuda.synchronize()
+    assert_routing_equal(rg, ro)
+    g = np.random.default_rng(S + E).standard_normal((S, k)).astype(np.float32)
+    dl_o, dg_o = orc.gate_bwd_ex(lg, ro, g, kind="sam", weight_mode=mode, group_logits=gl,
+                                 n_groups=G)
+    dl, dg = moe.gate_backward(dev(lg), rg, dev(g), group_logits=dev(gl), n_groups=G)
+    _bwd_close(host(dl), dl_o, g, ro)
+    _bwd_close(host(dg), dg_o, g, ro)
+
+
+@pytest.mark.parametrize("mode", ["renorm", "softmax"])
+@pytest.mark.parametrize("E,tau,train", [(8, 0.7, True), (64, 2.0, True), (32, 0.5, False)])
+def test_d2s_backward_parity(orc, mode, E, tau, train):
+    S = 1500
+    lg = synthgen.logits(S * 3 + E, S, E, gap=1e-3)
+    u = synthgen.uniforms_f32(S * 5 + E, S, E) if train else None
+    _d2s_inputs_valid(lg, u, tau, 1e-3)
+    cap = orc.capacity(S, E, E, 0.3)
+    ro = orc.gate_d2s(lg, cap=cap, tau=tau, uniforms=u, weight_mode=mode)
+    rg = moe.Gate(S, E, E, cap, "d2s", mode, tau=tau)(dev(lg), uniforms=None if u is None else dev(u))
+    torch.cuda.synchronize()
+    assert_routing_equal(rg, ro)
+    g = np.random.default_rng(S + E).standard_normal((S, E)).astype(np.float32)
+    dl_o, _ = orc.gate_bwd_ex(lg, ro, g, kind="d2s", weight_mode=mode, uniforms=u, tau=tau)
+    dl = moe.gate_backward(dev(lg), rg, dev(g), uniforms=None if u is None else dev(u), tau=tau)
+    _bwd_close(host(dl), dl_o, g, ro, 1.0 / tau)
