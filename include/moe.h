@@ -311,6 +311,20 @@ moe_status_t moe_gate_backward_ex(const moe_gate_desc_t* desc, const moe_gate_in
                                   const moe_routing_t* routing, const float* d_weight,
                                   float* d_logits, float* d_group_logits, moe_stream_t stream);
 
+/* Adjoints of the dropless packed form (NEXT-4): as moe_reverse_layout_backward
+ * / moe_layout_backward with row (e, s) at offsets[e] + s and no padding
+ * rows (d_back rows >= offsets[E] are not written). */
+moe_status_t moe_reverse_layout_packed_backward(const moe_gate_desc_t* desc,
+                                                const moe_routing_t* routing,
+                                                const int32_t* offsets, const void* dy,
+                                                const void* back, int32_t d, int32_t dtype,
+                                                void* d_back, float* d_weight,
+                                                moe_stream_t stream);
+moe_status_t moe_layout_packed_backward(const moe_gate_desc_t* desc,
+                                        const moe_routing_t* routing, const int32_t* offsets,
+                                        const void* d_packed, int32_t d, int32_t dtype, void* dx,
+                                        moe_stream_t stream);
+
 /* ---------------------------------------------------------------- AllToAll */
 
 typedef struct moe_comm moe_comm_t;

@@ -77,6 +77,12 @@ SIGNATURES = [
                                            i32, i32, vp, vp]),
     ("moe_gate_backward", ctypes.c_int, [ctypes.POINTER(GateDesc), vp, ctypes.POINTER(RoutingC),
                                          vp, vp, vp]),
+    ("moe_reverse_layout_packed_backward", ctypes.c_int, [ctypes.POINTER(GateDesc),
+                                                          ctypes.POINTER(RoutingC), vp, vp, vp,
+                                                          i32, i32, vp, vp, vp]),
+    ("moe_layout_packed_backward", ctypes.c_int, [ctypes.POINTER(GateDesc),
+                                                  ctypes.POINTER(RoutingC), vp, vp, i32, i32, vp,
+                                                  vp]),
     ("moe_gate_backward_ex", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),
                                             ctypes.POINTER(RoutingC), vp, vp, vp, vp]),
     ("moe_combine_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),

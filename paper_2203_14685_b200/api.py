@@ -242,6 +242,41 @@ def reverse_layout_packed(back: torch.Tensor, r: Routing, offsets: torch.Tensor,
     return out
 
 
+def reverse_layout_packed_backward(dy: torch.Tensor, back: torch.Tensor, r: Routing,
+                                   offsets: torch.Tensor, d_back: Optional[torch.Tensor] = None,
+                                   d_weight: Optional[torch.Tensor] = None):
+    """Adjoint of the packed combine: d_back rows at offsets[e] + s."""
+    _need_cuda(dy, "dy")
+    _need_cuda(offsets, "offsets", torch.int32)
+    d = dy.shape[-1]
+    if d_back is None:
+        d_back = torch.empty((r.S * r.k, d), dtype=dy.dtype, device=dy.device)
+    if d_weight is None:
+        d_weight = torch.empty((r.S, r.k), dtype=torch.float32, device=dy.device)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_reverse_layout_packed_backward(ctypes.byref(desc), ctypes.byref(rc),
+                                                   _p(offsets), _p(dy), _p(back), d,
+                                                   _DT[dy.dtype], _p(d_back), _p(d_weight),
+                                                   _stream(dy.device)),
+          "moe_reverse_layout_packed_backward")
+    return d_back, d_weight
+
+
+def layout_packed_backward(d_packed: torch.Tensor, r: Routing, offsets: torch.Tensor,
+                           out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Adjoint of the packed Layout_Transform: dx[t] = sum_j d_packed[offsets[e_j] + s_j]."""
+    _need_cuda(d_packed, "d_packed")
+    _need_cuda(offsets, "offsets", torch.int32)
+    d = d_packed.shape[-1]
+    if out is None:
+        out = torch.empty((r.S, d), dtype=d_packed.dtype, device=d_packed.device)
+    desc, rc = r.desc(), r.c()
+    check(lib().moe_layout_packed_backward(ctypes.byref(desc), ctypes.byref(rc), _p(offsets),
+                                           _p(d_packed), d, _DT[d_packed.dtype], _p(out),
+                                           _stream(d_packed.device)), "moe_layout_packed_backward")
+    return out
+
+
 def alltoallv_plan(offsets, recv_counts, nranks: int):
     """Host plan of the NCCL dropless exchange (NEXT-4): from this rank's
     expert offsets [E+1] (moe_expert_offsets) and the per-expert counts it

@@ -322,6 +322,47 @@ moe_status_t moe_layout_backward(const moe_gate_desc_t* desc, const moe_routing_
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+moe_status_t moe_reverse_layout_packed_backward(const moe_gate_desc_t* desc,
+                                                const moe_routing_t* routing,
+                                                const int32_t* offsets, const void* dy,
+                                                const void* back, int32_t d, int32_t dtype,
+                                                void* d_back, float* d_weight,
+                                                moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_reverse_layout_packed_backward", desc, routing, dy, "dy", back,
+                              "back", d, dtype, true, false);
+  if (s != MOE_OK) return s;
+  if (!offsets || !d_back || !d_weight) {
+    set_error("moe_reverse_layout_packed_backward: offsets, d_back and d_weight are required");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!aligned(d_back, 16)) {
+    set_error("moe_reverse_layout_packed_backward: d_back must be 16-byte aligned");
+    return MOE_ERR_ALIGNMENT;
+  }
+  PeerPtrs b{}, g{};
+  b.p[0] = const_cast<char*>(static_cast<const char*>(back));
+  g.p[0] = static_cast<char*>(d_back);
+  return combine_bwd_launch(*desc, *routing, dy, b, g, desc->E, 0, dtype, dtype_size(dtype), d,
+                            d_weight, reinterpret_cast<cudaStream_t>(stream), offsets);
+}
+
+moe_status_t moe_layout_packed_backward(const moe_gate_desc_t* desc,
+                                        const moe_routing_t* routing, const int32_t* offsets,
+                                        const void* d_packed, int32_t d, int32_t dtype, void* dx,
+                                        moe_stream_t stream) {
+  moe_status_t s = check_rows("moe_layout_packed_backward", desc, routing, d_packed, "d_packed",
+                              dx, "dx", d, dtype, false, false);
+  if (s != MOE_OK) return s;
+  if (!offsets) {
+    set_error("moe_layout_packed_backward: offsets is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  moe_routing_t unit = *routing;
+  unit.weight = nullptr;
+  return reverse_launch(*desc, unit, d_packed, dtype, dtype_size(dtype), d, dx,
+                        reinterpret_cast<cudaStream_t>(stream), offsets);
+}
+
 moe_status_t moe_gate_backward_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
                                   const moe_routing_t* routing, const float* d_weight,
                                   float* d_logits, float* d_group_logits, moe_stream_t stream) {

@@ -288,8 +288,11 @@ __global__ void __launch_bounds__(kRowThreads) k_combine_bwd16(RowArgs a, float*
 moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
                                 const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
                                 int rank, int dtype, int dtype_size, int dcols, float* d_weight,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, const int32_t* offsets,
+                                const int32_t* peer_base) {
   RowArgs a{};
+  a.offsets = offsets;      // packed form: no padding rows to zero
+  a.peer_base = peer_base;
   a.src = static_cast<const char*>(dy);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;

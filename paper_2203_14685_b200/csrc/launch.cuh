@@ -35,7 +35,8 @@ moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t*
 moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,
                                 const PeerPtrs& back, const PeerPtrs& d_back, int E_local,
                                 int rank, int dtype, int dtype_size, int dcols, float* d_weight,
-                                cudaStream_t stream);
+                                cudaStream_t stream, const int32_t* offsets = nullptr,
+                                const int32_t* peer_base = nullptr);
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
                                  int cap, int dcols, int dtype, int dtype_size,
                                  cudaStream_t stream);

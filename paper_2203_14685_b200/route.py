@@ -13,8 +13,8 @@ from typing import Optional
 import torch
 
 from .api import (Comm, Gate, Routing, expert_offsets, expert_scale, gate_backward, layout,
-                  layout_backward, layout_packed, reverse_layout, reverse_layout_backward,
-                  reverse_layout_packed)
+                  layout_backward, layout_packed, layout_packed_backward, reverse_layout,
+                  reverse_layout_backward, reverse_layout_packed, reverse_layout_packed_backward)
 
 
 class RoutePipeline:
@@ -154,8 +154,23 @@ class RoutePipeline:
         gate (d_logits, when the gate has logits).  Returns (dx, d_logits)."""
         r = self.routing
         if self.dropless:
-            raise NotImplementedError("backward of the dropless packed form is not built "
-                                      "(use the padded form)")
+            if self.P > 1:
+                raise NotImplementedError("backward of the dropless exchange across ranks is "
+                                          "not built (the padded form has it)")
+            if not hasattr(self, "d_weight"):
+                self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32,
+                                            device=self.device)
+                self.d_back = torch.empty_like(self.recv)
+                self.dx = torch.empty_like(self.y)
+                self.d_logits = torch.empty((self.S, self.E), dtype=torch.float32,
+                                            device=self.device)
+            reverse_layout_packed_backward(dy, self.recv, r, self.offsets, self.d_back,
+                                           self.d_weight)
+            layout_packed_backward(self.d_back, r, self.offsets, out=self.dx)
+            dl = None
+            if logits is not None and self.gate.kind not in (2, 3, 4):
+                dl = gate_backward(logits, r, self.d_weight, out=self.d_logits)
+            return self.dx, dl
         if not hasattr(self, "d_weight"):
             mk = lambda *shape: torch.empty(shape, dtype=self.y.dtype, device=self.device)
             self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32, device=self.device)

@@ -67,3 +67,46 @@ def test_packed_layout_and_combine(orc, c):
     assert_y_close(y_g, y_o, bound, bf16)
     if c["k"] == 1:
         assert y_g.tobytes() == y_o.tobytes()
+
+
+@pytest.mark.parametrize("c", [c for c in CASES if c["S"] > 1],
+                         ids=lambda c: "-".join("%s=%s" % kv for kv in c.items()))
+def test_packed_backward(orc, c):
+    """Adjoints of the packed form against the padded oracle adjoints with
+    the padding removed (the packed form IS the padded one minus padding)."""
+    ro, rg = _routing(orc, c)
+    S, E, k, d = c["S"], c["E"], c["k"], c["d"]
+    cap = ro.cap
+    off_o = orc.expert_offsets(ro)
+    off_g = moe.expert_offsets(rg)
+    R = int(off_o[-1])
+    dy = synthgen.tokens(S * 7 + d, S, d, c["dtype"])
+    back_pk = synthgen.tokens(S * 9 + d, R, d, c["dtype"])
+    # the same rows in the padded form (padding rows zero)
+    back_pad = np.zeros((E, cap, d), back_pk.dtype)
+    for e in range(E):
+        back_pad[e, :off_o[e + 1] - off_o[e]] = back_pk[off_o[e]:off_o[e + 1]]
+    db_o, dw_o = orc.reverse_layout_bwd(dy, back_pad, ro)
+    db_o_pk = np.concatenate([db_o[e, :off_o[e + 1] - off_o[e]] for e in range(E)])
+    pad_rows = np.concatenate([back_pk, np.zeros((S * k - R, d), back_pk.dtype)])
+    db_g, dw_g = moe.reverse_layout_packed_backward(dev(dy), dev(pad_rows), rg, off_g)
+    torch.cuda.synchronize()
+    assert host(db_g)[:R].tobytes() == db_o_pk.tobytes()
+    err = np.abs(host(dw_g).astype(np.float64) - dw_o.astype(np.float64))
+    bound = np.zeros_like(err)
+    b64, dy64 = as_f64(back_pad), as_f64(dy)
+    for j in range(k):
+        ok = ro.slot_idx[:, j] >= 0
+        bound[ok, j] = np.abs(dy64[ok] * b64[ro.expert_idx[ok, j], ro.slot_idx[ok, j]]).sum(1)
+    assert (err <= (d / 32 + 6) * 2.0 ** -24 * bound + 1e-30).all()
+    # layout adjoint: gradient rows in the packed form
+    g_pk = synthgen.tokens(S * 11 + d, R, d, c["dtype"])
+    g_pad = np.zeros((E, cap, d), g_pk.dtype)
+    for e in range(E):
+        g_pad[e, :off_o[e + 1] - off_o[e]] = g_pk[off_o[e]:off_o[e + 1]]
+    dx_o = orc.layout_bwd(g_pad, ro)
+    dx_g = host(moe.layout_packed_backward(
+        dev(np.concatenate([g_pk, np.zeros((S * k - R, d), g_pk.dtype)])), rg, off_g))
+    unit = type(ro)(**{**ro.__dict__, "weight": (ro.slot_idx >= 0).astype(np.float32)})
+    from gpu_util import combine_bound
+    assert_y_close(dx_g, dx_o, combine_bound(as_f64(g_pad), unit), c["dtype"] == "bf16")
