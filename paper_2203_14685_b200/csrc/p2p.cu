@@ -115,19 +115,21 @@ static moe_status_t host_barrier(moe_comm* c) {
 }
 
 // ------------------------------------------------------------ device barrier
-__global__ void k_barrier(PeerPtrs sig, int P, int rank) {
+__global__ void k_barrier(PeerPtrs sig, int P, int rank, int mode) {
   __shared__ unsigned long long s_e;
   unsigned long long* mine = reinterpret_cast<unsigned long long*>(sig.p[rank]);
-  pdl_wait();
+  pdl_wait();     // everything before us in the stream is complete
+  pdl_trigger();  // the next kernel may be scheduled now; it waits for our completion
   if (threadIdx.x == 0) {
     s_e = mine[kMaxRanks] + 1;
     mine[kMaxRanks] = s_e;
   }
   __syncthreads();
   const unsigned long long e = s_e;
+  if (mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");  // one fence, then releases
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     unsigned long long* flag = reinterpret_cast<unsigned long long*>(sig.p[q]) + rank;
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (mode == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
   }
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
@@ -139,8 +141,14 @@ __global__ void k_barrier(PeerPtrs sig, int P, int rank) {
 }
 
 moe_status_t barrier_launch(const PeerPtrs& sig, int nranks, int rank, cudaStream_t stream) {
-  k_barrier<<<1, 32, 0, stream>>>(sig, nranks, rank);
-  MOE_CHECK_LAUNCH("moe_comm_barrier: launch");
+  // PDL: the barrier's launch overlaps its predecessor's tail (it waits for
+  // the predecessor's completion in griddepcontrol.wait before signalling)
+  int mode = env_int("MOE_BARRIER_MODE", 1);  // 0: fence per peer, 1: one fence (default), 2: none
+  void* args[] = {(void*)&sig, &nranks, &rank, &mode};
+  cudaError_t e = env_int("MOE_BARRIER_PDL", 0)  // measured slower in the step graph: off
+                      ? launch_pdl((const void*)k_barrier, dim3(1), dim3(32), 0, stream, args)
+                      : cudaLaunchKernel((const void*)k_barrier, dim3(1), dim3(32), args, 0, stream);
+  if (e != cudaSuccess) return cuda_status(e, "moe_comm_barrier: launch");
   return MOE_OK;
 }
 
