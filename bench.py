@@ -466,30 +466,45 @@ def main():
         del g_bwd
         log("backward timing done")
 
-    # ---- end to end through the public API from pinned host buffers
+    # ---- end to end through the public API from pinned host buffers:
+    # RoutePipeline.run_host over K2 batches, the H2D of batch i+1 and the D2H
+    # of batch i-1 overlapping batch i's compute (PCIe is full duplex); every
+    # batch's input copy and output read is inside the timed region
     e2e = None
     if not a.no_e2e:
-        y_h = torch.empty((S, w.d), dtype=dt, pin_memory=True)
+        y_hs = [torch.empty((S, w.d), dtype=dt, pin_memory=True) for _ in range(2)]
+        batch = {"logits": host["logits"], "x": host["x"], "token_ids": host["token_ids"],
+                 "table": host["table"]}
+        K2 = max(4, a.steps // 2)
+        pipe.run_host([batch] * 2, y_hs)                      # warm-up (allocations)
+        torch.cuda.synchronize()
         staging = {}
-        for _ in range(2):
-            pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
-                           inputs=staging)
+        pipe.step_host(host["logits"], host["x"], y_hs[0], host["token_ids"], host["table"],
+                       inputs=staging)
         torch.cuda.synchronize()
-        K2 = max(3, a.steps // 2)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(K2)]
         barrier()
+        flush_l2()
+        align()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pipe.run_host([batch] * K2, [y_hs[i % 2] for i in range(K2)])
+        e1.record()
         torch.cuda.synchronize()
-        for i in range(K2):
+        barrier()
+        # the serial form (one batch at a time) for comparison
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(3)]
+        for i in range(3):
             flush_l2()
             align()
             evs[i][0].record()
-            pipe.step_host(host["logits"], host["x"], y_h, host["token_ids"], host["table"],
+            pipe.step_host(host["logits"], host["x"], y_hs[0], host["token_ids"], host["table"],
                            inputs=staging)
             evs[i][1].record()
         torch.cuda.synchronize()
         barrier()
-        t_e2e = torch.tensor([statistics.mean(s.elapsed_time(e) for s, e in evs)],
+        t_e2e = torch.tensor([e0.elapsed_time(e1) / K2,
+                              statistics.mean(s_.elapsed_time(e_) for s_, e_ in evs)],
                              dtype=torch.float64)
         if P > 1:
             t_d = t_e2e.to(dev)
@@ -500,7 +515,10 @@ def main():
             host["table"].numel() * 4 if host["table"] is not None else 0)
         e2e = {"value": P * S / (float(t_e2e[0]) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(S * row),
-               "ms_per_step": float(t_e2e[0])}
+               "ms_per_step": float(t_e2e[0]), "batches": K2,
+               "how": "RoutePipeline.run_host: pinned host batches, H2D / compute / D2H on "
+                      "separate streams, double-buffered (max over ranks)",
+               "serial_ms_per_step": float(t_e2e[1])}
 
     # ---- roofline of the dominant kernel
     admitted = int((pipe.routing.slot_idx >= 0).sum().item())

@@ -89,11 +89,17 @@ class RoutePipeline:
             self.comm.alltoall(send, recv, self.algo, self.group_size, self.ws)
 
     def step(self, logits=None, x=None, token_ids=None, table=None, expert: bool = False,
-             mark=None):
+             mark=None, y=None):
         """One pass of Algorithm 1 on device-resident inputs; returns y.
         `mark(name)` (optional) is called after each stage is enqueued (the
         bench records a CUDA event there)."""
         mark = mark or (lambda name: None)
+        if y is not None and y is not self.y:   # write this step's y elsewhere
+            saved, self.y = self.y, y
+            try:
+                return self.step(logits, x, token_ids, table, expert, mark)
+            finally:
+                self.y = saved
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         if self.dropless:
             return self._step_dropless(r, x, mark)
@@ -250,6 +256,57 @@ class RoutePipeline:
                     graphs[name] = g
         torch.cuda.current_stream(self.device).wait_stream(s)
         return graphs
+
+    def run_host(self, batches, outs, expert: bool = False):
+        """End-to-end over HOST batches with the copies overlapped: batch i's
+        inputs go host->device on a copy-in stream while batch i-1 computes,
+        and batch i-1's y goes device->host on a copy-out stream (PCIe is
+        full duplex), with double-buffered device staging.  `batches`: dicts
+        of pinned host tensors (logits, x, token_ids, table); `outs`: pinned
+        host y tensors, one per batch.  Enqueues everything; the caller
+        synchronises (or records events) as it likes."""
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_pipe_streams"):
+            self._pipe_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            self._pipe_stage = [{}, {}]
+            self._pipe_y = [torch.empty_like(self.y), torch.empty_like(self.y)]
+        s_in, s_out = self._pipe_streams
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_comp = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        for i, (b, y_h) in enumerate(zip(batches, outs)):
+            j = i % 2
+            stage = self._pipe_stage[j]
+            with torch.cuda.stream(s_in):
+                if used[j]:
+                    s_in.wait_event(ev_comp[j])       # step i-2 is done reading stage j
+                for name in ("logits", "x", "token_ids", "table"):
+                    h = b.get(name)
+                    if h is None:
+                        continue
+                    t = stage.get(name)
+                    if t is None:
+                        t = stage[name] = torch.empty(h.shape, dtype=h.dtype, device=dev)
+                    t.copy_(h, non_blocking=True)
+                ev_in[j].record(s_in)
+            cur.wait_event(ev_in[j])
+            if used[j]:
+                cur.wait_event(ev_out[j])             # y buffer j has been read out
+            self.step(stage.get("logits"), stage.get("x"), stage.get("token_ids"),
+                      stage.get("table"), expert, y=self._pipe_y[j])
+            ev_comp[j].record(cur)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[j])
+                y_h.copy_(self._pipe_y[j], non_blocking=True)
+                ev_out[j].record(s_out)
+            used[j] = True
+        cur.wait_stream(s_in)
+        cur.wait_stream(s_out)
+        return outs
 
     def step_host(self, logits_h=None, x_h=None, y_h=None, token_ids_h=None, table_h=None,
                   expert: bool = False, inputs=None):

@@ -241,3 +241,29 @@ def test_determinism(orc):
     r2 = [host(t) for t in (pipe.routing.slot_idx, pipe.routing.slot_src)]
     assert a.tobytes() == b.tobytes()
     assert all(u.tobytes() == v.tobytes() for u, v in zip(r1, r2))
+
+
+def test_run_host_pipelined_matches_step(orc):
+    """RoutePipeline.run_host (copies on their own streams, double-buffered
+    staging) returns, for every batch, exactly the y that step() gives for
+    that batch alone -- no buffer is overwritten while in use -- and the
+    oracle's y within the north_star bar."""
+    S, d, E, k = 4096, 512, 8, 2
+    cap = orc.capacity(S, E, k, 1.0)
+    pipe = moe.RoutePipeline(S, d, E, k, cap, torch.bfloat16)
+    batches, want = [], []
+    for i in range(5):
+        lg = synthgen.logits(300 + i, S, E, k)
+        x = synthgen.tokens(400 + i, S, d, "bf16")
+        batches.append({"logits": torch.from_numpy(lg).pin_memory(),
+                        "x": torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()})
+        want.append(host(pipe.step(dev(lg), dev(x))).copy())
+        _, disp, _, ys = orc.route_multi([x], [lg], E=E, k=k, cap=cap, scale=False)
+        ro = orc.gate(lg, E=E, k=k, cap=cap)
+        assert_y_close(want[-1], ys[0], combine_bound(as_f64(disp[0]), ro), True)
+    torch.cuda.synchronize()
+    outs = [torch.empty((S, d), dtype=torch.bfloat16).pin_memory() for _ in range(5)]
+    pipe.run_host(batches, outs)
+    torch.cuda.synchronize()
+    for i in range(5):
+        assert host(outs[i]).tobytes() == want[i].tobytes(), "batch %d" % i
