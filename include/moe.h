@@ -186,6 +186,16 @@ moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* i
                          const moe_routing_t* out, void* ws, size_t ws_bytes,
                          moe_stream_t stream);
 
+/* Steps 1 + 2 fused: exactly moe_gate_ex followed by
+ * moe_layout (same routing outputs, same dispatch buffer, bit for bit), with
+ * the gate's last pass (the capacity slots) done by the layout kernel itself,
+ * which saves a kernel boundary.  Falls back to the two calls for rows that
+ * are not a multiple of 32 bytes or k > 32.  Errors: as moe_gate_ex and
+ * moe_layout. */
+moe_status_t moe_gate_layout(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                             const moe_routing_t* out, void* ws, size_t ws_bytes, const void* x,
+                             int32_t d, int32_t dtype, void* dispatch, moe_stream_t stream);
+
 /* host, SYNCHRONISES `stream`.  Number of invalid hash tokens seen since the
  * last check (the counter is reset to 0). */
 moe_status_t moe_gate_check(void* ws, moe_stream_t stream, int32_t* bad_count);
@@ -414,6 +424,14 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
                              int32_t dtype, void* y, int32_t flags, moe_stream_t stream);
+
+/* Steps 1 + 2 + 3 fused: moe_gate_ex + moe_dispatch_p2p
+ * with the gate's capacity pass done by the dispatch kernel (as
+ * moe_gate_layout); same routing and receive buffers, bit for bit. */
+moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                   const moe_gate_inputs_t* in, const moe_routing_t* out,
+                                   void* ws, size_t ws_bytes, const void* x, int32_t d,
+                                   int32_t dtype, void* recv, int32_t flags, moe_stream_t stream);
 
 /* Backward of the fused steps over NVLink (adjoints of moe_combine_p2p and
  * moe_dispatch_p2p, same barrier flags).

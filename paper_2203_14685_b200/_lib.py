@@ -50,6 +50,8 @@ SIGNATURES = [
                                 ctypes.POINTER(RoutingC), vp, sz, vp]),
     ("moe_gate_ex", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),
                                    ctypes.POINTER(RoutingC), vp, sz, vp]),
+    ("moe_gate_layout", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),
+                                       ctypes.POINTER(RoutingC), vp, sz, vp, i32, i32, vp, vp]),
     ("moe_gate_check", ctypes.c_int, [vp, vp, ctypes.POINTER(i32)]),
     ("moe_layout", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp, i32,
                                   i32, vp, vp]),
@@ -85,6 +87,9 @@ SIGNATURES = [
                                                   vp]),
     ("moe_gate_backward_ex", ctypes.c_int, [ctypes.POINTER(GateDesc), ctypes.POINTER(GateInputs),
                                             ctypes.POINTER(RoutingC), vp, vp, vp, vp]),
+    ("moe_gate_dispatch_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                             ctypes.POINTER(GateInputs), ctypes.POINTER(RoutingC),
+                                             vp, sz, vp, i32, i32, vp, i32, vp]),
     ("moe_combine_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
                                                 ctypes.POINTER(RoutingC), vp, vp, i32, i32, vp,
                                                 vp, i32, vp]),

@@ -140,6 +140,50 @@ class Gate:
                                 self.ws.numel(), _stream(self.device)), "moe_gate")
         return out
 
+    def _inputs(self, logits, token_ids, table, group_logits, uniforms):
+        vocab = table.numel() if table is not None else 0
+        return GateInputs(_p(logits), _p(token_ids), _p(table), vocab, _p(group_logits),
+                          self.n_groups, _p(uniforms), float(self.tau), float(self.eps))
+
+    def with_layout(self, x: torch.Tensor, dispatch: torch.Tensor, logits=None, token_ids=None,
+                    table=None, out: Optional[Routing] = None, group_logits=None,
+                    uniforms=None) -> Routing:
+        """moe_gate_layout: the gate and Layout_Transform in one call, the
+        gate's capacity pass fused into the layout kernel.  Same routing and
+        dispatch as gate() then layout()."""
+        if out is None:
+            out = Routing.empty(self.S, self.E, self.k, self.cap, self.device, self.kind,
+                                self.mode, self.prio)
+        _need_cuda(x, "x")
+        _need_cuda(dispatch, "dispatch", x.dtype)
+        out.kind, out.weight_mode, out.priority = self.kind, self.mode, self.prio
+        d = GateDesc(self.S, self.E, self.k, self.cap, self.kind, self.mode, self.prio)
+        inp = self._inputs(logits, token_ids, table, group_logits, uniforms)
+        rc = out.c()
+        check(lib().moe_gate_layout(ctypes.byref(d), ctypes.byref(inp), ctypes.byref(rc),
+                                    _p(self.ws), self.ws.numel(), _p(x), x.shape[-1],
+                                    _DT[x.dtype], _p(dispatch), _stream(self.device)),
+              "moe_gate_layout")
+        return out
+
+    def with_dispatch_p2p(self, comm: "Comm", x: torch.Tensor, recv: torch.Tensor, logits=None,
+                          token_ids=None, table=None, out: Optional[Routing] = None,
+                          group_logits=None, uniforms=None, flags: int = 0) -> Routing:
+        """moe_gate_dispatch_p2p: gate + Layout_Transform + the NVLink dispatch
+        in one call (capacity pass fused into the dispatch kernel)."""
+        if out is None:
+            out = Routing.empty(self.S, self.E, self.k, self.cap, self.device, self.kind,
+                                self.mode, self.prio)
+        out.kind, out.weight_mode, out.priority = self.kind, self.mode, self.prio
+        d = GateDesc(self.S, self.E, self.k, self.cap, self.kind, self.mode, self.prio)
+        inp = self._inputs(logits, token_ids, table, group_logits, uniforms)
+        rc = out.c()
+        check(lib().moe_gate_dispatch_p2p(comm._h, ctypes.byref(d), ctypes.byref(inp),
+                                          ctypes.byref(rc), _p(self.ws), self.ws.numel(), _p(x),
+                                          x.shape[-1], _DT[x.dtype], _p(recv), flags,
+                                          _stream(self.device)), "moe_gate_dispatch_p2p")
+        return out
+
     def check(self) -> int:
         """Invalid hash ids since the last check (synchronises the stream)."""
         n = ctypes.c_int32(0)

@@ -158,6 +158,37 @@ size_t moe_gate_workspace_bytes(const moe_gate_desc_t* desc) {
 moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
                          const moe_routing_t* out, void* ws, size_t ws_bytes,
                          moe_stream_t stream) {
+  moe_status_t s = gate_validate(desc, in, out, ws, ws_bytes);
+  if (s != MOE_OK) return s;
+  return gate_launch(*desc, *in, *out, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_gate_layout(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                             const moe_routing_t* out, void* ws, size_t ws_bytes, const void* x,
+                             int32_t d, int32_t dtype, void* dispatch, moe_stream_t stream_) {
+  moe_status_t s = gate_validate(desc, in, out, ws, ws_bytes);
+  if (s != MOE_OK) return s;
+  s = check_rows("moe_gate_layout", desc, out, x, "x", dispatch, "dispatch", d, dtype, false, true);
+  if (s != MOE_OK) return s;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const int ds = dtype_size(dtype);
+  if (((long long)d * ds) % 32 != 0 || desc->k > 32 || !env_int("MOE_GATE_LAYOUT_FUSED", 1)) {
+    s = gate_launch(*desc, *in, *out, ws, stream);  // the unfused pair
+    if (s != MOE_OK) return s;
+    return layout_launch(*desc, *out, x, ds, d, dispatch, stream);
+  }
+  GateFinalize fin{};
+  s = gate_select_launch(*desc, *in, *out, ws, stream, &fin);
+  if (s != MOE_OK) return s;
+  PeerPtrs dst{};
+  dst.p[0] = static_cast<char*>(dispatch);
+  return layout_fin_launch(*desc, *out, x, ds, d, dst, desc->E, 0, fin, stream);
+}
+
+}  // extern "C"
+
+moe_status_t moe::gate_validate(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
+                                const moe_routing_t* out, void* ws, size_t ws_bytes) {
   moe_status_t s = check_desc("moe_gate", desc);
   if (s != MOE_OK) return s;
   if (!in) {
@@ -206,8 +237,10 @@ moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* i
     set_error("moe_gate: workspace must be 16-byte aligned");
     return MOE_ERR_ALIGNMENT;
   }
-  return gate_launch(*desc, *in, *out, ws, reinterpret_cast<cudaStream_t>(stream));
+  return MOE_OK;
 }
+
+extern "C" {
 
 moe_status_t moe_gate(const moe_gate_desc_t* desc, const float* logits, const int32_t* token_ids,
                       const int32_t* table, int32_t vocab, const moe_routing_t* out, void* ws,

@@ -25,7 +25,7 @@
 #include <climits>
 #include <algorithm>
 
-#include "common.cuh"
+#include "launch.cuh"
 
 namespace moe {
 
@@ -1034,6 +1034,81 @@ static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, Ga
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
   e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
+  return MOE_OK;
+}
+
+static void fill_args(GateArgs& a, const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                      const moe_routing_t& out, void* ws, const GatePlan& p, int ng) {
+  a = GateArgs{};
+  a.logits = in.logits;
+  a.ids = in.token_ids;
+  a.table = in.table;
+  a.vocab = in.vocab;
+  a.glogits = in.group_logits;
+  a.ngroups = ng;
+  a.uniforms = in.uniforms;
+  a.tau = in.tau;
+  a.eps = in.eps;
+  a.z_words = p.z_words;
+  a.S = d.S;
+  a.E = d.E;
+  a.k = d.k;
+  a.cap = d.capacity;
+  a.mode = d.weight_mode;
+  a.prio = d.priority;
+  a.tile_tokens = p.tile_tokens;
+  a.n_tiles = p.n_tiles;
+  a.ncols = p.ncols;
+  a.lg_words = p.lg_words;
+  a.expert_idx = out.expert_idx;
+  a.slot_idx = out.slot_idx;
+  a.weight = out.weight;
+  a.load = out.load;
+  a.slot_src = out.slot_src;
+  char* w = static_cast<char*>(ws);
+  a.ctrl = reinterpret_cast<GateCtrl*>(w);
+  a.status = reinterpret_cast<unsigned long long*>(w + p.status_off);
+  a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
+}
+
+moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                                const moe_routing_t& out, void* ws, cudaStream_t stream,
+                                GateFinalize* fin) {
+  const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
+  const GatePlan p = gate_plan(d, 256, ng);
+  if (p.ncols > kMaxCols) {
+    set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  GateArgs a;  // launch arguments are copied at launch
+  fill_args(a, d, in, out, ws, p, ng);
+  void* args[] = {&a};
+  GateKernel kern = pick_gate<false>(d, p);
+  if (p.smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p.smem);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
+  }
+  cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
+                             stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
+  fin->agg = reinterpret_cast<const unsigned*>(a.status);
+  fin->totals = a.totals;
+  fin->n_tiles = p.n_tiles;
+  fin->tile_tokens = p.tile_tokens;
+  fin->ncols = p.ncols;
+  fin->prio = d.priority;
+  fin->slot_idx = out.slot_idx;
+  fin->slot_src = out.slot_src;
+  fin->weight = out.weight;
+  fin->load = out.load;
+  // the layout reduces the raw table itself when it fits its shared memory
+  fin->scanned = (long long)p.n_tiles * p.ncols > env_int("MOE_FIN_SMEM_MAXW", 4096);
+  if (fin->scanned) {
+    e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
+                   dim3(kGateThreads), 0, stream, args);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
+  }
   return MOE_OK;
 }
 

@@ -381,6 +381,40 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
 }
 
+moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                   const moe_gate_inputs_t* in, const moe_routing_t* out,
+                                   void* ws, size_t ws_bytes, const void* x, int32_t d,
+                                   int32_t dtype, void* recv, int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  moe_status_t s = gate_validate(desc, in, out, ws, ws_bytes);
+  if (s != MOE_OK) return s;
+  PeerPtrs dst;
+  int ds = 0;
+  s = p2p_args("moe_gate_dispatch_p2p", comm, desc, out, x, recv, d, dtype, &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!out->load) {
+    set_error("moe_gate_dispatch_p2p: routing.load is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (((long long)d * ds) % 32 != 0 || desc->k > 32 || !env_int("MOE_GATE_LAYOUT_FUSED", 1)) {
+    s = gate_launch(*desc, *in, *out, ws, stream);  // the unfused pair
+    if (s != MOE_OK) return s;
+    return moe_dispatch_p2p(comm, desc, out, x, d, dtype, recv, flags, stream_);
+  }
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  GateFinalize fin{};
+  s = gate_select_launch(*desc, *in, *out, ws, stream, &fin);
+  if (s != MOE_OK) return s;
+  s = layout_fin_launch(*desc, *out, x, ds, d, dst, desc->E / P, comm->rank, fin, stream);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+}
+
 moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                                       const moe_routing_t* routing, const void* dy,
                                       const void* expert_out, int32_t d, int32_t dtype,

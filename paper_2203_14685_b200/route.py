@@ -21,13 +21,22 @@ class RoutePipeline:
     def __init__(self, S: int, d: int, E: int, k: int, cap: int, dtype=torch.bfloat16,
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
-                 device=None, slot_src: bool = True, dropless: bool = False):
+                 device=None, slot_src: bool = True, dropless: bool = False,
+                 fuse_gate_layout: Optional[bool] = None):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
         exchange (algo "p2p" only).  The expert stand-in is the identity."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
+        # the gate's capacity pass inside the layout / dispatch kernel
+        # (moe_gate_layout / moe_gate_dispatch_p2p): measured slower than the
+        # separate kernels under PDL (C2 51.6 vs 49.6 us for gate + layout),
+        # so off unless asked for (MOE_FUSE_GATE_LAYOUT=1)
+        if fuse_gate_layout is None:
+            import os
+            fuse_gate_layout = os.environ.get("MOE_FUSE_GATE_LAYOUT", "0") == "1"
+        self.fuse = fuse_gate_layout and not dropless and (algo in ("flat", "p2p") or comm is None)
         if dropless:
             cap = S * k
             slot_src = False
@@ -100,6 +109,8 @@ class RoutePipeline:
                 return self.step(logits, x, token_ids, table, expert, mark)
             finally:
                 self.y = saved
+        if self.fuse and (self.P == 1 or self.algo != "hier"):
+            return self._step_fused(logits, x, token_ids, table, expert, mark)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         if self.dropless:
             return self._step_dropless(r, x, mark)
@@ -120,6 +131,37 @@ class RoutePipeline:
         if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
             # entry barrier only if an expert wrote recv after the dispatch's
             # exit barrier; the exit barrier frees recv for the next step
+            self.comm.combine_p2p(self.recv, r, self.y,
+                                  flags=0 if expert else self.comm.NO_ENTRY_BARRIER)
+            mark("a2a_combine")
+            mark("reverse")
+            return self.y
+        self.alltoall(self.recv, self.back)                                # step 5
+        mark("a2a_combine")
+        reverse_layout(self.back, r, out=self.y)                           # step 6
+        mark("reverse")
+        return self.y
+
+    def _step_fused(self, logits, x, token_ids, table, expert, mark):
+        """The step with the gate's capacity pass fused into the layout
+        (P=1, NCCL flat) or into the one-sided dispatch (p2p)."""
+        if self.P > 1 and self.algo == "p2p":                              # steps 1+2+3
+            r = self.gate.with_dispatch_p2p(self.comm, x, self.recv, logits, token_ids, table,
+                                            out=self.routing, flags=self._first_flags())
+            mark("gate")
+            mark("layout")
+            mark("a2a_dispatch")
+        else:                                                              # steps 1+2
+            r = self.gate.with_layout(x, self.dispatch, logits, token_ids, table,
+                                      out=self.routing)
+            mark("gate")
+            mark("layout")
+            self.alltoall(self.dispatch, self.recv)                        # step 3
+            mark("a2a_dispatch")
+        if expert:                                                         # step 4 (stand-in)
+            expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
+            mark("expert")
+        if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
             self.comm.combine_p2p(self.recv, r, self.y,
                                   flags=0 if expert else self.comm.NO_ENTRY_BARRIER)
             mark("a2a_combine")

@@ -267,3 +267,30 @@ def test_run_host_pipelined_matches_step(orc):
     torch.cuda.synchronize()
     for i in range(5):
         assert host(outs[i]).tobytes() == want[i].tobytes(), "batch %d" % i
+
+
+@pytest.mark.parametrize("case", [c for c in LAYOUT_CASES] + [
+    dict(kind="topk", S=4096, E=64, k=1, d=2048, dtype="bf16", prio="slot"),
+    dict(kind="topk", S=65536, E=32, k=2, d=256, dtype="bf16"),             # scanned table
+    dict(kind="hash", S=3000, E=16, k=1, d=128, dtype="f32", bad_ids=[0, 7], bad_val=1 << 20),
+], ids=lambda c: "-".join("%s=%s" % kv for kv in c.items() if kv[0] != "bad_ids"))
+def test_gate_layout_fused_equals_gate_then_layout(orc, case):
+    """moe_gate_layout (the capacity pass inside the layout kernel) gives the
+    same routing and dispatch as the oracle (and thus as gate + layout)."""
+    kind, S, E, k, d = case["kind"], case["S"], case["E"], case["k"], case["d"]
+    cap = case.get("cap") or orc.capacity(S, E, k, case.get("C", 1.0))
+    mode, prio = case.get("mode", "renorm"), case.get("prio", "token")
+    lg, ids, table = _inputs(case)
+    ro = orc.gate(lg, E=E, k=k, cap=cap, kind=kind, weight_mode=mode, priority=prio,
+                  token_ids=ids, table=table)
+    x = synthgen.tokens(S + d + 1, S, d, case["dtype"])
+    g = moe.Gate(S, E, k, cap, kind, mode, prio)
+    xd = dev(x)
+    disp = torch.empty((E, cap, d), dtype=xd.dtype, device="cuda")
+    rg = g.with_layout(xd, disp, None if lg is None else dev(lg),
+                       None if ids is None else dev(ids), None if table is None else dev(table))
+    torch.cuda.synchronize()
+    assert_routing_equal(rg, ro, str(case))
+    assert host(disp).tobytes() == orc.layout(x, ro).tobytes()
+    if kind == "hash":
+        assert g.check() == ro.bad
