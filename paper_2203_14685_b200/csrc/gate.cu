@@ -1,7 +1,9 @@
 // gate.cu -- moe_gate: Step 1 of Algorithm 1 on given gate
-// logits, fused with capacity slot assignment.  Three kernels,
-// chained with programmatic dependent launch (each one's launch overlaps its
-// predecessor's tail), no spin-waits and no co-residency assumption:
+// logits, fused with capacity slot assignment.  Two or three
+// kernels, chained with programmatic dependent launch (each one's launch
+// overlaps its predecessor's tail), no spin-waits and no co-residency
+// assumption: select -> slots2 when tiles x columns <= 4096 (every CTA then
+// reduces the tile table itself), else select -> scan -> slots:
 //
 //   k_gate_select  one CTA per tile of tokens.  The tile's logits come into
 //                  shared memory with one TMA bulk copy.  Selection + weights
@@ -19,6 +21,12 @@
 //   k_gate_slots   slot = earlier tiles + provisional (SLOT priority: + the
 //                  items of earlier j); >= cap -> dropped, weight 0 (R4-R6);
 //                  slot_src and its empty entries.
+//   k_gate_slots2  scan + slots in one pass (per-CTA table reduction).
+// SAM (R17) and Dense-to-Sparse (R18) are further selection kinds of
+// k_gate_select.  Measured alternatives behind knobs: one cooperative
+// launch with a grid barrier (k_gate_fused, MOE_GATE_FUSED=1) and the
+// capacity pass inside the layout kernel (gate_select_launch +
+// layout.cu's k_layout_fin, moe_gate_layout).
 // Columns are experts (TOKEN priority, t-major admission) or (j, expert)
 // pairs (SLOT priority, j-major).  Traffic is O(tiles x columns).
 #include <cfloat>
