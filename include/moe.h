@@ -448,6 +448,20 @@ moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* d
                                       void* d_expert_out, float* d_weight, int32_t flags,
                                       moe_stream_t stream);
 
+/* moe_combine_backward_push_p2p: the same outputs as moe_combine_backward_p2p
+ * with half the NVLink bytes: dy rows (the dispatch kernel) and the slot
+ * weights are pushed to the experts' owners, each owner scales the rows in
+ * place into d_expert_out (same exact rounding) and dots them with its
+ * LOCAL expert_out rows, writing the results into the token owner's dw
+ * table, from which d_weight is read.  wtab, dwtab: symmetric fp32
+ * [E*cap] scratch.  Ends with barriers; d_expert_out is final on return
+ * (in stream order). */
+moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                           const moe_routing_t* routing, const void* dy,
+                                           const void* expert_out, int32_t d, int32_t dtype,
+                                           void* d_expert_out, float* wtab, float* dwtab,
+                                           float* d_weight, int32_t flags, moe_stream_t stream);
+
 /* moe_dispatch_backward_p2p: entry barrier; dx[t] = sum_j d_recv_q[r][e mod
  * E/P][s] read from each owner q over NVLink (fp32 accumulate, one RNE
  * store); exit barrier.  Equals moe_alltoall(FLAT) + moe_layout_backward.

@@ -583,6 +583,26 @@ class Comm:
               "moe_combine_backward_p2p")
         return d_expert_out, d_weight
 
+    def combine_backward_push_p2p(self, dy: torch.Tensor, expert_out: torch.Tensor, r: "Routing",
+                                  d_expert_out: torch.Tensor, wtab: torch.Tensor,
+                                  dwtab: torch.Tensor, d_weight: Optional[torch.Tensor] = None,
+                                  flags: int = 0):
+        """Adjoint of combine_p2p, push form: dy rows and weights go to the
+        experts' owners, which scale in place and dot with their local
+        expert_out (half the NVLink bytes of combine_backward_p2p).
+        wtab, dwtab: symmetric float32 [E*cap] scratch."""
+        _need_cuda(dy, "dy")
+        d = dy.shape[-1]
+        if d_weight is None:
+            d_weight = torch.empty((r.S, r.k), dtype=torch.float32, device=dy.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_combine_backward_push_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                                  _p(dy), _p(expert_out), d, _DT[dy.dtype],
+                                                  _p(d_expert_out), _p(wtab), _p(dwtab),
+                                                  _p(d_weight), flags, _stream(dy.device)),
+              "moe_combine_backward_push_p2p")
+        return d_expert_out, d_weight
+
     def dispatch_backward_p2p(self, d_recv: torch.Tensor, r: "Routing",
                               dx: Optional[torch.Tensor] = None, flags: int = 0) -> torch.Tensor:
         """Adjoint of dispatch_p2p: dx[t] = sum_j of the owners' d_recv rows."""

@@ -327,6 +327,119 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
   return MOE_OK;
 }
 
+// ------------------------------------------------------------ push-form combine adjoint
+// The NVLink combine adjoint without reading expert outputs across the link:
+// the token owner pushes dy rows (unscaled, by the dispatch kernel in peer
+// mode) and the slot weights to the experts' owners; each owner scales the
+// rows in place (d_expert_out = w * dy, the same exact rounding) and takes
+// the dot with its LOCAL expert output row, writing the 4-byte result into
+// the token owner's dw table; the token owner then picks d_weight from it.
+// NVLink bytes: one row per admitted slot instead of two.
+__global__ void k_scatter_w(const int32_t* expert_idx, const int32_t* slot_idx,
+                            const float* weight, PeerPtrs wtab, int n, int El, int cap,
+                            int rank) {
+  pdl_wait();
+  pdl_trigger();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = __ldg(slot_idx + i);
+    if (s < 0) continue;
+    const int e = __ldg(expert_idx + i), q = e / El;
+    reinterpret_cast<float*>(wtab.p[q])[(size_t)(rank * El + e - q * El) * cap + s] = __ldg(weight + i);
+  }
+  __threadfence_system();
+}
+
+// Owner side: rows [P][El][cap] of dbuf hold dy (padding rows 0).
+template <int DT, int U>
+__global__ void __launch_bounds__(kRowThreads) k_scale_dot(char* dbuf, const char* eo,
+                                                           const float* wtab, PeerPtrs dwtab,
+                                                           int El, int cap, int rank,
+                                                           int row_bytes, long long nrows) {
+  constexpr int VB = 32, SEG = 32 * U * VB;
+  const int lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
+  const long long nw = (long long)gridDim.x * kRowWarps;
+  for (long long row = (long long)blockIdx.x * kRowWarps + (threadIdx.x >> 5); row < nrows;
+       row += nw) {
+    const float w = __ldg(wtab + row);
+    char* g_row = dbuf + row * row_bytes;
+    const char* b_row = eo + row * row_bytes;
+    float dot = 0.f;
+    for (int seg = 0; seg < row_bytes; seg += SEG) {
+      V8 g[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int off = seg + (lane + 32 * u) * VB;
+        if (off < row_bytes) {
+          g[u] = ld_stream_v8(g_row + off);
+          b[u] = ld_stream_v8(b_row + off);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int off = seg + (lane + 32 * u) * VB;
+        if (off < row_bytes) {
+          st_v8(g_row + off, scale_vec<DT>(w, g[u]));
+          dot = dot_vec<DT>(g[u], b[u], dot);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, m);
+    if (lane == 0) {
+      const long long per_src = (long long)El * cap;
+      const int src = (int)(row / per_src);
+      const long long rem = row - src * per_src;  // le * cap + s
+      reinterpret_cast<float*>(dwtab.p[src])[(size_t)rank * per_src + rem] = dot;
+    }
+  }
+  __threadfence_system();
+}
+
+__global__ void k_gather_dw(const int32_t* expert_idx, const int32_t* slot_idx, const float* dwtab,
+                            float* d_weight, int n, int cap) {
+  pdl_wait();
+  pdl_trigger();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = __ldg(slot_idx + i);
+    d_weight[i] = s >= 0 ? dwtab[(size_t)__ldg(expert_idx + i) * cap + s] : 0.f;
+  }
+}
+
+moe_status_t push_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const PeerPtrs& wtab,
+                             const PeerPtrs& dwtab, char* dbuf_local, const char* eo_local,
+                             float* d_weight, int P, int rank, int dtype, int row_bytes, int phase,
+                             cudaStream_t stream) {
+  const int El = d.E / P, n = d.S * d.k;
+  cudaError_t e = cudaSuccess;
+  if (phase == 0) {  // token side: weights to the owners
+    const int grid = std::min((n + 255) / 256, device_sm_count() * 4);
+    void* args[] = {(void*)&r.expert_idx, (void*)&r.slot_idx, (void*)&r.weight, (void*)&wtab,
+                    (void*)&n, (void*)&El, (void*)&d.capacity, &rank};
+    e = launch_pdl((const void*)k_scatter_w, dim3(std::max(1, grid)), dim3(256), 0, stream, args);
+  } else if (phase == 1) {  // owner side
+    const bool f = dtype == MOE_F32;
+    const void* kern = row_bytes >= 2048 ? (f ? (const void*)k_scale_dot<MOE_F32, 2> : (const void*)k_scale_dot<MOE_BF16, 2>)
+                                         : (f ? (const void*)k_scale_dot<MOE_F32, 1> : (const void*)k_scale_dot<MOE_BF16, 1>);
+    long long nrows = (long long)d.E * d.capacity;
+    const float* wl = reinterpret_cast<const float*>(wtab.p[rank]);
+    int cap = d.capacity;
+    void* args[] = {&dbuf_local, (void*)&eo_local, (void*)&wl, (void*)&dwtab, (void*)&El, &cap,
+                    &rank, &row_bytes, &nrows};
+    e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
+  } else {  // token side: d_weight from the local dw table
+    const int grid = std::min((n + 255) / 256, device_sm_count() * 4);
+    const float* dwl = reinterpret_cast<const float*>(dwtab.p[rank]);
+    int cap = d.capacity;
+    void* args[] = {(void*)&r.expert_idx, (void*)&r.slot_idx, (void*)&dwl, (void*)&d_weight,
+                    (void*)&n, &cap};
+    e = launch_pdl((const void*)k_gather_dw, dim3(std::max(1, grid)), dim3(256), 0, stream, args);
+  }
+  if (e != cudaSuccess) return cuda_status(e, "moe_combine_backward_push_p2p: launch");
+  return MOE_OK;
+}
+
 // ------------------------------------------------------------ gate adjoint
 // L lanes per token (32/L tokens per warp in flight), each lane owning the
 // experts e = l, l+L, ... (coalesced stores of the d_logits row).  With G_e =

@@ -63,6 +63,10 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
                                 int rank, int dtype, int dtype_size, int dcols, float* d_weight,
                                 cudaStream_t stream, const int32_t* offsets = nullptr,
                                 const int32_t* peer_base = nullptr);
+moe_status_t push_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const PeerPtrs& wtab,
+                             const PeerPtrs& dwtab, char* dbuf_local, const char* eo_local,
+                             float* d_weight, int P, int rank, int dtype, int row_bytes, int phase,
+                             cudaStream_t stream);
 moe_status_t expert_scale_launch(const void* in, void* out, int nsrc, int E_local, int e_base,
                                  int cap, int dcols, int dtype, int dtype_size,
                                  cudaStream_t stream);

@@ -445,6 +445,53 @@ moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* d
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);
 }
 
+static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
+                               PeerPtrs* out);
+
+moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                           const moe_routing_t* routing, const void* dy,
+                                           const void* expert_out, int32_t d, int32_t dtype,
+                                           void* d_expert_out, float* wtab, float* dwtab,
+                                           float* d_weight, int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_combine_backward_push_p2p";
+  PeerPtrs src, dst, wt, dwt;
+  int ds = 0;
+  moe_status_t s = p2p_args(fn, comm, desc, routing, dy, expert_out, d, dtype, &src, &ds);
+  if (s != MOE_OK) return s;
+  s = p2p_args(fn, comm, desc, routing, dy, d_expert_out, d, dtype, &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight || !routing->load || !d_weight || !wtab || !dwtab) {
+    set_error("%s: routing.weight/load, wtab, dwtab and d_weight are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const size_t tb = sizeof(float) * (size_t)desc->E * desc->capacity;
+  s = symm_peers(fn, comm, wtab, tb, &wt);
+  if (s != MOE_OK) return s;
+  s = symm_peers(fn, comm, dwtab, tb, &dwt);
+  if (s != MOE_OK) return s;
+  const int P = comm->nranks, r = comm->rank;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, r, stream);
+    if (s != MOE_OK) return s;
+  }
+  // dy rows to the experts' owners (the dispatch kernel; padding rows zero)
+  s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, desc->E / P, r, stream);
+  if (s != MOE_OK) return s;
+  s = push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, nullptr, P, r, dtype, d * ds, 0,
+                      stream);
+  if (s != MOE_OK) return s;
+  s = barrier_launch(comm->sig.peer, P, r, stream);  // rows and weights landed
+  if (s != MOE_OK) return s;
+  s = push_bwd_launch(*desc, *routing, wt, dwt, static_cast<char*>(d_expert_out),
+                      static_cast<const char*>(expert_out), nullptr, P, r, dtype, d * ds, 1, stream);
+  if (s != MOE_OK) return s;
+  s = barrier_launch(comm->sig.peer, P, r, stream);  // dots landed, d_expert_out final
+  if (s != MOE_OK) return s;
+  return push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, d_weight, P, r, dtype,
+                         d * ds, 2, stream);
+}
+
 moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                                        const moe_routing_t* routing, const void* d_recv,
                                        int32_t d, int32_t dtype, void* dx, int32_t flags,

@@ -226,6 +226,8 @@ class RoutePipeline:
             self.d_logits = torch.empty((self.S, self.E), dtype=torch.float32, device=self.device)
             if self.P > 1 and self.algo == "p2p":
                 self.d_recv = self.comm.symm_empty((self.E, self.cap, self.d), self.y.dtype)
+                self.wtab = self.comm.symm_empty((self.E * self.cap,), torch.float32)
+                self.dwtab = self.comm.symm_empty((self.E * self.cap,), torch.float32)
             elif self.P > 1:
                 self.d_back, self.d_recv, self.d_disp = (mk(self.E, self.cap, self.d)
                                                          for _ in range(3))
@@ -234,7 +236,13 @@ class RoutePipeline:
         if self.P > 1 and self.algo == "p2p":
             # d_back rows are stored straight into the owners' d_recv, then
             # every dx row gathers its gradient rows back over NVLink
-            self.comm.combine_backward_p2p(dy, self.recv, r, self.d_recv, self.d_weight)
+            import os
+            if os.environ.get("MOE_BWD_PUSH", "1") != "0":
+                # push form: dy rows travel once, dots are taken at the owners
+                self.comm.combine_backward_push_p2p(dy, self.recv, r, self.d_recv, self.wtab,
+                                                    self.dwtab, self.d_weight)
+            else:
+                self.comm.combine_backward_p2p(dy, self.recv, r, self.d_recv, self.d_weight)
             self.comm.dispatch_backward_p2p(self.d_recv, r, self.dx,
                                             flags=self.comm.NO_ENTRY_BARRIER)
         else:

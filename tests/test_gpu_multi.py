@@ -107,7 +107,16 @@ def _bwd_rank_main(rank, world, port, q):
     _, dw = comm.combine_backward_p2p(dev(dy), expert_out, r, d_expert_out)
     dx = comm.dispatch_backward_p2p(d_recv, r)
     torch.cuda.synchronize()
-    q.put((rank, lg, eo, dr, dy, host(d_expert_out).copy(), host(dw).copy(), host(dx).copy()))
+    deo_pull = host(d_expert_out).copy()
+    # the push form: the same d_expert_out bytes and d_weight (same lane order)
+    wtab = comm.symm_empty((E * cap,), torch.float32)
+    dwtab = comm.symm_empty((E * cap,), torch.float32)
+    d_expert_out.fill_(5.0)
+    _, dw2 = comm.combine_backward_push_p2p(dev(dy), expert_out, r, d_expert_out, wtab, dwtab)
+    torch.cuda.synchronize()
+    assert host(d_expert_out).tobytes() == deo_pull.tobytes(), "push d_expert_out"
+    assert host(dw2).tobytes() == host(dw).tobytes(), "push d_weight"
+    q.put((rank, lg, eo, dr, dy, deo_pull, host(dw).copy(), host(dx).copy()))
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
