@@ -419,7 +419,7 @@ def main():
     # kernels of the same step (combine -> AllToAll x2 -> layout, + gate),
     # one CUDA graph, L2 flushed between replays, max over ranks
     bwd = None
-    if not a.no_backward and not a.dropless:
+    if not a.no_backward:
         dy = torch.from_numpy(synthgen.tokens(synthgen.seed_for(w.index, rank, 9), S, w.d,
                                               w.dtype))
         if w.dtype == "bf16":

@@ -462,6 +462,23 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
                                            void* d_expert_out, float* wtab, float* dwtab,
                                            float* d_weight, int32_t flags, moe_stream_t stream);
 
+/* Adjoints of the dropless NVLink exchange (NEXT-1 x NEXT-4): as
+ * moe_combine_backward_p2p / moe_dispatch_backward_p2p with rows at
+ * peer_base[q] + offsets[e] - offsets[q*E/P] + s of the owner's buffer
+ * (the layout moe_dispatch_packed_p2p produced; pass its peer_base), no
+ * padding rows.  rows: the symmetric buffers' row count (>= nranks*S*k). */
+moe_status_t moe_combine_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                            const moe_routing_t* routing, const int32_t* offsets,
+                                            const int32_t* peer_base, const void* dy,
+                                            const void* expert_out, int32_t d, int32_t dtype,
+                                            int64_t rows, void* d_expert_out, float* d_weight,
+                                            int32_t flags, moe_stream_t stream);
+moe_status_t moe_dispatch_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                             const moe_routing_t* routing, const int32_t* offsets,
+                                             const int32_t* peer_base, const void* d_recv,
+                                             int32_t d, int32_t dtype, int64_t rows, void* dx,
+                                             int32_t flags, moe_stream_t stream);
+
 /* moe_dispatch_backward_p2p: entry barrier; dx[t] = sum_j d_recv_q[r][e mod
  * E/P][s] read from each owner q over NVLink (fp32 accumulate, one RNE
  * store); exit barrier.  Equals moe_alltoall(FLAT) + moe_layout_backward.

@@ -96,6 +96,12 @@ SIGNATURES = [
     ("moe_combine_backward_push_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
                                                      ctypes.POINTER(RoutingC), vp, vp, i32, i32,
                                                      vp, vp, vp, vp, i32, vp]),
+    ("moe_combine_packed_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                                       ctypes.POINTER(RoutingC), vp, vp, vp, vp,
+                                                       i32, i32, i64, vp, vp, i32, vp]),
+    ("moe_dispatch_packed_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
+                                                        ctypes.POINTER(RoutingC), vp, vp, vp, i32,
+                                                        i32, i64, vp, i32, vp]),
     ("moe_dispatch_backward_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc),
                                                  ctypes.POINTER(RoutingC), vp, i32, i32, vp, i32,
                                                  vp]),

@@ -603,6 +603,38 @@ class Comm:
               "moe_combine_backward_push_p2p")
         return d_expert_out, d_weight
 
+    def combine_packed_backward_p2p(self, dy: torch.Tensor, expert_out: torch.Tensor,
+                                    r: "Routing", offsets: torch.Tensor, peer_base: torch.Tensor,
+                                    d_expert_out: torch.Tensor,
+                                    d_weight: Optional[torch.Tensor] = None, flags: int = 0):
+        """Adjoint of combine_packed_p2p (dropless, NVLink)."""
+        d = dy.shape[-1]
+        if d_weight is None:
+            d_weight = torch.empty((r.S, r.k), dtype=torch.float32, device=dy.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_combine_packed_backward_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                                    _p(offsets), _p(peer_base), _p(dy),
+                                                    _p(expert_out), d, _DT[dy.dtype],
+                                                    expert_out.shape[0], _p(d_expert_out),
+                                                    _p(d_weight), flags, _stream(dy.device)),
+              "moe_combine_packed_backward_p2p")
+        return d_expert_out, d_weight
+
+    def dispatch_packed_backward_p2p(self, d_recv: torch.Tensor, r: "Routing",
+                                     offsets: torch.Tensor, peer_base: torch.Tensor,
+                                     dx: Optional[torch.Tensor] = None, flags: int = 0):
+        """Adjoint of dispatch_packed_p2p (dropless, NVLink)."""
+        d = d_recv.shape[-1]
+        if dx is None:
+            dx = torch.empty((r.S, d), dtype=d_recv.dtype, device=d_recv.device)
+        desc, rc = r.desc(), r.c()
+        check(lib().moe_dispatch_packed_backward_p2p(self._h, ctypes.byref(desc), ctypes.byref(rc),
+                                                     _p(offsets), _p(peer_base), _p(d_recv), d,
+                                                     _DT[d_recv.dtype], d_recv.shape[0], _p(dx),
+                                                     flags, _stream(dx.device)),
+              "moe_dispatch_packed_backward_p2p")
+        return dx
+
     def dispatch_backward_p2p(self, d_recv: torch.Tensor, r: "Routing",
                               dx: Optional[torch.Tensor] = None, flags: int = 0) -> torch.Tensor:
         """Adjoint of dispatch_p2p: dx[t] = sum_j of the owners' d_recv rows."""

@@ -447,6 +447,10 @@ moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* d
 
 static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
                                PeerPtrs* out);
+static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                const moe_routing_t* routing, const int32_t* offsets,
+                                const void* a, const void* buf, int64_t rows, int32_t d,
+                                int32_t dtype, PeerPtrs* peers, int* ds);
 
 moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                                            const moe_routing_t* routing, const void* dy,
@@ -490,6 +494,67 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
   if (s != MOE_OK) return s;
   return push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, d_weight, P, r, dtype,
                          d * ds, 2, stream);
+}
+
+moe_status_t moe_combine_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                            const moe_routing_t* routing, const int32_t* offsets,
+                                            const int32_t* peer_base, const void* dy,
+                                            const void* expert_out, int32_t d, int32_t dtype,
+                                            int64_t rows, void* d_expert_out, float* d_weight,
+                                            int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_combine_packed_backward_p2p";
+  PeerPtrs src, dst;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, dy, expert_out, rows, d, dtype,
+                               &src, &ds);
+  if (s != MOE_OK) return s;
+  s = packed_args(fn, comm, desc, routing, offsets, dy, d_expert_out, rows, d, dtype, &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight || !peer_base || !d_weight) {
+    set_error("%s: routing.weight, peer_base and d_weight are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  s = combine_bwd_launch(*desc, *routing, dy, src, dst, desc->E / P, comm->rank, dtype, ds, d,
+                         d_weight, stream, offsets, peer_base);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+}
+
+moe_status_t moe_dispatch_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                             const moe_routing_t* routing, const int32_t* offsets,
+                                             const int32_t* peer_base, const void* d_recv,
+                                             int32_t d, int32_t dtype, int64_t rows, void* dx,
+                                             int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_dispatch_packed_backward_p2p";
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, dx, d_recv, rows, d, dtype, &src,
+                               &ds);
+  if (s != MOE_OK) return s;
+  if (!peer_base) {
+    set_error("%s: peer_base is required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    if (s != MOE_OK) return s;
+  }
+  moe_routing_t unit = *routing;
+  unit.weight = nullptr;
+  s = reverse_launch_peers(*desc, unit, src, desc->E / P, comm->rank, dtype, ds, d, dx, stream,
+                           offsets, peer_base);
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
 }
 
 moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,

@@ -201,10 +201,23 @@ class RoutePipeline:
         (d_back, d_weight) -> AllToAll -> AllToAll -> layout (dx), plus the
         gate (d_logits, when the gate has logits).  Returns (dx, d_logits)."""
         r = self.routing
+        if self.dropless and self.P > 1:
+            if not hasattr(self, "d_weight"):
+                self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32,
+                                            device=self.device)
+                self.d_recv = self.comm.symm_empty(tuple(self.recv.shape), self.y.dtype)
+                self.dx = torch.empty_like(self.y)
+                self.d_logits = torch.empty((self.S, self.E), dtype=torch.float32,
+                                            device=self.device)
+            self.comm.combine_packed_backward_p2p(dy, self.recv, r, self.offsets, self.peer_base,
+                                                  self.d_recv, self.d_weight)
+            self.comm.dispatch_packed_backward_p2p(self.d_recv, r, self.offsets, self.peer_base,
+                                                   self.dx, flags=self.comm.NO_ENTRY_BARRIER)
+            dl = None
+            if logits is not None and self.gate.kind not in (2, 3, 4):
+                dl = gate_backward(logits, r, self.d_weight, out=self.d_logits)
+            return self.dx, dl
         if self.dropless:
-            if self.P > 1:
-                raise NotImplementedError("backward of the dropless exchange across ranks is "
-                                          "not built (the padded form has it)")
             if not hasattr(self, "d_weight"):
                 self.d_weight = torch.empty((self.S, self.k), dtype=torch.float32,
                                             device=self.device)

@@ -204,7 +204,18 @@ def _packed_rank_main(rank, world, port, q):
     recv2 = torch.empty((int(rc.sum()), D), dtype=torch.bfloat16, device="cuda")
     comm.alltoallv(packed, sc, recv2, rc)
     torch.cuda.synchronize()
-    q.put((rank, lg, x, host(roff).copy(), recv_h, out_h, y, host(recv2).copy()))
+    # the adjoints of the dropless exchange (NEXT-1 x NEXT-4)
+    dy = synthgen.tokens(synthgen.seed_for(9, rank, 14), S, D, "bf16")
+    d_eo = comm.symm_empty((rows, D), torch.bfloat16)
+    _, dw = comm.combine_packed_backward_p2p(dev(dy), eo, r, off, pb, d_eo)
+    dr_h = synthgen.tokens(synthgen.seed_for(9, rank, 15), R_in, D, "bf16")
+    d_recv = comm.symm_empty((rows, D), torch.bfloat16)
+    d_recv[:R_in].copy_(dev(dr_h))
+    torch.cuda.synchronize()
+    dx = comm.dispatch_packed_backward_p2p(d_recv, r, off, pb)
+    torch.cuda.synchronize()
+    bwd = (dy, host(d_eo)[:R_in].copy(), host(dw).copy(), dr_h, host(dx).copy())
+    q.put((rank, lg, x, host(roff).copy(), recv_h, out_h, y, host(recv2).copy(), bwd))
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
@@ -252,3 +263,39 @@ def test_multi_gpu_dropless(orc, world):
             rows = offs[r][ros[r].expert_idx[ok, j]] + ros[r].slot_idx[ok, j]
             bound[ok] += np.abs(ros[r].weight[ok, j].astype(np.float64)[:, None] * b64[rows])
         assert_y_close(y, y_o, bound, True, "y")
+    # adjoints: the token owner's packed d_back rows (padded oracle adjoint
+    # minus padding) travel to the owners like the forward rows
+    d_backs, dws = [], []
+    for r in range(world):
+        dy = out[r][7][0]
+        ro, off = ros[r], offs[r]
+        cap = S * K
+        back_pad = np.zeros((E, cap, D), np.uint16)
+        for e in range(E):
+            back_pad[e, :off[e + 1] - off[e]] = backs[r][off[e]:off[e + 1]]
+        db, dw = orc.reverse_layout_bwd(dy, back_pad, ro)
+        d_backs.append(np.concatenate([db[e, :off[e + 1] - off[e]] for e in range(E)]))
+        dws.append(dw)
+    d_eo_want = orc.alltoallv(d_backs, counts)
+    d_disp = orc.alltoallv([out[q][7][3] for q in range(world)], counts.T)
+    for r in range(world):
+        _, d_eo, dw, _, dx = out[r][7]
+        assert d_eo.tobytes() == d_eo_want[r].tobytes()
+        err = np.abs(dw.astype(np.float64) - dws[r].astype(np.float64))
+        b64 = as_f64(backs[r])
+        dy64 = as_f64(out[r][7][0])
+        bound = np.zeros_like(err)
+        for j in range(K):
+            ok = ros[r].slot_idx[:, j] >= 0
+            rows_ = offs[r][ros[r].expert_idx[ok, j]] + ros[r].slot_idx[ok, j]
+            bound[ok, j] = np.abs(dy64[ok] * b64[rows_]).sum(1)
+        assert (err <= (D / 32 + 6) * 2.0 ** -24 * bound + 1e-30).all()
+        g_pad = np.zeros((E, S * K, D), np.uint16)
+        off = offs[r]
+        for e in range(E):
+            g_pad[e, :off[e + 1] - off[e]] = d_disp[r][off[e]:off[e + 1]]
+        dx_o = orc.layout_bwd(g_pad, ros[r])
+        from gpu_util import combine_bound
+        unit = type(ros[r])(**{**ros[r].__dict__,
+                               "weight": (ros[r].slot_idx >= 0).astype(np.float32)})
+        assert_y_close(dx, dx_o, combine_bound(as_f64(g_pad), unit), True, "dx")
