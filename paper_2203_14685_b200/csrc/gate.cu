@@ -90,10 +90,12 @@ static int choose_lanes(int E) {
   return L;
 }
 
+static int gate_tiles() { return env_int("MOE_GATE_TILES", 256); }
+
 // want_tiles: the three-kernel path wants >= 256 tiles when S allows (about
 // 1.7 CTAs per SM on 148 SMs); the single-launch path fewer, larger tiles
 // (every CTA reduces all tiles' aggregates after its grid barrier).
-static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles = 256, int ngroups = 1) {
+static GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles, int ngroups = 1) {
   GatePlan p{};
   p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.kind == MOE_GATE_SAM ? d.E / std::max(1, ngroups) : d.E);
   p.K = d.k <= 1 ? 1 : d.k <= 2 ? 2 : d.k <= 4 ? 4 : d.k <= 8 ? 8 : 0;
@@ -1014,7 +1016,9 @@ int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
 }
 
 size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
-  return std::max(gate_plan(d).bytes, gate_plan(d, fused_tiles()).bytes);
+  // room for every tile count the knobs may pick (the table is small)
+  return std::max({gate_plan(d, gate_tiles()).bytes, gate_plan(d, fused_tiles()).bytes,
+                   gate_plan(d, 1024).bytes});
 }
 
 // The three-kernel path (k_gate_select -> k_gate_scan -> k_gate_slots, PDL).
@@ -1083,7 +1087,7 @@ moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
                                 const moe_routing_t& out, void* ws, cudaStream_t stream,
                                 GateFinalize* fin) {
   const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
-  const GatePlan p = gate_plan(d, 256, ng);
+  const GatePlan p = gate_plan(d, gate_tiles(), ng);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
@@ -1128,7 +1132,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
   const GatePlan pf = gate_plan(d, fused_tiles(), ng);
   bool fused = env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH &&
                (long long)pf.n_tiles * pf.ncols <= env_int("MOE_GATE_FUSED_MAXW", 8192);
-  const GatePlan p = fused ? pf : gate_plan(d, 256, ng);
+  const GatePlan p = fused ? pf : gate_plan(d, gate_tiles(), ng);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
@@ -1176,7 +1180,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fk, kGateThreads, fsmem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: fused occupancy");
     if (p.n_tiles > per_sm * device_sm_count()) {
-      const GatePlan p3 = gate_plan(d, 256, ng);
+      const GatePlan p3 = gate_plan(d, gate_tiles(), ng);
       a.tile_tokens = p3.tile_tokens;
       a.n_tiles = p3.n_tiles;
       a.lg_words = p3.lg_words;
