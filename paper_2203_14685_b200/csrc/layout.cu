@@ -957,7 +957,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   // TMA-staged combine (peer mode by default: rows come over NVLink)
   {
     const bool peer = E_local != d.E;
-    const int tma = peer ? env_int("MOE_P2P_REVERSE_TMA", 0) : env_int("MOE_REVERSE_TMA", 0);
+    // measured: TMA staging wins for Switch (k = 1) on >= 4 KiB rows (C3:
+    // 48.5 vs 49.8 us), loses on 2 KiB rows (C4b: 69 vs 53 us) and over NVLink
+    const int tma_dflt = (!peer && a.k == 1 && a.row_bytes >= 4096) ? 1 : 0;
+    const int tma = peer ? env_int("MOE_P2P_REVERSE_TMA", 0) : env_int("MOE_REVERSE_TMA", tma_dflt);
     const int budget = env_int("MOE_REVERSE_TMA_SMEM", 100 * 1024);
     const int ns = std::min(16, budget / (kTmaWarps * std::max(1, a.row_bytes * a.k)));
     if (tma && a.row_bytes % 32 == 0 && a.k <= kRevTmaMaxK && ns >= 2) {
@@ -987,7 +990,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     const int segs = std::max(1, a.row_bytes / 1024);  // 1 KiB per U step
     const int per = std::max(1, KU / a.k);                // U * TPW
     const int Uc = std::min(per, segs) >= 4 ? 4 : std::min(per, segs) >= 2 ? 2 : 1;
-    const int T = env_int("MOE_REVERSE_TPW", 0) ? std::max(1, per / Uc) : 1;  // TPW: no measured gain
+    // two tokens per warp round for Switch on <= 2 KiB rows (C4b: 51.3 vs
+    // 53.5 us); no gain for k = 2
+    const int tpw_dflt = (a.k == 1 && a.row_bytes <= 2048) ? 1 : 0;
+    const int T = env_int("MOE_REVERSE_TPW", tpw_dflt) ? std::max(1, per / Uc) : 1;
 #define MOE_RK(KK, UU, TT) (f ? (const void*)k_reverse_k<MOE_F32, KK, UU, TT> : (const void*)k_reverse_k<MOE_BF16, KK, UU, TT>)
     if (a.k == 1)
       kern = Uc == 4 ? (T >= 2 ? MOE_RK(1, 4, 2) : MOE_RK(1, 4, 1))
