@@ -311,7 +311,10 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
   a.sys_fence = E_local != d.E;
   const bool f = dtype == MOE_F32;
   const void* kern;
-  const int U2 = a.row_bytes >= 2048 ? 2 : 1;
+  const int uenv = env_int("MOE_COMBINE_BWD_U", 0);
+  // measured: one 1 KiB segment per round beats two (more warps in flight):
+  // C2 65.5 -> 58.9 us, C3 63.5 -> 61.5, C4a 121 -> 111, C4b 73.8 -> 69.6
+  const int U2 = uenv >= 2 ? 2 : 1;
 #define MOE_CBK(KK, UU) (f ? (const void*)k_combine_bwd_k<MOE_F32, KK, UU> : (const void*)k_combine_bwd_k<MOE_BF16, KK, UU>)
   if (a.row_bytes % 32 == 0 && a.k <= 2 && env_int("MOE_COMBINE_BWD_KSPEC", 1))
     kern = a.k == 1 ? (U2 == 2 ? MOE_CBK(1, 2) : MOE_CBK(1, 1)) : (U2 == 2 ? MOE_CBK(2, 2) : MOE_CBK(2, 1));
