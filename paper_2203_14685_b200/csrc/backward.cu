@@ -423,8 +423,10 @@ moe_status_t push_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, c
     e = launch_pdl((const void*)k_scatter_w, dim3(std::max(1, grid)), dim3(256), 0, stream, args);
   } else if (phase == 1) {  // owner side
     const bool f = dtype == MOE_F32;
-    const void* kern = row_bytes >= 2048 ? (f ? (const void*)k_scale_dot<MOE_F32, 2> : (const void*)k_scale_dot<MOE_BF16, 2>)
-                                         : (f ? (const void*)k_scale_dot<MOE_F32, 1> : (const void*)k_scale_dot<MOE_BF16, 1>);
+    // one 1 KiB segment per round, as k_combine_bwd_k (more warps in flight)
+    const void* kern = env_int("MOE_COMBINE_BWD_U", 1) >= 2
+                           ? (f ? (const void*)k_scale_dot<MOE_F32, 2> : (const void*)k_scale_dot<MOE_BF16, 2>)
+                           : (f ? (const void*)k_scale_dot<MOE_F32, 1> : (const void*)k_scale_dot<MOE_BF16, 1>);
     long long nrows = (long long)d.E * d.capacity;
     const float* wl = reinterpret_cast<const float*>(wtab.p[rank]);
     int cap = d.capacity;
