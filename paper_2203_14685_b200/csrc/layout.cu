@@ -915,7 +915,12 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
     kern = segs >= 4 ? (const void*)k_layout_t<4, 1>
            : segs >= 2 ? (const void*)k_layout_t<2, 2> : (const void*)k_layout_t<1, 4>;
   } else if (a.row_bytes % 32 == 0)
-    kern = env_int("MOE_LAYOUT_U", 4) == 2 ? (const void*)k_layout<32, 2> : (const void*)k_layout<32, 4>;
+  {
+    // measured: 2 KiB segments for rows <= 2 KiB (C2 36.3 -> 35.4 us)
+    const int lu = env_int("MOE_LAYOUT_U", a.row_bytes <= 2048 ? 2 : 4);
+    kern = lu == 1 ? (const void*)k_layout<32, 1> : lu == 2 ? (const void*)k_layout<32, 2>
+                                                            : (const void*)k_layout<32, 4>;
+  }
   else
     kern = (const void*)k_layout<16, 4>;
   void* args[] = {&a};
@@ -981,7 +986,9 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   }
   const void* kern;
   const int U = env_int("MOE_REVERSE_U", 1);
-  const int KU = env_int("MOE_REVERSE_KU", 4);  // k <= 2 path: vectors per lane per round (x k rows)
+  // k <= 2 path: vectors per lane per round (x k rows); measured: 2 for
+  // k = 2 (one 1 KiB segment of both rows: C2 36.3 -> 35.6 us), 4 for k = 1
+  const int KU = env_int("MOE_REVERSE_KU", d.k == 2 ? 2 : 4);
   const bool kspec = env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
   if (kspec) {
     // TPW * k * U = KU (default 4) vectors in flight per lane, U covering at
