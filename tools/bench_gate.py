@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """E3 micro-bench (PAPER.md:108-121, 170-171 -- Fig. 3 "Topk kernel
 performance comparison with PyTorch", swept over #experts and #tokens):
-moe_gate (selection + fp64 weights + capacity slots, one kernel) against
+moe_gate (selection + fp64 weights + capacity slots, 2-3 PDL-chained kernels) against
 torch.topk + softmax of the selected logits (selection and weights only, no
 capacity), both replayed from CUDA graphs, L2 flushed between replays.
 
