@@ -272,6 +272,9 @@ def test_run_host_pipelined_matches_step(orc):
 @pytest.mark.parametrize("case", [c for c in LAYOUT_CASES] + [
     dict(kind="topk", S=4096, E=64, k=1, d=2048, dtype="bf16", prio="slot"),
     dict(kind="topk", S=65536, E=32, k=2, d=256, dtype="bf16"),             # scanned table
+    dict(kind="topk", S=3000, E=16, k=2, d=256, dtype="bf16", prio="slot", C=0.8),
+    dict(kind="topk", S=65536, E=32, k=2, d=128, dtype="f32", prio="slot", C=0.9),  # scanned, SLOT
+    dict(kind="ktop1", S=5000, E=32, k=4, d=64, dtype="f32", mode="softmax", C=0.7),
     dict(kind="hash", S=3000, E=16, k=1, d=128, dtype="f32", bad_ids=[0, 7], bad_val=1 << 20),
 ], ids=lambda c: "-".join("%s=%s" % kv for kv in c.items() if kv[0] != "bad_ids"))
 def test_gate_layout_fused_equals_gate_then_layout(orc, case):
