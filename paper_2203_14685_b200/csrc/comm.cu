@@ -158,7 +158,7 @@ moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, 
   // handle exchange inside symm_alloc stays matched.
   m->p2p_ok = false;
   if (nranks <= kMaxRanks && env_int("MOE_DISABLE_P2P", 0) == 0) {
-    moe_status_t ss = symm_alloc(m, 4096, &m->sig);
+    moe_status_t ss = symm_alloc(m, kSigBytes, &m->sig);
     m->p2p_ok = ss == MOE_OK;
   }
   *out = m;

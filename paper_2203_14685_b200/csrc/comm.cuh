@@ -11,6 +11,12 @@
 namespace moe {
 
 constexpr int kMaxRanks = 32;
+// The comm's signal buffer: barrier words at offset 0, then the padding-count
+// table of the padded one-sided dispatch: [kMaxRanks source ranks][256 local
+// experts] int32 (admitted rows per (source, local expert)).
+constexpr size_t kPadTabOff = 4096;
+constexpr int kPadTabStride = 256;
+constexpr size_t kSigBytes = kPadTabOff + sizeof(int) * kMaxRanks * kPadTabStride;
 
 // P pointers to the same symmetric buffer as mapped on every rank
 // (peer[r] == this rank's own allocation).  Passed to kernels by value.

@@ -50,7 +50,8 @@ moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, co
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets = nullptr,
-                                 const int32_t* peer_base = nullptr);
+                                 const int32_t* peer_base = nullptr,
+                                 const PeerPtrs* pad_tab = nullptr);
 moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,

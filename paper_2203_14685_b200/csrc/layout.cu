@@ -867,8 +867,12 @@ moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t*
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets,
-                                 const int32_t* peer_base) {
+                                 const int32_t* peer_base, const PeerPtrs* pad_tab) {
   RowArgs a{};
+  if (pad_tab) {
+    a.skip_pads = 1;
+    a.ptab = *pad_tab;
+  }
   a.offsets = offsets;
   a.peer_base = peer_base;
   a.src = static_cast<const char*>(x);

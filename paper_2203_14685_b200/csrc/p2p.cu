@@ -196,6 +196,58 @@ moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_
   return MOE_OK;
 }
 
+// ------------------------------------------------------------ local padding
+// After the padded one-sided dispatch's exit barrier: zero this rank's own
+// padding rows [cnt, cap) of every (source rank, local expert) block of recv
+// ([P][El][cap] rows), cnt from the padding-count table the senders filled.
+// The zero rows never cross NVLink (C4b's C = 1.25 makes them ~20% of it).
+__global__ void __launch_bounds__(256) k_pad_fill(char* recv, const int* tab, int P, int El,
+                                                  int cap, int row_bytes) {
+  __shared__ int s_cnt[256];
+  pdl_wait();
+  pdl_trigger();
+  const int n = P * El;  // = E <= 256
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int src = i / El, le = i - src * El;
+    const int c = ((const volatile int*)tab)[src * kPadTabStride + le];
+    s_cnt[i] = cap - min(max(c, 0), cap);
+  }
+  __syncthreads();
+  __shared__ int s_pre[257];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int v = i < n ? s_cnt[i] : 0;
+      int incl = v;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += o;
+      }
+      if (i < n) s_pre[i] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_pre[n] = carry;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x / 32);
+  const V4 z = V4{{0, 0, 0, 0}};
+  for (int p = gw; p < s_pre[n]; p += nw) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    const int s = cap - s_cnt[lo] + (p - s_pre[lo]);
+    char* row = recv + ((size_t)lo * cap + s) * row_bytes;
+    for (int off = lane * 16; off < row_bytes; off += 32 * 16) st_v4(row + off, z);
+  }
+}
+
 // ------------------------------------------------------------ dropless exchange
 // counts_q[r][le] = admitted rows of this rank r for q's local expert le
 // (stores into every owner's symmetric count table).
@@ -375,10 +427,34 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
     if (s != MOE_OK) return s;
   }
-  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, desc->E / P, comm->rank, stream);
+  // local padding: the zero rows are written by their owner after the exit
+  // barrier instead of crossing NVLink (needs that barrier; E/P <= 256)
+  const int El = desc->E / P;
+  // Default when at least ~5% of the rows are padding whatever the routing
+  // (E*cap > 1.05*S*k, e.g. the hash config's C = 1.25: C4b dispatch 165 ->
+  // 132 us at N=2); with C = 1 the padding is only the imbalance and the
+  // extra kernel costs more than it saves (C2: +1.7 us).
+  const bool pad_heavy = (double)desc->E * desc->capacity > 1.05 * (double)desc->S * desc->k;
+  const bool local_pad = !(flags & MOE_P2P_NO_EXIT_BARRIER) && El <= kPadTabStride &&
+                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy ? 1 : 0);
+  PeerPtrs tab{};
+  for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
+  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, nullptr, nullptr,
+                          local_pad ? &tab : nullptr);
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
+  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
+  if (s != MOE_OK || !local_pad) return s;
+  const int nrows_pad_max = P * El * desc->capacity;
+  const int grid = std::max(1, std::min(device_sm_count() * 4, (nrows_pad_max + 7) / 8));
+  char* rl = dst.p[comm->rank];
+  const int* tl = reinterpret_cast<const int*>(tab.p[comm->rank]);
+  int cap = desc->capacity, rb = d * ds;
+  int Pv = P, Elv = El;
+  void* args[] = {&rl, (void*)&tl, &Pv, &Elv, &cap, &rb};
+  cudaError_t e = launch_pdl((const void*)k_pad_fill, dim3(grid), dim3(256), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_dispatch_p2p: k_pad_fill launch");
+  return MOE_OK;
 }
 
 moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,

@@ -36,6 +36,12 @@ struct RowArgs {
   // rows earlier source ranks put there; 0 locally); no padding rows.
   const int32_t* offsets;
   const int32_t* peer_base;
+  // padded one-sided dispatch with LOCAL padding: the senders skip the zero
+  // rows and CTA 0 stores min(load, cap) of each owner's experts into the
+  // owner's padding-count table (ptab.p[q] + [rank][le]); the owner zero-fills
+  // its own padding rows after the exit barrier (k_pad_fill)
+  int skip_pads;
+  PeerPtrs ptab;
   // layout only: before waiting on the gate (PDL), the CTAs spread bulk L2
   // prefetches of x (the rows do not depend on the routing), so x streams
   // in from HBM while the latency-bound gate runs
@@ -110,8 +116,14 @@ struct Vec<16> {
 __device__ __forceinline__ void pad_prefix(const RowArgs& a, int* s_beg) {
   __shared__ int s_cnt[257];
   const int tid = threadIdx.x;
-  for (int e = tid; e < a.E; e += blockDim.x)
-    s_cnt[e] = a.offsets ? 0 : a.cap - min(__ldg(a.load + e), a.cap);  // packed: no padding
+  for (int e = tid; e < a.E; e += blockDim.x) {
+    const int adm = a.offsets ? 0 : min(__ldg(a.load + e), a.cap);
+    s_cnt[e] = (a.offsets || a.skip_pads) ? 0 : a.cap - adm;  // packed / local padding: none here
+    if (a.skip_pads && blockIdx.x == 0) {
+      const int q = e / a.E_local;
+      reinterpret_cast<int*>(a.ptab.p[q])[a.rank * kPadTabStride + (e - q * a.E_local)] = adm;
+    }
+  }
   __syncthreads();
   if (tid < 32) {
     int carry = 0;
