@@ -57,13 +57,18 @@ def _run(world, algo, G, port):
     return out
 
 
-@pytest.mark.parametrize("world,algo,G", [(2, "flat", 1), (2, "hier", 2), (2, "p2p", 1),
-                                          (4, "flat", 1), (4, "hier", 2), (4, "hier", 4),
-                                          (4, "p2p", 1)])
-def test_multi_gpu_route(orc, world, algo, G):
+@pytest.mark.parametrize("world,algo,G,env", [(2, "flat", 1, None), (2, "hier", 2, None),
+                                              (2, "p2p", 1, None), (2, "p2p", 1, "local_pad"),
+                                              (4, "flat", 1, None), (4, "hier", 2, None),
+                                              (4, "hier", 4, None), (4, "p2p", 1, None),
+                                              (4, "p2p", 1, "local_pad")])
+def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
-    out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo])
+    if env == "local_pad":   # the owners zero their own padding rows (inherited by the ranks)
+        monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
+    out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
+               (1 if env else 0))
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)
