@@ -892,9 +892,12 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.prefetch = env_int("MOE_LAYOUT_PREFETCH", 0);  // measured slower (C2 +3 us, C3 +11 us): off
   // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
   // ~100 KB per-CTA budget (two CTAs per SM)
-  // TMA bulk stores: slower than the register path into local HBM, faster
-  // into peers' memory over NVLink (C3 at P=2: 122 vs 132 us)
-  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", 1) : env_int("MOE_LAYOUT_TMA", 0);
+  // TMA bulk stores: slower than the register path into local HBM; into
+  // peers' memory over NVLink faster at P=2 (C3: 122 vs 132 us) and ~2%
+  // slower at P=4 (C2: 169.8 vs 166.6 us), so only for two ranks
+  const int P = E_local > 0 ? d.E / E_local : 1;
+  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", P <= 2 ? 1 : 0)
+                                  : env_int("MOE_LAYOUT_TMA", 0);
   const int budget = env_int("MOE_LAYOUT_TMA_SMEM", 100 * 1024);
   const int ns = std::min(16, (budget - a.row_bytes) / (kTmaWarps * std::max(1, a.row_bytes)));
   if (tma_env && a.row_bytes % 16 == 0 && ns >= 2) {
