@@ -248,6 +248,24 @@ __global__ void __launch_bounds__(256) k_pad_fill(char* recv, const int* tab, in
   }
 }
 
+static moe_status_t pad_fill_launch(moe_comm* comm, char* local, int El, int cap, int row_bytes,
+                                    cudaStream_t stream) {
+  const int P = comm->nranks;
+  const int nrows_pad_max = P * El * cap;
+  const int grid = std::max(1, std::min(device_sm_count() * 4, (nrows_pad_max + 7) / 8));
+  const int* tl = reinterpret_cast<const int*>(comm->sig.peer.p[comm->rank] + kPadTabOff);
+  int Pv = P, Elv = El, capv = cap, rb = row_bytes;
+  void* args[] = {&local, (void*)&tl, &Pv, &Elv, &capv, &rb};
+  cudaError_t e = launch_pdl((const void*)k_pad_fill, dim3(grid), dim3(256), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "k_pad_fill launch");
+  return MOE_OK;
+}
+
+// Local padding when at least ~5% of the rows are padding by construction.
+static bool pad_heavy(const moe_gate_desc_t* d) {
+  return (double)d->E * d->capacity > 1.05 * (double)d->S * d->k;
+}
+
 // ------------------------------------------------------------ dropless exchange
 // counts_q[r][le] = admitted rows of this rank r for q's local expert le
 // (stores into every owner's symmetric count table).
@@ -434,9 +452,8 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   // (E*cap > 1.05*S*k, e.g. the hash config's C = 1.25: C4b dispatch 165 ->
   // 132 us at N=2); with C = 1 the padding is only the imbalance and the
   // extra kernel costs more than it saves (C2: +1.7 us).
-  const bool pad_heavy = (double)desc->E * desc->capacity > 1.05 * (double)desc->S * desc->k;
   const bool local_pad = !(flags & MOE_P2P_NO_EXIT_BARRIER) && El <= kPadTabStride &&
-                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy ? 1 : 0);
+                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy(desc) ? 1 : 0);
   PeerPtrs tab{};
   for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
   s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, nullptr, nullptr,
@@ -445,16 +462,7 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
   if (s != MOE_OK || !local_pad) return s;
-  const int nrows_pad_max = P * El * desc->capacity;
-  const int grid = std::max(1, std::min(device_sm_count() * 4, (nrows_pad_max + 7) / 8));
-  char* rl = dst.p[comm->rank];
-  const int* tl = reinterpret_cast<const int*>(tab.p[comm->rank]);
-  int cap = desc->capacity, rb = d * ds;
-  int Pv = P, Elv = El;
-  void* args[] = {&rl, (void*)&tl, &Pv, &Elv, &cap, &rb};
-  cudaError_t e = launch_pdl((const void*)k_pad_fill, dim3(grid), dim3(256), 0, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_dispatch_p2p: k_pad_fill launch");
-  return MOE_OK;
+  return pad_fill_launch(comm, dst.p[comm->rank], El, desc->capacity, d * ds, stream);
 }
 
 moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -555,14 +563,24 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
     s = barrier_launch(comm->sig.peer, P, r, stream);
     if (s != MOE_OK) return s;
   }
-  // dy rows to the experts' owners (the dispatch kernel; padding rows zero)
-  s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, desc->E / P, r, stream);
+  // dy rows to the experts' owners (the dispatch kernel; padding rows zero,
+  // written by the owners themselves when padding is heavy)
+  const int El = desc->E / P;
+  const bool local_pad = El <= kPadTabStride && env_int("MOE_P2P_LOCAL_PAD", pad_heavy(desc) ? 1 : 0);
+  PeerPtrs tab{};
+  for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
+  s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, El, r, stream, nullptr, nullptr,
+                          local_pad ? &tab : nullptr);
   if (s != MOE_OK) return s;
   s = push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, nullptr, P, r, dtype, d * ds, 0,
                       stream);
   if (s != MOE_OK) return s;
   s = barrier_launch(comm->sig.peer, P, r, stream);  // rows and weights landed
   if (s != MOE_OK) return s;
+  if (local_pad) {
+    s = pad_fill_launch(comm, static_cast<char*>(d_expert_out), El, desc->capacity, d * ds, stream);
+    if (s != MOE_OK) return s;
+  }
   s = push_bwd_launch(*desc, *routing, wt, dwt, static_cast<char*>(d_expert_out),
                       static_cast<const char*>(expert_out), nullptr, P, r, dtype, d * ds, 1, stream);
   if (s != MOE_OK) return s;

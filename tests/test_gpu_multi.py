@@ -127,13 +127,15 @@ def _bwd_rank_main(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_backward_p2p(orc, world):
+@pytest.mark.parametrize("world,env", [(2, None), (2, "local_pad"), (4, None)])
+def test_multi_gpu_backward_p2p(orc, world, env, monkeypatch):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
+    if env == "local_pad":   # owners zero their own padding rows of the dy scatter
+        monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
-    port = 29700 + world
+    port = 29700 + world + (10 if env else 0)
     ps = [ctx.Process(target=_bwd_rank_main, args=(r, world, port, qu)) for r in range(world)]
     for p in ps:
         p.start()
