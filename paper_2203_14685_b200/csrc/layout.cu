@@ -995,8 +995,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   const int U = env_int("MOE_REVERSE_U", 1);
   // k <= 2 path: vectors per lane per round (x k rows); measured: 2 for
   // k = 2 (one 1 KiB segment of both rows: C2 36.3 -> 35.6 us), 4 for k = 1
-  const int KU = env_int("MOE_REVERSE_KU", d.k == 2 ? 2 : 4);
-  const bool kspec = env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
+  // (peer mode: 4 -- both 2 KiB rows in flight hide the NVLink latency better,
+  // C2 at P=2: 129.2 -> 127.3 us)
+  const int KU = env_int("MOE_REVERSE_KU", (d.k == 2 && E_local == d.E) ? 2 : 4);
+  const bool v16 = env_int("MOE_REVERSE_V16", 0) != 0;  // force 16-byte vectors (experiment)
+  const bool kspec = !v16 && env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
   if (kspec) {
     // TPW * k * U = KU (default 4) vectors in flight per lane, U covering at
     // most one row (1 KiB of row per U step)
@@ -1016,7 +1019,7 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     else
       kern = Uc >= 2 ? (T >= 2 ? MOE_RK(2, 2, 2) : MOE_RK(2, 2, 1)) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
 #undef MOE_RK
-  } else if (a.row_bytes % 32 == 0) {
+  } else if (a.row_bytes % 32 == 0 && !v16) {
     if (U == 1)
       kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
     else
