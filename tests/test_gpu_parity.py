@@ -154,6 +154,8 @@ LAYOUT_CASES = [
     dict(kind="topk", S=1500, E=16, k=4, d=2056, dtype="bf16", prio="slot", skew=1.0),
     dict(kind="topk", S=300, E=8, k=2, d=4096, dtype="f32", skew=40.0),
     dict(kind="topk", S=64, E=1, k=1, d=96, dtype="bf16"),
+    dict(kind="topk", S=1000, E=16, k=6, d=256, dtype="bf16", C=0.8),          # k > 4: inline dsts
+    dict(kind="ktop1", S=900, E=32, k=8, d=128, dtype="f32", mode="softmax"),  # 8 prototypes
 ]
 
 
