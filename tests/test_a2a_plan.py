@@ -139,7 +139,8 @@ def _worker(rank, world, algo, G, port, c, q):
 
 
 @pytest.mark.parametrize("world,algo,G", [(2, "flat", 1), (2, "hier", 1), (2, "hier", 2),
-                                          (4, "flat", 1), (4, "hier", 2)])
+                                          (4, "flat", 1), (4, "hier", 2),
+                                          (8, "hier", 4)])   # the paper's 4+4 split on 8 ranks
 def test_plan_executes_over_gloo(orc, world, algo, G):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
