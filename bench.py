@@ -535,6 +535,14 @@ def main():
             out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) &
                             ((ex // El) != rank)).sum().item())
             ab["a2a"] = out_rows * row
+    elif P > 1 and algo == "p2p" and w.E * cap > 1.05 * S * w.k and \
+            os.environ.get("MOE_P2P_LOCAL_PAD", "1") != "0":
+        # local padding: the zero rows are written by their
+        # owner, so only the admitted rows of other ranks' experts cross NVLink
+        El = w.E // P
+        ex = pipe.routing.expert_idx
+        out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) & ((ex // El) != rank)).sum().item())
+        ab["a2a"] = out_rows * row
     peak, peak_src = measured_peaks()
     traffic = None
     try:
