@@ -252,7 +252,8 @@ def main():
             algo = "p2p"
     try:
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
-                                 group_size=G, device=dev, dropless=a.dropless)
+                                 group_size=G, device=dev, dropless=a.dropless,
+                                 slot_src=os.environ.get("MOE_BENCH_SLOT_SRC", "1") != "0")
     except moe.MoeError as err:
         if algo != "p2p":
             raise

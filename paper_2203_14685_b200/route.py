@@ -294,6 +294,9 @@ class RoutePipeline:
                     self.step(logits, x, token_ids, table, expert, mark=mark)
                 graphs = g
             else:
+                if self.dropless or self.fuse:
+                    raise NotImplementedError("per-stage graphs cover the padded, unfused step; "
+                                              "use stages=False with events= instead")
                 r = self.routing
                 p2p = self.P > 1 and self.algo == "p2p"
                 fns = {
