@@ -26,9 +26,11 @@ def _rank_main(rank, world, algo, G, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     comm = moe.Comm.from_process_group()
     lg = synthgen.logits(synthgen.seed_for(9, rank, 1), S, E, K, skew=0.5)
-    x = synthgen.tokens(synthgen.seed_for(9, rank, 2), S, D, "bf16")
+    dts = os.environ.get("MOE_TEST_DTYPE", "bf16")
+    x = synthgen.tokens(synthgen.seed_for(9, rank, 2), S, D, dts)
     cap = moe.capacity(S, E, K, 1.0)
-    pipe = moe.RoutePipeline(S, D, E, K, cap, torch.bfloat16, comm=comm, algo=algo, group_size=G)
+    pipe = moe.RoutePipeline(S, D, E, K, cap, torch.bfloat16 if dts == "bf16" else torch.float32,
+                             comm=comm, algo=algo, group_size=G)
     pipe.step(dev(lg), dev(x), expert=False)     # identity expert: recv = dispatched rows
     torch.cuda.synchronize()
     recv = host(pipe.recv).copy()
@@ -59,6 +61,7 @@ def _run(world, algo, G, port):
 
 @pytest.mark.parametrize("world,algo,G,env", [(2, "flat", 1, None), (2, "hier", 2, None),
                                               (2, "p2p", 1, None), (2, "p2p", 1, "local_pad"),
+                                              (2, "p2p", 1, "f32"),
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
                                               (4, "p2p", 1, "local_pad")])
@@ -67,8 +70,11 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
         pytest.skip("needs %d GPUs" % world)
     if env == "local_pad":   # the owners zero their own padding rows (inherited by the ranks)
         monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
+    f32 = env == "f32"
+    if f32:                  # fp32 rows through the one-sided path
+        monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
-               (1 if env else 0))
+               {None: 0, "local_pad": 1, "f32": 2}[env])
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)
@@ -80,11 +86,11 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
         assert recv.tobytes() == recvs[r].tobytes()          # AllToAll bit-exact
         # identity expert, k=2 RENORM: y == combine of the original rows
         from gpu_util import as_f64, assert_y_close, combine_bound
-        assert_y_close(y_id, ys_id[r], combine_bound(as_f64(disp[r]), routings[r]), True)
+        assert_y_close(y_id, ys_id[r], combine_bound(as_f64(disp[r]), routings[r]), not f32)
         back = orc.alltoall_flat([orc.expert_scale(recvs[q].reshape(world, E // world, cap, D),
                                                    q * (E // world)).reshape(E, cap, D)
                                   for q in range(world)])[r]
-        assert_y_close(y, ys[r], combine_bound(as_f64(back), routings[r]), True)
+        assert_y_close(y, ys[r], combine_bound(as_f64(back), routings[r]), not f32)
 
 
 def _bwd_rank_main(rank, world, port, q):
