@@ -157,6 +157,17 @@ def algorithmic_bytes(w, S, cap, P, row):
     }
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ---------------------------------------------------------------- reference arm
 def oracle_step(orc, w, inputs, cap, P):
     xs = [i[3] for i in inputs]
@@ -206,7 +217,7 @@ def run_reference(a, w, world, rank):
         "config": {"workload": w.name, "S_per_rank": S_s, "d": w.d, "E": w.E, "k": w.k,
                    "gate": w.kind, "capacity_factor": w.C, "parallelism": "ep%d" % P},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -612,7 +623,8 @@ def main():
         cpu = {"value": S_s / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": "%d oracle steps (gate+layout+reverse, AllToAll identity at P=1) on "
                          "%d of %d tokens of %s, single thread pinned to one core; %d host cores "
-                         "present" % (n, S_s, w.S, w.name, os.cpu_count())}
+                         "present" % (n, S_s, w.S, w.name, os.cpu_count()),
+               "cpu_model": cpu_model()}
 
     # our kernels per step: gate (k_gate_select, k_gate_scan, k_gate_slots),
     # layout, reverse, on hierarchical leaders one chunk permute per AllToAll,
@@ -647,7 +659,7 @@ def main():
             "admitted_slots": admitted, "roofline": roof, "alltoall": a2a, "clocks": clocks,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches_per_step * a.steps,
             "backward": bwd,
-            "library": moe.version(),
+            "library": moe.version(), "gpu": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(out), flush=True)
     # CUDA graphs that captured NCCL work must go before the communicator
