@@ -72,6 +72,15 @@ __device__ __forceinline__ void st_v8(void* p, const V8& r) {
                "r"(r.w[7])
                : "memory");
 }
+// Store with an L2 evict-first policy (output that is not re-read soon).
+__device__ __forceinline__ void st_v8_ef(void* p, const V8& r) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+               "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3]), "r"(r.w[4]), "r"(r.w[5]),
+               "r"(r.w[6]), "r"(r.w[7]), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ V4 ld_stream_v4(const void* p) {
   V4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"

@@ -36,6 +36,10 @@ struct RowArgs {
   // rows earlier source ranks put there; 0 locally); no padding rows.
   const int32_t* offsets;
   const int32_t* peer_base;
+  // reverse only: walk the tokens from last to first (rev) -- the rows the
+  // layout wrote last are the ones still in L2 -- and store y evict-first
+  // (y_ef) so the stores do not push them out
+  int rev, y_ef;
   // padded one-sided dispatch with LOCAL padding: the senders skip the zero
   // rows and CTA 0 stores min(load, cap) of each owner's experts into the
   // owner's padding-count table (ptab.p[q] + [rank][le]); the owner zero-fills

@@ -96,7 +96,11 @@ GATE_CASES = [
 GATE_PATHS = {"fused": {"MOE_GATE_FUSED": "1"}, "two": {}, "three": {"MOE_GATE_TWO_MAXW": "0"},
               "fused_small_tiles": {"MOE_GATE_FUSED": "1", "MOE_GATE_FUSED_TILES": "512", "MOE_GATE_FUSED_MAXW": "1000000"}}
 ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"MOE_LAYOUT_U": "4", "MOE_REVERSE_KU": "4"}, "tma_layout": {"MOE_LAYOUT_TMA": "1"}, "tma_reverse": {"MOE_REVERSE_TMA": "1"}, "reverse_reg": {"MOE_REVERSE_TMA": "0", "MOE_REVERSE_TPW": "0"}, "no_prefetch": {"MOE_LAYOUT_PREFETCH": "0"}, "layout_tpw": {"MOE_LAYOUT_TPW": "1", "MOE_REVERSE_TPW": "1"},
-             "reverse_generic": {"MOE_REVERSE_KSPEC": "0"}, "reverse_u2": {"MOE_REVERSE_KU": "2"}}
+             "reverse_generic": {"MOE_REVERSE_KSPEC": "0"}, "reverse_u2": {"MOE_REVERSE_KU": "2"},
+             "forward_order": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_Y_EF": "0"},
+             "forward_order_tma": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_TMA": "1"},
+             "reverse_generic_fwd": {"MOE_REVERSE_KSPEC": "0", "MOE_REVERSE_BACKWARDS": "0"},
+             "reverse_v16": {"MOE_REVERSE_V16": "1"}}
 
 
 @pytest.mark.parametrize("path", sorted(GATE_PATHS))
