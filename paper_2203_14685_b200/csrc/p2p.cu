@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_a2a_p2p(const char* __restrict__ send, 
 moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_off_rank,
                             size_t bytes_per_peer, int nranks, int rank, cudaStream_t stream) {
   const size_t pieces = ((bytes_per_peer + 65535) / 65536) * nranks;
-  int grid = (int)std::min<size_t>(pieces, (size_t)device_sm_count() * 4);
+  int grid = (int)std::min<size_t>(pieces, (size_t)device_sm_count() * env_int("MOE_A2A_CTAS_PER_SM", 4));
   if (grid < 1) grid = 1;
   void* args[] = {(void*)&send, (void*)&recv, &recv_off_rank, &bytes_per_peer, &nranks, &rank};
   cudaError_t e = launch_pdl((const void*)k_a2a_p2p, dim3(grid), dim3(256), 0, stream, args);
