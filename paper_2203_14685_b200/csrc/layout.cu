@@ -987,9 +987,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   // TMA-staged combine (peer mode by default: rows come over NVLink)
   {
     const bool peer = E_local != d.E;
-    // measured: TMA staging wins for Switch (k = 1) on >= 4 KiB rows (C3:
-    // 48.5 vs 49.8 us), loses on 2 KiB rows (C4b: 69 vs 53 us) and over NVLink
-    const int tma_dflt = (!peer && a.k == 1 && a.row_bytes >= 4096) ? 1 : 0;
+    // measured: TMA staging won for Switch (k = 1) on >= 4 KiB rows in the
+    // forward walk (C3: 48.5 vs 49.8 us) but not with the reversed walk,
+    // where the register path finds the dispatch in L2 (C3: 40.0 vs 52.3 us);
+    // it loses on 2 KiB rows (C4b: 69 vs 53 us) and over NVLink.  Off.
+    const int tma_dflt = (!peer && a.k == 1 && a.row_bytes >= 4096 && !a.rev) ? 1 : 0;
     const int tma = peer ? env_int("MOE_P2P_REVERSE_TMA", 0) : env_int("MOE_REVERSE_TMA", tma_dflt);
     const int budget = env_int("MOE_REVERSE_TMA_SMEM", 100 * 1024);
     const int ns = std::min(16, budget / (kTmaWarps * std::max(1, a.row_bytes * a.k)));

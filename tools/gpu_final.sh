@@ -12,3 +12,7 @@ done
 for W in C3 C4a C4b; do
   timeout 300 python bench.py --steps 20 --warmup 5 --workload $W --no-e2e > gpurun_out/bench1_${TAG}_$W.json 2> gpurun_out/bench1_${TAG}_$W.err; echo bench1_$W=$? >> $S
 done
+# the combine in sequence with a warm L2 (no cache flush between kernels):
+# how much of the dispatch the reversed walk finds in L2
+B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-backward"
+timeout 600 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct -k regex:"k_(layout|reverse)" --csv --log-file gpurun_out/l2warm_$TAG.csv $B > gpurun_out/ncu_l2warm_$TAG.log 2>&1; echo ncu_l2warm=$? >> $S
