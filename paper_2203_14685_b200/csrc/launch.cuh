@@ -57,6 +57,13 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,
                                   const int32_t* offsets = nullptr,
                                   const int32_t* peer_base = nullptr);
+// At least ~5% of the padded rows are padding by construction (E*cap >
+// 1.05*S*k, e.g. the hash gate's C = 1.25): local padding over NVLink, and
+// the padding rows zeroed first in local mode (L2 order for the combine).
+inline bool pad_heavy(const moe_gate_desc_t& d) {
+  return (double)d.E * d.capacity > 1.05 * (double)d.S * d.k;
+}
+
 moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t* offsets,
                                    cudaStream_t stream);
 moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* dy,

@@ -261,11 +261,6 @@ static moe_status_t pad_fill_launch(moe_comm* comm, char* local, int El, int cap
   return MOE_OK;
 }
 
-// Local padding when at least ~5% of the rows are padding by construction.
-static bool pad_heavy(const moe_gate_desc_t* d) {
-  return (double)d->E * d->capacity > 1.05 * (double)d->S * d->k;
-}
-
 // ------------------------------------------------------------ dropless exchange
 // counts_q[r][le] = admitted rows of this rank r for q's local expert le
 // (stores into every owner's symmetric count table).
@@ -453,7 +448,7 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   // 132 us at N=2); with C = 1 the padding is only the imbalance and the
   // extra kernel costs more than it saves (C2: +1.7 us).
   const bool local_pad = !(flags & MOE_P2P_NO_EXIT_BARRIER) && El <= kPadTabStride &&
-                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy(desc) ? 1 : 0);
+                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
   PeerPtrs tab{};
   for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
   s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, nullptr, nullptr,
@@ -566,7 +561,7 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
   // dy rows to the experts' owners (the dispatch kernel; padding rows zero,
   // written by the owners themselves when padding is heavy)
   const int El = desc->E / P;
-  const bool local_pad = El <= kPadTabStride && env_int("MOE_P2P_LOCAL_PAD", pad_heavy(desc) ? 1 : 0);
+  const bool local_pad = El <= kPadTabStride && env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
   PeerPtrs tab{};
   for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
   s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, El, r, stream, nullptr, nullptr,

@@ -50,6 +50,10 @@ struct RowArgs {
   // prefetches of x (the rows do not depend on the routing), so x streams
   // in from HBM while the latency-bound gate runs
   int prefetch;
+  // layout only: zero the padding rows before the token rows, so the rows
+  // written last (still in L2 for the combine's reversed walk) are rows the
+  // combine reads
+  int pads_first;
 };
 
 // Bulk-prefetch this CTA's 1/gridDim share of [p, p + bytes) into L2 with an
@@ -185,6 +189,25 @@ __device__ __forceinline__ float row_weight(const RowArgs& a, size_t i) {
 }
 
 // Persistent grid: SMs x resident CTAs of `kern` at kRowThreads threads.
+// Zero-fill the padding rows [min(load_e, cap), cap) of every expert (the
+// prefix s_beg from pad_prefix), a warp per row, warps gw of nw.
+template <int VB>
+__device__ __forceinline__ void zero_pad_rows(const RowArgs& a, const int* s_beg, int gw, int nw) {
+  using V = Vec<VB>;
+  const int lane = threadIdx.x & 31;
+  const int npad = s_beg[a.E];
+  const typename V::T z = V::zero();
+  for (int p = gw; p < npad; p += nw) {
+    int lo = 0, hi = a.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    char* drow = dst_row_of(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
+    for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
+  }
+}
+
 inline int row_grid(const void* kern) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);

@@ -100,7 +100,7 @@ ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"MOE_LAYOUT_U": "4", "MOE_REVE
              "forward_order": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_Y_EF": "0"},
              "forward_order_tma": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_TMA": "1"},
              "reverse_generic_fwd": {"MOE_REVERSE_KSPEC": "0", "MOE_REVERSE_BACKWARDS": "0"},
-             "reverse_v16": {"MOE_REVERSE_V16": "1"}}
+             "reverse_v16": {"MOE_REVERSE_V16": "1"}, "pads_first": {"MOE_LAYOUT_PADS_FIRST": "1"}, "pads_last": {"MOE_LAYOUT_PADS_FIRST": "0"}}
 
 
 @pytest.mark.parametrize("path", sorted(GATE_PATHS))
