@@ -170,6 +170,7 @@ moe_status_t moe_comm_destroy(moe_comm_t* comm) {
   cudaDeviceSynchronize();
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
+  if (comm->dup.base) symm_release(comm, comm->dup);
   moe_status_t s = nccl_status(ncclCommDestroy(comm->nccl), "moe_comm_destroy");
   delete comm;
   return s;

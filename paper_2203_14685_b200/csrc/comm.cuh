@@ -39,6 +39,7 @@ struct moe_comm {
   int nranks, rank, device;
   std::vector<moe::SymmBuf> symm;  // live symmetric buffers
   moe::SymmBuf sig;                // barrier signals: [kMaxRanks] flags + local epoch
+  moe::SymmBuf dup{};              // one-sided dispatch: duplicate-row table (int32 per recv row)
   bool p2p_ok;                     // peer mappings could be made (NVLink / P2P)
 };
 

@@ -51,7 +51,13 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets = nullptr,
                                  const int32_t* peer_base = nullptr,
-                                 const PeerPtrs* pad_tab = nullptr);
+                                 const PeerPtrs* pad_tab = nullptr,
+                                 const PeerPtrs* dup_tab = nullptr);
+// The owner's half of the dispatch dedupe (RowArgs::dedupe): after the exit
+// barrier, copy every recv row whose table entry says "= row i" and clear
+// the entry.  tab: this rank's table, n_rows entries.
+moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_bytes,
+                             cudaStream_t stream);
 moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,

@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
         for (int j = 0; j < a.k; ++j) {
           const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
           if (s < 0) continue;
-          char* drow = dst_row_of(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
+          const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
+          if (j > 0 && dedupe_row(a, t, j, e, s, seg == 0 ? lane : 1)) continue;
+          char* drow = dst_row_of(a, e, s);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -436,7 +438,10 @@ __global__ void __launch_bounds__(kTmaThreads) k_layout_tma(TmaArgs ta) {
         for (int j = 0; j < kTmaMaxK; ++j) {
           if (j < a.k) {
             const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
-            if (s >= 0) dst[j] = dst_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
+            if (s >= 0) {
+              const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
+              if (j == 0 || !dedupe_row(a, t, j, e, s, 0)) dst[j] = dst_row(a, e, s);
+            }
           }
         }
       } else {
@@ -879,8 +884,13 @@ moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t*
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets,
-                                 const int32_t* peer_base, const PeerPtrs* pad_tab) {
+                                 const int32_t* peer_base, const PeerPtrs* pad_tab,
+                                 const PeerPtrs* dup_tab) {
   RowArgs a{};
+  if (dup_tab && !offsets) {
+    a.dedupe = 1;
+    a.dup = *dup_tab;
+  }
   if (pad_tab) {
     a.skip_pads = 1;
     a.ptab = *pad_tab;
@@ -907,12 +917,10 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.pads_first = env_int("MOE_LAYOUT_PADS_FIRST", E_local == d.E && pad_heavy(d) ? 1 : 0);
   // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
   // ~100 KB per-CTA budget (two CTAs per SM)
-  // TMA bulk stores: slower than the register path into local HBM; into
-  // peers' memory over NVLink faster at P=2 (C3: 122 vs 132 us) and ~2%
-  // slower at P=4 (C2: 169.8 vs 166.6 us), so only for two ranks
-  const int P = E_local > 0 ? d.E / E_local : 1;
-  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", P <= 2 ? 1 : 0)
-                                  : env_int("MOE_LAYOUT_TMA", 0);
+  // TMA bulk stores: slower than the register path into local HBM, and
+  // (re-measured at P=2 with the current barrier and dedupe) over NVLink
+  // too (C2 121.2 vs 117.5 us, C3 120.8 vs 118.1, C4b 129.9 vs 124.4): off
+  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", 0) : env_int("MOE_LAYOUT_TMA", 0);
   const int budget = env_int("MOE_LAYOUT_TMA_SMEM", 100 * 1024);
   const int ns = std::min(16, (budget - a.row_bytes) / (kTmaWarps * std::max(1, a.row_bytes)));
   if (tma_env && a.row_bytes % 16 == 0 && ns >= 2) {

@@ -261,6 +261,89 @@ static moe_status_t pad_fill_launch(moe_comm* comm, char* local, int El, int cap
   return MOE_OK;
 }
 
+// ------------------------------------------------------------ dispatch dedupe
+// Owner side: a warp per 32 table entries (coalesced), each nonzero entry
+// "= row v-1" copied by the warp (16-byte vectors, local HBM), then cleared
+// for the next step.  The entries were stored by the senders before their
+// exit barrier (release) and this kernel runs after it (acquire).
+__global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int kV = 8;  // 16-byte vectors per lane in flight: 4 KiB of a row per warp round
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  for (long long base = gw * 32; base < n; base += nw * 32) {
+    const long long i = base + lane;
+    const int v = i < n ? tab[i] : 0;
+    unsigned m = __ballot_sync(0xffffffffu, v != 0);
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      const long long src = (long long)__shfl_sync(0xffffffffu, v, l) - 1;
+      const char* sr = recv + src * row_bytes;
+      char* dr = recv + (base + l) * row_bytes;
+      for (int o0 = 0; o0 < row_bytes; o0 += 32 * 16 * kV) {
+        V4 r[kV];
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          const int off = o0 + (lane + 32 * u) * 16;
+          if (off < row_bytes) r[u] = ld_stream_v4(sr + off);
+        }
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          const int off = o0 + (lane + 32 * u) * 16;
+          if (off < row_bytes) st_v4(dr + off, r[u]);
+        }
+      }
+    }
+    if (v) tab[i] = 0;
+  }
+}
+
+moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_bytes,
+                             cudaStream_t stream) {
+  const long long groups = (n_rows + 31) / 32;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 7) / 8,
+                                                                    (long long)device_sm_count() * 4));
+  void* args[] = {&recv, &tab, &n_rows, &row_bytes};
+  cudaError_t e = launch_pdl((const void*)k_dup_fill, dim3(grid), dim3(256), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "k_dup_fill launch");
+  return MOE_OK;
+}
+
+// The duplicate-row table for a padded one-sided dispatch of E*cap recv
+// rows: used when k >= 2, two experts can share an owner (E/P >= 2) and the
+// exit barrier runs.  Allocated (collectively: every rank makes the same call)
+// on first use outside stream capture; inside a capture without a table the
+// dispatch just sends every row (same result).  nullptr: no dedupe.
+static const PeerPtrs* dup_table(moe_comm* c, const moe_gate_desc_t& d, int32_t flags,
+                                 cudaStream_t stream, moe_status_t* st) {
+  *st = MOE_OK;
+  const int P = c->nranks;
+  if (P < 2 || d.k < 2 || d.E / P < 2 || (flags & MOE_P2P_NO_EXIT_BARRIER) ||
+      !env_int("MOE_P2P_DEDUPE", 1))
+    return nullptr;
+  const size_t want = (size_t)d.E * d.capacity * sizeof(int);
+  if (c->dup.base && c->dup.bytes >= want) return &c->dup.peer;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  if (c->dup.base) {  // grow: every rank is done with the old table
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      *st = cuda_status(e, "dispatch dedupe table: sync");
+      return nullptr;
+    }
+    symm_release(c, c->dup);
+  }
+  *st = symm_alloc(c, want, &c->dup);
+  if (*st != MOE_OK) {
+    c->dup = SymmBuf{};
+    return nullptr;
+  }
+  return &c->dup.peer;
+}
+
 // ------------------------------------------------------------ dropless exchange
 // counts_q[r][le] = admitted rows of this rank r for q's local expert le
 // (stores into every owner's symmetric count table).
@@ -451,12 +534,20 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                          env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
   PeerPtrs tab{};
   for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
+  const PeerPtrs* dup = dup_table(comm, *desc, flags, stream, &s);
+  if (s != MOE_OK) return s;
   s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, nullptr, nullptr,
-                          local_pad ? &tab : nullptr);
+                          local_pad ? &tab : nullptr, dup);
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
-  if (s != MOE_OK || !local_pad) return s;
+  if (s != MOE_OK) return s;
+  if (dup) {
+    s = dup_fill_launch(dst.p[comm->rank], reinterpret_cast<int*>(dup->p[comm->rank]),
+                        (long long)desc->E * desc->capacity, d * ds, stream);
+    if (s != MOE_OK) return s;
+  }
+  if (!local_pad) return MOE_OK;
   return pad_fill_launch(comm, dst.p[comm->rank], El, desc->capacity, d * ds, stream);
 }
 
@@ -564,14 +655,22 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
   const bool local_pad = El <= kPadTabStride && env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
   PeerPtrs tab{};
   for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
+  // (a top-2 token's dy row goes once to an owner of both its experts)
+  const PeerPtrs* dup = dup_table(comm, *desc, 0, stream, &s);
+  if (s != MOE_OK) return s;
   s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, El, r, stream, nullptr, nullptr,
-                          local_pad ? &tab : nullptr);
+                          local_pad ? &tab : nullptr, dup);
   if (s != MOE_OK) return s;
   s = push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, nullptr, P, r, dtype, d * ds, 0,
                       stream);
   if (s != MOE_OK) return s;
   s = barrier_launch(comm->sig.peer, P, r, stream);  // rows and weights landed
   if (s != MOE_OK) return s;
+  if (dup) {
+    s = dup_fill_launch(static_cast<char*>(d_expert_out), reinterpret_cast<int*>(dup->p[r]),
+                        (long long)desc->E * desc->capacity, d * ds, stream);
+    if (s != MOE_OK) return s;
+  }
   if (local_pad) {
     s = pad_fill_launch(comm, static_cast<char*>(d_expert_out), El, desc->capacity, d * ds, stream);
     if (s != MOE_OK) return s;

@@ -54,6 +54,13 @@ struct RowArgs {
   // written last (still in L2 for the combine's reversed walk) are rows the
   // combine reads
   int pads_first;
+  // peer mode: a row going to the same remote owner as an earlier admitted
+  // row of the same token (top-2 with both experts on one peer) is not sent
+  // again; its recv row index gets "= row i" (i + 1) in the owner's table
+  // dup.p[q] (int32 per recv row) and the owner copies it locally after the
+  // exit barrier (k_dup_fill).
+  int dedupe;
+  PeerPtrs dup;
 };
 
 // Bulk-prefetch this CTA's 1/gridDim share of [p, p + bytes) into L2 with an
@@ -92,6 +99,26 @@ __device__ __forceinline__ const char* src_row(const RowArgs& a, int e, int s) {
 __device__ __forceinline__ char* dst_row_of(const RowArgs& a, int e, int s) {
   const int q = e / a.E_local;
   return a.dpeer.p[q] + row_index(a, q, e, s) * a.row_bytes;
+}
+
+// Dedupe (RowArgs::dedupe): if row j of token t (expert e, slot s, remote
+// owner q) duplicates an earlier admitted row j' < j of t on the same owner,
+// record it in q's table and return true (the caller skips the row).  Any
+// lane may call it; only lane 0 stores.
+__device__ __forceinline__ bool dedupe_row(const RowArgs& a, int t, int j, int e, int s, int lane) {
+  const int q = e / a.E_local;
+  if (!a.dedupe || q == a.rank) return false;
+  for (int jj = 0; jj < j; ++jj) {
+    const size_t i = (size_t)t * a.k + jj;
+    const int s2 = __ldg(a.slot_idx + i);
+    if (s2 < 0) continue;
+    const int e2 = __ldg(a.expert_idx + i);
+    if (e2 / a.E_local != q) continue;
+    if (lane == 0)
+      reinterpret_cast<int*>(a.dup.p[q])[row_index(a, q, e, s)] = (int)row_index(a, q, e2, s2) + 1;
+    return true;
+  }
+  return false;
 }
 
 template <int VB>

@@ -62,6 +62,7 @@ def _run(world, algo, G, port):
 @pytest.mark.parametrize("world,algo,G,env", [(2, "flat", 1, None), (2, "hier", 2, None),
                                               (2, "p2p", 1, None), (2, "p2p", 1, "local_pad"),
                                               (2, "p2p", 1, "f32"), (2, "p2p", 1, "rev"),
+                                              (2, "p2p", 1, "tma"), (2, "p2p", 1, "nodedupe"),
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
                                               (4, "p2p", 1, "local_pad")])
@@ -70,6 +71,10 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
         pytest.skip("needs %d GPUs" % world)
     if env == "local_pad":   # the owners zero their own padding rows (inherited by the ranks)
         monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
+    if env == "tma":         # TMA bulk-store dispatch (with the dedupe)
+        monkeypatch.setenv("MOE_P2P_LAYOUT_TMA", "1")
+    if env == "nodedupe":    # every row sent, even when a token's two experts share an owner
+        monkeypatch.setenv("MOE_P2P_DEDUPE", "0")
     if env == "rev":         # peer combine walking the tokens last to first
         monkeypatch.setenv("MOE_REVERSE_BACKWARDS", "1")
         monkeypatch.setenv("MOE_REVERSE_Y_EF", "1")
@@ -77,7 +82,7 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     if f32:                  # fp32 rows through the one-sided path
         monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
-               {None: 0, "local_pad": 1, "f32": 2, "rev": 3}[env])
+               {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "tma": 4, "nodedupe": 5}[env])
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)
