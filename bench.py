@@ -584,11 +584,19 @@ def main():
                 "unit": "GB/s", "frac": achieved / NVLINK_GBS, "traffic": None,
                 "algorithmic_bytes": ab["a2a"],
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md), 900 nominal"}
-    roof["per_kernel_gbs"] = {
-        "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
-        "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
-        "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9 if stage_ms["reverse"] > 1e-3
-        else None}
+    if fused:
+        # the layout / reverse stages ARE the NVLink dispatch / combine (the
+        # "reverse" and "a2a_dispatch" marks are empty stages: event resolution)
+        roof["per_kernel_gbs"] = {
+            "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+            "k_layout (peer dispatch), NVLink per direction": ab["a2a"] / (stage_ms["layout"] / 1e3) / 1e9,
+            "k_reverse (peer combine), NVLink per direction":
+                ab["a2a"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
+    else:
+        roof["per_kernel_gbs"] = {
+            "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+            "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
+            "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9}
     a2a = None
     if P > 1:
         if fused:
