@@ -419,7 +419,11 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
  * every admitted row read straight from its owner rank q's `expert_out` over
  * NVLink (fp32 accumulate in ascending j, one RNE store, 0 if all slots
  * dropped), then moe_comm_barrier (the buffers may be reused).  Same result
- * as moe_alltoall(FLAT) back + moe_reverse_layout.  expert_out: symmetric,
+ * as moe_alltoall(FLAT) back + moe_reverse_layout.  MOE_P2P_NO_ENTRY_BARRIER
+ * is ignored when the last moe_dispatch_p2p into expert_out sent a token's
+ * rows for one owner once (k >= 2, E/P >= 2, MOE_P2P_DEDUPE): its owners
+ * copy the duplicates after the dispatch's exit barrier, so the entry
+ * barrier is what orders those copies before the reads.  expert_out: symmetric,
  * [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,

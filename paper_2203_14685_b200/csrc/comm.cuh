@@ -40,6 +40,8 @@ struct moe_comm {
   std::vector<moe::SymmBuf> symm;  // live symmetric buffers
   moe::SymmBuf sig;                // barrier signals: [kMaxRanks] flags + local epoch
   moe::SymmBuf dup{};              // one-sided dispatch: duplicate-row table (int32 per recv row)
+  const void* dup_recv = nullptr;  // recv of the last dispatch whose owners fill duplicate rows
+                                   // after its exit barrier (the combine must not skip its entry one)
   bool p2p_ok;                     // peer mappings could be made (NVLink / P2P)
 };
 

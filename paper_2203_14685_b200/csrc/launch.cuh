@@ -62,7 +62,7 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,
                                   const int32_t* offsets = nullptr,
-                                  const int32_t* peer_base = nullptr);
+                                  const int32_t* peer_base = nullptr, int dup_alias = 0);
 // At least ~5% of the padded rows are padding by construction (E*cap >
 // 1.05*S*k, e.g. the hash gate's C = 1.25): local padding over NVLink, and
 // the padding rows zeroed first in local mode (L2 order for the combine).

@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         if (s0 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
           w0 = row_weight(a, (size_t)t * a.k + j);
-          const char* b = src_row(a, e, s0);
+          const char* b = src_row_item(a, t, j, e, s0);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
         if (s1 >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * a.k + j + 1);
           w1 = row_weight(a, (size_t)t * a.k + j + 1);
-          const char* b = src_row(a, e, s1);
+          const char* b = src_row_item(a, t, j + 1, e, s1);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
@@ -572,7 +572,9 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
 // instead of U*16.  Switch (k = 1) on 4 KiB rows: U = 4; on 2 KiB rows:
 // U = 2, TPW = 2.  Same arithmetic order as k_reverse: fp32 FMA from 0 in
 // ascending j, one RNE store.
-template <int DT, int KK, int U, int TPW>
+// AL (k = 2, alias-mode NVLink combine only): a token's two slots may name
+// the same row, which is then loaded once.
+template <int DT, int KK, int U, int TPW, bool AL = false>
 __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   constexpr int VB = 32;
   constexpr int NA = DT == MOE_F32 ? 8 : 16;
@@ -594,10 +596,16 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
         b[p][j] = nullptr;
         w[p][j] = 0.f;
         if (s >= 0) {
-          b[p][j] = src_row(a, __ldg(a.expert_idx + (size_t)t * KK + j), s);
+          const int e = __ldg(a.expert_idx + (size_t)t * KK + j);
+          b[p][j] = AL ? src_row_item(a, t, j, e, s) : src_row(a, e, s);
           w[p][j] = row_weight(a, (size_t)t * KK + j);
         }
       }
+    // alias-mode combine (src_row_item): both slots of a token may name the
+    // same row (sent once by the deduped dispatch); it is loaded once
+    bool dup1[TPW];
+#pragma unroll
+    for (int p = 0; p < TPW; ++p) dup1[p] = AL && KK == 2 && b[p][KK - 1] == b[p][0];
     for (int seg = 0; seg < a.row_bytes; seg += SEG) {
       V8 r[TPW][KK][U];
 #pragma unroll
@@ -607,8 +615,18 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
-            if (b[p][j] && off < a.row_bytes) r[p][j][u] = ld_stream_v8(b[p][j] + off);
+            if (b[p][j] && off < a.row_bytes && !(j == 1 && dup1[p]))
+              r[p][j][u] = ld_stream_v8(b[p][j] + off);
           }
+      if constexpr (AL) {
+#pragma unroll
+        for (int p = 0; p < TPW; ++p)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              r[p][KK - 1][u].w[q] = dup1[p] ? r[p][0][u].w[q] : r[p][KK - 1][u].w[q];
+      }
 #pragma unroll
       for (int p = 0; p < TPW; ++p) {
         if (tb + p >= a.S) break;
@@ -685,7 +703,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_reverse_tma(TmaArgs ta) {
           if (j < a.k && tl < end) {
             const int sl = __ldg(a.slot_idx + (size_t)t * a.k + j);
             if (sl >= 0) {
-              src[j] = src_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), sl);
+              src[j] = src_row_item(a, t, j, __ldg(a.expert_idx + (size_t)t * a.k + j), sl);
               wt[j] = row_weight(a, (size_t)t * a.k + j);
             }
           }
@@ -773,7 +791,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
         if (s < 0) continue;
         const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
         const float w = row_weight(a, (size_t)t * a.k + j);
-        const V4 v = ld_stream_v4(src_row(a, e, s) + off);
+        const V4 v = ld_stream_v4(src_row_item(a, t, j, e, s) + off);
         if constexpr (DT == MOE_F32) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[q] = fmaf(w, __uint_as_float(v.w[q]), acc[q]);
@@ -972,8 +990,10 @@ moe_status_t layout_launch(const moe_gate_desc_t& d, const moe_routing_t& r, con
 moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,
-                                  const int32_t* offsets, const int32_t* peer_base) {
+                                  const int32_t* offsets, const int32_t* peer_base,
+                                  int dup_alias) {
   RowArgs a{};
+  a.dedupe = dup_alias;  // reverse: read deduped slots from their first row (src_row_item)
   a.offsets = offsets;
   a.peer_base = peer_base;
   a.dst = static_cast<char*>(y);
@@ -1050,6 +1070,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
       kern = Uc == 4 ? (T >= 2 ? MOE_RK(1, 4, 2) : MOE_RK(1, 4, 1))
              : Uc == 2 ? (T >= 4 ? MOE_RK(1, 2, 4) : T >= 2 ? MOE_RK(1, 2, 2) : MOE_RK(1, 2, 1))
                        : (T >= 4 ? MOE_RK(1, 1, 4) : T >= 2 ? MOE_RK(1, 1, 2) : MOE_RK(1, 1, 1));
+    else if (a.dedupe)  // alias-mode NVLink combine
+      kern = Uc >= 2 ? (f ? (const void*)k_reverse_k<MOE_F32, 2, 2, 1, true>
+                          : (const void*)k_reverse_k<MOE_BF16, 2, 2, 1, true>)
+                     : (f ? (const void*)k_reverse_k<MOE_F32, 2, 1, 1, true>
+                          : (const void*)k_reverse_k<MOE_BF16, 2, 1, 1, true>);
     else
       kern = Uc >= 2 ? (T >= 2 ? MOE_RK(2, 2, 2) : MOE_RK(2, 2, 1)) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
 #undef MOE_RK

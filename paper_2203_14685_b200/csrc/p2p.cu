@@ -495,11 +495,22 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     return MOE_ERR_INVALID_ARG;
   }
   const int P = comm->nranks;
-  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // every rank's expert is done
+  // A dispatch that sent duplicate rows once left their copies to the owners
+  // (k_dup_fill after its exit barrier): reading recv before every owner got
+  // there races with those copies, so the entry barrier is kept then.
+  // With NO_ENTRY_BARRIER, recv still holds exactly what the dispatch sent,
+  // so the combine reads such a slot from the row that was sent (alias mode,
+  // default) instead of waiting for the copies (MOE_P2P_COMBINE_ALIAS=0).
+  const bool dup_pending = comm->dup_recv && comm->dup_recv == expert_out;
+  comm->dup_recv = nullptr;
+  const bool no_entry = flags & MOE_P2P_NO_ENTRY_BARRIER;
+  const int alias = dup_pending && no_entry && env_int("MOE_P2P_COMBINE_ALIAS", 1) ? 1 : 0;
+  if (!no_entry || (dup_pending && !alias)) {  // every rank's expert is done
     s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
     if (s != MOE_OK) return s;
   }
-  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream);
+  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream,
+                           nullptr, nullptr, alias);
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
   return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // nobody reads them any more
@@ -546,6 +557,7 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     s = dup_fill_launch(dst.p[comm->rank], reinterpret_cast<int*>(dup->p[comm->rank]),
                         (long long)desc->E * desc->capacity, d * ds, stream);
     if (s != MOE_OK) return s;
+    comm->dup_recv = recv;
   }
   if (!local_pad) return MOE_OK;
   return pad_fill_launch(comm, dst.p[comm->rank], El, desc->capacity, d * ds, stream);

@@ -121,6 +121,28 @@ __device__ __forceinline__ bool dedupe_row(const RowArgs& a, int t, int j, int e
   return false;
 }
 
+// Reverse source row of item (t, j) at (e, s).  With RowArgs::dedupe set on
+// a peer-mode combine that runs before the owners' duplicate-row copies
+// (moe_combine_p2p with NO_ENTRY_BARRIER after a deduped dispatch), a row
+// the dispatch sent once for two slots of t is read from the first slot's
+// row: recv still holds exactly what the dispatch sent, so the bytes are the
+// same and the owner's copy into the second row is not waited for.
+__device__ __forceinline__ const char* src_row_item(const RowArgs& a, int t, int j, int e, int s) {
+  if (a.dedupe) {
+    const int q = e / a.E_local;
+    if (q != a.rank) {
+      for (int jj = 0; jj < j; ++jj) {
+        const size_t i = (size_t)t * a.k + jj;
+        const int s2 = __ldg(a.slot_idx + i);
+        if (s2 < 0) continue;
+        const int e2 = __ldg(a.expert_idx + i);
+        if (e2 / a.E_local == q) return src_row(a, e2, s2);
+      }
+    }
+  }
+  return src_row(a, e, s);
+}
+
 template <int VB>
 struct Vec;
 template <>

@@ -63,6 +63,8 @@ def _run(world, algo, G, port):
                                               (2, "p2p", 1, None), (2, "p2p", 1, "local_pad"),
                                               (2, "p2p", 1, "f32"), (2, "p2p", 1, "rev"),
                                               (2, "p2p", 1, "tma"), (2, "p2p", 1, "nodedupe"),
+                                              (2, "p2p", 1, "f32_noalias"), (2, "p2p", 1, "noalias"),
+                                              (4, "p2p", 1, "f32"),
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
                                               (4, "p2p", 1, "local_pad")])
@@ -78,11 +80,14 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     if env == "rev":         # peer combine walking the tokens last to first
         monkeypatch.setenv("MOE_REVERSE_BACKWARDS", "1")
         monkeypatch.setenv("MOE_REVERSE_Y_EF", "1")
-    f32 = env == "f32"
+    if env in ("noalias", "f32_noalias"):   # the combine waits for the owners' duplicate copies
+        monkeypatch.setenv("MOE_P2P_COMBINE_ALIAS", "0")
+    f32 = env in ("f32", "f32_noalias")
     if f32:                  # fp32 rows through the one-sided path
         monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
-               {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "tma": 4, "nodedupe": 5}[env])
+               {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "tma": 4, "nodedupe": 5,
+                "f32_noalias": 7, "noalias": 8}[env] + (40 if env and world == 4 else 0))
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)
