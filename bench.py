@@ -555,6 +555,26 @@ def main():
         ex = pipe.routing.expert_idx
         out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) & ((ex // El) != rank)).sum().item())
         ab["a2a"] = out_rows * row
+    if P > 1 and algo == "p2p" and not a.dropless and w.k >= 2 and w.E // P >= 2 and \
+            os.environ.get("MOE_P2P_DEDUPE", "1") != "0":
+        # dedupe: a token's row crosses NVLink once per remote
+        # owner, however many of its slots that owner holds; the alias-mode
+        # combine reads it once too.  Padding rows cross unless padded locally.
+        El = w.E // P
+        ex, sl = pipe.routing.expert_idx.view(S, w.k), pipe.routing.slot_idx.view(S, w.k)
+        own = torch.where((ex >= 0) & (sl >= 0), ex // El, torch.full_like(ex, -1))
+        owners = torch.zeros((S, P), dtype=torch.bool, device=own.device)
+        for j in range(w.k):
+            m = own[:, j] >= 0
+            owners[torch.nonzero(m).squeeze(1), own[m, j].long()] = True
+        owners[:, rank] = False
+        pairs = int(owners.sum().item())
+        pads = 0
+        if not (w.E * cap > 1.05 * S * w.k and os.environ.get("MOE_P2P_LOCAL_PAD", "1") != "0"):
+            load = pipe.routing.load.view(P, El)
+            pads = int((cap - load.clamp(max=cap)).sum().item() - (cap - load[rank].clamp(max=cap)).sum().item())
+        ab["a2a_buffer"] = ab["a2a"]
+        ab["a2a"] = (pairs + pads) * row
     peak, peak_src = measured_peaks()
     traffic = None
     try:
@@ -606,6 +626,10 @@ def main():
             bw = {s_: ab["a2a"] / (stage_ms[s_] / 1e3) / 1e9 for s_ in ("a2a_dispatch", "a2a_combine")}
         a2a = {"bytes_out_per_rank": ab["a2a"], "busbw_gbs": bw, "peak_gbs": NVLINK_GBS,
                "algo": algo, "group_size": G if algo == "hier" else None}
+        if "a2a_buffer" in ab:
+            a2a["buffer_bytes_per_rank"] = ab["a2a_buffer"]
+            a2a["note"] = ("bytes_out_per_rank counts each token row once per remote owner "
+                           "(deduped dispatch, alias-mode combine) plus the padding rows")
         a2a["frac"] = min(bw.values()) / NVLINK_GBS
 
     # ---- CPU baseline: the oracle, rank 0, N=1 only, bounded sample
