@@ -25,6 +25,7 @@ def _rank_main(rank, world, algo, G, port, q):
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     comm = moe.Comm.from_process_group()
+    K = int(os.environ.get("MOE_TEST_K", "2"))
     lg = synthgen.logits(synthgen.seed_for(9, rank, 1), S, E, K, skew=0.5)
     dts = os.environ.get("MOE_TEST_DTYPE", "bf16")
     x = synthgen.tokens(synthgen.seed_for(9, rank, 2), S, D, dts)
@@ -64,7 +65,8 @@ def _run(world, algo, G, port):
                                               (2, "p2p", 1, "f32"), (2, "p2p", 1, "rev"),
                                               (2, "p2p", 1, "tma"), (2, "p2p", 1, "nodedupe"),
                                               (2, "p2p", 1, "f32_noalias"), (2, "p2p", 1, "noalias"),
-                                              (4, "p2p", 1, "f32"),
+                                              (4, "p2p", 1, "f32"), (2, "p2p", 1, "k4"),
+                                              (2, "p2p", 1, "k4_f32"),
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
                                               (4, "p2p", 1, "local_pad")])
@@ -82,12 +84,16 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
         monkeypatch.setenv("MOE_REVERSE_Y_EF", "1")
     if env in ("noalias", "f32_noalias"):   # the combine waits for the owners' duplicate copies
         monkeypatch.setenv("MOE_P2P_COMBINE_ALIAS", "0")
-    f32 = env in ("f32", "f32_noalias")
+    K = 2
+    if env in ("k4", "k4_f32"):  # k = 4: the generic peer combine (alias mode, rows read per slot)
+        K = 4
+        monkeypatch.setenv("MOE_TEST_K", "4")
+    f32 = env in ("f32", "f32_noalias", "k4_f32")
     if f32:                  # fp32 rows through the one-sided path
         monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
                {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "tma": 4, "nodedupe": 5,
-                "f32_noalias": 7, "noalias": 8}[env] + (40 if env and world == 4 else 0))
+                "f32_noalias": 7, "noalias": 8, "k4": 9, "k4_f32": 10}[env] + (40 if env and world == 4 else 0))
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)
