@@ -58,7 +58,8 @@ struct RowArgs {
   // row of the same token (top-2 with both experts on one peer) is not sent
   // again; its recv row index gets "= row i" (i + 1) in the owner's table
   // dup.p[q] (int32 per recv row) and the owner copies it locally after the
-  // exit barrier (k_dup_fill).
+  // exit barrier (k_dup_fill).  Reverse (peer combine): alias mode, see
+  // src_row_item.
   int dedupe;
   PeerPtrs dup;
 };
