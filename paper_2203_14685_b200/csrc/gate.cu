@@ -210,14 +210,14 @@ static int fused_tiles() { return env_int("MOE_GATE_FUSED_TILES", 128); }
 // fused single launch is off by default): 2 (select -> slots2) or 3.
 int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
   if (env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH) return -1;  // decided at launch
-  const GatePlan p = gate_plan(d, 256, ngroups);
+  const GatePlan p = gate_plan_default(d, ngroups);
   return (long long)p.n_tiles * p.ncols <= env_int("MOE_GATE_TWO_MAXW", 4096) ? 2 : 3;
 }
 
 size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
   // room for every tile count the knobs may pick (the table is small)
-  return std::max({gate_plan(d, gate_tiles()).bytes, gate_plan(d, fused_tiles()).bytes,
-                   gate_plan(d, 1024).bytes});
+  return std::max({gate_plan_default(d).bytes, gate_plan(d, gate_tiles()).bytes,
+                   gate_plan(d, fused_tiles()).bytes, gate_plan(d, 1024).bytes});
 }
 
 // The three-kernel path (k_gate_select -> k_gate_scan -> k_gate_slots, PDL).
@@ -286,7 +286,7 @@ moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
                                 const moe_routing_t& out, void* ws, cudaStream_t stream,
                                 GateFinalize* fin) {
   const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
-  const GatePlan p = gate_plan(d, gate_tiles(), ng);
+  const GatePlan p = gate_plan_default(d, ng);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
@@ -331,7 +331,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
   const GatePlan pf = gate_plan(d, fused_tiles(), ng);
   bool fused = env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH &&
                (long long)pf.n_tiles * pf.ncols <= env_int("MOE_GATE_FUSED_MAXW", 8192);
-  const GatePlan p = fused ? pf : gate_plan(d, gate_tiles(), ng);
+  const GatePlan p = fused ? pf : gate_plan_default(d, ng);
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
@@ -379,7 +379,7 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fk, kGateThreads, fsmem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: fused occupancy");
     if (p.n_tiles > per_sm * device_sm_count()) {
-      const GatePlan p3 = gate_plan(d, gate_tiles(), ng);
+      const GatePlan p3 = gate_plan_default(d, ng);
       a.tile_tokens = p3.tile_tokens;
       a.n_tiles = p3.n_tiles;
       a.lg_words = p3.lg_words;

@@ -65,16 +65,26 @@ inline int choose_lanes(int E) {
 }
 
 inline int gate_tiles() { return env_int("MOE_GATE_TILES", 256); }
+// Largest tile of the select -> (scan ->) slots path for the logit gates:
+// 128 tokens (S = 64K: 512 tiles; measured C4a gate 22.6 -> 21.4 us, step
+// 148 -> 145 us vs 256-token tiles; C2/C3 already get 128-token tiles from the
+// >= 256 tiles rule).  The hash gate stages no logits and keeps 256 (C4b: gate
+// unchanged, step 97.2 vs 98.3 us with 128).
+inline int gate_max_tile(int kind) {
+  return env_int("MOE_GATE_MAX_TILE", kind == MOE_GATE_HASH ? 256 : 128);
+}
 
 // want_tiles: the three-kernel path wants >= 256 tiles when S allows (about
 // 1.7 CTAs per SM on 148 SMs); the single-launch path fewer, larger tiles
 // (every CTA reduces all tiles' aggregates after its grid barrier).
-inline GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles, int ngroups = 1) {
+inline GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles, int ngroups = 1,
+                          int max_tile = 256) {
   GatePlan p{};
   p.L = d.kind == MOE_GATE_HASH ? 1 : choose_lanes(d.kind == MOE_GATE_SAM ? d.E / std::max(1, ngroups) : d.E);
   p.K = d.k <= 1 ? 1 : d.k <= 2 ? 2 : d.k <= 4 ? 4 : d.k <= 8 ? 8 : 0;
   // tiles of 32..256 tokens, at most kMaxTileItems items per tile
   int tt = 256;
+  while (tt > 32 && tt > max_tile) tt >>= 1;
   while (tt > 32 && (d.S + tt - 1) / tt < want_tiles) tt >>= 1;
   while (tt > 1 && tt * d.k > kMaxTileItems) tt >>= 1;
   // the staged logits tile stays within kMaxTileLogitBytes of shared memory
@@ -92,6 +102,11 @@ inline GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles, int ngroups 
   p.z_words = d.kind == MOE_GATE_D2S ? 2 * tt * d.E : 0;
   p.smem = sizeof(int) * (p.lg_words + p.z_words + 2 * items + (size_t)kGateWarps * p.ncols);
   return p;
+}
+
+// The plan of the default (non-cooperative) gate launch.
+inline GatePlan gate_plan_default(const moe_gate_desc_t& d, int ngroups = 1) {
+  return gate_plan(d, gate_tiles(), ngroups, gate_max_tile(d.kind));
 }
 
 // ------------------------------------------------------------ selection

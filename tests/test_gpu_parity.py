@@ -94,6 +94,9 @@ GATE_CASES = [
 
 # kernel variants selected by the library's tuning knobs (read per call)
 GATE_PATHS = {"fused": {"MOE_GATE_FUSED": "1"}, "two": {}, "three": {"MOE_GATE_TWO_MAXW": "0"},
+              "two_forced": {"MOE_GATE_TWO_MAXW": "1000000"},
+              "tile256": {"MOE_GATE_MAX_TILE": "256", "MOE_GATE_TILES": "1"},
+              "tile32": {"MOE_GATE_MAX_TILE": "32"},
               "fused_small_tiles": {"MOE_GATE_FUSED": "1", "MOE_GATE_FUSED_TILES": "512", "MOE_GATE_FUSED_MAXW": "1000000"}}
 ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"MOE_LAYOUT_U": "4", "MOE_REVERSE_KU": "4"}, "tma_layout": {"MOE_LAYOUT_TMA": "1"}, "tma_reverse": {"MOE_REVERSE_TMA": "1"}, "reverse_reg": {"MOE_REVERSE_TMA": "0", "MOE_REVERSE_TPW": "0"}, "no_prefetch": {"MOE_LAYOUT_PREFETCH": "0"}, "layout_tpw": {"MOE_LAYOUT_TPW": "1", "MOE_REVERSE_TPW": "1"},
              "reverse_generic": {"MOE_REVERSE_KSPEC": "0"}, "reverse_u2": {"MOE_REVERSE_KU": "2"},
