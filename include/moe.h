@@ -48,7 +48,8 @@ typedef enum {
   MOE_ERR_ALIGNMENT = 3,   /* pointer or row size not 16-byte aligned        */
   MOE_ERR_WORKSPACE = 4,   /* workspace NULL or smaller than *_workspace_bytes */
   MOE_ERR_CUDA = 5,        /* a CUDA launch / runtime call failed            */
-  MOE_ERR_NCCL = 6         /* an NCCL call failed                            */
+  MOE_ERR_NCCL = 6,        /* an NCCL call failed                            */
+  MOE_ERR_TIMEOUT = 7      /* a device barrier gave up waiting for a peer    */
 } moe_status_t;
 
 typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype_t;
@@ -83,8 +84,18 @@ typedef enum { MOE_PRIO_TOKEN = 0, MOE_PRIO_SLOT = 1 } moe_priority_t;
  *                 `group_size` consecutive ranks on one box (Fig. 6, R13)
  *   P2P         : one-sided: SM stores straight into the peers' receive
  *                 buffers over NVLink (recv must be a symmetric buffer,
- *                 moe_comm_symm_alloc), between two device-side barriers */
-typedef enum { MOE_A2A_FLAT = 0, MOE_A2A_HIER_LEADER = 1, MOE_A2A_P2P = 2 } moe_a2a_algo_t;
+ *                 moe_comm_symm_alloc), between two device-side barriers
+ *   HIER_2D     : two-level decoupled form: an exchange inside
+ *                 each group of `group_size` ranks, then one aggregated
+ *                 message per group pair between ranks of equal local index
+ *                 (every rank works; no leader), R21.
+ * (SURVEY §8(b) numbered HIER_2D 2; P2P took slot 2 first.) */
+typedef enum {
+  MOE_A2A_FLAT = 0,
+  MOE_A2A_HIER_LEADER = 1,
+  MOE_A2A_P2P = 2,
+  MOE_A2A_HIER_2D = 3
+} moe_a2a_algo_t;
 
 /* Gate problem description.  Enums are carried as int32 for a fixed ABI. */
 typedef struct {
@@ -351,8 +362,26 @@ moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank,
 moe_status_t moe_comm_destroy(moe_comm_t* comm);
 moe_status_t moe_comm_size(const moe_comm_t* comm, int32_t* nranks, int32_t* rank);
 
-/* host.  Device workspace moe_alltoall needs (0 for FLAT; for HIER_LEADER the
- * leader's staging, 2 * group_size * nranks * bytes_per_peer). */
+/* host, SYNCHRONISES `stream` (the stream the communicator's calls use).
+ * Failure detection: MOE_OK, or
+ *   MOE_ERR_TIMEOUT -- a device barrier of this rank waited longer than the
+ *     tuning's barrier_timeout_ms for a peer (a rank died, hung, or skipped
+ *     a matching call) and gave up; the stream went on with incomplete
+ *     data and the ranks' barrier epochs are out of step: the communicator
+ *     is unusable (moe_comm_abort).  The condition is sticky.
+ *   MOE_ERR_NCCL -- ncclCommGetAsyncError reports an error.
+ * A bounded barrier cannot hang the stream; an NCCL collective waiting on
+ * a dead peer can: call moe_comm_abort from another host thread. */
+moe_status_t moe_comm_check(moe_comm_t* comm, moe_stream_t stream);
+
+/* host.  ncclCommAbort (unblocks this rank's NCCL kernels), then releases
+ * the symmetric buffers and frees comm, without waiting for the peers. */
+moe_status_t moe_comm_abort(moe_comm_t* comm);
+
+/* host.  Device workspace moe_alltoall needs (0 for FLAT and P2P; for
+ * HIER_LEADER the leader's staging, 2 * group_size * nranks * bytes_per_peer
+ * (members need none); for HIER_2D 2 * nranks * bytes_per_peer on every
+ * rank).  (SURVEY §8(b) took the communicator; this takes its size.) */
 size_t moe_alltoall_workspace_bytes(int32_t nranks, int32_t algo, int32_t group_size,
                                     size_t bytes_per_peer);
 
@@ -368,12 +397,15 @@ size_t moe_alltoall_workspace_bytes(int32_t nranks, int32_t algo, int32_t group_
  * their leader (local rank 0) sub-messages addressed by destination group,
  * (3) leaders exchange one aggregated message per group pair (B*G/N bytes,
  * PAPER.md:213), (4) the leader permutes chunks by destination device, (5)
- * scatters.  Result byte-identical to FLAT (R13).
+ * scatters.  HIER_2D: (0) local transpose [dst group][dst local] ->
+ * [dst local][dst group], (1) exchange inside the group, (2) local
+ * transpose, (3) one message of group_size chunks (B*G/P bytes) to the rank
+ * of equal local index in every group.  Results byte-identical to FLAT (R13).
  * Collective: every rank must call it with the same algo, group_size and
  * bytes_per_peer, in the same order relative to its other NCCL calls.
  * send != recv when nranks > 1 (nranks == 1: a device copy, or nothing if
  * send == recv).  Errors: INVALID_ARG (nranks % group_size, in-place),
- * WORKSPACE (HIER_LEADER on a leader), NCCL. */
+ * WORKSPACE (HIER_LEADER on a leader, HIER_2D), NCCL. */
 moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size,
                           const void* send, void* recv, size_t bytes_per_peer,
                           void* ws, size_t ws_bytes, moe_stream_t stream);
@@ -396,13 +428,31 @@ moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* local);
  * buffers) are visible to every rank after it. */
 moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream);
 
-/* Barrier flags of moe_dispatch_p2p / moe_combine_p2p (default 0: both).
- * The entry barrier guarantees no rank writes into (dispatch) or reads from
- * (combine) a peer's buffer before that peer's stream reached the call; the
- * exit barrier that every store landed (dispatch) / every read finished
- * (combine).  A caller that orders its steps itself may skip redundant ones,
- * e.g. dispatch(NO_ENTRY) after a combine with its exit barrier. */
-enum { MOE_P2P_NO_ENTRY_BARRIER = 1, MOE_P2P_NO_EXIT_BARRIER = 2 };
+/* Flags of the one-sided calls (default 0: both barriers, no assumption).
+ * MOE_P2P_NO_ENTRY_BARRIER / MOE_P2P_NO_EXIT_BARRIER skip the entry / exit
+ * device barrier.  The entry barrier guarantees no rank writes into
+ * (dispatch) or reads from (combine) a peer's buffer before that peer's
+ * stream reached the call, and (combine) that every rank's writes into the
+ * buffer -- its expert's, and the library's own duplicate-row copies after a
+ * deduped moe_dispatch_p2p -- are complete; the exit barrier that every
+ * store landed (dispatch) / every read finished (combine).  A caller that
+ * orders its steps itself (e.g. moe_comm_barrier after its expert) may skip
+ * redundant ones, e.g. dispatch(NO_ENTRY) after a combine with its exit
+ * barrier.  Exception: a combine of a buffer whose last moe_dispatch_p2p
+ * sent some token rows once for two slots (k >= 2, two experts of the token
+ * on one remote owner, tuning p2p_dedupe) keeps its entry barrier under
+ * NO_ENTRY_BARRIER, because the owners' duplicate-row copies run after the
+ * dispatch's exit barrier -- unless MOE_P2P_RECV_UNMODIFIED is also given.
+ * MOE_P2P_RECV_UNMODIFIED (combine only): the caller asserts that nothing
+ * wrote expert_out since the moe_dispatch_p2p that filled it (an identity
+ * expert); the combine then reads such a slot from the row that was sent
+ * (one read for both slots, no wait for the copies).  Passing it after an
+ * expert wrote the buffer gives wrong results (undefined). */
+enum {
+  MOE_P2P_NO_ENTRY_BARRIER = 1,
+  MOE_P2P_NO_EXIT_BARRIER = 2,
+  MOE_P2P_RECV_UNMODIFIED = 4
+};
 
 /* Steps 2+3 fused: for every admitted item (t,j) with
  * expert e and slot s, the row x[t] is stored into rank q = e/(E/P)'s
@@ -419,12 +469,9 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
  * every admitted row read straight from its owner rank q's `expert_out` over
  * NVLink (fp32 accumulate in ascending j, one RNE store, 0 if all slots
  * dropped), then moe_comm_barrier (the buffers may be reused).  Same result
- * as moe_alltoall(FLAT) back + moe_reverse_layout.  MOE_P2P_NO_ENTRY_BARRIER
- * is ignored when the last moe_dispatch_p2p into expert_out sent a token's
- * rows for one owner once (k >= 2, E/P >= 2, MOE_P2P_DEDUPE): its owners
- * copy the duplicates after the dispatch's exit barrier, so the entry
- * barrier is what orders those copies before the reads.  expert_out: symmetric,
- * [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
+ * as moe_alltoall(FLAT) back + moe_reverse_layout.  Flags: see above
+ * (NO_ENTRY_BARRIER, NO_EXIT_BARRIER, RECV_UNMODIFIED).  expert_out:
+ * symmetric, [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
                              int32_t dtype, void* y, int32_t flags, moe_stream_t stream);
@@ -492,6 +539,17 @@ moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* 
                                        int32_t d, int32_t dtype, void* dx, int32_t flags,
                                        moe_stream_t stream);
 
+/* host.  The plan of the NCCL dropless exchange from this rank's expert
+ * offsets [E+1] (moe_expert_offsets, copied to the host) and the per-expert
+ * row counts it receives, recv_counts[src*E/P + le] (an AllToAll of the
+ * [P][E/P] count tables): send_rows[q] = rows for rank q's experts,
+ * recv_rows[q] = rows from rank q, recv_offsets[E+1] = where (src, le)
+ * starts in the receive buffer (source-rank major, R20).  Experts are
+ * contiguous blocks of E/P per rank (R10).  All arrays host memory. */
+moe_status_t moe_alltoallv_plan(int32_t nranks, int32_t E, const int32_t* offsets,
+                                const int32_t* recv_counts, int64_t* send_rows,
+                                int64_t* recv_rows, int32_t* recv_offsets);
+
 /* Variable-size AllToAll (the NCCL dropless exchange): rank r sends
  * send_rows[q] rows of row_bytes to every rank q, taken consecutively from
  * `send` in ascending q, and receives recv_rows[q] rows from every q into
@@ -536,20 +594,110 @@ moe_status_t moe_combine_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* des
 
 /* One step of an AllToAll schedule, as executed by moe_alltoall.  Exported
  * (host) so the schedule can be checked without GPUs.  Buffers: 0 = send,
- * 1 = recv, 2 = ws staging A, 3 = ws staging B (each G*P*bytes_per_peer).
- * Offsets/bytes are in units of bytes_per_peer chunks. */
+ * 1 = recv, 2 = ws staging A, 3 = ws staging B (each half of the
+ * workspace).  Offsets/bytes are in units of bytes_per_peer chunks. */
 typedef struct {
-  int32_t phase; /* ops of one phase run as one NCCL group; phases in order */
-  int32_t op;    /* 0 = SEND, 1 = RECV, 2 = COPY (local), 3 = PERMUTE      */
-  int32_t peer;  /* SEND/RECV: peer rank; PERMUTE: N (groups)              */
+  int32_t phase; /* ops of one phase: the SEND/RECVs as one NCCL group, then
+                    the local ops in order; phases in order                 */
+  int32_t op;    /* 0 = SEND, 1 = RECV, 2 = COPY (local), 3 = PERMUTE
+                    (dst (n,g,m) <- src (g,m,n)), 4 = TRANSPOSE (dst [y][x]
+                    <- src [x][y])                                         */
+  int32_t peer;  /* SEND/RECV: peer rank; PERMUTE: N (groups); TRANSPOSE: X */
   int32_t src_buf, dst_buf;
-  int64_t src_off, dst_off, chunks; /* PERMUTE: chunks = G (group size)   */
+  int64_t src_off, dst_off, chunks; /* PERMUTE: G (group size); TRANSPOSE: Y */
 } moe_a2a_op_t;
 
 /* host.  Fills ops[0..*n_ops) with rank `rank`'s schedule; returns
  * INVALID_ARG if capacity is too small (*n_ops then holds the count needed). */
 moe_status_t moe_alltoall_plan(int32_t nranks, int32_t rank, int32_t algo, int32_t group_size,
                                moe_a2a_op_t* ops, int32_t capacity, int32_t* n_ops);
+
+/* ---------------------------------------------------------------- simulated ranks
+ * TEST INFRASTRUCTURE: P ranks of the multi-GPU path simulated on ONE GPU,
+ * so every exchange step (Alg. 1 steps 3 and 5) is
+ * parity-testable without NVLink.  A world owns P simulated communicators
+ * (each a moe_comm_t* usable with every call above that takes one).  Their
+ * symmetric buffers are P ordinary allocations on the current device, each
+ * mapped to its "peers" directly.  Calls on a simulated rank validate their
+ * arguments and then do NOT launch: they append their steps to the rank's
+ * program.  moe_sim_world_run executes every rank's program on `stream`:
+ * kernels of a rank in its call order; a device barrier waits until every
+ * rank reached its matching barrier (a step boundary, no spinning kernel);
+ * NCCL send/recv groups are matched across the ranks in issue order per
+ * (source, destination) and executed as device copies.  The kernels are the
+ * ones the real path launches (same peer-pointer tables, same flags).
+ * No NCCL communicator exists; moe_comm_check of a simulated rank reads its
+ * device error word.  Not for production use. */
+typedef struct moe_sim_world moe_sim_world_t;
+
+/* host.  nranks in 1..32.  Allocates the signal buffers on the current
+ * device. */
+moe_status_t moe_sim_world_create(int32_t nranks, moe_sim_world_t** out);
+/* host.  The simulated communicator of `rank` (owned by the world). */
+moe_status_t moe_sim_world_comm(moe_sim_world_t* w, int32_t rank, moe_comm_t** out);
+/* Execute (enqueue on `stream`) every rank's queued steps, then clear them.
+ * INVALID_ARG if the programs do not match (a rank reaches a barrier or a
+ * send that no other rank matches); what ran before stays enqueued. */
+moe_status_t moe_sim_world_run(moe_sim_world_t* w, moe_stream_t stream);
+/* host.  Enqueue ONE rank's real barrier kernel (k_barrier on the world's
+ * signal words, bounded by the tuning's barrier_timeout_ms), for testing the
+ * timeout: with no other rank arriving it gives up and sets the rank's error
+ * word (moe_comm_check -> MOE_ERR_TIMEOUT).  Only one spinning kernel runs. */
+moe_status_t moe_sim_live_barrier(moe_sim_world_t* w, int32_t rank, moe_stream_t stream);
+/* host.  Synchronises the device and frees everything the world owns. */
+moe_status_t moe_sim_world_destroy(moe_sim_world_t* w);
+
+/* ---------------------------------------------------------------- tuning
+ * Kernel-variant choices of the row movers and the gate.  Every default is
+ * the measured-best one; the other values select variants
+ * that compute the SAME bits (the parity tests run each).  One process-wide
+ * table: it is filled once, at the first call into the library, from the
+ * MOE_<FIELD> environment variables (upper case, e.g. MOE_GATE_TILES) when
+ * set; moe_set_tuning replaces it.  No call reads the environment after
+ * that.  "auto" = decided per call from the shapes, as documented. */
+typedef struct {
+  int32_t gate_tiles;        /* gate: aim for >= this many tiles (256)             */
+  int32_t gate_max_tile;     /* gate: largest tile in tokens; 0 = auto (128 for
+                                logit gates, 256 for hash)                         */
+  int32_t gate_two_maxw;     /* gate: tiles x columns <= this -> select + slots2,
+                                else select + scan + slots (4096)                  */
+  int32_t fin_smem_maxw;     /* moe_gate_layout: tiles x columns <= this -> the
+                                layout reduces the tile table itself (4096)        */
+  int32_t layout_u;          /* layout: 32-byte vectors per lane per segment;
+                                0 = auto (2 for rows <= 2 KiB, else 4); 1, 2, 4    */
+  int32_t layout_pads_first; /* layout + combine adjoint: zero the padding rows
+                                before the token rows; -1 = auto (local buffers
+                                with >= 5% padding by construction), 0, 1          */
+  int32_t reverse_ku;        /* combine (k <= 2): vectors in flight per lane;
+                                0 = auto (2 for local k = 2, else 4); 2, 4         */
+  int32_t reverse_tpw;       /* combine (k = 1): two tokens per warp round on
+                                rows <= 2 KiB; -1 = auto (on), 0, 1                */
+  int32_t reverse_kspec;     /* combine: 1 = the k <= 2 specialised kernel, 0 =
+                                the generic one (1)                                */
+  int32_t reverse_backwards; /* combine: walk tokens last to first; -1 = auto
+                                (local buffers), 0, 1                              */
+  int32_t reverse_y_ef;      /* combine: evict-first y stores; -1 = auto (local), 0, 1 */
+  int32_t row_ctas_per_sm;   /* row movers: CTAs per SM; 0 = occupancy limit       */
+  int32_t combine_bwd_kspec; /* combine adjoint: k <= 2 specialised kernel (1)      */
+  int32_t gate_bwd_lanes;    /* gate adjoint: lanes per token; 0 = auto (~8 experts
+                                per lane)                                          */
+  int32_t p2p_dedupe;        /* one-sided dispatch: a token's row crosses once per
+                                owner (1)                                          */
+  int32_t p2p_local_pad;     /* one-sided dispatch: owners zero their own padding
+                                rows; -1 = auto (>= 5% padding by construction)    */
+  int32_t a2a_ctas_per_sm;   /* moe_alltoall(P2P): CTAs per SM (4)                 */
+  int32_t barrier_timeout_ms;/* device barriers give up after this long and
+                                report MOE_ERR_TIMEOUT (moe_comm_check); 0 = wait
+                                forever (60000)                                    */
+  int32_t disable_p2p;       /* moe_comm_init: do not map peer memory (0)          */
+} moe_tuning_t;
+
+/* host.  Copy of the current table (after the one-time environment read). */
+moe_status_t moe_get_tuning(moe_tuning_t* out);
+/* host.  Replace the table.  INVALID_ARG (and no change) if a field is out of
+ * its range.  Affects calls made after it returns; not synchronised with
+ * calls running on other host threads. */
+moe_status_t moe_set_tuning(const moe_tuning_t* t);
 
 /* ---------------------------------------------------------------- misc */
 

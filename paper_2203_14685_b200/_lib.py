@@ -41,6 +41,18 @@ class A2AOp(ctypes.Structure):
                 ("src_off", i64), ("dst_off", i64), ("chunks", i64)]
 
 
+TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "fin_smem_maxw", "layout_u",
+                 "layout_pads_first", "reverse_ku", "reverse_tpw", "reverse_kspec",
+                 "reverse_backwards", "reverse_y_ef", "row_ctas_per_sm", "combine_bwd_kspec",
+                 "gate_bwd_lanes", "p2p_dedupe", "p2p_local_pad", "a2a_ctas_per_sm",
+                 "barrier_timeout_ms", "disable_p2p")
+
+
+class Tuning(ctypes.Structure):
+    """moe_tuning_t"""
+    _fields_ = [(f, i32) for f in TUNING_FIELDS]
+
+
 # (name, restype, argtypes) for every symbol include/moe.h declares
 SIGNATURES = [
     ("moe_capacity", i32, [i32, i32, i32, ctypes.c_double]),
@@ -120,6 +132,16 @@ SIGNATURES = [
                                         i32, i32, vp, i32, vp]),
     ("moe_combine_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
                                        i32, i32, vp, i32, vp]),
+    ("moe_comm_check", ctypes.c_int, [vp, vp]),
+    ("moe_comm_abort", ctypes.c_int, [vp]),
+    ("moe_alltoallv_plan", ctypes.c_int, [i32, i32, vp, vp, vp, vp, vp]),
+    ("moe_sim_world_create", ctypes.c_int, [i32, ctypes.POINTER(vp)]),
+    ("moe_sim_world_comm", ctypes.c_int, [vp, i32, ctypes.POINTER(vp)]),
+    ("moe_sim_world_run", ctypes.c_int, [vp, vp]),
+    ("moe_sim_live_barrier", ctypes.c_int, [vp, i32, vp]),
+    ("moe_sim_world_destroy", ctypes.c_int, [vp]),
+    ("moe_get_tuning", ctypes.c_int, [ctypes.POINTER(Tuning)]),
+    ("moe_set_tuning", ctypes.c_int, [ctypes.POINTER(Tuning)]),
     ("moe_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("moe_last_error", ctypes.c_char_p, []),
     ("moe_version", ctypes.c_char_p, []),

@@ -14,12 +14,14 @@ from typing import Optional
 
 import torch
 
-from ._lib import A2AOp, GateDesc, GateInputs, RoutingC, check, lib
+import contextlib
+
+from ._lib import A2AOp, GateDesc, GateInputs, RoutingC, Tuning, TUNING_FIELDS, check, lib
 
 KINDS = {"topk": 0, "ktop1": 1, "hash": 2, "sam": 3, "d2s": 4}
 MODES = {"renorm": 0, "softmax": 1}
 PRIOS = {"token": 0, "slot": 1}
-ALGOS = {"flat": 0, "hier": 1, "p2p": 2}
+ALGOS = {"flat": 0, "hier": 1, "p2p": 2, "hier2d": 3}
 _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 
@@ -322,24 +324,21 @@ def layout_packed_backward(d_packed: torch.Tensor, r: Routing, offsets: torch.Te
 
 
 def alltoallv_plan(offsets, recv_counts, nranks: int):
-    """Host plan of the NCCL dropless exchange (NEXT-4): from this rank's
-    expert offsets [E+1] (moe_expert_offsets) and the per-expert counts it
-    receives, recv_counts[src*E/P + le] (an AllToAll of the count table),
-    return (send_rows[P], recv_rows[P], recv_offsets[E+1]) for moe_alltoallv.
-    Experts are contiguous blocks of E/P per rank (R10); the receive buffer
-    is source-rank major, then local expert (R20).  Pure host arithmetic."""
-    offsets = [int(v) for v in offsets]
-    recv_counts = [int(v) for v in recv_counts]
-    E = len(offsets) - 1
-    if E % nranks or len(recv_counts) != E:
-        raise ValueError("need E %% nranks == 0 and E recv counts (E=%d, P=%d)" % (E, nranks))
-    El = E // nranks
-    send_rows = [offsets[(q + 1) * El] - offsets[q * El] for q in range(nranks)]
-    recv_rows = [sum(recv_counts[q * El:(q + 1) * El]) for q in range(nranks)]
-    recv_offsets = [0]
-    for c in recv_counts:
-        recv_offsets.append(recv_offsets[-1] + c)
-    return send_rows, recv_rows, recv_offsets
+    """Host plan of the NCCL dropless exchange (NEXT-4, moe_alltoallv_plan):
+    from this rank's expert offsets [E+1] (moe_expert_offsets) and the
+    per-expert counts it receives, recv_counts[src*E/P + le] (an AllToAll of
+    the count table), return (send_rows[P], recv_rows[P], recv_offsets[E+1])
+    for moe_alltoallv (R10, R20)."""
+    off = [int(v) for v in offsets]
+    rc = [int(v) for v in recv_counts]
+    E = len(off) - 1
+    if len(rc) != E:
+        raise ValueError("need E recv counts (E=%d, got %d)" % (E, len(rc)))
+    i32a, i64a = ctypes.c_int32 * (E + 1), ctypes.c_int64 * max(1, nranks)
+    o, c = i32a(*off), (ctypes.c_int32 * max(1, E))(*rc)
+    sr, rr, ro = i64a(), i64a(), i32a()
+    check(lib().moe_alltoallv_plan(nranks, E, o, c, sr, rr, ro), "moe_alltoallv_plan")
+    return list(sr)[:nranks], list(rr)[:nranks], list(ro)
 
 
 def reverse_layout_backward(dy: torch.Tensor, back: torch.Tensor, r: Routing,
@@ -438,8 +437,12 @@ def alltoall_plan(nranks: int, rank: int, algo: str = "flat", group_size: int = 
 class Comm:
     """The library-owned NCCL communicator (moe_comm_t)."""
 
-    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, _handle=None):
         self.nranks, self.rank = nranks, rank
+        self._owned = _handle is None
+        if _handle is not None:        # a simulated rank (SimWorld.comm): owned by its world
+            self._h = _handle
+            return
         h = ctypes.c_void_p()
         check(lib().moe_comm_init(unique_id, nranks, rank, ctypes.byref(h)), "moe_comm_init")
         self._h = h
@@ -493,7 +496,7 @@ class Comm:
         """Device-side barrier of all ranks on the current stream."""
         check(lib().moe_comm_barrier(self._h, _stream()), "moe_comm_barrier")
 
-    NO_ENTRY_BARRIER, NO_EXIT_BARRIER = 1, 2
+    NO_ENTRY_BARRIER, NO_EXIT_BARRIER, RECV_UNMODIFIED = 1, 2, 4
 
     def dispatch_p2p(self, x: torch.Tensor, r: "Routing", recv: torch.Tensor,
                      flags: int = 0) -> torch.Tensor:
@@ -647,10 +650,65 @@ class Comm:
                                               _stream(dx.device)), "moe_dispatch_backward_p2p")
         return dx
 
+    def check(self):
+        """Failure detection (moe_comm_check; synchronises the current
+        stream): raises MoeError with status MOE_ERR_TIMEOUT if a device
+        barrier gave up waiting for a peer, MOE_ERR_NCCL on an asynchronous
+        NCCL error."""
+        check(lib().moe_comm_check(self._h, _stream()), "moe_comm_check")
+
+    def abort(self):
+        """ncclCommAbort + release, without waiting for the peers."""
+        if getattr(self, "_h", None) and self._owned:
+            check(lib().moe_comm_abort(self._h), "moe_comm_abort")
+        self._h = None
+
+    def destroy(self):
+        if getattr(self, "_h", None) and self._owned:
+            check(lib().moe_comm_destroy(self._h), "moe_comm_destroy")
+        self._h = None
+
+
+class SimWorld:
+    """TEST INFRASTRUCTURE (moe_sim_world): P ranks of the multi-GPU path
+    simulated on the current GPU.  comm(r) is a Comm usable with every
+    method; its calls are queued, and run() executes all ranks' queued steps
+    phase by phase (barriers as step boundaries, NCCL groups matched across
+    ranks) on the current stream, with the real kernels."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        h = ctypes.c_void_p()
+        check(lib().moe_sim_world_create(nranks, ctypes.byref(h)), "moe_sim_world_create")
+        self._h = h
+        self.comms = []
+        for r in range(nranks):
+            c = ctypes.c_void_p()
+            check(lib().moe_sim_world_comm(self._h, r, ctypes.byref(c)), "moe_sim_world_comm")
+            self.comms.append(Comm(b"", nranks, r, _handle=c))
+
+    def comm(self, rank: int) -> Comm:
+        return self.comms[rank]
+
+    def run(self):
+        check(lib().moe_sim_world_run(self._h, _stream()), "moe_sim_world_run")
+
+    def live_barrier(self, rank: int):
+        """One rank's real (bounded) barrier kernel: tests the timeout."""
+        check(lib().moe_sim_live_barrier(self._h, rank, _stream()), "moe_sim_live_barrier")
+
     def destroy(self):
         if getattr(self, "_h", None):
-            check(lib().moe_comm_destroy(self._h), "moe_comm_destroy")
+            for c in self.comms:
+                c._h = None
+            check(lib().moe_sim_world_destroy(self._h), "moe_sim_world_destroy")
             self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
 
 
 def _tensor_from_ptr(ptr: int, shape, dtype, device_index: int) -> torch.Tensor:
@@ -666,6 +724,36 @@ def _tensor_from_ptr(ptr: int, shape, dtype, device_index: int) -> torch.Tensor:
     if dtype == torch.bfloat16:
         t = t.view(torch.bfloat16)
     return t.view(shape)
+
+
+def get_tuning() -> dict:
+    """The library's process-wide tuning table (moe_tuning_t) as a dict."""
+    t = Tuning()
+    check(lib().moe_get_tuning(ctypes.byref(t)), "moe_get_tuning")
+    return {f: getattr(t, f) for f in TUNING_FIELDS}
+
+
+def set_tuning(**fields) -> dict:
+    """Change fields of the tuning table; returns the previous table."""
+    old = get_tuning()
+    bad = set(fields) - set(TUNING_FIELDS)
+    if bad:
+        raise KeyError("unknown tuning fields: %s" % sorted(bad))
+    new = dict(old, **fields)
+    t = Tuning(*[int(new[f]) for f in TUNING_FIELDS])
+    check(lib().moe_set_tuning(ctypes.byref(t)), "moe_set_tuning")
+    return old
+
+
+@contextlib.contextmanager
+def tuned(**fields):
+    """Run a block with some tuning fields changed (kernel-variant selection;
+    every variant computes the same bits), restoring the table after."""
+    old = set_tuning(**fields)
+    try:
+        yield
+    finally:
+        set_tuning(**old)
 
 
 def version() -> str:

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "launch.cuh"
 
@@ -41,9 +42,69 @@ int device_sm_count() {
   return cache[dev];
 }
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
+// ------------------------------------------------------------ tuning table
+// Filled once from the environment (MOE_<FIELD>), then only by
+// moe_set_tuning: no launch reads the environment.
+namespace {
+struct TuneField {
+  const char* env;
+  int32_t moe_tuning_t::*f;
+  int32_t dflt, lo, hi;
+};
+const TuneField kTune[] = {
+    {"MOE_GATE_TILES", &moe_tuning_t::gate_tiles, 256, 1, 1 << 20},
+    {"MOE_GATE_MAX_TILE", &moe_tuning_t::gate_max_tile, 0, 0, 256},
+    {"MOE_GATE_TWO_MAXW", &moe_tuning_t::gate_two_maxw, 4096, 0, 1 << 30},
+    {"MOE_FIN_SMEM_MAXW", &moe_tuning_t::fin_smem_maxw, 4096, 0, 1 << 30},
+    {"MOE_LAYOUT_U", &moe_tuning_t::layout_u, 0, 0, 4},
+    {"MOE_LAYOUT_PADS_FIRST", &moe_tuning_t::layout_pads_first, -1, -1, 1},
+    {"MOE_REVERSE_KU", &moe_tuning_t::reverse_ku, 0, 0, 4},
+    {"MOE_REVERSE_TPW", &moe_tuning_t::reverse_tpw, -1, -1, 1},
+    {"MOE_REVERSE_KSPEC", &moe_tuning_t::reverse_kspec, 1, 0, 1},
+    {"MOE_REVERSE_BACKWARDS", &moe_tuning_t::reverse_backwards, -1, -1, 1},
+    {"MOE_REVERSE_Y_EF", &moe_tuning_t::reverse_y_ef, -1, -1, 1},
+    {"MOE_ROW_CTAS_PER_SM", &moe_tuning_t::row_ctas_per_sm, 0, 0, 64},
+    {"MOE_COMBINE_BWD_KSPEC", &moe_tuning_t::combine_bwd_kspec, 1, 0, 1},
+    {"MOE_GATE_BWD_LANES", &moe_tuning_t::gate_bwd_lanes, 0, 0, 32},
+    {"MOE_P2P_DEDUPE", &moe_tuning_t::p2p_dedupe, 1, 0, 1},
+    {"MOE_P2P_LOCAL_PAD", &moe_tuning_t::p2p_local_pad, -1, -1, 1},
+    {"MOE_A2A_CTAS_PER_SM", &moe_tuning_t::a2a_ctas_per_sm, 4, 1, 64},
+    {"MOE_BARRIER_TIMEOUT_MS", &moe_tuning_t::barrier_timeout_ms, 60000, 0, 1 << 30},
+    {"MOE_DISABLE_P2P", &moe_tuning_t::disable_p2p, 0, 0, 1},
+};
+moe_tuning_t g_tune;
+std::once_flag g_tune_once;
+
+bool tune_valid(const moe_tuning_t& t) {
+  for (const TuneField& f : kTune)
+    if (t.*(f.f) < f.lo || t.*(f.f) > f.hi) {
+      set_error("moe_set_tuning: %s = %d outside [%d, %d]", f.env, t.*(f.f), f.lo, f.hi);
+      return false;
+    }
+  if (t.layout_u == 3 || t.reverse_ku == 1 || t.reverse_ku == 3) {
+    set_error("moe_set_tuning: layout_u must be 0, 1, 2 or 4 and reverse_ku 0, 2 or 4");
+    return false;
+  }
+  if (t.gate_bwd_lanes & (t.gate_bwd_lanes - 1)) {
+    set_error("moe_set_tuning: gate_bwd_lanes must be 0 or a power of two");
+    return false;
+  }
+  return true;
+}
+}  // namespace
+
+const moe_tuning_t& tuning() {
+  std::call_once(g_tune_once, [] {
+    moe_tuning_t t{};
+    for (const TuneField& f : kTune) {
+      const char* v = getenv(f.env);
+      t.*(f.f) = (v && *v) ? atoi(v) : f.dflt;
+    }
+    if (!tune_valid(t))  // a bad environment value: keep the defaults
+      for (const TuneField& f : kTune) t.*(f.f) = f.dflt;
+    g_tune = t;
+  });
+  return g_tune;
 }
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -172,7 +233,7 @@ moe_status_t moe_gate_layout(const moe_gate_desc_t* desc, const moe_gate_inputs_
   if (s != MOE_OK) return s;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const int ds = dtype_size(dtype);
-  if (((long long)d * ds) % 32 != 0 || desc->k > 32 || !env_int("MOE_GATE_LAYOUT_FUSED", 1)) {
+  if (((long long)d * ds) % 32 != 0 || desc->k > 32) {
     s = gate_launch(*desc, *in, *out, ws, stream);  // the unfused pair
     if (s != MOE_OK) return s;
     return layout_launch(*desc, *out, x, ds, d, dispatch, stream);
@@ -454,6 +515,26 @@ moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E
                              reinterpret_cast<cudaStream_t>(stream));
 }
 
+moe_status_t moe_get_tuning(moe_tuning_t* out) {
+  if (!out) {
+    set_error("moe_get_tuning: out is NULL");
+    return MOE_ERR_INVALID_ARG;
+  }
+  *out = tuning();
+  return MOE_OK;
+}
+
+moe_status_t moe_set_tuning(const moe_tuning_t* t) {
+  if (!t) {
+    set_error("moe_set_tuning: NULL table");
+    return MOE_ERR_INVALID_ARG;
+  }
+  tuning();  // the one-time environment read happens first, never after
+  if (!tune_valid(*t)) return MOE_ERR_INVALID_ARG;
+  g_tune = *t;
+  return MOE_OK;
+}
+
 const char* moe_status_str(moe_status_t s) {
   switch (s) {
     case MOE_OK: return "MOE_OK";
@@ -463,6 +544,7 @@ const char* moe_status_str(moe_status_t s) {
     case MOE_ERR_WORKSPACE: return "MOE_ERR_WORKSPACE";
     case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
     case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
+    case MOE_ERR_TIMEOUT: return "MOE_ERR_TIMEOUT";
   }
   return "MOE_ERR_UNKNOWN";
 }

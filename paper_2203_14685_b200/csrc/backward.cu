@@ -285,16 +285,16 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
   a.sys_fence = E_local != d.E;
   // padding rows first when they are many (C4b: combine 46.2 -> 42.0 us,
   // its adjoint likewise; C3's 2% gained nothing)
-  a.pads_first = env_int("MOE_LAYOUT_PADS_FIRST", E_local == d.E && pad_heavy(d) ? 1 : 0);
+  const moe_tuning_t& tu = tuning();
+  a.pads_first = tu.layout_pads_first >= 0 ? tu.layout_pads_first
+                                           : (E_local == d.E && pad_heavy(d) ? 1 : 0);
   const bool f = dtype == MOE_F32;
   const void* kern;
-  const int uenv = env_int("MOE_COMBINE_BWD_U", 0);
   // measured: one 1 KiB segment per round beats two (more warps in flight):
   // C2 65.5 -> 58.9 us, C3 63.5 -> 61.5, C4a 121 -> 111, C4b 73.8 -> 69.6
-  const int U2 = uenv >= 2 ? 2 : 1;
 #define MOE_CBK(KK, UU) (f ? (const void*)k_combine_bwd_k<MOE_F32, KK, UU> : (const void*)k_combine_bwd_k<MOE_BF16, KK, UU>)
-  if (a.row_bytes % 32 == 0 && a.k <= 2 && env_int("MOE_COMBINE_BWD_KSPEC", 1))
-    kern = a.k == 1 ? (U2 == 2 ? MOE_CBK(1, 2) : MOE_CBK(1, 1)) : (U2 == 2 ? MOE_CBK(2, 2) : MOE_CBK(2, 1));
+  if (a.row_bytes % 32 == 0 && a.k <= 2 && tu.combine_bwd_kspec)
+    kern = a.k == 1 ? MOE_CBK(1, 1) : MOE_CBK(2, 1);
   else if (a.row_bytes % 32 == 0)
     kern = a.row_bytes >= 2048 ? (f ? (const void*)k_combine_bwd<MOE_F32, 2> : (const void*)k_combine_bwd<MOE_BF16, 2>)
                                : (f ? (const void*)k_combine_bwd<MOE_F32, 1> : (const void*)k_combine_bwd<MOE_BF16, 1>);
@@ -401,9 +401,7 @@ moe_status_t push_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r, c
   } else if (phase == 1) {  // owner side
     const bool f = dtype == MOE_F32;
     // one 1 KiB segment per round, as k_combine_bwd_k (more warps in flight)
-    const void* kern = env_int("MOE_COMBINE_BWD_U", 1) >= 2
-                           ? (f ? (const void*)k_scale_dot<MOE_F32, 2> : (const void*)k_scale_dot<MOE_BF16, 2>)
-                           : (f ? (const void*)k_scale_dot<MOE_F32, 1> : (const void*)k_scale_dot<MOE_BF16, 1>);
+    const void* kern = f ? (const void*)k_scale_dot<MOE_F32, 1> : (const void*)k_scale_dot<MOE_BF16, 1>;
     long long nrows = (long long)d.E * d.capacity;
     const float* wl = reinterpret_cast<const float*>(wtab.p[rank]);
     int cap = d.capacity;
@@ -618,8 +616,8 @@ moe_status_t gate_bwd_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& 
   GateBwdArgs a{in.logits, r.expert_idx, r.slot_idx, d_weight, d_logits, d.S, d.E, d.k, d.kind,
                 d.weight_mode, in.group_logits, d.kind == MOE_GATE_SAM ? in.n_groups : 1,
                 d_group_logits, in.uniforms, in.tau};
-  // lanes per token (MOE_GATE_BWD_LANES overrides)
-  int L = env_int("MOE_GATE_BWD_LANES", 0);
+  // lanes per token (tuning gate_bwd_lanes overrides)
+  int L = tuning().gate_bwd_lanes;
   if (L <= 0) {
     L = 1;  // ~8 experts per lane (one per lane measured slower at E = 8)
     while (L < 32 && d.E / (L * 2) >= 8) L *= 2;

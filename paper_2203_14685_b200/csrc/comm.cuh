@@ -4,6 +4,7 @@
 #pragma once
 #include <nccl.h>
 
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -16,7 +17,10 @@ constexpr int kMaxRanks = 32;
 // experts] int32 (admitted rows per (source, local expert)).
 constexpr size_t kPadTabOff = 4096;
 constexpr int kPadTabStride = 256;
+// device error word of this rank (a barrier that timed out sets it)
+constexpr size_t kErrOff = 2048;
 constexpr size_t kSigBytes = kPadTabOff + sizeof(int) * kMaxRanks * kPadTabStride;
+enum { kErrBarrierTimeout = 1 };
 
 // P pointers to the same symmetric buffer as mapped on every rank
 // (peer[r] == this rank's own allocation).  Passed to kernels by value.
@@ -30,9 +34,29 @@ struct SymmBuf {
   PeerPtrs peer;
 };
 
-moe_status_t barrier_launch(const PeerPtrs& sig, int nranks, int rank, cudaStream_t stream);
+// One step of a rank's program on a SIMULATED communicator (moe_sim_*):
+// calls on a simulated rank do not launch; they append their steps here and
+// moe_sim_world_run executes every rank's program on one GPU, phase by
+// phase: a BARRIER step waits until every rank reached its matching barrier;
+// a GROUP step is one NCCL group of send/recv ops, matched across ranks in
+// issue order per (source, destination) pair as NCCL matches them.
+struct SimOp {
+  int send;  // 1 = send, 0 = recv
+  int peer;
+  char* ptr;
+  size_t bytes;
+  int done;
+};
+struct SimItem {
+  enum Kind { FN = 0, BARRIER = 1, GROUP = 2 } kind;
+  std::function<moe_status_t(cudaStream_t)> fn;
+  std::vector<SimOp> ops;
+  int posted = 0, pending_sends = 0;
+};
 
 }  // namespace moe
+
+struct moe_sim_world;
 
 struct moe_comm {
   ncclComm_t nccl;
@@ -43,9 +67,28 @@ struct moe_comm {
   const void* dup_recv = nullptr;  // recv of the last dispatch whose owners fill duplicate rows
                                    // after its exit barrier (the combine must not skip its entry one)
   bool p2p_ok;                     // peer mappings could be made (NVLink / P2P)
+  // simulated rank (moe_sim_world): no NCCL; calls queue their steps
+  moe_sim_world* sim = nullptr;
+  std::vector<moe::SimItem> queue;
+  int sim_nalloc = 0;              // symmetric allocations made by this rank so far
 };
 
 namespace moe {
+
+// Run `fn` on `stream` now (a real communicator) or append it to a simulated
+// rank's program (moe_sim_world_run executes it later, in order).
+moe_status_t run_or_queue(moe_comm* c, cudaStream_t stream,
+                          std::function<moe_status_t(cudaStream_t)> fn);
+// The device barrier of all ranks (k_barrier, bounded by the tuning's
+// barrier_timeout_ms), or a barrier step of a simulated rank.
+moe_status_t comm_barrier(moe_comm* c, cudaStream_t stream);
+// One NCCL group of send/recv ops (ncclGroupStart .. End), or a group step
+// of a simulated rank.
+moe_status_t comm_group(moe_comm* c, std::vector<SimOp> ops, cudaStream_t stream);
+// Symmetric allocation over the communicator's ranks (CUDA IPC), or from the
+// simulated world's per-rank buffers; release is collective too.
+moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out);
+moe_status_t symm_release_coll(moe_comm* c, SymmBuf& b);
 
 // The symmetric buffer containing [p, p + bytes), or nullptr.
 inline const SymmBuf* find_symm(const moe_comm* c, const void* p, size_t bytes) {

@@ -32,7 +32,7 @@ inline cudaError_t launch_pdl(const void* kern, dim3 grid, dim3 block, size_t sm
   cfg.numAttrs = 1;
   return cudaLaunchKernelExC(&cfg, kern, args);
 }
-int env_int(const char* name, int dflt);  // tuning knobs (api.cu)
+const moe_tuning_t& tuning();  // the process-wide tuning table (api.cu)
 
 #define MOE_CHECK_LAUNCH(what)                                   \
   do {                                                           \

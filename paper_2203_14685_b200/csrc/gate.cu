@@ -23,10 +23,8 @@
 //                  slot_src and its empty entries.
 //   k_gate_slots2  scan + slots in one pass (per-CTA table reduction).
 // SAM (R17) and Dense-to-Sparse (R18) are further selection kinds of
-// k_gate_select.  Measured alternatives behind knobs: one cooperative
-// launch with a grid barrier (k_gate_fused, MOE_GATE_FUSED=1) and the
-// capacity pass inside the layout kernel (gate_select_launch +
-// layout.cu's k_layout_fin, moe_gate_layout).
+// k_gate_select.  The capacity pass can also run inside the layout kernel
+// (gate_select_launch + layout.cu's k_layout_fin, moe_gate_layout).
 // Columns are experts (TOKEN priority, t-major admission) or (j, expert)
 // pairs (SLOT priority, j-major).  Traffic is O(tiles x columns).
 #include "gate_impl.cuh"
@@ -195,57 +193,28 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
 }
 
 // ------------------------------------------------------------ host side
-template <bool FUSED>
 static GateKernel pick_gate(const moe_gate_desc_t& d, const GatePlan& p) {
-  if (!FUSED && d.kind == MOE_GATE_SAM) return pick_sam(p.L, p.K);
-  if (!FUSED && d.kind == MOE_GATE_D2S) return pick_d2s(p.L);
-  return d.kind == MOE_GATE_HASH    ? pick_hash(FUSED)
-         : d.kind == MOE_GATE_KTOP1 ? pick_ktop1(p.L, p.K, FUSED)
-                                    : pick_topk(p.L, p.K, FUSED);
+  if (d.kind == MOE_GATE_SAM) return pick_sam(p.L, p.K);
+  if (d.kind == MOE_GATE_D2S) return pick_d2s(p.L);
+  return d.kind == MOE_GATE_HASH    ? pick_hash()
+         : d.kind == MOE_GATE_KTOP1 ? pick_ktop1(p.L, p.K)
+                                    : pick_topk(p.L, p.K);
 }
 
-static int fused_tiles() { return env_int("MOE_GATE_FUSED_TILES", 128); }
+// select -> slots2 (every CTA reduces the tile table itself) when the table
+// is small, else select -> scan -> slots.
+static bool two_kernels(const GatePlan& p) {
+  return (long long)p.n_tiles * p.ncols <= tuning().gate_two_maxw;
+}
 
-// Kernels one moe_gate call enqueues for `d` with the default knobs (the
-// fused single launch is off by default): 2 (select -> slots2) or 3.
+// Kernels one moe_gate call enqueues for `d`: 2 (select -> slots2) or 3.
 int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
-  if (env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH) return -1;  // decided at launch
-  const GatePlan p = gate_plan_default(d, ngroups);
-  return (long long)p.n_tiles * p.ncols <= env_int("MOE_GATE_TWO_MAXW", 4096) ? 2 : 3;
+  return two_kernels(gate_plan_default(d, ngroups)) ? 2 : 3;
 }
 
 size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
-  // room for every tile count the knobs may pick (the table is small)
-  return std::max({gate_plan_default(d).bytes, gate_plan(d, gate_tiles()).bytes,
-                   gate_plan(d, fused_tiles()).bytes, gate_plan(d, 1024).bytes});
-}
-
-// The three-kernel path (k_gate_select -> k_gate_scan -> k_gate_slots, PDL).
-static moe_status_t gate_launch3(const moe_gate_desc_t& d, const GatePlan& p, GateArgs& a,
-                                 cudaStream_t stream) {
-  void* args[] = {&a};
-  GateKernel kern = pick_gate<false>(d, p);
-  if (p.smem > 40 * 1024) {  // + static shared memory
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p.smem);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
-  }
-  cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
-                             stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
-  // two kernels (select -> slots2) when the per-CTA column reduction is small
-  if ((long long)p.n_tiles * p.ncols <= env_int("MOE_GATE_TWO_MAXW", 4096)) {
-    e = launch_pdl((const void*)k_gate_slots2, dim3(p.n_tiles), dim3(kGateThreads), 0, stream,
-                   args);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots2 launch");
-    return MOE_OK;
-  }
-  e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
-                 dim3(kGateThreads), 0, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
-  e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
-  return MOE_OK;
+  // room for every tile count the tuning may pick (the table is small)
+  return std::max({gate_plan_default(d).bytes, gate_plan(d, 1 << 20, 1, 32).bytes});
 }
 
 static void fill_args(GateArgs& a, const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
@@ -282,20 +251,15 @@ static void fill_args(GateArgs& a, const moe_gate_desc_t& d, const moe_gate_inpu
   a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
 }
 
-moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
-                                const moe_routing_t& out, void* ws, cudaStream_t stream,
-                                GateFinalize* fin) {
-  const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
-  const GatePlan p = gate_plan_default(d, ng);
+static moe_status_t select_launch(const moe_gate_desc_t& d, const GatePlan& p, GateArgs& a,
+                                  cudaStream_t stream) {
   if (p.ncols > kMaxCols) {
     set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
     return MOE_ERR_UNSUPPORTED;
   }
-  GateArgs a;  // launch arguments are copied at launch
-  fill_args(a, d, in, out, ws, p, ng);
   void* args[] = {&a};
-  GateKernel kern = pick_gate<false>(d, p);
-  if (p.smem > 40 * 1024) {
+  GateKernel kern = pick_gate(d, p);
+  if (p.smem > 40 * 1024) {  // + static shared memory
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)p.smem);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: smem attribute");
@@ -303,6 +267,18 @@ moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   cudaError_t e = launch_pdl((const void*)kern, dim3(p.n_tiles), dim3(kGateThreads), p.smem,
                              stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_select launch");
+  return MOE_OK;
+}
+
+moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                                const moe_routing_t& out, void* ws, cudaStream_t stream,
+                                GateFinalize* fin) {
+  const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
+  const GatePlan p = gate_plan_default(d, ng);
+  GateArgs a;  // launch arguments are copied at launch
+  fill_args(a, d, in, out, ws, p, ng);
+  moe_status_t s = select_launch(d, p, a, stream);
+  if (s != MOE_OK) return s;
   fin->agg = reinterpret_cast<const unsigned*>(a.status);
   fin->totals = a.totals;
   fin->n_tiles = p.n_tiles;
@@ -314,101 +290,39 @@ moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   fin->weight = out.weight;
   fin->load = out.load;
   // the layout reduces the raw table itself when it fits its shared memory
-  fin->scanned = (long long)p.n_tiles * p.ncols > env_int("MOE_FIN_SMEM_MAXW", 4096);
+  fin->scanned = (long long)p.n_tiles * p.ncols > tuning().fin_smem_maxw;
   if (fin->scanned) {
-    e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
-                   dim3(kGateThreads), 0, stream, args);
+    void* args[] = {&a};
+    cudaError_t e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
+                               dim3(kGateThreads), 0, stream, args);
     if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
   }
   return MOE_OK;
 }
 
+// k_gate_select -> (k_gate_slots2 | k_gate_scan -> k_gate_slots), PDL-chained.
 moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
                          const moe_routing_t& out, void* ws, cudaStream_t stream) {
-  // one launch with a grid barrier when every tile's CTA fits on the device
-  // at once and the per-CTA reduction (tiles x columns words) is small
   const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
-  const GatePlan pf = gate_plan(d, fused_tiles(), ng);
-  bool fused = env_int("MOE_GATE_FUSED", 0) && d.kind <= MOE_GATE_HASH &&
-               (long long)pf.n_tiles * pf.ncols <= env_int("MOE_GATE_FUSED_MAXW", 8192);
-  const GatePlan p = fused ? pf : gate_plan_default(d, ng);
-  if (p.ncols > kMaxCols) {
-    set_error("moe_gate: SLOT priority needs k*E <= %d (k=%d, E=%d)", kMaxCols, d.k, d.E);
-    return MOE_ERR_UNSUPPORTED;
-  }
-  GateArgs a{};
-  a.logits = in.logits;
-  a.ids = in.token_ids;
-  a.table = in.table;
-  a.vocab = in.vocab;
-  a.glogits = in.group_logits;
-  a.ngroups = ng;
-  a.uniforms = in.uniforms;
-  a.tau = in.tau;
-  a.eps = in.eps;
-  a.z_words = p.z_words;
-  a.S = d.S;
-  a.E = d.E;
-  a.k = d.k;
-  a.cap = d.capacity;
-  a.mode = d.weight_mode;
-  a.prio = d.priority;
-  a.tile_tokens = p.tile_tokens;
-  a.n_tiles = p.n_tiles;
-  a.ncols = p.ncols;
-  a.lg_words = p.lg_words;
-  a.expert_idx = out.expert_idx;
-  a.slot_idx = out.slot_idx;
-  a.weight = out.weight;
-  a.load = out.load;
-  a.slot_src = out.slot_src;
-  char* w = static_cast<char*>(ws);
-  a.ctrl = reinterpret_cast<GateCtrl*>(w);
-  a.status = reinterpret_cast<unsigned long long*>(w + p.status_off);
-  a.totals = reinterpret_cast<int32_t*>(w + p.totals_off);
-
+  const GatePlan p = gate_plan_default(d, ng);
+  GateArgs a;
+  fill_args(a, d, in, out, ws, p, ng);
+  moe_status_t s = select_launch(d, p, a, stream);
+  if (s != MOE_OK) return s;
   void* args[] = {&a};
-  if (fused) {
-    GateKernel fk = pick_gate<true>(d, p);
-    const size_t fsmem = p.smem + 2 * sizeof(int) * (size_t)p.ncols;
-    cudaError_t e = cudaSuccess;
-    if (fsmem > 40 * 1024)
-      e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-    int per_sm = 0;
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fk, kGateThreads, fsmem);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: fused occupancy");
-    if (p.n_tiles > per_sm * device_sm_count()) {
-      const GatePlan p3 = gate_plan_default(d, ng);
-      a.tile_tokens = p3.tile_tokens;
-      a.n_tiles = p3.n_tiles;
-      a.lg_words = p3.lg_words;
-      a.totals = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p3.totals_off);
-      return gate_launch3(d, p3, a, stream);
-    }
-    {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(p.n_tiles);
-      cfg.blockDim = dim3(kGateThreads);
-      cfg.dynamicSmemBytes = fsmem;
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[2];
-      attr[0].id = cudaLaunchAttributeCooperative;
-      attr[0].val.cooperative = 1;
-      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[1].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 2;
-      if (!env_int("MOE_GATE_COOP", 0)) {  // co-residency from the occupancy check alone
-        cfg.attrs = attr + 1;
-        cfg.numAttrs = 1;
-      }
-      e = cudaLaunchKernelExC(&cfg, (const void*)fk, args);
-      if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_fused launch");
-      return MOE_OK;
-    }
+  cudaError_t e;
+  if (two_kernels(p)) {
+    e = launch_pdl((const void*)k_gate_slots2, dim3(p.n_tiles), dim3(kGateThreads), 0, stream,
+                   args);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots2 launch");
+    return MOE_OK;
   }
-  return gate_launch3(d, p, a, stream);
+  e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
+                 dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
+  e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
+  return MOE_OK;
 }
 
 moe_status_t gate_check(void* ws, cudaStream_t stream, int32_t* bad) {

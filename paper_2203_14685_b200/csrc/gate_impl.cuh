@@ -1,5 +1,5 @@
 // gate_impl.cuh -- the gate's device code (selection functions, gate_tile,
-// the templated k_gate_select / k_gate_fused kernels) and the launch plan,
+// the templated k_gate_select kernel) and the launch plan,
 // shared by gate.cu (host side + the non-template kernels) and the picker
 // TUs that instantiate the kernel templates (gate_pick_*.cu, compiled in
 // parallel).  See gate.cu for the design.
@@ -20,9 +20,7 @@ constexpr size_t kMaxTileLogitBytes = 64 * 1024;
 
 struct GateCtrl {  // 64 bytes at the head of the workspace
   unsigned bad;        // invalid hash ids since the last moe_gate_check
-  unsigned bar_count;  // k_gate_fused grid barrier: arrivals (reset by the last)
-  unsigned bar_gen;    // and generation
-  unsigned pad[13];
+  unsigned pad[15];
 };
 
 struct GateArgs {
@@ -64,19 +62,18 @@ inline int choose_lanes(int E) {
   return L;
 }
 
-inline int gate_tiles() { return env_int("MOE_GATE_TILES", 256); }
+inline int gate_tiles() { return tuning().gate_tiles; }
 // Largest tile of the select -> (scan ->) slots path for the logit gates:
 // 128 tokens (S = 64K: 512 tiles; measured C4a gate 22.6 -> 21.4 us, step
 // 148 -> 145 us vs 256-token tiles; C2/C3 already get 128-token tiles from the
 // >= 256 tiles rule).  The hash gate stages no logits and keeps 256 (C4b: gate
 // unchanged, step 97.2 vs 98.3 us with 128).
 inline int gate_max_tile(int kind) {
-  return env_int("MOE_GATE_MAX_TILE", kind == MOE_GATE_HASH ? 256 : 128);
+  const int t = tuning().gate_max_tile;
+  return t > 0 ? t : kind == MOE_GATE_HASH ? 256 : 128;
 }
 
-// want_tiles: the three-kernel path wants >= 256 tiles when S allows (about
-// 1.7 CTAs per SM on 148 SMs); the single-launch path fewer, larger tiles
-// (every CTA reduces all tiles' aggregates after its grid barrier).
+// want_tiles: >= 256 tiles when S allows (about 1.7 CTAs per SM on 148 SMs)
 inline GatePlan gate_plan(const moe_gate_desc_t& d, int want_tiles, int ngroups = 1,
                           int max_tile = 256) {
   GatePlan p{};
@@ -465,7 +462,7 @@ __device__ __forceinline__ void select_d2s(const GateArgs& a, const float* row, 
 // ------------------------------------------------------------ the kernel
 enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2, KIND_SAM = 3, KIND_D2S = 4 };
 
-// Phases A and B of one tile (shared by k_gate_select and k_gate_fused):
+// Phases A and B of one tile (k_gate_select):
 // stage the logits, select + weights (expert_idx, weight written), in-tile
 // ranks per column (s_exp, s_rank), s_hist[w][c] turned into the exclusive
 // prefix over warps, and the tile aggregates agg[c][tile] written.  Returns
@@ -644,162 +641,35 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
 }
 
-// ------------------------------------------------------------ single launch
-// The three kernels above as ONE cooperative launch (every tile's CTA is
-// co-resident): phases A/B as in k_gate_select, one grid barrier, then each
-// CTA reduces every column's tile aggregates itself (the exclusive prefix
-// over earlier tiles and the column total, O(tiles x columns) L2 reads per
-// CTA) and finishes its own slots from the ranks still in shared memory.
-// Saves two launches and the global round trip of the provisional slots.
-// Used when the tiles fit on the device at once (host checks occupancy).
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Sense-reversing grid barrier on two words of the control block: the last
-// arriver resets the count and bumps the generation, so it works for any
-// grid size and is CUDA-graph replay safe.
-__device__ __forceinline__ void grid_barrier(GateCtrl* c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_u32(&c->bar_gen);
-    __threadfence();
-    const unsigned old = atomicAdd(&c->bar_count, 1u);
-    if (old == gridDim.x - 1) {
-      c->bar_count = 0;
-      __threadfence();
-      atomicAdd(&c->bar_gen, 1u);
-    } else {
-      while (ld_acquire_u32(&c->bar_gen) == gen) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-template <int KIND, int L, int K>
-__global__ void __launch_bounds__(kGateThreads) k_gate_fused(GateArgs a) {
-  extern __shared__ __align__(16) int smem[];
-  __shared__ unsigned s_bad;
-  __shared__ __align__(8) unsigned long long s_mbar;
-  pdl_wait();
-  pdl_trigger();
-  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int items = a.tile_tokens * a.k;
-  const int* s_exp = smem + a.lg_words + a.z_words;
-  const int* s_rank = s_exp + items;
-  const int* s_hist = s_rank + items;
-  int* s_pre = const_cast<int*>(s_hist) + kGateWarps * a.ncols;  // [ncols] earlier tiles
-  int* s_tot = s_pre + a.ncols;                                   // [ncols] column totals
-  const int tile = blockIdx.x;
-  const int t0 = tile * a.tile_tokens;
-  const int nt = min(a.tile_tokens, a.S - t0);
-  const bool slot_prio = a.prio == MOE_PRIO_SLOT;
-  const int per = (items + kGateWarps - 1) / kGateWarps;
-  if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-
-  grid_barrier(a.ctrl);
-
-  // every column: prefix over tiles < tile and the total, warp per column
-  const unsigned* agg = reinterpret_cast<const unsigned*>(a.status);
-  for (int c = warp; c < a.ncols; c += kGateWarps) {
-    const unsigned* col = agg + (size_t)c * a.n_tiles;
-    unsigned pre = 0, tot = 0;
-    // 8 independent loads in flight per lane per round (one L2 round trip
-    // covers 256 tiles)
-    for (int base = 0; base < a.n_tiles; base += 256) {
-      unsigned v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + u * 32 + lane;
-        v[u] = i < a.n_tiles ? __ldcg(col + i) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + u * 32 + lane;
-        tot += v[u];
-        if (i < tile) pre += v[u];
-      }
-    }
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) {
-      pre += __shfl_xor_sync(0xffffffffu, pre, m);
-      tot += __shfl_xor_sync(0xffffffffu, tot, m);
-    }
-    if (lane == 0) {
-      s_pre[c] = (int)pre;
-      s_tot[c] = (int)tot;
-    }
-  }
-  __syncthreads();
-
-  // final slots: (SLOT: items of earlier j) + earlier tiles + warps before + rank
-  for (int i = tid; i < nt * a.k; i += kGateThreads) {
-    const int e = s_exp[i];
-    const size_t gi = (size_t)t0 * a.k + i;
-    if (e < 0) {
-      a.slot_idx[gi] = -1;  // invalid hash id: routed as dropped
-      continue;
-    }
-    const int tt = i / a.k, j = i - tt * a.k;
-    const int pos = slot_prio ? j * a.tile_tokens + tt : i;
-    const int col = slot_prio ? j * a.E + e : e;
-    int s = s_pre[col] + s_hist[(pos / per) * a.ncols + col] + s_rank[i];
-    if (slot_prio)
-      for (int jj = 0; jj < j; ++jj) s += s_tot[jj * a.E + e];
-    if (s < a.cap) {
-      a.slot_idx[gi] = s;
-      if (a.slot_src) a.slot_src[(size_t)e * a.cap + s] = (int)gi;
-    } else {
-      a.slot_idx[gi] = -1;
-      a.weight[gi] = 0.f;
-    }
-  }
-  // load[] and the empty slot_src entries, warp per expert across the grid
-  for (int e = tile * kGateWarps + warp; e < a.E; e += gridDim.x * kGateWarps) {
-    int ld = 0;
-    if (slot_prio)
-      for (int jj = 0; jj < a.k; ++jj) ld += s_tot[jj * a.E + e];
-    else
-      ld = s_tot[e];
-    if (lane == 0) a.load[e] = ld;
-    if (a.slot_src)
-      for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
-  }
-}
-
 // ------------------------------------------------------------ kernel pickers
 using GateKernel = void (*)(GateArgs);
 
-template <int KIND, int L, bool FUSED>
+template <int KIND, int L>
 inline GateKernel pick_k(int K) {
   switch (K) {
-    case 1: return FUSED ? k_gate_fused<KIND, L, 1> : k_gate_select<KIND, L, 1>;
-    case 2: return FUSED ? k_gate_fused<KIND, L, 2> : k_gate_select<KIND, L, 2>;
-    case 4: return FUSED ? k_gate_fused<KIND, L, 4> : k_gate_select<KIND, L, 4>;
-    case 8: return FUSED ? k_gate_fused<KIND, L, 8> : k_gate_select<KIND, L, 8>;
-    default: return FUSED ? k_gate_fused<KIND, L, 0> : k_gate_select<KIND, L, 0>;
+    case 1: return k_gate_select<KIND, L, 1>;
+    case 2: return k_gate_select<KIND, L, 2>;
+    case 4: return k_gate_select<KIND, L, 4>;
+    case 8: return k_gate_select<KIND, L, 8>;
+    default: return k_gate_select<KIND, L, 0>;
   }
 }
-template <int KIND, bool FUSED>
+template <int KIND>
 inline GateKernel pick_l(int L, int K) {
   switch (L) {
-    case 1: return pick_k<KIND, 1, FUSED>(K);
-    case 2: return pick_k<KIND, 2, FUSED>(K);
-    case 4: return pick_k<KIND, 4, FUSED>(K);
-    case 8: return pick_k<KIND, 8, FUSED>(K);
-    case 16: return pick_k<KIND, 16, FUSED>(K);
-    default: return pick_k<KIND, 32, FUSED>(K);
+    case 1: return pick_k<KIND, 1>(K);
+    case 2: return pick_k<KIND, 2>(K);
+    case 4: return pick_k<KIND, 4>(K);
+    case 8: return pick_k<KIND, 8>(K);
+    case 16: return pick_k<KIND, 16>(K);
+    default: return pick_k<KIND, 32>(K);
   }
 }
 
 // one translation unit each (they dominate the build)
-GateKernel pick_topk(int L, int K, bool fused);   // gate_pick_topk.cu
-GateKernel pick_ktop1(int L, int K, bool fused);  // gate_pick_ktop1.cu
-GateKernel pick_hash(bool fused);                 // gate_pick_misc.cu
+GateKernel pick_topk(int L, int K);   // gate_pick_topk.cu
+GateKernel pick_ktop1(int L, int K);  // gate_pick_ktop1.cu
+GateKernel pick_hash();               // gate_pick_misc.cu
 GateKernel pick_sam(int L, int K);                // gate_pick_misc.cu
 GateKernel pick_d2s(int L);                       // gate_pick_misc.cu
 

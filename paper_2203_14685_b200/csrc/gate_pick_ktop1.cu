@@ -2,7 +2,5 @@
 #include "gate_impl.cuh"
 
 namespace moe {
-GateKernel pick_ktop1(int L, int K, bool fused) {
-  return fused ? pick_l<KIND_KTOP1, true>(L, K) : pick_l<KIND_KTOP1, false>(L, K);
-}
+GateKernel pick_ktop1(int L, int K) { return pick_l<KIND_KTOP1>(L, K); }
 }  // namespace moe

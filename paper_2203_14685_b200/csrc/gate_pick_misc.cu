@@ -4,9 +4,7 @@
 
 namespace moe {
 
-GateKernel pick_hash(bool fused) {
-  return fused ? k_gate_fused<KIND_HASH, 1, 1> : k_gate_select<KIND_HASH, 1, 1>;
-}
+GateKernel pick_hash() { return k_gate_select<KIND_HASH, 1, 1>; }
 
 template <int L>
 static GateKernel pick_sam_k(int K) {

@@ -25,7 +25,6 @@ template <int VB, int U>
 __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   using V = Vec<VB>;
   __shared__ int s_beg[257];
-  if (a.prefetch) prefetch_share_l2(a.src, (size_t)a.S * a.row_bytes);
   pdl_wait();     // routing comes from moe_gate
   pdl_trigger();
   pad_prefix(a, s_beg);
@@ -73,64 +72,6 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
       const typename V::T z = V::zero();
       for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) V::st(drow + off, z);
     }
-  }
-  if (a.sys_fence) __threadfence_system();
-}
-
-// Layout for 32-byte-vector rows with TPW consecutive tokens per warp
-// iteration: all TPW*U row loads are in flight before the first store (a
-// 2 KiB row with U = 2, TPW = 2 keeps 4 KiB per warp in flight, like a
-// 4 KiB row with U = 4).  The zero padding rows follow as their own
-// grid-stride loop over warps.
-template <int U, int TPW>
-__global__ void __launch_bounds__(kRowThreads) k_layout_t(RowArgs a) {
-  constexpr int VB = 32;
-  constexpr int SEG = 32 * U * VB;
-  __shared__ int s_beg[257];
-  pdl_wait();
-  pdl_trigger();
-  pad_prefix(a, s_beg);
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
-  const int nw = gridDim.x * kRowWarps;
-  for (int tb = gw * TPW; tb < a.S; tb += nw * TPW) {
-    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
-      V8 r[TPW][U];
-#pragma unroll
-      for (int p = 0; p < TPW; ++p)
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int off = seg + (lane + 32 * u) * VB;
-          if (tb + p < a.S && off < a.row_bytes)
-            r[p][u] = ld_stream_v8(a.src + (size_t)(tb + p) * a.row_bytes + off);
-        }
-#pragma unroll
-      for (int p = 0; p < TPW; ++p) {
-        const int t = tb + p;
-        if (t >= a.S) break;
-        for (int j = 0; j < a.k; ++j) {
-          const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
-          if (s < 0) continue;
-          char* drow = dst_row_of(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int off = seg + (lane + 32 * u) * VB;
-            if (off < a.row_bytes) st_v8(drow + off, r[p][u]);
-          }
-        }
-      }
-    }
-  }
-  const int npad = s_beg[a.E];
-  const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
-  for (int p = gw; p < npad; p += nw) {
-    int lo = 0, hi = a.E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
-    }
-    char* drow = dst_row_of(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
-    for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) st_v8(drow + off, z);
   }
   if (a.sys_fence) __threadfence_system();
 }
@@ -329,174 +270,6 @@ moe_status_t layout_fin_launch(const moe_gate_desc_t& d, const moe_routing_t& r,
   return MOE_OK;
 }
 
-// ------------------------------------------------------------ Layout_Transform, TMA
-// The same contract as k_layout, with the rows moved by the copy engine
-// instead of registers: every warp is an independent pipeline whose lane 0
-// bulk-loads x rows into a ring of NS shared-memory stages
-// (cp.async.bulk global->shared, mbarrier completion; SASS UBLKCP) and
-// bulk-stores each staged row to its <= k destinations (cp.async.bulk
-// shared->global, bulk groups).  A stage is reloaded once the stores issued
-// kTmaLag tasks ago have finished READING it, so NS - kTmaLag loads and
-// kTmaLag store groups are in flight per warp without a single register of
-// payload: bytes in flight per SM are set by shared memory, not by occupancy.
-// Each warp owns one contiguous range of the task list (x rows, then the
-// zero padding rows, which are bulk-stored from a zeroed shared row).  The
-// routing of 32 tasks is fetched at once (lane l: task base + l) and
-// broadcast with shuffles, so lane 0 never waits on an index load.
-constexpr int kTmaWarps = 4;
-constexpr int kTmaThreads = kTmaWarps * 32;
-constexpr int kTmaLag = 2;
-constexpr int kTmaMaxK = 4;  // destinations fetched per lane; larger k reads the rest inline
-
-struct TmaArgs {
-  RowArgs a;
-  int ns;  // stages per warp
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  unsigned done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_store(void* dst, unsigned src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-__device__ __forceinline__ char* dst_row(const RowArgs& a, int e, int s) { return dst_row_of(a, e, s); }
-
-__global__ void __launch_bounds__(kTmaThreads) k_layout_tma(TmaArgs ta) {
-  const RowArgs& a = ta.a;
-  const int NS = ta.ns;
-  extern __shared__ __align__(128) char smem[];
-  __shared__ int s_beg[257];
-  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps * 16];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned rb = (unsigned)a.row_bytes;
-  char* zero_row = smem;  // [row], then [warps][NS][row] stages
-  char* stages = smem + rb;
-  for (unsigned o = threadIdx.x * 16; o < rb; o += kTmaThreads * 16)
-    *reinterpret_cast<uint4*>(zero_row + o) = make_uint4(0, 0, 0, 0);
-  if (lane == 0)
-    for (int s = 0; s < NS; ++s) mbar_init(smem_u32(&s_bar[warp * 16 + s]), 1);
-  // generic-proxy zeros and barrier inits must be visible to the async proxy
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  pdl_wait();  // routing comes from moe_gate
-  pdl_trigger();
-  pad_prefix(a, s_beg);  // ends with __syncthreads (also publishes the above)
-
-  const long long n_tasks = (long long)a.S + s_beg[a.E];
-  const long long gw = (long long)blockIdx.x * kTmaWarps + warp, GW = (long long)gridDim.x * kTmaWarps;
-  const long long beg = n_tasks * gw / GW, end = n_tasks * (gw + 1) / GW;
-  const long long tok_end = min(end, (long long)a.S);
-  const int ntok = tok_end > beg ? (int)(tok_end - beg) : 0;  // x rows of this warp
-  const unsigned st0 = smem_u32(stages + (size_t)warp * NS * rb);
-  const unsigned bar0 = smem_u32(&s_bar[warp * 16]);
-
-  // prologue: the first NS x rows
-  if (lane == 0)
-    for (int o = 0; o < min(NS, ntok); ++o)
-      bulk_load(st0 + o * rb, a.src + (size_t)(beg + o) * rb, rb, bar0 + 8 * o);
-
-  int ord = 0;  // x-row ordinal of the store cursor
-  for (long long base = beg; base < end; base += 32) {
-    // routing of tasks base .. base+31, one task per lane
-    const long long my = base + lane;
-    char* dst[kTmaMaxK];
-#pragma unroll
-    for (int j = 0; j < kTmaMaxK; ++j) dst[j] = nullptr;
-    if (my < end) {
-      if (my < a.S) {
-        const int t = (int)my;
-#pragma unroll
-        for (int j = 0; j < kTmaMaxK; ++j) {
-          if (j < a.k) {
-            const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
-            if (s >= 0) {
-              const int e = __ldg(a.expert_idx + (size_t)t * a.k + j);
-              if (j == 0 || !dedupe_row(a, t, j, e, s, 0)) dst[j] = dst_row(a, e, s);
-            }
-          }
-        }
-      } else {
-        const int p = (int)(my - a.S);
-        int lo = 0, hi = a.E - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
-        }
-        dst[0] = dst_row(a, lo, min(__ldg(a.load + lo), a.cap) + (p - s_beg[lo]));
-      }
-    }
-    const int cnt = (int)min(32LL, end - base);
-    for (int u = 0; u < cnt; ++u) {
-      char* d[kTmaMaxK];
-#pragma unroll
-      for (int j = 0; j < kTmaMaxK; ++j)
-        d[j] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst[j]), u));
-      if (lane == 0) {
-        const long long task = base + u;
-        if (task < a.S) {
-          const int st = ord % NS;
-          mbar_wait(bar0 + 8 * st, (unsigned)(ord / NS) & 1u);
-          const unsigned src = st0 + st * rb;
-#pragma unroll
-          for (int j = 0; j < kTmaMaxK; ++j)
-            if (d[j]) bulk_store(d[j], src, rb);
-          for (int j = kTmaMaxK; j < a.k; ++j) {  // k > kTmaMaxK (rare)
-            const int t = (int)task;
-            const int s = __ldg(a.slot_idx + (size_t)t * a.k + j);
-            if (s >= 0) bulk_store(dst_row(a, __ldg(a.expert_idx + (size_t)t * a.k + j), s), src, rb);
-          }
-          bulk_commit();
-          // the stage of ordinal ord - kTmaLag is free once its stores have read it
-          const int o2 = ord - kTmaLag;
-          if (o2 >= 0 && o2 + NS < ntok) {
-            bulk_wait_read<kTmaLag>();
-            const int st2 = o2 % NS;
-            bulk_load(st0 + st2 * rb, a.src + (size_t)(beg + o2 + NS) * rb, rb, bar0 + 8 * st2);
-          }
-          ++ord;
-        } else {
-          bulk_store(d[0], smem_u32(zero_row), rb);
-          bulk_commit();
-        }
-      }
-    }
-  }
-  if (lane == 0) bulk_wait_all();
-  if (a.sys_fence) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence_system();
-  }
-}
-
 // ------------------------------------------------------------ Reverse + combine
 template <int DT, int U>
 __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
@@ -650,127 +423,6 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   }
 }
 
-// ------------------------------------------------------------ Reverse, TMA
-// The combine with the k admitted rows of a token brought into shared memory
-// by the copy engine: each warp is an independent pipeline over a contiguous
-// token range.  Lane 0 bulk-loads the token's rows (cp.async.bulk, one
-// mbarrier per stage with the summed expect_tx) up to NS tokens ahead; the
-// whole warp then accumulates from shared memory in fp32 (ascending j from
-// 0, the same order as k_reverse) and stores y with 32-byte vectors.  The
-// routing of 32 tokens is fetched at once (lane l: token base + l) and
-// handed to lane 0 by shuffles.  Meant for the NVLink combine, where the
-// rows come from peers' memory: bytes in flight are set by shared memory.
-constexpr int kRevTmaMaxK = 4;
-
-template <int DT>
-__global__ void __launch_bounds__(kTmaThreads) k_reverse_tma(TmaArgs ta) {
-  const RowArgs& a = ta.a;
-  const int NS = ta.ns;
-  extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps * 16];
-  __shared__ float s_w[kTmaWarps][16][kRevTmaMaxK];  // per stage: weights (0 = no row)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned rb = (unsigned)a.row_bytes, sb = rb * a.k;  // stage bytes
-  if (lane == 0)
-    for (int s = 0; s < NS; ++s) mbar_init(smem_u32(&s_bar[warp * 16 + s]), 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-  pdl_wait();
-  pdl_trigger();
-  const long long gw = (long long)blockIdx.x * kTmaWarps + warp, GW = (long long)gridDim.x * kTmaWarps;
-  const int beg = (int)((long long)a.S * gw / GW), end = (int)((long long)a.S * (gw + 1) / GW);
-  const int ntok = end - beg;
-  char* stages = smem + (size_t)warp * NS * sb;
-  const unsigned st0 = smem_u32(stages), bar0 = smem_u32(&s_bar[warp * 16]);
-  constexpr int NA = DT == MOE_F32 ? 8 : 16;
-
-  // routing of the current issue batch: lane l holds token (ibase + l)
-  const char* src[kRevTmaMaxK];
-  float wt[kRevTmaMaxK];
-  int ibase = -32;
-  int issued = 0;
-  for (int o = 0; o < ntok; ++o) {
-    // keep up to NS tokens issued ahead of the consumer
-    while (issued < ntok && issued < o + NS) {
-      if (issued >= ibase + 32) {  // next routing batch (warp-uniform)
-        ibase = issued;
-        const int tl = beg + ibase + lane;
-        const int t = a.rev ? a.S - 1 - tl : tl;  // rev: last tokens first (L2 reuse)
-#pragma unroll
-        for (int j = 0; j < kRevTmaMaxK; ++j) {
-          src[j] = nullptr;
-          wt[j] = 0.f;
-          if (j < a.k && tl < end) {
-            const int sl = __ldg(a.slot_idx + (size_t)t * a.k + j);
-            if (sl >= 0) {
-              src[j] = src_row_item(a, t, j, __ldg(a.expert_idx + (size_t)t * a.k + j), sl);
-              wt[j] = row_weight(a, (size_t)t * a.k + j);
-            }
-          }
-        }
-      }
-      const int from = issued - ibase;
-      const int st = issued % NS;
-      unsigned nrows = 0;
-      const char* ps[kRevTmaMaxK];
-#pragma unroll
-      for (int j = 0; j < kRevTmaMaxK; ++j) {
-        ps[j] = reinterpret_cast<const char*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src[j]), from));
-        const float w = __shfl_sync(0xffffffffu, wt[j], from);
-        if (lane == 0) s_w[warp][st][j] = ps[j] ? w : 0.f;
-        nrows += ps[j] ? 1u : 0u;
-      }
-      if (lane == 0) {
-        const unsigned bar = bar0 + 8 * st;
-        if (nrows == 0) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-        } else {
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                       "r"(nrows * rb)
-                       : "memory");
-#pragma unroll
-          for (int j = 0; j < kRevTmaMaxK; ++j)
-            if (ps[j])
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                  ::"r"(st0 + st * sb + j * rb), "l"(ps[j]), "r"(rb), "r"(bar)
-                  : "memory");
-        }
-      }
-      ++issued;
-    }
-    __syncwarp();
-    const int st = o % NS;
-    mbar_wait(bar0 + 8 * st, (unsigned)(o / NS) & 1u);
-    const char* stage = stages + (size_t)st * sb;
-    char* yrow = a.dst + (size_t)(a.rev ? a.S - 1 - (beg + o) : beg + o) * rb;
-    for (unsigned off = lane * 32u; off < rb; off += 32u * 32u) {
-      float acc[NA];
-#pragma unroll
-      for (int q = 0; q < NA; ++q) acc[q] = 0.f;
-      for (int j = 0; j < a.k; ++j) {
-        const float w = s_w[warp][st][j];
-        // a dropped slot has no row; a zero weight adds an exact +0 (acc
-        // starts at +0), so skipping it leaves the same bits
-        if (w == 0.f) continue;
-        const V4* v4 = reinterpret_cast<const V4*>(stage + j * rb + off);
-        V8 v;
-        const V4 lo = v4[0], hi = v4[1];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          v.w[q] = lo.w[q];
-          v.w[q + 4] = hi.w[q];
-        }
-        fma_vec<DT>(acc, w, v);
-      }
-      if (a.y_ef) st_v8_ef(yrow + off, pack_vec<DT>(acc));
-      else st_v8(yrow + off, pack_vec<DT>(acc));
-    }
-    __syncwarp();  // every lane done with the stage before lane 0 refills it
-  }
-}
-
 // 16-byte fallback of the combine for rows that are not a multiple of 32 B.
 template <int DT>
 __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
@@ -865,6 +517,20 @@ __global__ void __launch_bounds__(kRowThreads) k_chunk_permute(const char* src, 
   }
 }
 
+// dst chunk [y][x] <- src chunk [x][y] for x < X, y < Y: the two local
+// reorders of the two-level hierarchical AllToAll (HIER_2D).
+__global__ void __launch_bounds__(kRowThreads) k_chunk_transpose(const char* src, char* dst, int X,
+                                                                 int Y, long long chunk_bytes) {
+  const long long vecs = chunk_bytes / 16;
+  const long long total = (long long)X * Y * vecs;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long c = i / vecs, v = i % vecs;  // c = destination chunk (y, x)
+    const long long y = c / X, x = c % X;
+    st_v4(dst + c * chunk_bytes + v * 16, ld_stream_v4(src + (x * Y + y) * chunk_bytes + v * 16));
+  }
+}
+
 // ------------------------------------------------------------ expert offsets
 // Dropless packed form (NEXT-4; SPEC.md:241-245 Permutation.expert_offsets):
 // offsets[e] = sum_{e' < e} min(load[e'], cap), one CTA, warp scan (E <= 256).
@@ -929,52 +595,25 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.E_local = E_local;
   a.rank = rank;
   a.sys_fence = E_local != d.E;
-  a.prefetch = env_int("MOE_LAYOUT_PREFETCH", 0);  // measured slower (C2 +3 us, C3 +11 us): off
   // padding rows first when they are many (C4b: combine 46.2 -> 42.0 us,
   // its adjoint likewise; C3's 2% gained nothing)
-  a.pads_first = env_int("MOE_LAYOUT_PADS_FIRST", E_local == d.E && pad_heavy(d) ? 1 : 0);
-  // TMA pipeline: rows of 16-byte multiples with >= 2 stages per warp in a
-  // ~100 KB per-CTA budget (two CTAs per SM)
-  // TMA bulk stores: slower than the register path into local HBM, and
-  // (re-measured at P=2 with the current barrier and dedupe) over NVLink
-  // too (C2 121.2 vs 117.5 us, C3 120.8 vs 118.1, C4b 129.9 vs 124.4): off
-  const int tma_env = a.sys_fence ? env_int("MOE_P2P_LAYOUT_TMA", 0) : env_int("MOE_LAYOUT_TMA", 0);
-  const int budget = env_int("MOE_LAYOUT_TMA_SMEM", 100 * 1024);
-  const int ns = std::min(16, (budget - a.row_bytes) / (kTmaWarps * std::max(1, a.row_bytes)));
-  if (tma_env && a.row_bytes % 16 == 0 && ns >= 2) {
-    TmaArgs ta{a, ns};
-    const size_t smem = (size_t)a.row_bytes * (1 + kTmaWarps * ns);
-    cudaError_t e = cudaFuncSetAttribute((const void*)k_layout_tma,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "moe_layout: smem attribute");
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_layout_tma, kTmaThreads, smem);
-    const int occ = env_int("MOE_LAYOUT_CTAS_PER_SM", 0);
-    const int grid = (occ > 0 ? occ : std::max(1, per_sm)) * device_sm_count();
-    void* args[] = {&ta};
-    e = launch_pdl((const void*)k_layout_tma, dim3(grid), dim3(kTmaThreads), smem, stream, args);
-    if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout_tma launch");
-    return MOE_OK;
-  }
+  const moe_tuning_t& tu = tuning();
+  a.pads_first = tu.layout_pads_first >= 0 ? tu.layout_pads_first
+                                           : (E_local == d.E && pad_heavy(d) ? 1 : 0);
+  // Measured alternatives, removed: a TMA bulk-copy pipeline (slower into
+  // local HBM and over NVLink: C2 at P=2 121.2 vs 117.5 us), two tokens per
+  // warp (no gain), an L2 prefetch of x before the PDL wait (C2 +3 us).
   const void* kern;
-  const int LT = env_int("MOE_LAYOUT_TPW", 0);  // measured: no gain over k_layout<32,4>;  // TPW * U = 4 vectors in flight per lane
-  if (a.row_bytes % 32 == 0 && LT) {
-    const int segs = std::max(1, a.row_bytes / 1024);
-    kern = segs >= 4 ? (const void*)k_layout_t<4, 1>
-           : segs >= 2 ? (const void*)k_layout_t<2, 2> : (const void*)k_layout_t<1, 4>;
-  } else if (a.row_bytes % 32 == 0)
-  {
+  if (a.row_bytes % 32 == 0) {
     // measured: 2 KiB segments for rows <= 2 KiB (C2 36.3 -> 35.4 us)
-    const int lu = env_int("MOE_LAYOUT_U", a.row_bytes <= 2048 ? 2 : 4);
+    const int lu = tu.layout_u > 0 ? tu.layout_u : (a.row_bytes <= 2048 ? 2 : 4);
     kern = lu == 1 ? (const void*)k_layout<32, 1> : lu == 2 ? (const void*)k_layout<32, 2>
                                                             : (const void*)k_layout<32, 4>;
-  }
-  else
+  } else {
     kern = (const void*)k_layout<16, 4>;
+  }
   void* args[] = {&a};
-  const int occ = env_int("MOE_LAYOUT_CTAS_PER_SM", 0);
-  const int grid = occ > 0 ? occ * device_sm_count() : row_grid(kern);
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
+  cudaError_t e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout launch");
   return MOE_OK;
 }
@@ -1003,9 +642,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   // evict-first so it does not push them out.  Measured at N=1: C2 reverse
   // 36.0 -> 31.6 us, C4a 72.2 -> 64.7 us.  Over NVLink the rows live in the
   // peers' L2s and the order does not help (C2 at N=2: 252 -> 255 us).
+  const moe_tuning_t& tu = tuning();
   const int local_dflt = E_local == d.E ? 1 : 0;
-  a.rev = env_int("MOE_REVERSE_BACKWARDS", local_dflt);
-  a.y_ef = env_int("MOE_REVERSE_Y_EF", local_dflt);
+  a.rev = tu.reverse_backwards >= 0 ? tu.reverse_backwards : local_dflt;
+  a.y_ef = tu.reverse_y_ef >= 0 ? tu.reverse_y_ef : local_dflt;
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
   a.weight = r.weight;
@@ -1018,53 +658,27 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   a.speer = src;
   a.E_local = E_local;
   a.rank = rank;
-  // TMA-staged combine (peer mode by default: rows come over NVLink)
-  {
-    const bool peer = E_local != d.E;
-    // measured: TMA staging won for Switch (k = 1) on >= 4 KiB rows in the
-    // forward walk (C3: 48.5 vs 49.8 us) but not with the reversed walk,
-    // where the register path finds the dispatch in L2 (C3: 40.0 vs 52.3 us);
-    // it loses on 2 KiB rows (C4b: 69 vs 53 us) and over NVLink.  Off.
-    const int tma_dflt = (!peer && a.k == 1 && a.row_bytes >= 4096 && !a.rev) ? 1 : 0;
-    const int tma = peer ? env_int("MOE_P2P_REVERSE_TMA", 0) : env_int("MOE_REVERSE_TMA", tma_dflt);
-    const int budget = env_int("MOE_REVERSE_TMA_SMEM", 100 * 1024);
-    const int ns = std::min(16, budget / (kTmaWarps * std::max(1, a.row_bytes * a.k)));
-    if (tma && a.row_bytes % 32 == 0 && a.k <= kRevTmaMaxK && ns >= 2) {
-      TmaArgs ta{a, ns};
-      const size_t smem = (size_t)a.row_bytes * a.k * kTmaWarps * ns;
-      const void* kt = dtype == MOE_F32 ? (const void*)k_reverse_tma<MOE_F32>
-                                        : (const void*)k_reverse_tma<MOE_BF16>;
-      cudaError_t e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: smem attribute");
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, kTmaThreads, smem);
-      const int grid = std::max(1, per_sm) * device_sm_count();
-      void* args[] = {&ta};
-      e = launch_pdl(kt, dim3(grid), dim3(kTmaThreads), smem, stream, args);
-      if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: k_reverse_tma launch");
-      return MOE_OK;
-    }
-  }
+  // Measured alternatives, removed: a TMA-staged combine (won for Switch on
+  // >= 4 KiB rows only in the forward walk; the reversed register walk is
+  // faster, C3 40.0 vs 52.3 us), 16-byte vectors, two segments per round.
   const void* kern;
-  const int U = env_int("MOE_REVERSE_U", 1);
   // k <= 2 path: vectors per lane per round (x k rows); measured: 2 for
   // k = 2 (one 1 KiB segment of both rows: C2 36.3 -> 35.6 us), 4 for k = 1
   // (peer mode: 4 -- both 2 KiB rows in flight hide the NVLink latency better,
   // C2 at P=2: 129.2 -> 127.3 us)
-  const int KU = env_int("MOE_REVERSE_KU", (d.k == 2 && E_local == d.E) ? 2 : 4);
-  const bool v16 = env_int("MOE_REVERSE_V16", 0) != 0;  // force 16-byte vectors (experiment)
-  const bool kspec = !v16 && env_int("MOE_REVERSE_KSPEC", 1) && a.row_bytes % 32 == 0 && a.k <= 2;
+  const int KU = tu.reverse_ku > 0 ? tu.reverse_ku : (d.k == 2 && E_local == d.E) ? 2 : 4;
+  const bool kspec = tu.reverse_kspec && a.row_bytes % 32 == 0 && a.k <= 2;
   if (kspec) {
-    // TPW * k * U = KU (default 4) vectors in flight per lane, U covering at
-    // most one row (1 KiB of row per U step)
+    // TPW * k * U = KU vectors in flight per lane, U covering at most one
+    // row (1 KiB of row per U step)
     const bool f = dtype == MOE_F32;
     const int segs = std::max(1, a.row_bytes / 1024);  // 1 KiB per U step
     const int per = std::max(1, KU / a.k);                // U * TPW
     const int Uc = std::min(per, segs) >= 4 ? 4 : std::min(per, segs) >= 2 ? 2 : 1;
     // two tokens per warp round for Switch on <= 2 KiB rows (C4b: 51.3 vs
     // 53.5 us); no gain for k = 2
-    const int tpw_dflt = (a.k == 1 && a.row_bytes <= 2048) ? 1 : 0;
-    const int T = env_int("MOE_REVERSE_TPW", tpw_dflt) ? std::max(1, per / Uc) : 1;
+    const int tpw = tu.reverse_tpw >= 0 ? tu.reverse_tpw : (a.k == 1 && a.row_bytes <= 2048);
+    const int T = tpw ? std::max(1, per / Uc) : 1;
 #define MOE_RK(KK, UU, TT) (f ? (const void*)k_reverse_k<MOE_F32, KK, UU, TT> : (const void*)k_reverse_k<MOE_BF16, KK, UU, TT>)
     if (a.k == 1)
       kern = Uc == 4 ? (T >= 2 ? MOE_RK(1, 4, 2) : MOE_RK(1, 4, 1))
@@ -1078,18 +692,13 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     else
       kern = Uc >= 2 ? (T >= 2 ? MOE_RK(2, 2, 2) : MOE_RK(2, 2, 1)) : (T >= 2 ? MOE_RK(2, 1, 2) : MOE_RK(2, 1, 1));
 #undef MOE_RK
-  } else if (a.row_bytes % 32 == 0 && !v16) {
-    if (U == 1)
-      kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
-    else
-      kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 2> : (const void*)k_reverse<MOE_BF16, 2>;
+  } else if (a.row_bytes % 32 == 0) {
+    kern = dtype == MOE_F32 ? (const void*)k_reverse<MOE_F32, 1> : (const void*)k_reverse<MOE_BF16, 1>;
   } else {
     kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
   }
   void* args[] = {&a};
-  const int occ = env_int(E_local != d.E ? "MOE_COMBINE_CTAS_PER_SM" : "MOE_REVERSE_CTAS_PER_SM", 0);
-  const int grid = occ > 0 ? occ * device_sm_count() : row_grid(kern);
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
+  cudaError_t e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
   return MOE_OK;
 }
@@ -1130,6 +739,18 @@ moe_status_t chunk_permute_launch(const void* src, void* dst, int N, int G, long
   k_chunk_permute<<<grid, kRowThreads, 0, stream>>>(static_cast<const char*>(src),
                                                     static_cast<char*>(dst), N, G, chunk_bytes);
   MOE_CHECK_LAUNCH("moe_alltoall: k_chunk_permute launch");
+  return MOE_OK;
+}
+
+moe_status_t chunk_transpose_launch(const void* src, void* dst, int X, int Y, long long chunk_bytes,
+                                    cudaStream_t stream) {
+  const long long total = (long long)X * Y * (chunk_bytes / 16);
+  int grid = (int)std::min<long long>((total + kRowThreads - 1) / kRowThreads,
+                                      (long long)row_grid((const void*)k_chunk_transpose));
+  if (grid < 1) return MOE_OK;
+  k_chunk_transpose<<<grid, kRowThreads, 0, stream>>>(static_cast<const char*>(src),
+                                                      static_cast<char*>(dst), X, Y, chunk_bytes);
+  MOE_CHECK_LAUNCH("moe_alltoall: k_chunk_transpose launch");
   return MOE_OK;
 }
 

@@ -8,7 +8,10 @@
 //    every rank maps every peer's allocation;
 //  - device-side barrier: each rank bumps a local epoch, stores it (release,
 //    system scope) into every peer's flag slot for this rank, and spins
-//    (acquire, system scope) until all peers' flags reach it.  The epoch lives
+//    (acquire, system scope) until all peers' flags reach it, or until the
+//    tuning's barrier_timeout_ms passes (%globaltimer): then it sets this
+//    rank's device error word and returns, and moe_comm_check reports
+//    MOE_ERR_TIMEOUT instead of the stream hanging forever.  The epoch lives
 //    in device memory, so the barrier is CUDA-graph replay safe;
 //  - k_a2a_p2p: rank r copies its chunk q into rank q's receive buffer at
 //    chunk r; destinations are interleaved so all NVLink ports stay busy;
@@ -16,6 +19,12 @@
 //    the zero padding rows) directly into recv[r][e mod E/P][slot] of the
 //    expert's owner.  Both end with the barrier, so when the call completes in
 //    stream order every rank's receive buffer is complete.
+//
+// Every entry point is written as a program of steps separated by barriers
+// (run_or_queue / comm_barrier): on a real communicator each step launches
+// at once; on a simulated rank (sim.cu) the steps are queued and run later,
+// all ranks phase by phase on one GPU, so the same code is parity-tested
+// for P simulated ranks without NVLink.
 #include <cstring>
 
 #include "launch.cuh"
@@ -29,7 +38,10 @@ static moe_status_t nccl_st(ncclResult_t r, const char* what) {
 }
 
 // ------------------------------------------------------------ symmetric memory
-moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out) {
+moe_status_t sim_symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out);  // sim.cu
+moe_status_t sim_symm_release(moe_comm* c, SymmBuf& b);                // sim.cu
+
+static moe_status_t symm_alloc_ipc(moe_comm* c, size_t bytes, SymmBuf* out) {
   const int P = c->nranks, r = c->rank;
   if (P > kMaxRanks) {
     set_error("symmetric memory supports up to %d ranks (got %d)", kMaxRanks, P);
@@ -90,6 +102,10 @@ moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out) {
   return MOE_OK;
 }
 
+moe_status_t symm_alloc(moe_comm* c, size_t bytes, SymmBuf* out) {
+  return c->sim ? sim_symm_alloc(c, bytes, out) : symm_alloc_ipc(c, bytes, out);
+}
+
 void symm_release(moe_comm* c, SymmBuf& b) {
   for (int q = 0; q < c->nranks; ++q)
     if (q != c->rank && b.peer.p[q]) cudaIpcCloseMemHandle(b.peer.p[q]);
@@ -114,8 +130,37 @@ static moe_status_t host_barrier(moe_comm* c) {
   return s;
 }
 
+// Collective release: every rank is done with the buffer before anyone
+// unmaps or frees it, and nobody allocates again before every rank freed.
+moe_status_t symm_release_coll(moe_comm* c, SymmBuf& b) {
+  if (c->sim) return sim_symm_release(c, b);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_status(e, "symmetric free: sync");
+  moe_status_t s = host_barrier(c);
+  if (s != MOE_OK) return s;
+  symm_release(c, b);
+  return host_barrier(c);
+}
+
+// ------------------------------------------------------------ programs
+moe_status_t run_or_queue(moe_comm* c, cudaStream_t stream,
+                          std::function<moe_status_t(cudaStream_t)> fn) {
+  if (!c->sim) return fn(stream);
+  SimItem it;
+  it.kind = SimItem::FN;
+  it.fn = std::move(fn);
+  c->queue.push_back(std::move(it));
+  return MOE_OK;
+}
+
 // ------------------------------------------------------------ device barrier
-__global__ void k_barrier(PeerPtrs sig, int P, int rank, int mode) {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_barrier(PeerPtrs sig, int P, int rank, unsigned long long timeout_ns) {
   __shared__ unsigned long long s_e;
   unsigned long long* mine = reinterpret_cast<unsigned long long*>(sig.p[rank]);
   pdl_wait();     // everything before us in the stream is complete
@@ -126,30 +171,40 @@ __global__ void k_barrier(PeerPtrs sig, int P, int rank, int mode) {
   }
   __syncthreads();
   const unsigned long long e = s_e;
-  if (mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");  // one fence, then releases
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // one fence, then the releases
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     unsigned long long* flag = reinterpret_cast<unsigned long long*>(sig.p[q]) + rank;
-    if (mode == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
   }
+  const unsigned long long t0 = globaltimer_ns();
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     unsigned long long v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + q) : "memory");
-    } while (v < e);
+      if (v >= e) break;
+      if (timeout_ns && globaltimer_ns() - t0 > timeout_ns) {
+        // a peer never arrived: flag it and let the stream go on
+        atomicOr(reinterpret_cast<unsigned*>(sig.p[rank] + kErrOff), (unsigned)kErrBarrierTimeout);
+        return;
+      }
+    }
   }
 }
 
 moe_status_t barrier_launch(const PeerPtrs& sig, int nranks, int rank, cudaStream_t stream) {
-  // PDL: the barrier's launch overlaps its predecessor's tail (it waits for
-  // the predecessor's completion in griddepcontrol.wait before signalling)
-  int mode = env_int("MOE_BARRIER_MODE", 1);  // 0: fence per peer, 1: one fence (default), 2: none
-  void* args[] = {(void*)&sig, &nranks, &rank, &mode};
-  cudaError_t e = env_int("MOE_BARRIER_PDL", 0)  // measured slower in the step graph: off
-                      ? launch_pdl((const void*)k_barrier, dim3(1), dim3(32), 0, stream, args)
-                      : cudaLaunchKernel((const void*)k_barrier, dim3(1), dim3(32), args, 0, stream);
+  // a plain launch (with PDL it measured slower in the step graph)
+  unsigned long long to = (unsigned long long)tuning().barrier_timeout_ms * 1000000ull;
+  void* args[] = {(void*)&sig, &nranks, &rank, &to};
+  cudaError_t e = cudaLaunchKernel((const void*)k_barrier, dim3(1), dim3(32), args, 0, stream);
   if (e != cudaSuccess) return cuda_status(e, "moe_comm_barrier: launch");
   return MOE_OK;
+}
+
+moe_status_t sim_barrier(moe_comm* c, cudaStream_t stream);  // sim.cu
+
+moe_status_t comm_barrier(moe_comm* c, cudaStream_t stream) {
+  if (c->sim) return sim_barrier(c, stream);
+  return barrier_launch(c->sig.peer, c->nranks, c->rank, stream);
 }
 
 // ------------------------------------------------------------ P2P AllToAll
@@ -188,7 +243,7 @@ __global__ void __launch_bounds__(256) k_a2a_p2p(const char* __restrict__ send, 
 moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_off_rank,
                             size_t bytes_per_peer, int nranks, int rank, cudaStream_t stream) {
   const size_t pieces = ((bytes_per_peer + 65535) / 65536) * nranks;
-  int grid = (int)std::min<size_t>(pieces, (size_t)device_sm_count() * env_int("MOE_A2A_CTAS_PER_SM", 4));
+  int grid = (int)std::min<size_t>(pieces, (size_t)device_sm_count() * tuning().a2a_ctas_per_sm);
   if (grid < 1) grid = 1;
   void* args[] = {(void*)&send, (void*)&recv, &recv_off_rank, &bytes_per_peer, &nranks, &rank};
   cudaError_t e = launch_pdl((const void*)k_a2a_p2p, dim3(grid), dim3(256), 0, stream, args);
@@ -197,6 +252,11 @@ moe_status_t a2a_p2p_launch(const char* send, const PeerPtrs& recv, size_t recv_
 }
 
 // ------------------------------------------------------------ local padding
+static bool local_pad_on(const moe_gate_desc_t& d) {
+  const int t = tuning().p2p_local_pad;
+  return t >= 0 ? t != 0 : pad_heavy(d);
+}
+
 // After the padded one-sided dispatch's exit barrier: zero this rank's own
 // padding rows [cnt, cap) of every (source rank, local expert) block of recv
 // ([P][El][cap] rows), cnt from the padding-count table the senders filled.
@@ -248,14 +308,12 @@ __global__ void __launch_bounds__(256) k_pad_fill(char* recv, const int* tab, in
   }
 }
 
-static moe_status_t pad_fill_launch(moe_comm* comm, char* local, int El, int cap, int row_bytes,
-                                    cudaStream_t stream) {
-  const int P = comm->nranks;
+// tab: this rank's padding-count table (sig + kPadTabOff)
+static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, int cap,
+                                    int row_bytes, cudaStream_t stream) {
   const int nrows_pad_max = P * El * cap;
   const int grid = std::max(1, std::min(device_sm_count() * 4, (nrows_pad_max + 7) / 8));
-  const int* tl = reinterpret_cast<const int*>(comm->sig.peer.p[comm->rank] + kPadTabOff);
-  int Pv = P, Elv = El, capv = cap, rb = row_bytes;
-  void* args[] = {&local, (void*)&tl, &Pv, &Elv, &capv, &rb};
+  void* args[] = {&local, (void*)&tab, &P, &El, &cap, &row_bytes};
   cudaError_t e = launch_pdl((const void*)k_pad_fill, dim3(grid), dim3(256), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "k_pad_fill launch");
   return MOE_OK;
@@ -315,33 +373,31 @@ moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_byt
 // rows: used when k >= 2, two experts can share an owner (E/P >= 2) and the
 // exit barrier runs.  Allocated (collectively: every rank makes the same call)
 // on first use outside stream capture; inside a capture without a table the
-// dispatch just sends every row (same result).  nullptr: no dedupe.
-static const PeerPtrs* dup_table(moe_comm* c, const moe_gate_desc_t& d, int32_t flags,
-                                 cudaStream_t stream, moe_status_t* st) {
+// dispatch just sends every row (same result).  Returns false: no dedupe.
+static bool dup_table(moe_comm* c, const moe_gate_desc_t& d, int32_t flags, cudaStream_t stream,
+                      PeerPtrs* out, moe_status_t* st) {
   *st = MOE_OK;
   const int P = c->nranks;
-  if (P < 2 || d.k < 2 || d.E / P < 2 || (flags & MOE_P2P_NO_EXIT_BARRIER) ||
-      !env_int("MOE_P2P_DEDUPE", 1))
-    return nullptr;
+  if (P < 2 || d.k < 2 || d.E / P < 2 || (flags & MOE_P2P_NO_EXIT_BARRIER) || !tuning().p2p_dedupe)
+    return false;
   const size_t want = (size_t)d.E * d.capacity * sizeof(int);
-  if (c->dup.base && c->dup.bytes >= want) return &c->dup.peer;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-    return nullptr;
-  if (c->dup.base) {  // grow: every rank is done with the old table
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) {
-      *st = cuda_status(e, "dispatch dedupe table: sync");
-      return nullptr;
+  if (!(c->dup.base && c->dup.bytes >= want)) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return false;
+    if (c->dup.base) {  // grow: collectively, after every rank is done with the old table
+      *st = symm_release_coll(c, c->dup);
+      c->dup = SymmBuf{};
+      if (*st != MOE_OK) return false;
     }
-    symm_release(c, c->dup);
+    *st = symm_alloc(c, want, &c->dup);
+    if (*st != MOE_OK) {
+      c->dup = SymmBuf{};
+      return false;
+    }
   }
-  *st = symm_alloc(c, want, &c->dup);
-  if (*st != MOE_OK) {
-    c->dup = SymmBuf{};
-    return nullptr;
-  }
-  return &c->dup.peer;
+  *out = c->dup.peer;
+  return true;
 }
 
 // ------------------------------------------------------------ dropless exchange
@@ -390,6 +446,143 @@ __global__ void __launch_bounds__(256) k_a2av_plan(PeerPtrs counts, int P, int E
   }
 }
 
+// ------------------------------------------------------------ argument checks
+static moe_status_t need_p2p(const char* fn, moe_comm_t* comm) {
+  if (!comm) {
+    set_error("%s: comm is NULL", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (!comm->p2p_ok) {
+    set_error("%s: peer memory is not available between these GPUs", fn);
+    return MOE_ERR_UNSUPPORTED;
+  }
+  return MOE_OK;
+}
+
+// The symmetric buffer of `bytes` at p, with its per-rank mappings.
+static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
+                               PeerPtrs* out) {
+  const SymmBuf* b = find_symm(comm, p, bytes);
+  if (!b) {
+    set_error("%s: a buffer of %zu bytes is not inside a symmetric buffer (moe_comm_symm_alloc)",
+              fn, bytes);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const size_t off = static_cast<const char*>(p) - b->base;
+  *out = PeerPtrs{};
+  for (int q = 0; q < comm->nranks; ++q) out->p[q] = b->peer.p[q] + off;
+  return MOE_OK;
+}
+
+// Shared checks of the padded entry points; fills the peer pointers of `buf`.
+static moe_status_t p2p_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
+                             const moe_routing_t* routing, const void* a, const void* buf,
+                             int32_t d, int32_t dtype, PeerPtrs* peers, int* ds) {
+  moe_status_t s = need_p2p(fn, comm);
+  if (s != MOE_OK) return s;
+  if (!desc || !routing || !routing->expert_idx || !routing->slot_idx || !a || !buf || d < 1 ||
+      (dtype != MOE_F32 && dtype != MOE_BF16)) {
+    set_error("%s: bad arguments", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (desc->E % P != 0 || desc->E > 256 || desc->S < 1 || desc->k < 1 || desc->capacity < 1) {
+    set_error("%s: E=%d experts must shard over %d ranks (E <= 256, S, k, cap >= 1)", fn, desc->E, P);
+    return MOE_ERR_INVALID_ARG;
+  }
+  *ds = dtype == MOE_F32 ? 4 : 2;
+  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
+      reinterpret_cast<uintptr_t>(buf) % 16) {
+    set_error("%s: rows and pointers must be 16-byte aligned", fn);
+    return MOE_ERR_ALIGNMENT;
+  }
+  return symm_peers(fn, comm, buf, (size_t)desc->E * desc->capacity * d * *ds, peers);
+}
+
+static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                const moe_routing_t* routing, const int32_t* offsets,
+                                const void* a, const void* buf, int64_t rows, int32_t d,
+                                int32_t dtype, PeerPtrs* peers, int* ds) {
+  moe_status_t s = need_p2p(fn, comm);
+  if (s != MOE_OK) return s;
+  if (!desc || !routing || !routing->expert_idx || !routing->slot_idx || !offsets || !a || !buf ||
+      d < 1 || (dtype != MOE_F32 && dtype != MOE_BF16)) {
+    set_error("%s: bad arguments", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks;
+  if (desc->E % P != 0 || desc->E > 256) {
+    set_error("%s: E=%d experts must shard over %d ranks (E <= 256)", fn, desc->E, P);
+    return MOE_ERR_INVALID_ARG;
+  }
+  if ((int64_t)P * desc->S * desc->k > rows) {
+    set_error("%s: buffer of %lld rows < nranks*S*k = %lld (the worst case)", fn, (long long)rows,
+              (long long)P * desc->S * desc->k);
+    return MOE_ERR_INVALID_ARG;
+  }
+  *ds = dtype == MOE_F32 ? 4 : 2;
+  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
+      reinterpret_cast<uintptr_t>(buf) % 16) {
+    set_error("%s: rows and pointers must be 16-byte aligned", fn);
+    return MOE_ERR_ALIGNMENT;
+  }
+  return symm_peers(fn, comm, buf, (size_t)rows * d * *ds, peers);
+}
+
+static PeerPtrs pad_tables(const moe_comm* c) {
+  PeerPtrs tab{};
+  for (int q = 0; q < c->nranks; ++q) tab.p[q] = c->sig.peer.p[q] + kPadTabOff;
+  return tab;
+}
+
+// Padded one-sided dispatch after the entry barrier (shared by the dispatch
+// and the push-form combine adjoint's dy scatter): rows into the owners'
+// `dst`, then (unless NO_EXIT) the exit barrier, the owners' duplicate-row
+// copies and local padding.  *dup_pending: duplicate copies were enqueued.
+static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, const moe_routing_t& R,
+                                  const void* x, int ds, int d, const PeerPtrs& dst, int32_t flags,
+                                  cudaStream_t stream, bool* dup_pending) {
+  const int P = comm->nranks, r = comm->rank, El = D.E / P;
+  const bool exit_bar = !(flags & MOE_P2P_NO_EXIT_BARRIER);
+  // local padding: the zero rows are written by their owner after the exit
+  // barrier instead of crossing NVLink (needs that barrier; E/P <= 256).
+  // Default when at least ~5% of the rows are padding whatever the routing
+  // (E*cap > 1.05*S*k, e.g. the hash config's C = 1.25: C4b dispatch 165 ->
+  // 132 us at N=2); with C = 1 the padding is only the imbalance and the
+  // extra kernel costs more than it saves (C2: +1.7 us).
+  const bool local_pad = exit_bar && El <= kPadTabStride && local_pad_on(D);
+  const PeerPtrs tab = pad_tables(comm);
+  PeerPtrs dup{};
+  moe_status_t s;
+  const bool dedupe = dup_table(comm, D, flags, stream, &dup, &s);
+  if (s != MOE_OK) return s;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, nullptr, nullptr,
+                               local_pad ? &tab : nullptr, dedupe ? &dup : nullptr);
+  });
+  if (s != MOE_OK) return s;
+  *dup_pending = false;
+  if (!exit_bar) return MOE_OK;
+  s = comm_barrier(comm, stream);  // every row has landed
+  if (s != MOE_OK) return s;
+  const long long nrows = (long long)D.E * D.capacity;
+  const int rb = d * ds;
+  char* mine = dst.p[r];
+  if (dedupe) {
+    int* dtab = reinterpret_cast<int*>(dup.p[r]);
+    s = run_or_queue(comm, stream,
+                     [=](cudaStream_t st) { return dup_fill_launch(mine, dtab, nrows, rb, st); });
+    if (s != MOE_OK) return s;
+    *dup_pending = true;
+  }
+  if (!local_pad) return MOE_OK;
+  const int* ptab = reinterpret_cast<const int*>(tab.p[r]);
+  const int cap = D.capacity;
+  return run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return pad_fill_launch(mine, ptab, P, El, cap, rb, st);
+  });
+}
+
 }  // namespace moe
 
 using namespace moe;
@@ -401,12 +594,10 @@ moe_status_t moe_comm_symm_alloc(moe_comm_t* comm, size_t bytes, void** out) {
     set_error("moe_comm_symm_alloc: bad arguments");
     return MOE_ERR_INVALID_ARG;
   }
-  if (!comm->p2p_ok) {
-    set_error("moe_comm_symm_alloc: peer memory is not available between these GPUs");
-    return MOE_ERR_UNSUPPORTED;
-  }
+  moe_status_t s = need_p2p("moe_comm_symm_alloc", comm);
+  if (s != MOE_OK) return s;
   SymmBuf b;
-  moe_status_t s = symm_alloc(comm, bytes, &b);
+  s = symm_alloc(comm, bytes, &b);
   if (s != MOE_OK) return s;
   comm->symm.push_back(b);
   *out = b.base;
@@ -420,13 +611,9 @@ moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* p) {
   }
   for (size_t i = 0; i < comm->symm.size(); ++i) {
     if (comm->symm[i].base == p) {
-      cudaError_t e = cudaDeviceSynchronize();
-      if (e != cudaSuccess) return cuda_status(e, "moe_comm_symm_free: sync");
-      moe_status_t s = host_barrier(comm);  // nobody still reads/writes it
-      if (s != MOE_OK) return s;
-      symm_release(comm, comm->symm[i]);
+      moe_status_t s = symm_release_coll(comm, comm->symm[i]);
       comm->symm.erase(comm->symm.begin() + i);
-      return host_barrier(comm);
+      return s;
     }
   }
   set_error("moe_comm_symm_free: %p is not a symmetric buffer of this communicator", p);
@@ -434,50 +621,31 @@ moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* p) {
 }
 
 moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream) {
-  if (!comm) {
-    set_error("moe_comm_barrier: comm is NULL");
-    return MOE_ERR_INVALID_ARG;
-  }
-  if (!comm->p2p_ok) {
-    set_error("moe_comm_barrier: peer memory is not available between these GPUs");
-    return MOE_ERR_UNSUPPORTED;
-  }
-  return barrier_launch(comm->sig.peer, comm->nranks, comm->rank,
-                        reinterpret_cast<cudaStream_t>(stream));
+  moe_status_t s = need_p2p("moe_comm_barrier", comm);
+  if (s != MOE_OK) return s;
+  return comm_barrier(comm, reinterpret_cast<cudaStream_t>(stream));
 }
 
-// Shared checks of the fused entry points; fills the peer pointers of `buf`.
-static moe_status_t p2p_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
-                             const moe_routing_t* routing, const void* a, const void* buf,
-                             int32_t d, int32_t dtype, PeerPtrs* peers, int* ds) {
-  if (!comm || !desc || !routing || !a || !buf || d < 1 || (dtype != MOE_F32 && dtype != MOE_BF16)) {
-    set_error("%s: bad arguments", fn);
+moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                              const moe_routing_t* routing, const void* x, int32_t d,
+                              int32_t dtype, void* recv, int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs dst;
+  int ds = 0;
+  moe_status_t s = p2p_args("moe_dispatch_p2p", comm, desc, routing, x, recv, d, dtype, &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->load) {
+    set_error("moe_dispatch_p2p: routing.load is NULL");
     return MOE_ERR_INVALID_ARG;
   }
-  if (!comm->p2p_ok) {
-    set_error("%s: peer memory is not available between these GPUs", fn);
-    return MOE_ERR_UNSUPPORTED;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // every owner is ready to receive
+    s = comm_barrier(comm, stream);
+    if (s != MOE_OK) return s;
   }
-  const int P = comm->nranks;
-  if (desc->E % P != 0) {
-    set_error("%s: E=%d experts do not shard over %d ranks", fn, desc->E, P);
-    return MOE_ERR_INVALID_ARG;
-  }
-  *ds = dtype == MOE_F32 ? 4 : 2;
-  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
-      reinterpret_cast<uintptr_t>(buf) % 16) {
-    set_error("%s: rows and pointers must be 16-byte aligned", fn);
-    return MOE_ERR_ALIGNMENT;
-  }
-  const size_t bytes = (size_t)desc->E * desc->capacity * d * *ds;
-  const SymmBuf* b = find_symm(comm, buf, bytes);
-  if (!b) {
-    set_error("%s: the [E,cap,d] buffer (%zu bytes) is not inside a symmetric buffer "
-              "(moe_comm_symm_alloc)", fn, bytes);
-    return MOE_ERR_INVALID_ARG;
-  }
-  const size_t off = static_cast<const char*>(buf) - b->base;
-  for (int q = 0; q < P; ++q) peers->p[q] = b->peer.p[q] + off;
+  bool dup_pending = false;
+  s = dispatch_body(comm, *desc, *routing, x, ds, d, dst, flags, stream, &dup_pending);
+  if (s != MOE_OK) return s;
+  comm->dup_recv = dup_pending ? recv : nullptr;
   return MOE_OK;
 }
 
@@ -494,73 +662,31 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     set_error("moe_combine_p2p: routing.weight is NULL");
     return MOE_ERR_INVALID_ARG;
   }
-  const int P = comm->nranks;
+  const int P = comm->nranks, r = comm->rank;
   // A dispatch that sent duplicate rows once left their copies to the owners
-  // (k_dup_fill after its exit barrier): reading recv before every owner got
-  // there races with those copies, so the entry barrier is kept then.
-  // With NO_ENTRY_BARRIER, recv still holds exactly what the dispatch sent,
-  // so the combine reads such a slot from the row that was sent (alias mode,
-  // default) instead of waiting for the copies (MOE_P2P_COMBINE_ALIAS=0).
+  // (k_dup_fill after its exit barrier).  Unless the caller says recv still
+  // holds exactly what that dispatch sent (MOE_P2P_RECV_UNMODIFIED: no
+  // expert wrote it), those copies must be complete before any read, so the
+  // entry barrier is kept even under NO_ENTRY_BARRIER.  With
+  // RECV_UNMODIFIED the combine reads such a slot from the row that was sent
+  // (alias mode: the bytes are the same) and does not wait for the copies.
   const bool dup_pending = comm->dup_recv && comm->dup_recv == expert_out;
   comm->dup_recv = nullptr;
   const bool no_entry = flags & MOE_P2P_NO_ENTRY_BARRIER;
-  const int alias = dup_pending && no_entry && env_int("MOE_P2P_COMBINE_ALIAS", 1) ? 1 : 0;
+  const int alias = dup_pending && (flags & MOE_P2P_RECV_UNMODIFIED) ? 1 : 0;
   if (!no_entry || (dup_pending && !alias)) {  // every rank's expert is done
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream,
-                           nullptr, nullptr, alias);
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return reverse_launch_peers(D, R, src, D.E / P, r, dtype, ds, d, y, st, nullptr, nullptr,
+                                alias);
+  });
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // nobody reads them any more
-}
-
-moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
-                              const moe_routing_t* routing, const void* x, int32_t d,
-                              int32_t dtype, void* recv, int32_t flags, moe_stream_t stream_) {
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  PeerPtrs dst;
-  int ds = 0;
-  moe_status_t s0 = p2p_args("moe_dispatch_p2p", comm, desc, routing, x, recv, d, dtype, &dst, &ds);
-  if (s0 != MOE_OK) return s0;
-  if (!routing->load) {
-    set_error("moe_dispatch_p2p: routing.load is NULL");
-    return MOE_ERR_INVALID_ARG;
-  }
-  const int P = comm->nranks;
-  moe_status_t s;
-  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // every owner is ready to receive
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
-    if (s != MOE_OK) return s;
-  }
-  // local padding: the zero rows are written by their owner after the exit
-  // barrier instead of crossing NVLink (needs that barrier; E/P <= 256)
-  const int El = desc->E / P;
-  // Default when at least ~5% of the rows are padding whatever the routing
-  // (E*cap > 1.05*S*k, e.g. the hash config's C = 1.25: C4b dispatch 165 ->
-  // 132 us at N=2); with C = 1 the padding is only the imbalance and the
-  // extra kernel costs more than it saves (C2: +1.7 us).
-  const bool local_pad = !(flags & MOE_P2P_NO_EXIT_BARRIER) && El <= kPadTabStride &&
-                         env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
-  PeerPtrs tab{};
-  for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
-  const PeerPtrs* dup = dup_table(comm, *desc, flags, stream, &s);
-  if (s != MOE_OK) return s;
-  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, nullptr, nullptr,
-                          local_pad ? &tab : nullptr, dup);
-  if (s != MOE_OK) return s;
-  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
-  if (s != MOE_OK) return s;
-  if (dup) {
-    s = dup_fill_launch(dst.p[comm->rank], reinterpret_cast<int*>(dup->p[comm->rank]),
-                        (long long)desc->E * desc->capacity, d * ds, stream);
-    if (s != MOE_OK) return s;
-    comm->dup_recv = recv;
-  }
-  if (!local_pad) return MOE_OK;
-  return pad_fill_launch(comm, dst.p[comm->rank], El, desc->capacity, d * ds, stream);
+  return comm_barrier(comm, stream);  // nobody reads them any more
 }
 
 moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -578,23 +704,29 @@ moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc
     set_error("moe_gate_dispatch_p2p: routing.load is NULL");
     return MOE_ERR_INVALID_ARG;
   }
-  if (((long long)d * ds) % 32 != 0 || desc->k > 32 || !env_int("MOE_GATE_LAYOUT_FUSED", 1)) {
-    s = gate_launch(*desc, *in, *out, ws, stream);  // the unfused pair
+  const moe_gate_desc_t D = *desc;
+  const moe_gate_inputs_t I = *in;
+  const moe_routing_t R = *out;
+  if (((long long)d * ds) % 32 != 0 || desc->k > 32) {
+    s = run_or_queue(comm, stream, [=](cudaStream_t st) { return gate_launch(D, I, R, ws, st); });
     if (s != MOE_OK) return s;
     return moe_dispatch_p2p(comm, desc, out, x, d, dtype, recv, flags, stream_);
   }
-  const int P = comm->nranks;
+  const int P = comm->nranks, r = comm->rank;
   if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  GateFinalize fin{};
-  s = gate_select_launch(*desc, *in, *out, ws, stream, &fin);
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    GateFinalize fin{};
+    moe_status_t s2 = gate_select_launch(D, I, R, ws, st, &fin);
+    if (s2 != MOE_OK) return s2;
+    return layout_fin_launch(D, R, x, ds, d, dst, D.E / P, r, fin, st);
+  });
   if (s != MOE_OK) return s;
-  s = layout_fin_launch(*desc, *out, x, ds, d, dst, desc->E / P, comm->rank, fin, stream);
-  if (s != MOE_OK) return s;
+  comm->dup_recv = nullptr;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+  return comm_barrier(comm, stream);
 }
 
 moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -603,36 +735,31 @@ moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* d
                                       void* d_expert_out, float* d_weight, int32_t flags,
                                       moe_stream_t stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_combine_backward_p2p";
   PeerPtrs src, dst;
   int ds = 0;
-  moe_status_t s = p2p_args("moe_combine_backward_p2p", comm, desc, routing, dy, expert_out, d,
-                            dtype, &src, &ds);
+  moe_status_t s = p2p_args(fn, comm, desc, routing, dy, expert_out, d, dtype, &src, &ds);
   if (s != MOE_OK) return s;
-  s = p2p_args("moe_combine_backward_p2p", comm, desc, routing, dy, d_expert_out, d, dtype, &dst,
-               &ds);
+  s = p2p_args(fn, comm, desc, routing, dy, d_expert_out, d, dtype, &dst, &ds);
   if (s != MOE_OK) return s;
   if (!routing->weight || !routing->load || !d_weight) {
-    set_error("moe_combine_backward_p2p: routing.weight, routing.load and d_weight are required");
+    set_error("%s: routing.weight, routing.load and d_weight are required", fn);
     return MOE_ERR_INVALID_ARG;
   }
-  const int P = comm->nranks;
+  const int P = comm->nranks, r = comm->rank;
   if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  s = combine_bwd_launch(*desc, *routing, dy, src, dst, desc->E / P, comm->rank, dtype, ds, d,
-                         d_weight, stream);
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return combine_bwd_launch(D, R, dy, src, dst, D.E / P, r, dtype, ds, d, d_weight, st);
+  });
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+  return comm_barrier(comm, stream);
 }
-
-static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
-                               PeerPtrs* out);
-static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
-                                const moe_routing_t* routing, const int32_t* offsets,
-                                const void* a, const void* buf, int64_t rows, int32_t d,
-                                int32_t dtype, PeerPtrs* peers, int* ds);
 
 moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                                            const moe_routing_t* routing, const void* dy,
@@ -658,42 +785,135 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
   if (s != MOE_OK) return s;
   const int P = comm->nranks, r = comm->rank;
   if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, r, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  // dy rows to the experts' owners (the dispatch kernel; padding rows zero,
-  // written by the owners themselves when padding is heavy)
-  const int El = desc->E / P;
-  const bool local_pad = El <= kPadTabStride && env_int("MOE_P2P_LOCAL_PAD", pad_heavy(*desc) ? 1 : 0);
-  PeerPtrs tab{};
-  for (int q = 0; q < P; ++q) tab.p[q] = comm->sig.peer.p[q] + kPadTabOff;
-  // (a top-2 token's dy row goes once to an owner of both its experts)
-  const PeerPtrs* dup = dup_table(comm, *desc, 0, stream, &s);
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  // the slot weights to the experts' owners, then dy rows (the dispatch
+  // kernel: a top-2 token's dy row goes once to an owner of both its
+  // experts; padding rows zero, written by the owners themselves when
+  // padding is heavy); exit barrier; the owners' duplicate copies, padding
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return push_bwd_launch(D, R, wt, dwt, nullptr, nullptr, nullptr, P, r, dtype, d * ds, 0, st);
+  });
   if (s != MOE_OK) return s;
-  s = layout_launch_peers(*desc, *routing, dy, ds, d, dst, El, r, stream, nullptr, nullptr,
-                          local_pad ? &tab : nullptr, dup);
+  bool dup_pending = false;
+  s = dispatch_body(comm, D, R, dy, ds, d, dst, 0, stream, &dup_pending);
   if (s != MOE_OK) return s;
-  s = push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, nullptr, P, r, dtype, d * ds, 0,
-                      stream);
+  // owners: scale in place, dot with the local expert rows into the token
+  // owners' dw tables; barrier; token owners gather d_weight
+  char* deo = static_cast<char*>(d_expert_out);
+  const char* eo = static_cast<const char*>(expert_out);
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return push_bwd_launch(D, R, wt, dwt, deo, eo, nullptr, P, r, dtype, d * ds, 1, st);
+  });
   if (s != MOE_OK) return s;
-  s = barrier_launch(comm->sig.peer, P, r, stream);  // rows and weights landed
+  s = comm_barrier(comm, stream);  // dots landed, d_expert_out final
   if (s != MOE_OK) return s;
-  if (dup) {
-    s = dup_fill_launch(static_cast<char*>(d_expert_out), reinterpret_cast<int*>(dup->p[r]),
-                        (long long)desc->E * desc->capacity, d * ds, stream);
+  return run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return push_bwd_launch(D, R, wt, dwt, nullptr, nullptr, d_weight, P, r, dtype, d * ds, 2, st);
+  });
+}
+
+moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                       const moe_routing_t* routing, const void* d_recv,
+                                       int32_t d, int32_t dtype, void* dx, int32_t flags,
+                                       moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = p2p_args("moe_dispatch_backward_p2p", comm, desc, routing, dx, d_recv, d, dtype,
+                            &src, &ds);
+  if (s != MOE_OK) return s;
+  const int P = comm->nranks, r = comm->rank;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  if (local_pad) {
-    s = pad_fill_launch(comm, static_cast<char*>(d_expert_out), El, desc->capacity, d * ds, stream);
+  const moe_gate_desc_t D = *desc;
+  moe_routing_t unit = *routing;
+  unit.weight = nullptr;  // adjoint of the dispatch copy: unit-weight combine
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return reverse_launch_peers(D, unit, src, D.E / P, r, dtype, ds, d, dx, st);
+  });
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return comm_barrier(comm, stream);
+}
+
+moe_status_t moe_dispatch_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                     const moe_routing_t* routing, const int32_t* offsets,
+                                     int32_t* counts, int32_t* peer_base, int32_t* recv_offsets,
+                                     const void* x, int32_t d, int32_t dtype, void* recv,
+                                     int64_t recv_cap_rows, int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_dispatch_packed_p2p";
+  PeerPtrs dst, cnt;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, x, recv, recv_cap_rows, d, dtype,
+                               &dst, &ds);
+  if (s != MOE_OK) return s;
+  if (!counts || !peer_base || !recv_offsets) {
+    set_error("%s: counts, peer_base and recv_offsets are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  s = symm_peers(fn, comm, counts, sizeof(int32_t) * (size_t)desc->E, &cnt);
+  if (s != MOE_OK) return s;
+  const int P = comm->nranks, r = comm->rank, El = desc->E / P;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // owners done with the previous step's tables
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  s = push_bwd_launch(*desc, *routing, wt, dwt, static_cast<char*>(d_expert_out),
-                      static_cast<const char*>(expert_out), nullptr, P, r, dtype, d * ds, 1, stream);
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    k_a2av_counts<<<1, 256, 0, st>>>(offsets, cnt, D.E, El, r);
+    MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: counts launch");
+    return MOE_OK;
+  });
   if (s != MOE_OK) return s;
-  s = barrier_launch(comm->sig.peer, P, r, stream);  // dots landed, d_expert_out final
+  s = comm_barrier(comm, stream);  // every table complete
   if (s != MOE_OK) return s;
-  return push_bwd_launch(*desc, *routing, wt, dwt, nullptr, nullptr, d_weight, P, r, dtype,
-                         d * ds, 2, stream);
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    k_a2av_plan<<<1, 256, 0, st>>>(cnt, P, El, r, peer_base, recv_offsets);
+    MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: plan launch");
+    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, offsets, peer_base);
+  });
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return comm_barrier(comm, stream);  // every row has landed
+}
+
+moe_status_t moe_combine_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
+                                    const moe_routing_t* routing, const int32_t* offsets,
+                                    const int32_t* peer_base, const void* expert_out, int32_t d,
+                                    int32_t dtype, int64_t expert_out_rows, void* y,
+                                    int32_t flags, moe_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const char* fn = "moe_combine_packed_p2p";
+  PeerPtrs src;
+  int ds = 0;
+  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, y, expert_out, expert_out_rows, d,
+                               dtype, &src, &ds);
+  if (s != MOE_OK) return s;
+  if (!routing->weight || !peer_base) {
+    set_error("%s: routing.weight and peer_base are required", fn);
+    return MOE_ERR_INVALID_ARG;
+  }
+  const int P = comm->nranks, r = comm->rank;
+  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
+    s = comm_barrier(comm, stream);
+    if (s != MOE_OK) return s;
+  }
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return reverse_launch_peers(D, R, src, D.E / P, r, dtype, ds, d, y, st, offsets, peer_base);
+  });
+  if (s != MOE_OK) return s;
+  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
+  return comm_barrier(comm, stream);
 }
 
 moe_status_t moe_combine_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -715,16 +935,20 @@ moe_status_t moe_combine_packed_backward_p2p(moe_comm_t* comm, const moe_gate_de
     set_error("%s: routing.weight, peer_base and d_weight are required", fn);
     return MOE_ERR_INVALID_ARG;
   }
-  const int P = comm->nranks;
+  const int P = comm->nranks, r = comm->rank;
   if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  s = combine_bwd_launch(*desc, *routing, dy, src, dst, desc->E / P, comm->rank, dtype, ds, d,
-                         d_weight, stream, offsets, peer_base);
+  const moe_gate_desc_t D = *desc;
+  const moe_routing_t R = *routing;
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return combine_bwd_launch(D, R, dy, src, dst, D.E / P, r, dtype, ds, d, d_weight, st, offsets,
+                              peer_base);
+  });
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+  return comm_barrier(comm, stream);
 }
 
 moe_status_t moe_dispatch_packed_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -743,151 +967,20 @@ moe_status_t moe_dispatch_packed_backward_p2p(moe_comm_t* comm, const moe_gate_d
     set_error("%s: peer_base is required", fn);
     return MOE_ERR_INVALID_ARG;
   }
-  const int P = comm->nranks;
+  const int P = comm->nranks, r = comm->rank;
   if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
+    s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
+  const moe_gate_desc_t D = *desc;
   moe_routing_t unit = *routing;
   unit.weight = nullptr;
-  s = reverse_launch_peers(*desc, unit, src, desc->E / P, comm->rank, dtype, ds, d, dx, stream,
-                           offsets, peer_base);
+  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+    return reverse_launch_peers(D, unit, src, D.E / P, r, dtype, ds, d, dx, st, offsets, peer_base);
+  });
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
-}
-
-moe_status_t moe_dispatch_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
-                                       const moe_routing_t* routing, const void* d_recv,
-                                       int32_t d, int32_t dtype, void* dx, int32_t flags,
-                                       moe_stream_t stream_) {
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  PeerPtrs src;
-  int ds = 0;
-  moe_status_t s = p2p_args("moe_dispatch_backward_p2p", comm, desc, routing, dx, d_recv, d, dtype,
-                            &src, &ds);
-  if (s != MOE_OK) return s;
-  const int P = comm->nranks;
-  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
-    if (s != MOE_OK) return s;
-  }
-  moe_routing_t unit = *routing;
-  unit.weight = nullptr;  // adjoint of the dispatch copy: unit-weight combine
-  s = reverse_launch_peers(*desc, unit, src, desc->E / P, comm->rank, dtype, ds, d, dx, stream);
-  if (s != MOE_OK) return s;
-  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
-}
-
-// The symmetric buffer of `bytes` at p, with its per-rank mappings.
-static moe_status_t symm_peers(const char* fn, moe_comm_t* comm, const void* p, size_t bytes,
-                               PeerPtrs* out) {
-  const SymmBuf* b = find_symm(comm, p, bytes);
-  if (!b) {
-    set_error("%s: a buffer of %zu bytes is not inside a symmetric buffer (moe_comm_symm_alloc)",
-              fn, bytes);
-    return MOE_ERR_INVALID_ARG;
-  }
-  const size_t off = static_cast<const char*>(p) - b->base;
-  for (int q = 0; q < comm->nranks; ++q) out->p[q] = b->peer.p[q] + off;
-  return MOE_OK;
-}
-
-static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate_desc_t* desc,
-                                const moe_routing_t* routing, const int32_t* offsets,
-                                const void* a, const void* buf, int64_t rows, int32_t d,
-                                int32_t dtype, PeerPtrs* peers, int* ds) {
-  if (!comm || !desc || !routing || !routing->expert_idx || !routing->slot_idx || !offsets ||
-      !a || !buf || d < 1 || (dtype != MOE_F32 && dtype != MOE_BF16)) {
-    set_error("%s: bad arguments", fn);
-    return MOE_ERR_INVALID_ARG;
-  }
-  if (!comm->p2p_ok) {
-    set_error("%s: peer memory is not available between these GPUs", fn);
-    return MOE_ERR_UNSUPPORTED;
-  }
-  const int P = comm->nranks;
-  if (desc->E % P != 0 || desc->E > 256) {
-    set_error("%s: E=%d experts must shard over %d ranks (E <= 256)", fn, desc->E, P);
-    return MOE_ERR_INVALID_ARG;
-  }
-  if ((int64_t)P * desc->S * desc->k > rows) {
-    set_error("%s: buffer of %lld rows < nranks*S*k = %lld (the worst case)", fn, (long long)rows,
-              (long long)P * desc->S * desc->k);
-    return MOE_ERR_INVALID_ARG;
-  }
-  *ds = dtype == MOE_F32 ? 4 : 2;
-  if (((long long)d * *ds) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 ||
-      reinterpret_cast<uintptr_t>(buf) % 16) {
-    set_error("%s: rows and pointers must be 16-byte aligned", fn);
-    return MOE_ERR_ALIGNMENT;
-  }
-  return symm_peers(fn, comm, buf, (size_t)rows * d * *ds, peers);
-}
-
-moe_status_t moe_dispatch_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
-                                     const moe_routing_t* routing, const int32_t* offsets,
-                                     int32_t* counts, int32_t* peer_base, int32_t* recv_offsets,
-                                     const void* x, int32_t d, int32_t dtype, void* recv,
-                                     int64_t recv_cap_rows, int32_t flags, moe_stream_t stream_) {
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  const char* fn = "moe_dispatch_packed_p2p";
-  PeerPtrs dst, cnt;
-  int ds = 0;
-  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, x, recv, recv_cap_rows, d, dtype,
-                               &dst, &ds);
-  if (s != MOE_OK) return s;
-  if (!counts || !peer_base || !recv_offsets) {
-    set_error("%s: counts, peer_base and recv_offsets are required", fn);
-    return MOE_ERR_INVALID_ARG;
-  }
-  s = symm_peers(fn, comm, counts, sizeof(int32_t) * (size_t)desc->E, &cnt);
-  if (s != MOE_OK) return s;
-  const int P = comm->nranks, El = desc->E / P;
-  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {  // owners done with the previous step's tables
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
-    if (s != MOE_OK) return s;
-  }
-  k_a2av_counts<<<1, 256, 0, stream>>>(offsets, cnt, desc->E, El, comm->rank);
-  MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: counts launch");
-  s = barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every table complete
-  if (s != MOE_OK) return s;
-  k_a2av_plan<<<1, 256, 0, stream>>>(cnt, P, El, comm->rank, peer_base, recv_offsets);
-  MOE_CHECK_LAUNCH("moe_dispatch_packed_p2p: plan launch");
-  s = layout_launch_peers(*desc, *routing, x, ds, d, dst, El, comm->rank, stream, offsets,
-                          peer_base);
-  if (s != MOE_OK) return s;
-  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);  // every row has landed
-}
-
-moe_status_t moe_combine_packed_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
-                                    const moe_routing_t* routing, const int32_t* offsets,
-                                    const int32_t* peer_base, const void* expert_out, int32_t d,
-                                    int32_t dtype, int64_t expert_out_rows, void* y,
-                                    int32_t flags, moe_stream_t stream_) {
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  const char* fn = "moe_combine_packed_p2p";
-  PeerPtrs src;
-  int ds = 0;
-  moe_status_t s = packed_args(fn, comm, desc, routing, offsets, y, expert_out, expert_out_rows, d,
-                               dtype, &src, &ds);
-  if (s != MOE_OK) return s;
-  if (!routing->weight || !peer_base) {
-    set_error("%s: routing.weight and peer_base are required", fn);
-    return MOE_ERR_INVALID_ARG;
-  }
-  const int P = comm->nranks;
-  if (!(flags & MOE_P2P_NO_ENTRY_BARRIER)) {
-    s = barrier_launch(comm->sig.peer, P, comm->rank, stream);
-    if (s != MOE_OK) return s;
-  }
-  s = reverse_launch_peers(*desc, *routing, src, desc->E / P, comm->rank, dtype, ds, d, y, stream,
-                           offsets, peer_base);
-  if (s != MOE_OK) return s;
-  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return barrier_launch(comm->sig.peer, P, comm->rank, stream);
+  return comm_barrier(comm, stream);
 }
 
 }  // extern "C"

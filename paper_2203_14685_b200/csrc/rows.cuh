@@ -46,10 +46,6 @@ struct RowArgs {
   // its own padding rows after the exit barrier (k_pad_fill)
   int skip_pads;
   PeerPtrs ptab;
-  // layout only: before waiting on the gate (PDL), the CTAs spread bulk L2
-  // prefetches of x (the rows do not depend on the routing), so x streams
-  // in from HBM while the latency-bound gate runs
-  int prefetch;
   // layout only: zero the padding rows before the token rows, so the rows
   // written last (still in L2 for the combine's reversed walk) are rows the
   // combine reads
@@ -63,26 +59,6 @@ struct RowArgs {
   int dedupe;
   PeerPtrs dup;
 };
-
-// Bulk-prefetch this CTA's 1/gridDim share of [p, p + bytes) into L2 with an
-// evict-last policy (cp.async.bulk.prefetch.L2; 16 KiB pieces, one per
-// thread).  Fire and forget: no shared memory, no completion to wait for.
-__device__ __forceinline__ void prefetch_share_l2(const char* p, size_t bytes) {
-  const size_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
-  const size_t beg = (size_t)blockIdx.x * per;
-  const size_t end = beg + per < bytes ? beg + per : bytes;
-  constexpr size_t kPiece = 16384;
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  for (size_t o = beg + (size_t)threadIdx.x * kPiece; o < end; o += (size_t)blockDim.x * kPiece) {
-    const size_t n = (end - o) < kPiece ? (end - o) : kPiece;
-    const unsigned nb = (unsigned)(n & ~(size_t)15);
-    if (nb)
-      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p + o),
-                   "r"(nb), "l"(pol)
-                   : "memory");
-  }
-}
 
 __device__ __forceinline__ size_t row_index(const RowArgs& a, int q, int e, int s) {
   if (a.offsets) {
@@ -259,8 +235,8 @@ __device__ __forceinline__ void zero_pad_rows(const RowArgs& a, const int* s_beg
 }
 
 inline int row_grid(const void* kern) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);
+  int per_sm = tuning().row_ctas_per_sm;
+  if (per_sm <= 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0);
   return std::max(1, per_sm) * device_sm_count();
 }
 

@@ -22,11 +22,15 @@ class RoutePipeline:
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
                  device=None, slot_src: bool = True, dropless: bool = False,
-                 fuse_gate_layout: Optional[bool] = None):
+                 fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
-        exchange (algo "p2p" only).  The expert stand-in is the identity."""
+        exchange (algo "p2p" only).  The expert stand-in is the identity.
+        identity_alias=True (p2p only): a step with expert=False tells the
+        combine that recv is unmodified (MOE_P2P_RECV_UNMODIFIED): no entry
+        barrier and one read of a row sent once for two slots.  A measurement
+        of the routing alone; a real expert always takes the default path."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
         # the gate's capacity pass inside the layout / dispatch kernel
@@ -37,6 +41,7 @@ class RoutePipeline:
             import os
             fuse_gate_layout = os.environ.get("MOE_FUSE_GATE_LAYOUT", "0") == "1"
         self.fuse = fuse_gate_layout and not dropless and (algo in ("flat", "p2p") or comm is None)
+        self.identity_alias = identity_alias
         if dropless:
             cap = S * k
             slot_src = False
@@ -129,10 +134,10 @@ class RoutePipeline:
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
             mark("expert")
         if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
-            # entry barrier only if an expert wrote recv after the dispatch's
-            # exit barrier; the exit barrier frees recv for the next step
-            self.comm.combine_p2p(self.recv, r, self.y,
-                                  flags=0 if expert else self.comm.NO_ENTRY_BARRIER)
+            # the entry barrier orders every rank's expert (and the owners'
+            # duplicate-row copies) before the reads; the exit barrier frees
+            # recv for the next step
+            self.comm.combine_p2p(self.recv, r, self.y, flags=self._combine_flags(expert))
             mark("a2a_combine")
             mark("reverse")
             return self.y
@@ -141,6 +146,11 @@ class RoutePipeline:
         reverse_layout(self.back, r, out=self.y)                           # step 6
         mark("reverse")
         return self.y
+
+    def _combine_flags(self, expert: bool) -> int:
+        if self.identity_alias and not expert:
+            return self.comm.NO_ENTRY_BARRIER | self.comm.RECV_UNMODIFIED
+        return 0
 
     def _step_fused(self, logits, x, token_ids, table, expert, mark):
         """The step with the gate's capacity pass fused into the layout
@@ -162,8 +172,7 @@ class RoutePipeline:
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
             mark("expert")
         if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
-            self.comm.combine_p2p(self.recv, r, self.y,
-                                  flags=0 if expert else self.comm.NO_ENTRY_BARRIER)
+            self.comm.combine_p2p(self.recv, r, self.y, flags=self._combine_flags(expert))
             mark("a2a_combine")
             mark("reverse")
             return self.y

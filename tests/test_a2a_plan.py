@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 
 import paper_2203_14685_b200 as moe
 
-SEND, RECV, COPY, PERMUTE = 0, 1, 2, 3
+SEND, RECV, COPY, PERMUTE, TRANSPOSE = 0, 1, 2, 3, 4
 
 
 def _bufs(send, P, G, c):
@@ -35,6 +35,14 @@ def _permute(src, dst, N, G, c):
                 d = (n * N + g) * G + m
                 s = (g * G + m) * G + n
                 dst[d * c:(d + 1) * c] = src[s * c:(s + 1) * c]
+
+
+def _transpose(src, dst, X, Y, c):
+    """dst chunk [y][x] <- src chunk [x][y] (HIER_2D's local reorders)."""
+    for x in range(X):
+        for y in range(Y):
+            d, s = y * X + x, x * Y + y
+            dst[d * c:(d + 1) * c] = src[s * c:(s + 1) * c]
 
 
 def interpret(P, algo, G, sends, c):
@@ -66,12 +74,15 @@ def interpret(P, algo, G, sends, c):
                     bufs[r][o["dst_buf"]][b:b + n] = bufs[r][o["src_buf"]][a:a + n]
                 elif o["op"] == PERMUTE:
                     _permute(bufs[r][o["src_buf"]], bufs[r][o["dst_buf"]], o["peer"], o["chunks"], c)
+                elif o["op"] == TRANSPOSE:
+                    _transpose(bufs[r][o["src_buf"]], bufs[r][o["dst_buf"]], o["peer"],
+                               o["chunks"], c)
     return [bufs[r][1] for r in range(P)], plans
 
 
 @pytest.mark.parametrize("P,G", [(1, 1), (2, 1), (2, 2), (4, 2), (4, 4), (6, 3), (8, 4), (8, 2),
                                  (8, 8), (8, 1), (16, 4)])
-@pytest.mark.parametrize("algo", ["flat", "hier"])
+@pytest.mark.parametrize("algo", ["flat", "hier", "hier2d"])
 def test_plan_reproduces_oracle_alltoall(orc, P, G, algo):
     c = 3
     rng = np.random.default_rng(P * 31 + G)
@@ -88,6 +99,16 @@ def test_plan_reproduces_oracle_alltoall(orc, P, G, algo):
         sizes = set(o["chunks"] for r in range(P) for o in plans[r]
                     if o["op"] == SEND and o["peer"] // G != r // G)
         assert sizes <= {G * G}                   # B*G/N per group pair
+    if algo == "hier2d" and P > 1:
+        # two-level: inside the group N chunks per peer, across groups one
+        # message of G chunks per group pair per local index (B*G/P bytes)
+        N = P // G
+        for r in range(P):
+            for o in plans[r]:
+                if o["op"] == SEND:
+                    same = o["peer"] // G == r // G
+                    assert o["chunks"] == (N if o["phase"] == 1 else G)
+                    assert same if o["phase"] == 1 else o["peer"] % G == r % G
 
 
 # ------------------------------------------------------------ real processes (gloo)
@@ -133,6 +154,9 @@ def _worker(rank, world, algo, G, port, c, q):
             elif o["op"] == PERMUTE:
                 dst = bufs[o["dst_buf"]].numpy()
                 _permute(bufs[o["src_buf"]].numpy().copy(), dst, o["peer"], o["chunks"], c)
+            elif o["op"] == TRANSPOSE:
+                dst = bufs[o["dst_buf"]].numpy()
+                _transpose(bufs[o["src_buf"]].numpy().copy(), dst, o["peer"], o["chunks"], c)
     q.put((rank, send.tobytes(), bufs[1].numpy().tobytes()))
     dist.barrier()
     dist.destroy_process_group()
@@ -140,11 +164,12 @@ def _worker(rank, world, algo, G, port, c, q):
 
 @pytest.mark.parametrize("world,algo,G", [(2, "flat", 1), (2, "hier", 1), (2, "hier", 2),
                                           (4, "flat", 1), (4, "hier", 2),
-                                          (8, "hier", 4)])   # the paper's 4+4 split on 8 ranks
+                                          (8, "hier", 4),    # the paper's 4+4 split on 8 ranks
+                                          (4, "hier2d", 2), (8, "hier2d", 4)])
 def test_plan_executes_over_gloo(orc, world, algo, G):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + world * 10 + G + (5 if algo == "hier" else 0)
+    port = 29500 + world * 10 + G + {"flat": 0, "hier": 5, "hier2d": 7}[algo]
     procs = [ctx.Process(target=_worker, args=(r, world, algo, G, port, 4, q)) for r in range(world)]
     for p in procs:
         p.start()

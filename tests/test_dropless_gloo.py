@@ -70,5 +70,8 @@ def test_alltoallv_plan_rejects_bad_shapes():
     import paper_2203_14685_b200 as moe
     with pytest.raises(ValueError):
         moe.alltoallv_plan([0, 1, 2], [1, 1, 1], 2)       # E = 2, 3 counts
-    with pytest.raises(ValueError):
+    with pytest.raises(moe.MoeError) as ei:
         moe.alltoallv_plan([0, 1, 2, 3], [1, 1, 1], 2)    # E = 3 not divisible by 2
+    assert ei.value.status == 1                           # MOE_ERR_INVALID_ARG, from the C plan
+    with pytest.raises(moe.MoeError):
+        moe.alltoallv_plan([0, 2, 1, 3, 4], [1, 1, 1, 1], 2)   # offsets must not decrease

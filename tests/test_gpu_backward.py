@@ -66,10 +66,14 @@ def _dot_bound(dy64, back64, ro):
     return (d / 32 + 6) * 2.0 ** -24 * out
 
 
-@pytest.mark.parametrize("pads_first", ["0", "1"])   # padding rows of d_back zeroed last / first
+@pytest.mark.parametrize("pads_first", [0, 1])   # padding rows of d_back zeroed last / first
 @pytest.mark.parametrize("c", CASES, ids=lambda c: "-".join("%s=%s" % kv for kv in c.items()))
-def test_combine_and_layout_backward(orc, c, pads_first, monkeypatch):
-    monkeypatch.setenv("MOE_LAYOUT_PADS_FIRST", pads_first)
+def test_combine_and_layout_backward(orc, c, pads_first):
+    with moe.tuned(layout_pads_first=pads_first):
+        _combine_and_layout_backward(orc, c)
+
+
+def _combine_and_layout_backward(orc, c):
     lg, ro, rg, cap = _setup(orc, c)
     S, E, d, bf16 = c["S"], c["E"], c["d"], c["dtype"] == "bf16"
     dy = synthgen.tokens(S * 7 + d, S, d, c["dtype"])

@@ -31,7 +31,8 @@ def _rank_main(rank, world, algo, G, port, q):
     x = synthgen.tokens(synthgen.seed_for(9, rank, 2), S, D, dts)
     cap = moe.capacity(S, E, K, 1.0)
     pipe = moe.RoutePipeline(S, D, E, K, cap, torch.bfloat16 if dts == "bf16" else torch.float32,
-                             comm=comm, algo=algo, group_size=G)
+                             comm=comm, algo=algo, group_size=G,
+                             identity_alias=os.environ.get("MOE_TEST_ALIAS") == "1")
     pipe.step(dev(lg), dev(x), expert=False)     # identity expert: recv = dispatched rows
     torch.cuda.synchronize()
     recv = host(pipe.recv).copy()
@@ -63,37 +64,37 @@ def _run(world, algo, G, port):
 @pytest.mark.parametrize("world,algo,G,env", [(2, "flat", 1, None), (2, "hier", 2, None),
                                               (2, "p2p", 1, None), (2, "p2p", 1, "local_pad"),
                                               (2, "p2p", 1, "f32"), (2, "p2p", 1, "rev"),
-                                              (2, "p2p", 1, "tma"), (2, "p2p", 1, "nodedupe"),
-                                              (2, "p2p", 1, "f32_noalias"), (2, "p2p", 1, "noalias"),
+                                              (2, "p2p", 1, "nodedupe"),
+                                              (2, "p2p", 1, "f32_alias"), (2, "p2p", 1, "alias"),
                                               (4, "p2p", 1, "f32"), (2, "p2p", 1, "k4"),
-                                              (2, "p2p", 1, "k4_f32"),
+                                              (2, "p2p", 1, "k4_f32"), (2, "p2p", 1, "k4_alias"),
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
+                                              (4, "p2p", 1, "alias"),
                                               (4, "p2p", 1, "local_pad")])
 def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
     if env == "local_pad":   # the owners zero their own padding rows (inherited by the ranks)
         monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
-    if env == "tma":         # TMA bulk-store dispatch (with the dedupe)
-        monkeypatch.setenv("MOE_P2P_LAYOUT_TMA", "1")
     if env == "nodedupe":    # every row sent, even when a token's two experts share an owner
         monkeypatch.setenv("MOE_P2P_DEDUPE", "0")
     if env == "rev":         # peer combine walking the tokens last to first
         monkeypatch.setenv("MOE_REVERSE_BACKWARDS", "1")
         monkeypatch.setenv("MOE_REVERSE_Y_EF", "1")
-    if env in ("noalias", "f32_noalias"):   # the combine waits for the owners' duplicate copies
-        monkeypatch.setenv("MOE_P2P_COMBINE_ALIAS", "0")
+    if env in ("alias", "f32_alias", "k4_alias"):   # identity step: RECV_UNMODIFIED combine
+        monkeypatch.setenv("MOE_TEST_ALIAS", "1")
     K = 2
-    if env in ("k4", "k4_f32"):  # k = 4: the generic peer combine (alias mode, rows read per slot)
+    if env in ("k4", "k4_f32", "k4_alias"):  # k = 4: the generic peer combine
         K = 4
         monkeypatch.setenv("MOE_TEST_K", "4")
-    f32 = env in ("f32", "f32_noalias", "k4_f32")
+    f32 = env in ("f32", "f32_alias", "k4_f32")
     if f32:                  # fp32 rows through the one-sided path
         monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
-               {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "tma": 4, "nodedupe": 5,
-                "f32_noalias": 7, "noalias": 8, "k4": 9, "k4_f32": 10}[env] + (40 if env and world == 4 else 0))
+               {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "nodedupe": 5, "f32_alias": 7,
+                "alias": 8, "k4": 9, "k4_f32": 10, "k4_alias": 11}[env] +
+               (40 if env and world == 4 else 0))
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]
     cap = orc.capacity(S, E, K, 1.0)

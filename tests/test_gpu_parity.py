@@ -92,38 +92,41 @@ GATE_CASES = [
 ]
 
 
-# kernel variants selected by the library's tuning knobs (read per call)
-GATE_PATHS = {"fused": {"MOE_GATE_FUSED": "1"}, "two": {}, "three": {"MOE_GATE_TWO_MAXW": "0"},
-              "two_forced": {"MOE_GATE_TWO_MAXW": "1000000"},
-              "tile256": {"MOE_GATE_MAX_TILE": "256", "MOE_GATE_TILES": "1"},
-              "tile32": {"MOE_GATE_MAX_TILE": "32"},
-              "fused_small_tiles": {"MOE_GATE_FUSED": "1", "MOE_GATE_FUSED_TILES": "512", "MOE_GATE_FUSED_MAXW": "1000000"}}
-ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"MOE_LAYOUT_U": "4", "MOE_REVERSE_KU": "4"}, "tma_layout": {"MOE_LAYOUT_TMA": "1"}, "tma_reverse": {"MOE_REVERSE_TMA": "1"}, "reverse_reg": {"MOE_REVERSE_TMA": "0", "MOE_REVERSE_TPW": "0"}, "no_prefetch": {"MOE_LAYOUT_PREFETCH": "0"}, "layout_tpw": {"MOE_LAYOUT_TPW": "1", "MOE_REVERSE_TPW": "1"},
-             "reverse_generic": {"MOE_REVERSE_KSPEC": "0"}, "reverse_u2": {"MOE_REVERSE_KU": "2"},
-             "forward_order": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_Y_EF": "0"},
-             "forward_order_tma": {"MOE_REVERSE_BACKWARDS": "0", "MOE_REVERSE_TMA": "1"},
-             "reverse_generic_fwd": {"MOE_REVERSE_KSPEC": "0", "MOE_REVERSE_BACKWARDS": "0"},
-             "reverse_v16": {"MOE_REVERSE_V16": "1"}, "pads_first": {"MOE_LAYOUT_PADS_FIRST": "1"}, "pads_last": {"MOE_LAYOUT_PADS_FIRST": "0"}}
+# kernel variants selected by the library's tuning table (moe.tuned)
+GATE_PATHS = {"two": {}, "three": {"gate_two_maxw": 0},
+              "two_forced": {"gate_two_maxw": 1000000},
+              "tile256": {"gate_max_tile": 256, "gate_tiles": 1},
+              "tile32": {"gate_max_tile": 32}}
+ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"layout_u": 4, "reverse_ku": 4},
+             "layout_u1": {"layout_u": 1},
+             "reverse_tpw_off": {"reverse_tpw": 0}, "reverse_tpw_on": {"reverse_tpw": 1},
+             "reverse_generic": {"reverse_kspec": 0}, "reverse_u2": {"reverse_ku": 2},
+             "forward_order": {"reverse_backwards": 0, "reverse_y_ef": 0},
+             "reverse_generic_fwd": {"reverse_kspec": 0, "reverse_backwards": 0},
+             "pads_first": {"layout_pads_first": 1}, "pads_last": {"layout_pads_first": 0},
+             "one_cta_per_sm": {"row_ctas_per_sm": 1}}
 
 
 @pytest.mark.parametrize("path", sorted(GATE_PATHS))
 @pytest.mark.parametrize("case", GATE_CASES, ids=lambda c: "-".join(
     "%s=%s" % (k, v) for k, v in c.items() if k not in ("bad_ids",)))
-def test_gate_parity(orc, case, path, monkeypatch):
-    for k, v in GATE_PATHS[path].items():
-        monkeypatch.setenv(k, v)
-    rg, ro, g, _ = _run_gate(orc, case)
+def test_gate_parity(orc, case, path):
+    with moe.tuned(**GATE_PATHS[path]):
+        rg, ro, g, _ = _run_gate(orc, case)
     assert_routing_equal(rg, ro, str(case))
     if case["kind"] == "hash":
         assert g.check() == ro.bad
 
 
 @pytest.mark.parametrize("path", sorted(GATE_PATHS))
-def test_gate_workspace_reuse_and_graph_replay(orc, path, monkeypatch):
-    """The workspace resets itself (grid-barrier words, counters): repeated
-    calls, and CUDA-graph replays with new inputs, each match the oracle."""
-    for k, v in GATE_PATHS[path].items():
-        monkeypatch.setenv(k, v)
+def test_gate_workspace_reuse_and_graph_replay(orc, path):
+    """The workspace resets itself (counters): repeated calls, and CUDA-graph
+    replays with new inputs, each match the oracle."""
+    with moe.tuned(**GATE_PATHS[path]):
+        _gate_reuse_and_replay(orc)
+
+
+def _gate_reuse_and_replay(orc):
     S, E, k = 3000, 16, 2
     cap = orc.capacity(S, E, k, 1.0)
     g = moe.Gate(S, E, k, cap)
@@ -169,9 +172,12 @@ LAYOUT_CASES = [
 @pytest.mark.parametrize("path", sorted(ROW_PATHS))
 @pytest.mark.parametrize("case", LAYOUT_CASES, ids=lambda c: "-".join(
     "%s=%s" % (k, v) for k, v in c.items()))
-def test_layout_and_reverse_parity(orc, case, path, monkeypatch):
-    for k, v in ROW_PATHS[path].items():
-        monkeypatch.setenv(k, v)
+def test_layout_and_reverse_parity(orc, case, path):
+    with moe.tuned(**ROW_PATHS[path]):
+        _layout_and_reverse(orc, case)
+
+
+def _layout_and_reverse(orc, case):
     rg, ro, _, _ = _run_gate(orc, case)
     assert_routing_equal(rg, ro)
     S, d, bf16 = case["S"], case["d"], case["dtype"] == "bf16"
