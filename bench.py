@@ -3,8 +3,10 @@
 B200 (BASELINE.json metric), one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
-                    [--algo flat|hier] [--group-size G] [--impl ours|reference]
-    # N > 1: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+                    [--algo p2p|flat|hier|hier2d] [--group-size G] [--impl ours|reference]
+    # N > 1 is launched either way:
+    #   python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+    #   python bench.py --gpus N ...   (re-executes itself under torch.distributed.run)
 
 A step is one pass of the whole routing path on one batch of S tokens per
 rank (Algorithm 1): gate (select + weights + capacity) ->
@@ -48,9 +50,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
-    ap.add_argument("--algo", default="p2p", choices=["p2p", "flat", "hier"],
+    ap.add_argument("--algo", default="p2p", choices=["p2p", "flat", "hier", "hier2d"],
                     help="AllToAll at N>1: p2p = fused one-sided NVLink path (falls back to "
-                         "flat if the GPUs cannot map each other's memory); flat/hier = NCCL")
+                         "flat if the GPUs cannot map each other's memory); flat / hier (the "
+                         "paper's leader scheme) / hier2d (two-level) = NCCL")
     ap.add_argument("--group-size", type=int, default=0, help="hier group size (default N/2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -65,6 +68,30 @@ def parse():
 
 
 # ---------------------------------------------------------------- helpers
+def relaunch_if_needed():
+    """`bench.py --gpus N` without torchrun: re-execute under
+    torch.distributed.run with N ranks (one per GPU) and return its exit
+    code; None when this process is already one rank of the right world.
+    A WORLD_SIZE that disagrees with --gpus is an error."""
+    a = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != a.gpus:
+            sys.stderr.write("bench.py: --gpus %d but WORLD_SIZE=%s\n" % (a.gpus, world))
+            return 2
+        return None
+    if a.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as s:          # a free rendezvous port on 127.0.0.1
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(a.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -406,6 +433,35 @@ def main():
     log("stage timing done")
     eager = timed_eager(max(3, a.steps // 2))
     log("eager timing done")
+    # N > 1 one-sided path: the identity-expert alias form, an extra (the
+    # headline above keeps the combine's entry barrier and reads every slot)
+    alias_ms = None
+    if P > 1 and algo == "p2p" and not a.dropless:
+        pipe.identity_alias = True
+        step()
+        torch.cuda.synchronize()
+        g_alias = pipe.capture(d_in["logits"], d_in["x"], d_in["token_ids"], d_in["table"])
+        g_alias.replay()
+        torch.cuda.synchronize()
+        ev_a = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(max(3, a.steps // 2))]
+        barrier()
+        torch.cuda.synchronize()
+        for s_, e_ in ev_a:
+            flush_l2()
+            align()
+            s_.record()
+            g_alias.replay()
+            e_.record()
+        torch.cuda.synchronize()
+        barrier()
+        t_a = torch.tensor([statistics.mean(s_.elapsed_time(e_) for s_, e_ in ev_a)],
+                           dtype=torch.float64, device=dev)
+        dist.all_reduce(t_a, op=dist.ReduceOp.MAX)
+        alias_ms = float(t_a.item())
+        pipe.identity_alias = False
+        del g_alias
+        log("identity-alias timing done")
     # max over ranks (per step mean, per stage mean)
     vals = torch.tensor([statistics.mean(tot)] + [statistics.mean(s) for s in st] +
                         [min(tot), statistics.mean(eager)], dtype=torch.float64)
@@ -536,45 +592,48 @@ def main():
     admitted = int((pipe.routing.slot_idx >= 0).sum().item())
     ab = algorithmic_bytes(w, S, cap, P, row)
     ab["reverse"] = admitted * row + S * row + 12 * S * w.k
+    tun = moe.get_tuning()
+    p2p_flags = {"dedupe": False, "local_pad": False}
     if a.dropless:
         # packed: no padding rows; the rows leaving this rank are the admitted
         # rows of other ranks' experts
         ab["layout"] = S * row + admitted * row + 8 * S * w.k
         ab["gate"] = S * (4 * w.E if w.kind != "hash" else 8) + 12 * S * w.k + 8 * w.E
-        if P > 1:
-            El = w.E // P
-            ex = pipe.routing.expert_idx
-            out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) &
-                            ((ex // El) != rank)).sum().item())
-            ab["a2a"] = out_rows * row
-    elif P > 1 and algo == "p2p" and w.E * cap > 1.05 * S * w.k and \
-            os.environ.get("MOE_P2P_LOCAL_PAD", "1") != "0":
-        # local padding: the zero rows are written by their
-        # owner, so only the admitted rows of other ranks' experts cross NVLink
-        El = w.E // P
-        ex = pipe.routing.expert_idx
-        out_rows = int(((ex >= 0) & (pipe.routing.slot_idx >= 0) & ((ex // El) != rank)).sum().item())
-        ab["a2a"] = out_rows * row
-    if P > 1 and algo == "p2p" and not a.dropless and w.k >= 2 and w.E // P >= 2 and \
-            os.environ.get("MOE_P2P_DEDUPE", "1") != "0":
-        # dedupe: a token's row crosses NVLink once per remote
-        # owner, however many of its slots that owner holds; the alias-mode
-        # combine reads it once too.  Padding rows cross unless padded locally.
+    if P > 1 and algo == "p2p":
+        # bytes that actually cross NVLink per rank and direction (DESIGN.md
+        # §6): admitted rows of other ranks' experts -- a token's row once per
+        # remote owner when the dispatch dedupes (k >= 2, E/P >= 2) -- plus,
+        # in the padded form, the padding rows of the remote chunks unless the
+        # owners write them (local padding).  The timed combine reads every
+        # admitted remote slot (an expert may have written recv); the
+        # identity-expert alias form reads a deduped row once.
         El = w.E // P
         ex, sl = pipe.routing.expert_idx.view(S, w.k), pipe.routing.slot_idx.view(S, w.k)
-        own = torch.where((ex >= 0) & (sl >= 0), ex // El, torch.full_like(ex, -1))
+        adm = (ex >= 0) & (sl >= 0)
+        own = torch.where(adm, ex // El, torch.full_like(ex, -1))
+        remote_slots = int((adm & (own != rank)).sum().item())
         owners = torch.zeros((S, P), dtype=torch.bool, device=own.device)
         for j in range(w.k):
             m = own[:, j] >= 0
             owners[torch.nonzero(m).squeeze(1), own[m, j].long()] = True
         owners[:, rank] = False
         pairs = int(owners.sum().item())
+        dedupe = (not a.dropless) and tun["p2p_dedupe"] and w.k >= 2 and El >= 2
+        heavy = w.E * cap > 1.05 * S * w.k
+        local_pad = a.dropless or (heavy if tun["p2p_local_pad"] < 0 else bool(tun["p2p_local_pad"]))
         pads = 0
-        if not (w.E * cap > 1.05 * S * w.k and os.environ.get("MOE_P2P_LOCAL_PAD", "1") != "0"):
+        if not local_pad:
             load = pipe.routing.load.view(P, El)
-            pads = int((cap - load.clamp(max=cap)).sum().item() - (cap - load[rank].clamp(max=cap)).sum().item())
+            padrows = cap - load.clamp(max=cap)
+            pads = int(padrows.sum().item() - padrows[rank].sum().item())
+        p2p_flags = {"dedupe": bool(dedupe), "local_pad": bool(local_pad)}
         ab["a2a_buffer"] = ab["a2a"]
-        ab["a2a"] = (pairs + pads) * row
+        ab["a2a_dispatch"] = ((pairs if dedupe else remote_slots) + pads) * row
+        ab["a2a_combine"] = remote_slots * row
+        ab["a2a_combine_alias"] = (pairs if dedupe else remote_slots) * row
+        ab["a2a"] = ab["a2a_dispatch"]
+    elif P > 1:
+        ab["a2a_dispatch"] = ab["a2a_combine"] = ab["a2a"]
     peak, peak_src = measured_peaks()
     traffic = None
     try:
@@ -595,23 +654,25 @@ def main():
     else:
         # fused one-sided path: the dispatch (k_layout in peer mode) and the
         # combine (k_reverse in peer mode) are bound by the bytes that must
-        # cross NVLink, (P-1)/P of the [E,cap,d] buffer each way
-        dom = "layout" if stage_ms["layout"] >= stage_ms["a2a_combine"] else "a2a_combine"
-        t = stage_ms[dom] / 1e3
-        achieved = ab["a2a"] / t / 1e9
+        # cross NVLink (ab["a2a_dispatch"], ab["a2a_combine"])
+        t_d, t_c = stage_ms["layout"] / 1e3, stage_ms["a2a_combine"] / 1e3
+        dom = "layout" if t_d >= t_c else "a2a_combine"
+        nb = ab["a2a_dispatch"] if dom == "layout" else ab["a2a_combine"]
+        achieved = nb / (t_d if dom == "layout" else t_c) / 1e9
         roof = {"bound": "nvlink", "kernel": "k_layout (peer dispatch)" if dom == "layout"
-                else "k_reverse (peer combine)", "achieved": achieved, "peak": NVLINK_GBS,
+                else "k_reverse_k (peer combine)", "achieved": achieved, "peak": NVLINK_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_GBS, "traffic": None,
-                "algorithmic_bytes": ab["a2a"],
+                "algorithmic_bytes": nb,
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md), 900 nominal"}
     if fused:
         # the layout / reverse stages ARE the NVLink dispatch / combine (the
         # "reverse" and "a2a_dispatch" marks are empty stages: event resolution)
         roof["per_kernel_gbs"] = {
             "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
-            "k_layout (peer dispatch), NVLink per direction": ab["a2a"] / (stage_ms["layout"] / 1e3) / 1e9,
-            "k_reverse (peer combine), NVLink per direction":
-                ab["a2a"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
+            "k_layout (peer dispatch), NVLink per direction":
+                ab["a2a_dispatch"] / (stage_ms["layout"] / 1e3) / 1e9,
+            "k_reverse_k (peer combine), NVLink per direction":
+                ab["a2a_combine"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
     else:
         roof["per_kernel_gbs"] = {
             "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
@@ -620,17 +681,29 @@ def main():
     a2a = None
     if P > 1:
         if fused:
-            bw = {"dispatch (fused with layout)": ab["a2a"] / (stage_ms["layout"] / 1e3) / 1e9,
-                  "combine (fused with reverse)": ab["a2a"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
+            bw = {"dispatch (fused with layout)": ab["a2a_dispatch"] / (stage_ms["layout"] / 1e3) / 1e9,
+                  "combine (fused with reverse)":
+                      ab["a2a_combine"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
         else:
             bw = {s_: ab["a2a"] / (stage_ms[s_] / 1e3) / 1e9 for s_ in ("a2a_dispatch", "a2a_combine")}
         a2a = {"bytes_out_per_rank": ab["a2a"], "busbw_gbs": bw, "peak_gbs": NVLINK_GBS,
-               "algo": algo, "group_size": G if algo == "hier" else None}
+               "algo": algo, "group_size": G if algo in ("hier", "hier2d") else None}
         if "a2a_buffer" in ab:
             a2a["buffer_bytes_per_rank"] = ab["a2a_buffer"]
-            a2a["note"] = ("bytes_out_per_rank counts each token row once per remote owner "
-                           "(deduped dispatch, alias-mode combine) plus the padding rows")
+            a2a["dispatch_bytes_per_rank"] = ab["a2a_dispatch"]
+            a2a["combine_bytes_per_rank"] = ab["a2a_combine"]
+            a2a["note"] = ("bytes that cross NVLink per rank and direction: the dispatch sends a "
+                           "token's row once per remote owner (dedupe) plus the padding rows the "
+                           "owners do not write themselves; the combine reads every admitted "
+                           "remote slot (entry barrier kept, as with a real expert)")
         a2a["frac"] = min(bw.values()) / NVLINK_GBS
+        if alias_ms is not None:
+            a2a["identity_alias"] = {
+                "ms_per_step": alias_ms, "value": P * S / (alias_ms / 1e3),
+                "combine_bytes_per_rank": ab["a2a_combine_alias"],
+                "what": "extra, not the headline: the same step with an identity expert "
+                        "declared to the combine (MOE_P2P_RECV_UNMODIFIED: no entry barrier, a "
+                        "row sent once for two slots read once)"}
 
     # ---- CPU baseline: the oracle, rank 0, N=1 only, bounded sample
     cpu = None
@@ -659,8 +732,10 @@ def main():
                "cpu_model": cpu_model()}
 
     # our kernels per step: gate (k_gate_select, k_gate_scan, k_gate_slots),
-    # layout, reverse, on hierarchical leaders one chunk permute per AllToAll,
-    # and on the one-sided path the dispatch's and the combine's exit barriers
+    # layout, reverse; on hierarchical leaders one chunk permute per AllToAll,
+    # with the two-level form two transposes per AllToAll on every rank; on
+    # the one-sided path three barriers (dispatch exit, combine entry and
+    # exit), the owners' duplicate-row copies (dedupe) and padding fill
     import ctypes
     from paper_2203_14685_b200._lib import lib as _moelib
     gate_k = _moelib().moe_gate_kernel_count(ctypes.byref(pipe.routing.desc()), 1)
@@ -669,8 +744,13 @@ def main():
         # P>1: counts, barrier, plan, layout, exit barrier, reverse, exit barrier)
         launches_per_step = gate_k + 1 + (7 if P > 1 else 2)
     else:
-        launches_per_step = gate_k + 2 + (2 if (P > 1 and algo == "hier" and rank % G == 0) else 0) + \
-            (2 if (P > 1 and algo == "p2p") else 0)
+        launches_per_step = gate_k + 2
+        if P > 1 and algo == "hier" and rank % G == 0:
+            launches_per_step += 2
+        elif P > 1 and algo == "hier2d":
+            launches_per_step += 4
+        elif P > 1 and algo == "p2p":
+            launches_per_step += 3 + int(p2p_flags["dedupe"]) + int(p2p_flags["local_pad"])
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
@@ -715,5 +795,8 @@ def _json_stdout():
 
 
 if __name__ == "__main__":
+    rc = relaunch_if_needed()
+    if rc is not None:
+        sys.exit(rc)
     _json_stdout()
     main()

@@ -86,7 +86,7 @@ class RoutePipeline:
             self.recv = self.back = self.dispatch
         self.y = mk(S, d)
         self.ws = None
-        if self.P > 1 and algo == "hier":
+        if self.P > 1 and algo in ("hier", "hier2d"):
             nb = comm.workspace_bytes(algo, group_size, self.dispatch.nbytes // self.P)
             self.ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
 
@@ -114,7 +114,7 @@ class RoutePipeline:
                 return self.step(logits, x, token_ids, table, expert, mark)
             finally:
                 self.y = saved
-        if self.fuse and (self.P == 1 or self.algo != "hier"):
+        if self.fuse and (self.P == 1 or self.algo in ("flat", "p2p")):
             return self._step_fused(logits, x, token_ids, table, expert, mark)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         if self.dropless:

@@ -332,3 +332,44 @@ def test_multi_gpu_dropless(orc, world):
         unit = type(ros[r])(**{**ros[r].__dict__,
                                "weight": (ros[r].slot_idx >= 0).astype(np.float32)})
         assert_y_close(dx, dx_o, combine_bound(as_f64(g_pad), unit), True, "dx")
+
+
+def _timeout_rank_main(rank, world, port, q):
+    """Rank 0 enters a device barrier that rank 1 never enters."""
+    import torch.distributed as dist
+    import paper_2203_14685_b200 as moe
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    moe.set_tuning(barrier_timeout_ms=200)
+    comm = moe.Comm.from_process_group()
+    comm.check()
+    status = 0
+    if rank == 0:
+        comm.barrier()
+        try:
+            comm.check()
+        except moe.MoeError as e:
+            status = e.status
+    q.put((rank, status))
+    dist.barrier()            # rank 1 waits here (host side) until rank 0 has its answer
+    comm.abort()
+    dist.destroy_process_group()
+
+
+def test_multi_gpu_barrier_timeout():
+    """SURVEY §5 failure detection: a rank that never arrives makes the
+    peer's bounded device barrier give up; moe_comm_check reports
+    MOE_ERR_TIMEOUT; moe_comm_abort releases the communicator."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    ps = [ctx.Process(target=_timeout_rank_main, args=(r, 2, 29790, qu)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(qu.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[0] == 7 and got[1] == 0     # MOE_ERR_TIMEOUT on the waiting rank only

@@ -7,7 +7,9 @@ phase, barriers as step boundaries.  Every receive buffer must equal the
 oracle's P-rank simulation of Algorithm 1 steps 3 and 5 (PAPER.md:53-54,
 62-63) byte for byte; y within the north_star tolerance.
 
-No `multigpu` marker: these run on a single-GPU box."""
+No `multigpu` marker: these run on a single-GPU box.  Calls on a simulated
+rank are queued until SimWorld.run(): every tensor they use must stay alive
+until then."""
 import numpy as np
 import pytest
 import torch
@@ -289,12 +291,13 @@ def test_sim_backward_p2p(orc, form, P, E, k, C, local_pad):
             d_eo[r].fill_(3.0)
         dws = [torch.empty((S, k), dtype=torch.float32, device="cuda") for _ in range(P)]
         dxs = [torch.empty((S, d), dtype=torch.bfloat16, device="cuda") for _ in range(P)]
+        dy_dev = [dev(v) for v in dy]   # alive until run(): the queued kernels read them
         for r in range(P):
             if form == "pull":
-                comms[r].combine_backward_p2p(dev(dy[r]), expert_out[r], R.routings[r], d_eo[r],
+                comms[r].combine_backward_p2p(dy_dev[r], expert_out[r], R.routings[r], d_eo[r],
                                               dws[r])
             else:
-                comms[r].combine_backward_push_p2p(dev(dy[r]), expert_out[r], R.routings[r],
+                comms[r].combine_backward_push_p2p(dy_dev[r], expert_out[r], R.routings[r],
                                                    d_eo[r], wt[r], dwt[r], dws[r])
             comms[r].dispatch_backward_p2p(d_recv[r], R.routings[r], dxs[r])
         world.run()
