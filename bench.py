@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="gate and layout as separate kernels (default: one fused kernel)")
     ap.add_argument("--dropless", action="store_true",
                     help="NEXT-4: packed dropless layout (capacity = S*k), device-side exchange")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -291,14 +293,14 @@ def main():
     try:
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
                                  group_size=G, device=dev, dropless=a.dropless,
-                                 slot_src=os.environ.get("MOE_BENCH_SLOT_SRC", "1") != "0")
+                                 fuse_gate_layout=not a.no_fuse)
     except moe.MoeError as err:
         if algo != "p2p":
             raise
         log("p2p unavailable (%s): NCCL flat AllToAll instead" % err)
         algo = "flat"
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
-                                 group_size=G, device=dev)
+                                 group_size=G, device=dev, fuse_gate_layout=not a.no_fuse)
 
     lg, ids, table, x = synthgen.workload_inputs(w, rank)
 
@@ -634,6 +636,11 @@ def main():
         ab["a2a"] = ab["a2a_dispatch"]
     elif P > 1:
         ab["a2a_dispatch"] = ab["a2a_combine"] = ab["a2a"]
+    # gate + layout as one kernel (moe_gate_layout / moe_gate_dispatch_p2p):
+    # its time is the "layout" stage and its bytes are both steps' bytes
+    fused_gl = pipe.fuse and w.kind in ("topk", "ktop1", "hash") and w.k <= 8 and row % 32 == 0
+    if fused_gl:
+        ab["layout"] += ab["gate"]
     peak, peak_src = measured_peaks()
     traffic = None
     try:
@@ -646,7 +653,8 @@ def main():
         # N=1 (or NCCL AllToAll): layout / reverse are HBM-bound row movers
         dom = "layout" if stage_ms["layout"] >= stage_ms["reverse"] else "reverse"
         achieved = ab[dom] / (stage_ms[dom] / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_" + dom, "achieved": achieved, "peak": peak,
+        kname = "k_gate_layout" if (dom == "layout" and fused_gl) else "k_" + dom
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
                 "traffic": tr.get("%s/%s" % (w.name, dom + ("_k" if dom == "reverse" and w.k <= 2 else "")),
                                   tr.get("%s/%s" % (w.name, dom))),
@@ -659,7 +667,8 @@ def main():
         dom = "layout" if t_d >= t_c else "a2a_combine"
         nb = ab["a2a_dispatch"] if dom == "layout" else ab["a2a_combine"]
         achieved = nb / (t_d if dom == "layout" else t_c) / 1e9
-        roof = {"bound": "nvlink", "kernel": "k_layout (peer dispatch)" if dom == "layout"
+        roof = {"bound": "nvlink", "kernel": ("k_gate_layout" if fused_gl else "k_layout") +
+                " (peer dispatch)" if dom == "layout"
                 else "k_reverse_k (peer combine)", "achieved": achieved, "peak": NVLINK_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_GBS, "traffic": None,
                 "algorithmic_bytes": nb,
@@ -668,14 +677,14 @@ def main():
         # the layout / reverse stages ARE the NVLink dispatch / combine (the
         # "reverse" and "a2a_dispatch" marks are empty stages: event resolution)
         roof["per_kernel_gbs"] = {
-            "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+            "gate": None if fused_gl else ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
             "k_layout (peer dispatch), NVLink per direction":
                 ab["a2a_dispatch"] / (stage_ms["layout"] / 1e3) / 1e9,
             "k_reverse_k (peer combine), NVLink per direction":
                 ab["a2a_combine"] / (stage_ms["a2a_combine"] / 1e3) / 1e9}
     else:
         roof["per_kernel_gbs"] = {
-            "gate": ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
+            "gate": None if fused_gl else ab["gate"] / (stage_ms["gate"] / 1e3) / 1e9,
             "layout": ab["layout"] / (stage_ms["layout"] / 1e3) / 1e9,
             "reverse": ab["reverse"] / (stage_ms["reverse"] / 1e3) / 1e9}
     a2a = None
@@ -744,7 +753,7 @@ def main():
         # P>1: counts, barrier, plan, layout, exit barrier, reverse, exit barrier)
         launches_per_step = gate_k + 1 + (7 if P > 1 else 2)
     else:
-        launches_per_step = gate_k + 2
+        launches_per_step = (1 if fused_gl else gate_k + 1) + 1
         if P > 1 and algo == "hier" and rank % G == 0:
             launches_per_step += 2
         elif P > 1 and algo == "hier2d":
@@ -763,7 +772,8 @@ def main():
                        "layout_form": "packed dropless (NEXT-4)" if a.dropless else "padded [E,cap,d]",
                        "parallelism": "ep%d (experts sharded, tokens data-parallel)" % P,
                        "l2": "flushed between timed steps (2x L2 memset + 2x L2 read, outside events)",
-                       "expert": "identity in the timed step; s_e stand-in timed separately"},
+                       "expert": "identity in the timed step; s_e stand-in timed separately",
+                       "gate_layout": "one fused kernel" if fused_gl else "separate kernels"},
             "stages_ms": stage_ms, "expert_ms": expert_ms, "min_ms_per_step": float(vals[-2]),
             "eager_ms_per_step": float(vals[-1]),
             "timing": "CUDA-graph replay of the whole step (events outside the graph); stages_ms "

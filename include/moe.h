@@ -198,11 +198,14 @@ moe_status_t moe_gate_ex(const moe_gate_desc_t* desc, const moe_gate_inputs_t* i
                          moe_stream_t stream);
 
 /* Steps 1 + 2 fused: exactly moe_gate_ex followed by
- * moe_layout (same routing outputs, same dispatch buffer, bit for bit), with
- * the gate's last pass (the capacity slots) done by the layout kernel itself,
- * which saves a kernel boundary.  Falls back to the two calls for rows that
- * are not a multiple of 32 bytes or k > 32.  Errors: as moe_gate_ex and
- * moe_layout. */
+ * moe_layout (same routing outputs, same dispatch buffer, bit for bit), as
+ * ONE persistent kernel: tiles of tokens are gated in order of a device-side
+ * counter, each resolves its per-expert slot offsets by a decoupled
+ * look-back over earlier tiles and scatters its rows at once, so the gate's
+ * latency hides behind the row traffic.  TOKEN priority,
+ * TOPK / KTOP1 with k <= 8 and HASH, rows a multiple of 32 bytes; other
+ * shapes run moe_gate_ex then moe_layout.  Uses the same workspace as
+ * moe_gate.  Errors: as moe_gate_ex and moe_layout. */
 moe_status_t moe_gate_layout(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
                              const moe_routing_t* out, void* ws, size_t ws_bytes, const void* x,
                              int32_t d, int32_t dtype, void* dispatch, moe_stream_t stream);
@@ -477,8 +480,10 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              int32_t dtype, void* y, int32_t flags, moe_stream_t stream);
 
 /* Steps 1 + 2 + 3 fused: moe_gate_ex + moe_dispatch_p2p
- * with the gate's capacity pass done by the dispatch kernel (as
- * moe_gate_layout); same routing and receive buffers, bit for bit. */
+ * with the gate and the NVLink row scatter as one persistent kernel (as
+ * moe_gate_layout; same dedupe and local padding as moe_dispatch_p2p); same
+ * routing and receive buffers, bit for bit.  Shapes without a fused kernel
+ * run moe_gate_ex then moe_dispatch_p2p. */
 moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                                    const moe_gate_inputs_t* in, const moe_routing_t* out,
                                    void* ws, size_t ws_bytes, const void* x, int32_t d,
@@ -661,8 +666,8 @@ typedef struct {
                                 logit gates, 256 for hash)                         */
   int32_t gate_two_maxw;     /* gate: tiles x columns <= this -> select + slots2,
                                 else select + scan + slots (4096)                  */
-  int32_t fin_smem_maxw;     /* moe_gate_layout: tiles x columns <= this -> the
-                                layout reduces the tile table itself (4096)        */
+  int32_t gate_layout_tile;  /* moe_gate_layout / moe_gate_dispatch_p2p: tokens per
+                                tile of the fused kernel, power of two 32..256 (32) */
   int32_t layout_u;          /* layout: 32-byte vectors per lane per segment;
                                 0 = auto (2 for rows <= 2 KiB, else 4); 1, 2, 4    */
   int32_t layout_pads_first; /* layout + combine adjoint: zero the padding rows

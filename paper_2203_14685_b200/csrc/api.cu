@@ -55,7 +55,7 @@ const TuneField kTune[] = {
     {"MOE_GATE_TILES", &moe_tuning_t::gate_tiles, 256, 1, 1 << 20},
     {"MOE_GATE_MAX_TILE", &moe_tuning_t::gate_max_tile, 0, 0, 256},
     {"MOE_GATE_TWO_MAXW", &moe_tuning_t::gate_two_maxw, 4096, 0, 1 << 30},
-    {"MOE_FIN_SMEM_MAXW", &moe_tuning_t::fin_smem_maxw, 4096, 0, 1 << 30},
+    {"MOE_GATE_LAYOUT_TILE", &moe_tuning_t::gate_layout_tile, 32, 32, 256},
     {"MOE_LAYOUT_U", &moe_tuning_t::layout_u, 0, 0, 4},
     {"MOE_LAYOUT_PADS_FIRST", &moe_tuning_t::layout_pads_first, -1, -1, 1},
     {"MOE_REVERSE_KU", &moe_tuning_t::reverse_ku, 0, 0, 4},
@@ -85,8 +85,8 @@ bool tune_valid(const moe_tuning_t& t) {
     set_error("moe_set_tuning: layout_u must be 0, 1, 2 or 4 and reverse_ku 0, 2 or 4");
     return false;
   }
-  if (t.gate_bwd_lanes & (t.gate_bwd_lanes - 1)) {
-    set_error("moe_set_tuning: gate_bwd_lanes must be 0 or a power of two");
+  if ((t.gate_bwd_lanes & (t.gate_bwd_lanes - 1)) || (t.gate_layout_tile & (t.gate_layout_tile - 1))) {
+    set_error("moe_set_tuning: gate_bwd_lanes and gate_layout_tile must be powers of two");
     return false;
   }
   return true;
@@ -233,17 +233,15 @@ moe_status_t moe_gate_layout(const moe_gate_desc_t* desc, const moe_gate_inputs_
   if (s != MOE_OK) return s;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const int ds = dtype_size(dtype);
-  if (((long long)d * ds) % 32 != 0 || desc->k > 32) {
-    s = gate_launch(*desc, *in, *out, ws, stream);  // the unfused pair
+  if (!gate_layout_supported(*desc, d * ds)) {  // the two steps, one after the other
+    s = gate_launch(*desc, *in, *out, ws, stream);
     if (s != MOE_OK) return s;
     return layout_launch(*desc, *out, x, ds, d, dispatch, stream);
   }
-  GateFinalize fin{};
-  s = gate_select_launch(*desc, *in, *out, ws, stream, &fin);
-  if (s != MOE_OK) return s;
   PeerPtrs dst{};
   dst.p[0] = static_cast<char*>(dispatch);
-  return layout_fin_launch(*desc, *out, x, ds, d, dst, desc->E, 0, fin, stream);
+  return gate_layout_launch(*desc, *in, *out, ws, x, ds, d, dst, desc->E, 0, nullptr, nullptr,
+                            stream);
 }
 
 }  // extern "C"

@@ -23,11 +23,11 @@
 //                  slot_src and its empty entries.
 //   k_gate_slots2  scan + slots in one pass (per-CTA table reduction).
 // SAM (R17) and Dense-to-Sparse (R18) are further selection kinds of
-// k_gate_select.  The capacity pass can also run inside the layout kernel
-// (gate_select_launch + layout.cu's k_layout_fin, moe_gate_layout).
+// k_gate_select.  With the layout, gate and scatter run as one persistent
+// kernel (gate_layout.cuh, moe_gate_layout / moe_gate_dispatch_p2p).
 // Columns are experts (TOKEN priority, t-major admission) or (j, expert)
 // pairs (SLOT priority, j-major).  Traffic is O(tiles x columns).
-#include "gate_impl.cuh"
+#include "gate_layout.cuh"
 
 namespace moe {
 
@@ -212,9 +212,38 @@ int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
   return two_kernels(gate_plan_default(d, ngroups)) ? 2 : 3;
 }
 
+// The fused gate + layout plan: tiles of T tokens (tuning gate_layout_tile,
+// default 32: enough tiles that every CTA of the persistent grid gets work
+// while the gate's latency hides behind other CTAs' scatter), doubled while
+// there would be more than 8192 tiles; its control block and status words
+// follow the gate's own workspace.
+struct FusedPlan {
+  GatePlan p;
+  size_t ctrl_off, st_off, bytes;
+};
+
+static FusedPlan fused_plan(const moe_gate_desc_t& d) {
+  int T = tuning().gate_layout_tile;
+  while ((d.S + T - 1) / T > 8192 && T < 256) T *= 2;
+  FusedPlan f;
+  f.p = gate_plan(d, 1 << 30, 1, T);
+  const size_t base = std::max({gate_plan_default(d).bytes, gate_plan(d, 1 << 20, 1, 32).bytes});
+  f.ctrl_off = (base + 255) & ~(size_t)255;
+  f.st_off = f.ctrl_off + 256;
+  f.bytes = f.st_off + sizeof(unsigned long long) * (size_t)f.p.n_tiles * d.E;
+  f.bytes = (f.bytes + 255) & ~(size_t)255;
+  return f;
+}
+
 size_t gate_workspace_bytes(const moe_gate_desc_t& d) {
-  // room for every tile count the tuning may pick (the table is small)
-  return std::max({gate_plan_default(d).bytes, gate_plan(d, 1 << 20, 1, 32).bytes});
+  // room for every tile count the tuning may pick (the table is small) and
+  // for the fused gate + layout kernel's status words
+  return fused_plan(d).bytes;
+}
+
+bool gate_layout_supported(const moe_gate_desc_t& d, int row_bytes) {
+  return (d.kind == MOE_GATE_TOPK || d.kind == MOE_GATE_KTOP1 || d.kind == MOE_GATE_HASH) &&
+         d.priority == MOE_PRIO_TOKEN && d.k <= 8 && d.E <= 256 && row_bytes % 32 == 0;
 }
 
 static void fill_args(GateArgs& a, const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
@@ -270,36 +299,6 @@ static moe_status_t select_launch(const moe_gate_desc_t& d, const GatePlan& p, G
   return MOE_OK;
 }
 
-moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
-                                const moe_routing_t& out, void* ws, cudaStream_t stream,
-                                GateFinalize* fin) {
-  const int ng = d.kind == MOE_GATE_SAM ? in.n_groups : 1;
-  const GatePlan p = gate_plan_default(d, ng);
-  GateArgs a;  // launch arguments are copied at launch
-  fill_args(a, d, in, out, ws, p, ng);
-  moe_status_t s = select_launch(d, p, a, stream);
-  if (s != MOE_OK) return s;
-  fin->agg = reinterpret_cast<const unsigned*>(a.status);
-  fin->totals = a.totals;
-  fin->n_tiles = p.n_tiles;
-  fin->tile_tokens = p.tile_tokens;
-  fin->ncols = p.ncols;
-  fin->prio = d.priority;
-  fin->slot_idx = out.slot_idx;
-  fin->slot_src = out.slot_src;
-  fin->weight = out.weight;
-  fin->load = out.load;
-  // the layout reduces the raw table itself when it fits its shared memory
-  fin->scanned = (long long)p.n_tiles * p.ncols > tuning().fin_smem_maxw;
-  if (fin->scanned) {
-    void* args[] = {&a};
-    cudaError_t e = launch_pdl((const void*)k_gate_scan, dim3((p.ncols + kGateWarps - 1) / kGateWarps),
-                               dim3(kGateThreads), 0, stream, args);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
-  }
-  return MOE_OK;
-}
-
 // k_gate_select -> (k_gate_slots2 | k_gate_scan -> k_gate_slots), PDL-chained.
 moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
                          const moe_routing_t& out, void* ws, cudaStream_t stream) {
@@ -322,6 +321,67 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_scan launch");
   e = launch_pdl((const void*)k_gate_slots, dim3(p.n_tiles), dim3(kGateThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_gate: k_gate_slots launch");
+  return MOE_OK;
+}
+
+moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                                const moe_routing_t& out, void* ws, const void* x,
+                                int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
+                                int rank, const PeerPtrs* pad_tab, const PeerPtrs* dup_tab,
+                                cudaStream_t stream) {
+  const int row_bytes = dtype_size * dcols;
+  if (!gate_layout_supported(d, row_bytes)) {
+    set_error("moe_gate_layout: no fused kernel for this gate (SLOT priority, SAM, D2S, k > 8 "
+              "or rows not a multiple of 32 bytes)");
+    return MOE_ERR_UNSUPPORTED;
+  }
+  const FusedPlan fp = fused_plan(d);
+  const GatePlan& p = fp.p;
+  FusedArgs f{};
+  fill_args(f.g, d, in, out, ws, p, 1);
+  RowArgs& a = f.r;
+  a.src = static_cast<const char*>(x);
+  a.expert_idx = out.expert_idx;
+  a.slot_idx = out.slot_idx;
+  a.weight = out.weight;
+  a.load = out.load;
+  a.S = d.S;
+  a.E = d.E;
+  a.k = d.k;
+  a.cap = d.capacity;
+  a.row_bytes = row_bytes;
+  a.d = dcols;
+  a.dpeer = dst;
+  a.E_local = E_local;
+  a.rank = rank;
+  a.sys_fence = E_local != d.E;
+  if (pad_tab) {
+    a.skip_pads = 1;
+    a.ptab = *pad_tab;
+  }
+  if (dup_tab) {
+    a.dedupe = 1;
+    a.dup = *dup_tab;
+  }
+  char* w = static_cast<char*>(ws);
+  f.fc = reinterpret_cast<FusedCtrl*>(w + fp.ctrl_off);
+  f.st = reinterpret_cast<unsigned long long*>(w + fp.st_off);
+  const int U = row_bytes <= 2048 ? 2 : 4;  // as k_layout: 2 KiB segments for rows <= 2 KiB
+  FusedKernel kern = d.kind == MOE_GATE_HASH    ? pick_fused_hash(U)
+                     : d.kind == MOE_GATE_KTOP1 ? pick_fused_ktop1(p.L, p.K, U)
+                                                : pick_fused_topk(p.L, p.K, U);
+  if (p.smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)kern,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return cuda_status(e, "moe_gate_layout: smem attribute");
+  }
+  int per_sm = tuning().row_ctas_per_sm;
+  if (per_sm <= 0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, kGateThreads, p.smem);
+  const int grid = std::max(1, per_sm) * device_sm_count();
+  void* args[] = {&f};
+  cudaError_t e = launch_pdl((const void*)kern, dim3(grid), dim3(kGateThreads), p.smem, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "moe_gate_layout: k_gate_layout launch");
   return MOE_OK;
 }
 

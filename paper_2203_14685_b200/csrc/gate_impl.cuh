@@ -462,14 +462,25 @@ __device__ __forceinline__ void select_d2s(const GateArgs& a, const float* row, 
 // ------------------------------------------------------------ the kernel
 enum { KIND_TOPK = 0, KIND_KTOP1 = 1, KIND_HASH = 2, KIND_SAM = 3, KIND_D2S = 4 };
 
-// Phases A and B of one tile (k_gate_select):
+// The logits-tile mbarrier: initialised once per CTA (thread 0, then a
+// __syncthreads before its first use); gate_tile's n-th use waits on parity
+// n & 1.
+__device__ __forceinline__ void gate_mbar_init(unsigned long long& s_mbar) {
+  const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Phases A and B of one tile (k_gate_select, k_gate_layout):
 // stage the logits, select + weights (expert_idx, weight written), in-tile
 // ranks per column (s_exp, s_rank), s_hist[w][c] turned into the exclusive
-// prefix over warps, and the tile aggregates agg[c][tile] written.  Returns
+// prefix over warps, and the tile aggregates written: agg[c][tile] in the
+// workspace, or s_agg[c] in shared memory when s_agg is given.  Returns
 // with the CTA synchronised.
 template <int KIND, int L, int K>
 __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned& s_bad,
-                                          unsigned long long& s_mbar) {
+                                          unsigned long long& s_mbar, int tile, unsigned parity,
+                                          int* s_agg = nullptr) {
   const int items = a.tile_tokens * a.k;
   float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
   double* s_z = reinterpret_cast<double*>(smem + a.lg_words);  // D2S: [tile_tokens][E]
@@ -482,7 +493,6 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
   for (int i = tid; i < items; i += kGateThreads) s_exp[i] = -1;
   for (int i = tid; i < kGateWarps * a.ncols; i += kGateThreads) s_hist[i] = 0;
   __syncthreads();
-  const int tile = blockIdx.x;
   const int t0 = tile * a.tile_tokens;
   const int nt = min(a.tile_tokens, a.S - t0);
   if constexpr (KIND != KIND_HASH) {
@@ -493,8 +503,8 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
     const float* g = a.logits + (size_t)t0 * a.E;
     const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar);
     if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // the previous tile's generic-proxy reads of the buffer come first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bulk)
                    : "memory");
       const unsigned dst = (unsigned)__cvta_generic_to_shared(s_lg);
@@ -507,13 +517,13 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
       }
     }
     for (unsigned i = bulk / 4 + tid; i < bytes / 4; i += kGateThreads) s_lg[i] = __ldg(g + i);
-    __syncthreads();  // mbarrier initialised before anyone waits on it
+    __syncthreads();  // the tail's plain stores
     unsigned done = 0;
     while (!done)
       asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
           : "=r"(done)
-          : "r"(mbar)
+          : "r"(mbar), "r"(parity)
           : "memory");
   }
 
@@ -602,7 +612,10 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
       s_hist[w * a.ncols + c] = (int)run;
       run += v;
     }
-    agg[(size_t)c * a.n_tiles + tile] = run;
+    if (s_agg)
+      s_agg[c] = (int)run;
+    else
+      agg[(size_t)c * a.n_tiles + tile] = run;
   }
   __syncthreads();
 }
@@ -614,7 +627,9 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   __shared__ __align__(8) unsigned long long s_mbar;
   pdl_wait();     // the producer of the logits / the previous step must be done
   pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
-  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar);
+  if (threadIdx.x == 0) gate_mbar_init(s_mbar);
+  __syncthreads();
+  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, blockIdx.x, 0);
   const int tid = threadIdx.x;
   const int items = a.tile_tokens * a.k;
   const int* s_exp = smem + a.lg_words + a.z_words;

@@ -5,29 +5,18 @@
 
 namespace moe {
 
-// What a layout kernel needs to finish the gate's capacity slots itself (the
-// gate-layout fusion): the select kernel has written expert_idx, weights and
-// the PROVISIONAL slots (rank inside the tile's column) plus the per-tile
-// column aggregates; the final slot adds the column prefix over earlier
-// tiles (and, for SLOT priority, the totals of earlier j).
-struct GateFinalize {
-  const unsigned* agg;   // [ncols][n_tiles]: raw aggregates (scanned = 0) or
-                         // exclusive prefixes (scanned = 1, k_gate_scan ran)
-  const int32_t* totals; // [ncols] (scanned = 1)
-  int scanned, n_tiles, tile_tokens, ncols, prio;
-  int32_t* slot_idx;     // provisional in, final out
-  int32_t* slot_src;     // may be NULL
-  float* weight;         // dropped slots get 0
-  int32_t* load;         // [E] written by the layout
-};
-// Launch only the gate's select kernel (+ k_gate_scan when the tile x column
-// table is too big for one CTA's shared memory) and describe the finalize.
-moe_status_t gate_select_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
-                                const moe_routing_t& out, void* ws, cudaStream_t stream,
-                                GateFinalize* fin);
-moe_status_t layout_fin_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                               int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
-                               int rank, const GateFinalize& fin, cudaStream_t stream);
+// Steps 1 + 2 in one persistent kernel (gate_layout.cuh): the gate and the
+// row scatter into `dst` (local: dst.p[0] = dispatch, E_local = E; peer
+// mode: the owners' receive buffers, with the optional duplicate-row and
+// padding-count tables of the one-sided dispatch).  UNSUPPORTED (nothing
+// launched) when the shape has no fused kernel: SLOT priority, SAM, D2S,
+// k > 8, rows not a multiple of 32 bytes; callers then launch gate + layout.
+bool gate_layout_supported(const moe_gate_desc_t& d, int row_bytes);
+moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
+                                const moe_routing_t& out, void* ws, const void* x,
+                                int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
+                                int rank, const PeerPtrs* pad_tab, const PeerPtrs* dup_tab,
+                                cudaStream_t stream);
 size_t gate_workspace_bytes(const moe_gate_desc_t& d);
 // host checks of moe_gate_ex's arguments (api.cu), without launching
 moe_status_t gate_validate(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,

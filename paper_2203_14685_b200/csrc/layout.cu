@@ -76,200 +76,6 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   if (a.sys_fence) __threadfence_system();
 }
 
-// ------------------------------------------------------------ gate-finalize + layout
-// Layout_Transform fused with the last pass of the gate (the capacity
-// slots): the select kernel left the provisional slots (rank inside the
-// tile's column) and the per-tile column aggregates; every CTA reduces the
-// aggregates into the exclusive prefix over tiles in shared memory (or reads
-// the prefixes k_gate_scan made, for big tables), and each token's warp
-// finishes its k slots (lane j: slot j) -- drop at >= cap, weight 0, slot_src
-// -- then scatters the row to the final slots.  One kernel boundary fewer
-// than gate (select -> slots) -> layout, with the same outputs bit for bit.
-template <int U>
-__global__ void __launch_bounds__(kRowThreads) k_layout_fin(RowArgs a, GateFinalize f) {
-  constexpr int VB = 32, SEG = 32 * U * VB;
-  extern __shared__ int fsm[];
-  int* T = fsm;                // [ncols] column totals
-  int* Pt = fsm + f.ncols;     // [ncols][n_tiles] exclusive prefixes (scanned == 0)
-  __shared__ int s_beg[257];
-  __shared__ int s_cnt[257];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  pdl_wait();  // the select (and scan) kernels are complete
-  pdl_trigger();
-  for (int c = warp; c < f.ncols; c += kRowWarps) {
-    if (f.scanned) {
-      if (lane == 0) T[c] = __ldcg(f.totals + c);
-      continue;
-    }
-    const unsigned* col = f.agg + (size_t)c * f.n_tiles;
-    unsigned carry = 0;
-    for (int base = 0; base < f.n_tiles; base += 256) {
-      unsigned v[8], run = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + lane * 8 + u;
-        v[u] = i < f.n_tiles ? __ldcg(col + i) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const unsigned x = v[u];
-        v[u] = run;
-        run += x;
-      }
-      unsigned incl = run;
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        const unsigned o = __shfl_up_sync(0xffffffffu, incl, m);
-        if (lane >= m) incl += o;
-      }
-      const unsigned ex = carry + incl - run;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + lane * 8 + u;
-        if (i < f.n_tiles) Pt[(size_t)c * f.n_tiles + i] = (int)(ex + v[u]);
-      }
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) T[c] = (int)carry;
-  }
-  __syncthreads();
-  const bool slot_prio = f.prio == MOE_PRIO_SLOT;
-  // per-expert requests (load), padding counts, and this CTA's share of the
-  // load[] stores and of the empty slot_src entries
-  for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
-    int ld = 0;
-    if (slot_prio)
-      for (int j = 0; j < a.k; ++j) ld += T[j * a.E + e];
-    else
-      ld = T[e];
-    s_cnt[e] = a.cap - min(ld, a.cap);
-  }
-  __syncthreads();
-  for (int e = blockIdx.x * kRowWarps + warp; e < a.E; e += gridDim.x * kRowWarps) {
-    const int ld = a.cap - s_cnt[e] < a.cap ? a.cap - s_cnt[e] : a.cap;  // min(load, cap)
-    if (lane == 0) {
-      int full = 0;
-      if (slot_prio)
-        for (int j = 0; j < a.k; ++j) full += T[j * a.E + e];
-      else
-        full = T[e];
-      f.load[e] = full;
-    }
-    if (f.slot_src)
-      for (int s = ld + lane; s < a.cap; s += 32) f.slot_src[(size_t)e * a.cap + s] = -1;
-  }
-  if (threadIdx.x < 32) {
-    int carry = 0;
-    for (int base = 0; base < a.E; base += 32) {
-      const int e = base + lane;
-      const int v = e < a.E ? s_cnt[e] : 0;
-      int incl = v;
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        const int o = __shfl_up_sync(0xffffffffu, incl, m);
-        if (lane >= m) incl += o;
-      }
-      if (e < a.E) s_beg[e] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) s_beg[a.E] = carry;
-  }
-  __syncthreads();
-
-  const int gw = blockIdx.x * kRowWarps + warp, nw = gridDim.x * kRowWarps;
-  for (int t = gw; t < a.S; t += nw) {
-    // finish the token's slots: lane j owns item t*k + j
-    int my_e = -1, my_s = -1;
-    if (lane < a.k) {
-      const size_t gi = (size_t)t * a.k + lane;
-      const int e = a.expert_idx[gi];
-      if (e >= 0) {
-        const int tile = t / f.tile_tokens;
-        const int col = slot_prio ? lane * a.E + e : e;
-        int s = f.slot_idx[gi] +
-                (f.scanned ? (int)__ldcg(f.agg + (size_t)col * f.n_tiles + tile)
-                           : Pt[(size_t)col * f.n_tiles + tile]);
-        if (slot_prio)
-          for (int jj = 0; jj < lane; ++jj) s += T[jj * a.E + e];
-        if (s < a.cap) {
-          if (f.slot_src) f.slot_src[(size_t)e * a.cap + s] = (int)gi;
-        } else {
-          s = -1;
-          f.weight[gi] = 0.f;
-        }
-        f.slot_idx[gi] = s;
-        my_e = e;
-        my_s = s;
-      }
-    }
-    const char* srow = a.src + (size_t)t * a.row_bytes;
-    for (int seg = 0; seg < a.row_bytes; seg += SEG) {
-      V8 r[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int off = seg + (lane + 32 * u) * VB;
-        if (off < a.row_bytes) r[u] = ld_stream_v8(srow + off);
-      }
-      for (int j = 0; j < a.k; ++j) {
-        const int s = __shfl_sync(0xffffffffu, my_s, j);
-        if (s < 0) continue;
-        char* drow = dst_row_of(a, __shfl_sync(0xffffffffu, my_e, j), s);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int off = seg + (lane + 32 * u) * VB;
-          if (off < a.row_bytes) st_v8(drow + off, r[u]);
-        }
-      }
-    }
-  }
-  // zero padding rows
-  const int npad = s_beg[a.E];
-  const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
-  for (int p = gw; p < npad; p += nw) {
-    int lo = 0, hi = a.E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_beg[mid] <= p) lo = mid; else hi = mid - 1;
-    }
-    char* drow = dst_row_of(a, lo, a.cap - s_cnt[lo] + (p - s_beg[lo]));
-    for (int off = lane * VB; off < a.row_bytes; off += 32 * VB) st_v8(drow + off, z);
-  }
-  if (a.sys_fence) __threadfence_system();
-}
-
-moe_status_t layout_fin_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
-                               int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
-                               int rank, const GateFinalize& fin, cudaStream_t stream) {
-  RowArgs a{};
-  a.src = static_cast<const char*>(x);
-  a.expert_idx = r.expert_idx;
-  a.slot_idx = r.slot_idx;
-  a.load = r.load;
-  a.S = d.S;
-  a.E = d.E;
-  a.k = d.k;
-  a.cap = d.capacity;
-  a.row_bytes = dtype_size * dcols;
-  a.d = dcols;
-  a.dpeer = dst;
-  a.E_local = E_local;
-  a.rank = rank;
-  a.sys_fence = E_local != d.E;
-  const size_t smem = sizeof(int) * ((size_t)fin.ncols + (fin.scanned ? 0 : (size_t)fin.ncols * fin.n_tiles));
-  const void* kern = a.row_bytes > 2048 ? (const void*)k_layout_fin<4> : (const void*)k_layout_fin<2>;
-  if (smem > 40 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "moe_gate_layout: smem attribute");
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem);
-  const int grid = std::max(1, per_sm) * device_sm_count();
-  void* args[] = {&a, (void*)&fin};
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), smem, stream, args);
-  if (e != cudaSuccess) return cuda_status(e, "moe_gate_layout: k_layout_fin launch");
-  return MOE_OK;
-}
-
 // ------------------------------------------------------------ Reverse + combine
 template <int DT, int U>
 __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {

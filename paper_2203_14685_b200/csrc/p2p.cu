@@ -535,13 +535,17 @@ static PeerPtrs pad_tables(const moe_comm* c) {
   return tab;
 }
 
-// Padded one-sided dispatch after the entry barrier (shared by the dispatch
-// and the push-form combine adjoint's dy scatter): rows into the owners'
-// `dst`, then (unless NO_EXIT) the exit barrier, the owners' duplicate-row
-// copies and local padding.  *dup_pending: duplicate copies were enqueued.
-static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, const moe_routing_t& R,
-                                  const void* x, int ds, int d, const PeerPtrs& dst, int32_t flags,
-                                  cudaStream_t stream, bool* dup_pending) {
+// Padded one-sided dispatch after the entry barrier (shared by the dispatch,
+// the fused gate + dispatch and the push-form combine adjoint's dy scatter):
+// rows into the owners' `dst` by `rows` (k_layout in peer mode, or the fused
+// gate + layout kernel), then (unless NO_EXIT) the exit barrier, the owners'
+// duplicate-row copies and local padding.  *dup_pending: copies enqueued.
+using RowLauncher = std::function<moe_status_t(cudaStream_t, const PeerPtrs* pad_tab,
+                                               const PeerPtrs* dup_tab)>;
+
+static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int row_bytes,
+                                  const PeerPtrs& dst, int32_t flags, cudaStream_t stream,
+                                  RowLauncher rows, bool* dup_pending) {
   const int P = comm->nranks, r = comm->rank, El = D.E / P;
   const bool exit_bar = !(flags & MOE_P2P_NO_EXIT_BARRIER);
   // local padding: the zero rows are written by their owner after the exit
@@ -557,8 +561,7 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, cons
   const bool dedupe = dup_table(comm, D, flags, stream, &dup, &s);
   if (s != MOE_OK) return s;
   s = run_or_queue(comm, stream, [=](cudaStream_t st) {
-    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, nullptr, nullptr,
-                               local_pad ? &tab : nullptr, dedupe ? &dup : nullptr);
+    return rows(st, local_pad ? &tab : nullptr, dedupe ? &dup : nullptr);
   });
   if (s != MOE_OK) return s;
   *dup_pending = false;
@@ -566,12 +569,12 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, cons
   s = comm_barrier(comm, stream);  // every row has landed
   if (s != MOE_OK) return s;
   const long long nrows = (long long)D.E * D.capacity;
-  const int rb = d * ds;
   char* mine = dst.p[r];
   if (dedupe) {
     int* dtab = reinterpret_cast<int*>(dup.p[r]);
-    s = run_or_queue(comm, stream,
-                     [=](cudaStream_t st) { return dup_fill_launch(mine, dtab, nrows, rb, st); });
+    s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+      return dup_fill_launch(mine, dtab, nrows, row_bytes, st);
+    });
     if (s != MOE_OK) return s;
     *dup_pending = true;
   }
@@ -579,8 +582,16 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, cons
   const int* ptab = reinterpret_cast<const int*>(tab.p[r]);
   const int cap = D.capacity;
   return run_or_queue(comm, stream, [=](cudaStream_t st) {
-    return pad_fill_launch(mine, ptab, P, El, cap, rb, st);
+    return pad_fill_launch(mine, ptab, P, El, cap, row_bytes, st);
   });
+}
+
+// k_layout in peer mode as the dispatch's row kernel
+static RowLauncher layout_rows(const moe_gate_desc_t& D, const moe_routing_t& R, const void* x,
+                               int ds, int d, const PeerPtrs& dst, int El, int r) {
+  return [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup) {
+    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, nullptr, nullptr, pad, dup);
+  };
 }
 
 }  // namespace moe
@@ -643,7 +654,9 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
     if (s != MOE_OK) return s;
   }
   bool dup_pending = false;
-  s = dispatch_body(comm, *desc, *routing, x, ds, d, dst, flags, stream, &dup_pending);
+  s = dispatch_body(comm, *desc, d * ds, dst, flags, stream,
+                    layout_rows(*desc, *routing, x, ds, d, dst, desc->E / comm->nranks, comm->rank),
+                    &dup_pending);
   if (s != MOE_OK) return s;
   comm->dup_recv = dup_pending ? recv : nullptr;
   return MOE_OK;
@@ -707,7 +720,7 @@ moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc
   const moe_gate_desc_t D = *desc;
   const moe_gate_inputs_t I = *in;
   const moe_routing_t R = *out;
-  if (((long long)d * ds) % 32 != 0 || desc->k > 32) {
+  if (!gate_layout_supported(D, d * ds)) {  // gate, then the dispatch
     s = run_or_queue(comm, stream, [=](cudaStream_t st) { return gate_launch(D, I, R, ws, st); });
     if (s != MOE_OK) return s;
     return moe_dispatch_p2p(comm, desc, out, x, d, dtype, recv, flags, stream_);
@@ -717,16 +730,16 @@ moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc
     s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
   }
-  s = run_or_queue(comm, stream, [=](cudaStream_t st) {
-    GateFinalize fin{};
-    moe_status_t s2 = gate_select_launch(D, I, R, ws, st, &fin);
-    if (s2 != MOE_OK) return s2;
-    return layout_fin_launch(D, R, x, ds, d, dst, D.E / P, r, fin, st);
-  });
+  bool dup_pending = false;
+  s = dispatch_body(comm, D, d * ds, dst, flags, stream,
+                    [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup) {
+                      return gate_layout_launch(D, I, R, ws, x, ds, d, dst, D.E / P, r, pad, dup,
+                                                st);
+                    },
+                    &dup_pending);
   if (s != MOE_OK) return s;
-  comm->dup_recv = nullptr;
-  if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
-  return comm_barrier(comm, stream);
+  comm->dup_recv = dup_pending ? recv : nullptr;
+  return MOE_OK;
 }
 
 moe_status_t moe_combine_backward_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
@@ -799,7 +812,8 @@ moe_status_t moe_combine_backward_push_p2p(moe_comm_t* comm, const moe_gate_desc
   });
   if (s != MOE_OK) return s;
   bool dup_pending = false;
-  s = dispatch_body(comm, D, R, dy, ds, d, dst, 0, stream, &dup_pending);
+  s = dispatch_body(comm, D, d * ds, dst, 0, stream, layout_rows(D, R, dy, ds, d, dst, D.E / P, r),
+                    &dup_pending);
   if (s != MOE_OK) return s;
   // owners: scale in place, dot with the local expert rows into the token
   // owners' dw tables; barrier; token owners gather d_weight

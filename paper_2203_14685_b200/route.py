@@ -22,25 +22,21 @@ class RoutePipeline:
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
                  device=None, slot_src: bool = True, dropless: bool = False,
-                 fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False):
+                 fuse_gate_layout: bool = True, identity_alias: bool = False):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
         exchange (algo "p2p" only).  The expert stand-in is the identity.
+        fuse_gate_layout (default): steps 1 + 2 as one persistent kernel
+        (moe_gate_layout / moe_gate_dispatch_p2p; the library runs the two
+        steps separately for shapes it has no fused kernel for).
         identity_alias=True (p2p only): a step with expert=False tells the
         combine that recv is unmodified (MOE_P2P_RECV_UNMODIFIED): no entry
         barrier and one read of a row sent once for two slots.  A measurement
         of the routing alone; a real expert always takes the default path."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
-        # the gate's capacity pass inside the layout / dispatch kernel
-        # (moe_gate_layout / moe_gate_dispatch_p2p): measured slower than the
-        # separate kernels under PDL (C2 51.6 vs 49.6 us for gate + layout),
-        # so off unless asked for (MOE_FUSE_GATE_LAYOUT=1)
-        if fuse_gate_layout is None:
-            import os
-            fuse_gate_layout = os.environ.get("MOE_FUSE_GATE_LAYOUT", "0") == "1"
-        self.fuse = fuse_gate_layout and not dropless and (algo in ("flat", "p2p") or comm is None)
+        self.fuse = fuse_gate_layout and not dropless
         self.identity_alias = identity_alias
         if dropless:
             cap = S * k
@@ -114,7 +110,7 @@ class RoutePipeline:
                 return self.step(logits, x, token_ids, table, expert, mark)
             finally:
                 self.y = saved
-        if self.fuse and (self.P == 1 or self.algo in ("flat", "p2p")):
+        if self.fuse:
             return self._step_fused(logits, x, token_ids, table, expert, mark)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         if self.dropless:
@@ -153,18 +149,18 @@ class RoutePipeline:
         return 0
 
     def _step_fused(self, logits, x, token_ids, table, expert, mark):
-        """The step with the gate's capacity pass fused into the layout
-        (P=1, NCCL flat) or into the one-sided dispatch (p2p)."""
+        """The step with the gate and the layout as one kernel (P=1, NCCL
+        AllToAlls) or the gate and the one-sided dispatch (p2p).  Its time
+        is the "layout" stage (the "gate" stage is empty)."""
+        mark("gate")
         if self.P > 1 and self.algo == "p2p":                              # steps 1+2+3
             r = self.gate.with_dispatch_p2p(self.comm, x, self.recv, logits, token_ids, table,
                                             out=self.routing, flags=self._first_flags())
-            mark("gate")
             mark("layout")
             mark("a2a_dispatch")
         else:                                                              # steps 1+2
             r = self.gate.with_layout(x, self.dispatch, logits, token_ids, table,
                                       out=self.routing)
-            mark("gate")
             mark("layout")
             self.alltoall(self.dispatch, self.recv)                        # step 3
             mark("a2a_dispatch")

@@ -312,3 +312,71 @@ def test_gate_layout_fused_equals_gate_then_layout(orc, case):
     assert host(disp).tobytes() == orc.layout(x, ro).tobytes()
     if kind == "hash":
         assert g.check() == ro.bad
+
+
+@pytest.mark.parametrize("tile", [32, 64, 256])
+@pytest.mark.parametrize("case", [
+    dict(kind="topk", S=32768, E=8, k=2, d=1024),           # C2 shape
+    dict(kind="topk", S=8192, E=64, k=1, d=2048),           # C3 rows (4 KiB, U = 4)
+    dict(kind="ktop1", S=20000, E=32, k=2, d=512),
+    dict(kind="hash", S=20000, E=32, k=1, d=512, C=1.25),
+    dict(kind="topk", S=3333, E=256, k=8, d=128, C=0.7),     # widest gate, K = 8
+    dict(kind="topk", S=1, E=4, k=2, d=64),                  # one token
+], ids=lambda c: "-".join("%s=%s" % kv for kv in c.items()))
+def test_gate_layout_fused_replays(orc, case, tile):
+    """The fused kernel's device-side tile counter, epoch-tagged look-back
+    words and ready word reset themselves: eager calls and CUDA-graph replays
+    with new inputs each match the oracle, for every tile size."""
+    kind, S, E, k, d = case["kind"], case["S"], case["E"], case["k"], case["d"]
+    cap = orc.capacity(S, E, k, case.get("C", 1.0))
+    with moe.tuned(gate_layout_tile=tile):
+        g = moe.Gate(S, E, k, cap, kind)
+        xd = torch.empty((S, d), dtype=torch.bfloat16, device="cuda")
+        lgd = torch.empty((S, E), dtype=torch.float32, device="cuda")
+        idd = torch.empty((S,), dtype=torch.int32, device="cuda")
+        disp = torch.empty((E, cap, d), dtype=torch.bfloat16, device="cuda")
+        out = moe.Routing.empty(S, E, k, cap, "cuda", g.kind, g.mode, g.prio)
+        table = None
+        if kind == "hash":
+            ids, table = synthgen.hash_inputs(4242, S, 32768, E)
+            table_d = dev(table)
+
+        def fill(it):
+            x = synthgen.tokens(700 + it, S, d, "bf16")
+            xd.copy_(dev(x))
+            if kind == "hash":
+                ids = synthgen.hash_inputs(4300 + it, S, 32768, E)[0]
+                idd.copy_(dev(ids))
+                return x, None, ids
+            lg = synthgen.logits(800 + it, S, E, k, kind, skew=0.2 * it)
+            lgd.copy_(dev(lg))
+            return x, lg, None
+
+        def call():
+            if kind == "hash":
+                g.with_layout(xd, disp, None, idd, table_d, out=out)
+            else:
+                g.with_layout(xd, disp, lgd, out=out)
+
+        def check(x, lg, ids, what):
+            ro = orc.gate(lg, E=E, k=k, cap=cap, kind=kind, token_ids=ids, table=table)
+            assert_routing_equal(out, ro, what)
+            assert host(disp).tobytes() == orc.layout(x, ro).tobytes(), what
+
+        for it in range(2):
+            v = fill(it)
+            call()
+            torch.cuda.synchronize()
+            check(*v, "eager %d" % it)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                call()
+        torch.cuda.current_stream().wait_stream(s)
+        for it in range(2, 5):
+            v = fill(it)
+            graph.replay()
+            torch.cuda.synchronize()
+            check(*v, "replay %d" % it)
