@@ -381,6 +381,13 @@ moe_status_t moe_comm_check(moe_comm_t* comm, moe_stream_t stream);
  * the symmetric buffers and frees comm, without waiting for the peers. */
 moe_status_t moe_comm_abort(moe_comm_t* comm);
 
+/* host.  Device memory from ncclMemAlloc, registered with the communicator
+ * (ncclCommRegister) so NCCL's send/recv move it without staging through its
+ * own buffers (zero-copy over NVLink).  For moe_alltoall / moe_alltoallv
+ * send and receive buffers.  Freed by moe_comm_mem_free or destroy. */
+moe_status_t moe_comm_mem_alloc(moe_comm_t* comm, size_t bytes, void** ptr);
+moe_status_t moe_comm_mem_free(moe_comm_t* comm, void* ptr);
+
 /* host.  Device workspace moe_alltoall needs (0 for FLAT and P2P; for
  * HIER_LEADER the leader's staging, 2 * group_size * nranks * bytes_per_peer
  * (members need none); for HIER_2D 2 * nranks * bytes_per_peer on every
@@ -695,6 +702,12 @@ typedef struct {
                                 report MOE_ERR_TIMEOUT (moe_comm_check); 0 = wait
                                 forever (60000)                                    */
   int32_t disable_p2p;       /* moe_comm_init: do not map peer memory (0)          */
+  int32_t nccl_alltoall;     /* moe_alltoall(FLAT): 1 = ncclAlltoAll, 0 = one group
+                                of ncclSend/ncclRecv pairs (0)                     */
+  int32_t nccl_max_ctas;     /* moe_comm_init: ncclConfig_t maxCTAs; 0 = NCCL's    */
+  int32_t nccl_min_ctas;     /* moe_comm_init: ncclConfig_t minCTAs; 0 = NCCL's    */
+  int32_t nccl_cta_policy;   /* moe_comm_init: ncclConfig_t CTAPolicy (0 default, 1
+                                efficiency, 2 zero); -1 = NCCL's                   */
 } moe_tuning_t;
 
 /* host.  Copy of the current table (after the one-time environment read). */

@@ -45,7 +45,8 @@ TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "gate_layout_ti
                  "layout_pads_first", "reverse_ku", "reverse_tpw", "reverse_kspec",
                  "reverse_backwards", "reverse_y_ef", "row_ctas_per_sm", "combine_bwd_kspec",
                  "gate_bwd_lanes", "p2p_dedupe", "p2p_local_pad", "a2a_ctas_per_sm",
-                 "barrier_timeout_ms", "disable_p2p")
+                 "barrier_timeout_ms", "disable_p2p", "nccl_alltoall", "nccl_max_ctas",
+                 "nccl_min_ctas", "nccl_cta_policy")
 
 
 class Tuning(ctypes.Structure):
@@ -133,6 +134,8 @@ SIGNATURES = [
     ("moe_combine_p2p", ctypes.c_int, [vp, ctypes.POINTER(GateDesc), ctypes.POINTER(RoutingC), vp,
                                        i32, i32, vp, i32, vp]),
     ("moe_comm_check", ctypes.c_int, [vp, vp]),
+    ("moe_comm_mem_alloc", ctypes.c_int, [vp, sz, ctypes.POINTER(vp)]),
+    ("moe_comm_mem_free", ctypes.c_int, [vp, vp]),
     ("moe_comm_abort", ctypes.c_int, [vp]),
     ("moe_alltoallv_plan", ctypes.c_int, [i32, i32, vp, vp, vp, vp, vp]),
     ("moe_sim_world_create", ctypes.c_int, [i32, ctypes.POINTER(vp)]),

@@ -489,6 +489,17 @@ class Comm:
         check(lib().moe_comm_symm_alloc(self._h, nb, ctypes.byref(p)), "moe_comm_symm_alloc")
         return _tensor_from_ptr(p.value, shape, dtype, torch.cuda.current_device())
 
+    def mem_empty(self, shape, dtype) -> torch.Tensor:
+        """A tensor over NCCL-registered memory (ncclMemAlloc +
+        ncclCommRegister): zero-copy send/recv buffers for alltoall."""
+        nb = int(torch.Size(shape).numel()) * torch.empty((), dtype=dtype).element_size()
+        p = ctypes.c_void_p()
+        check(lib().moe_comm_mem_alloc(self._h, nb, ctypes.byref(p)), "moe_comm_mem_alloc")
+        return _tensor_from_ptr(p.value, shape, dtype, torch.cuda.current_device())
+
+    def mem_free(self, t: torch.Tensor):
+        check(lib().moe_comm_mem_free(self._h, _p(t)), "moe_comm_mem_free")
+
     def symm_free(self, t: torch.Tensor):
         check(lib().moe_comm_symm_free(self._h, _p(t)), "moe_comm_symm_free")
 

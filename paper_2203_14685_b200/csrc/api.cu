@@ -71,6 +71,10 @@ const TuneField kTune[] = {
     {"MOE_A2A_CTAS_PER_SM", &moe_tuning_t::a2a_ctas_per_sm, 4, 1, 64},
     {"MOE_BARRIER_TIMEOUT_MS", &moe_tuning_t::barrier_timeout_ms, 60000, 0, 1 << 30},
     {"MOE_DISABLE_P2P", &moe_tuning_t::disable_p2p, 0, 0, 1},
+    {"MOE_NCCL_ALLTOALL", &moe_tuning_t::nccl_alltoall, 0, 0, 1},
+    {"MOE_NCCL_MAX_CTAS", &moe_tuning_t::nccl_max_ctas, 0, 0, 64},
+    {"MOE_NCCL_MIN_CTAS", &moe_tuning_t::nccl_min_ctas, 0, 0, 64},
+    {"MOE_NCCL_CTA_POLICY", &moe_tuning_t::nccl_cta_policy, -1, -1, 2},
 };
 moe_tuning_t g_tune;
 std::once_flag g_tune_once;

@@ -194,6 +194,10 @@ moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, 
   if (ce != cudaSuccess) return cuda_status(ce, "moe_comm_init: cudaGetDevice");
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   cfg.blocking = 1;
+  const moe_tuning_t& tu = tuning();
+  if (tu.nccl_max_ctas > 0) cfg.maxCTAs = tu.nccl_max_ctas;
+  if (tu.nccl_min_ctas > 0) cfg.minCTAs = tu.nccl_min_ctas;
+  if (tu.nccl_cta_policy >= 0) cfg.CTAPolicy = tu.nccl_cta_policy;
   ncclComm_t c;
   moe_status_t s = nccl_status(ncclCommInitRankConfig(&c, nranks, u, rank, &cfg), "moe_comm_init");
   if (s != MOE_OK) return s;
@@ -216,6 +220,14 @@ moe_status_t moe_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, 
   return MOE_OK;
 }
 
+static void release_regs(moe_comm_t* comm) {
+  for (auto& pr : comm->regs) {
+    if (pr.second) ncclCommDeregister(comm->nccl, pr.second);
+    ncclMemFree(pr.first);
+  }
+  comm->regs.clear();
+}
+
 moe_status_t moe_comm_destroy(moe_comm_t* comm) {
   if (!comm) return MOE_OK;
   if (comm->sim) {
@@ -223,6 +235,7 @@ moe_status_t moe_comm_destroy(moe_comm_t* comm) {
     return MOE_ERR_INVALID_ARG;
   }
   cudaDeviceSynchronize();
+  release_regs(comm);
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
   if (comm->dup.base) symm_release(comm, comm->dup);
@@ -268,11 +281,62 @@ moe_status_t moe_comm_abort(moe_comm_t* comm) {
   // NCCL first: it unblocks this rank's NCCL kernels, so the device drains
   moe_status_t s = nccl_status(ncclCommAbort(comm->nccl), "moe_comm_abort");
   cudaDeviceSynchronize();
+  for (auto& pr : comm->regs) ncclMemFree(pr.first);  // the registrations died with the comm
+  comm->regs.clear();
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
   if (comm->dup.base) symm_release(comm, comm->dup);
   delete comm;
   return s;
+}
+
+moe_status_t moe_comm_mem_alloc(moe_comm_t* comm, size_t bytes, void** out) {
+  if (!comm || !out || bytes == 0) {
+    set_error("moe_comm_mem_alloc: bad arguments");
+    return MOE_ERR_INVALID_ARG;
+  }
+  if (comm->sim) {  // simulated ranks: plain device memory
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) return cuda_status(e, "moe_comm_mem_alloc");
+    comm->regs.emplace_back(*out, nullptr);
+    return MOE_OK;
+  }
+  void* p = nullptr;
+  moe_status_t s = nccl_status(ncclMemAlloc(&p, bytes), "moe_comm_mem_alloc: ncclMemAlloc");
+  if (s != MOE_OK) return s;
+  void* h = nullptr;
+  s = nccl_status(ncclCommRegister(comm->nccl, p, bytes, &h), "moe_comm_mem_alloc: ncclCommRegister");
+  if (s != MOE_OK) {
+    ncclMemFree(p);
+    return s;
+  }
+  comm->regs.emplace_back(p, h);
+  *out = p;
+  return MOE_OK;
+}
+
+moe_status_t moe_comm_mem_free(moe_comm_t* comm, void* p) {
+  if (!comm || !p) {
+    set_error("moe_comm_mem_free: bad arguments");
+    return MOE_ERR_INVALID_ARG;
+  }
+  for (size_t i = 0; i < comm->regs.size(); ++i) {
+    if (comm->regs[i].first != p) continue;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "moe_comm_mem_free: sync");
+    moe_status_t s = MOE_OK;
+    if (comm->sim) {
+      cudaFree(p);
+    } else {
+      s = nccl_status(ncclCommDeregister(comm->nccl, comm->regs[i].second),
+                      "moe_comm_mem_free: ncclCommDeregister");
+      ncclMemFree(p);
+    }
+    comm->regs.erase(comm->regs.begin() + i);
+    return s;
+  }
+  set_error("moe_comm_mem_free: %p was not allocated by moe_comm_mem_alloc", p);
+  return MOE_ERR_INVALID_ARG;
 }
 
 moe_status_t moe_comm_size(const moe_comm_t* comm, int32_t* nranks, int32_t* rank) {
@@ -456,6 +520,11 @@ moe_status_t moe_alltoall(moe_comm_t* comm, int32_t algo, int32_t group_size, co
                 bytes_per_peer);
       return MOE_ERR_ALIGNMENT;
     }
+  }
+  if (algo == MOE_A2A_FLAT && tuning().nccl_alltoall && !comm->sim) {
+    // NCCL's own AllToAll (2.28): the same bytes as the grouped send/recv
+    return nccl_status(ncclAlltoAll(send, recv, bytes_per_peer, ncclInt8, comm->nccl, stream),
+                       "moe_alltoall: ncclAlltoAll");
   }
   std::vector<moe_a2a_op_t> plan = make_plan(P, r, algo, group_size);
   const size_t b = bytes_per_peer;

@@ -71,6 +71,8 @@ struct moe_comm {
   moe_sim_world* sim = nullptr;
   std::vector<moe::SimItem> queue;
   int sim_nalloc = 0;              // symmetric allocations made by this rank so far
+  // NCCL-registered buffers of moe_comm_mem_alloc: (pointer, registration)
+  std::vector<std::pair<void*, void*>> regs;
 };
 
 namespace moe {
