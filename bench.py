@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
+    ap.add_argument("--tokens", type=int, default=0,
+                    help="tokens per rank instead of the workload's S (e.g. C5's end-to-end "
+                         "points: S = 4096 / 32768 / 262144 for B = 16 / 128 / 1024 MiB)")
     ap.add_argument("--algo", default="p2p", choices=["p2p", "flat", "hier", "hier2d"],
                     help="AllToAll at N>1: p2p = fused one-sided NVLink path (falls back to "
                          "flat if the GPUs cannot map each other's memory); flat / hier (the "
@@ -256,6 +259,9 @@ def main():
     a = parse()
     import synthgen
     w = synthgen.WORKLOADS[a.workload]
+    if a.tokens:
+        import dataclasses
+        w = dataclasses.replace(w, S=a.tokens)
     world, rank, local = dist_env()
     if a.impl == "reference":
         run_reference(a, w, world, rank)

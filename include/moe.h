@@ -669,12 +669,11 @@ moe_status_t moe_sim_world_destroy(moe_sim_world_t* w);
  * that.  "auto" = decided per call from the shapes, as documented. */
 typedef struct {
   int32_t gate_tiles;        /* gate: aim for >= this many tiles (256)             */
-  int32_t gate_max_tile;     /* gate: largest tile in tokens; 0 = auto (128 for
-                                logit gates, 256 for hash)                         */
+  int32_t gate_max_tile;     /* gate (and the fused gate + layout): largest tile in
+                                tokens; 0 = auto (128 for logit gates, 256 for
+                                hash)                                              */
   int32_t gate_two_maxw;     /* gate: tiles x columns <= this -> select + slots2,
                                 else select + scan + slots (4096)                  */
-  int32_t gate_layout_tile;  /* moe_gate_layout / moe_gate_dispatch_p2p: tokens per
-                                tile of the fused kernel, power of two 32..256 (32) */
   int32_t layout_u;          /* layout: 32-byte vectors per lane per segment;
                                 0 = auto (2 for rows <= 2 KiB, else 4); 1, 2, 4    */
   int32_t layout_pads_first; /* layout + combine adjoint: zero the padding rows
@@ -716,6 +715,16 @@ moe_status_t moe_get_tuning(moe_tuning_t* out);
  * its range.  Affects calls made after it returns; not synchronised with
  * calls running on other host threads. */
 moe_status_t moe_set_tuning(const moe_tuning_t* t);
+
+/* host.  PROFILING: a device buffer of `bytes` that the fused gate + layout
+ * kernel (moe_gate_layout, moe_gate_dispatch_p2p) fills with %globaltimer
+ * stamps (ns, uint64) on every launch made while it is set: per tile of the
+ * gate [claim, aggregate published, prefix published, ready] at 4*tile, per
+ * 32-token scatter chunk [claim, its tile seen ready] at 4*n_tiles + 2*chunk,
+ * per CTA [start, end] after those; stamps beyond `bytes` are dropped.
+ * NULL (or 0 bytes) turns it off.  Affects launches made after it returns
+ * (a captured graph keeps the buffer it was captured with). */
+moe_status_t moe_set_trace(void* buf, size_t bytes);
 
 /* ---------------------------------------------------------------- misc */
 

@@ -55,7 +55,6 @@ const TuneField kTune[] = {
     {"MOE_GATE_TILES", &moe_tuning_t::gate_tiles, 256, 1, 1 << 20},
     {"MOE_GATE_MAX_TILE", &moe_tuning_t::gate_max_tile, 0, 0, 256},
     {"MOE_GATE_TWO_MAXW", &moe_tuning_t::gate_two_maxw, 4096, 0, 1 << 30},
-    {"MOE_GATE_LAYOUT_TILE", &moe_tuning_t::gate_layout_tile, 32, 32, 256},
     {"MOE_LAYOUT_U", &moe_tuning_t::layout_u, 0, 0, 4},
     {"MOE_LAYOUT_PADS_FIRST", &moe_tuning_t::layout_pads_first, -1, -1, 1},
     {"MOE_REVERSE_KU", &moe_tuning_t::reverse_ku, 0, 0, 4},
@@ -89,8 +88,8 @@ bool tune_valid(const moe_tuning_t& t) {
     set_error("moe_set_tuning: layout_u must be 0, 1, 2 or 4 and reverse_ku 0, 2 or 4");
     return false;
   }
-  if ((t.gate_bwd_lanes & (t.gate_bwd_lanes - 1)) || (t.gate_layout_tile & (t.gate_layout_tile - 1))) {
-    set_error("moe_set_tuning: gate_bwd_lanes and gate_layout_tile must be powers of two");
+  if (t.gate_bwd_lanes & (t.gate_bwd_lanes - 1)) {
+    set_error("moe_set_tuning: gate_bwd_lanes must be 0 or a power of two");
     return false;
   }
   return true;
@@ -515,6 +514,12 @@ moe_status_t moe_expert_scale(const void* in, void* out, int32_t nsrc, int32_t E
   }
   return expert_scale_launch(in, out, nsrc, E_local, e_base, cap, d, dtype, ds,
                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+moe_status_t moe_set_trace(void* buf, size_t bytes) {
+  g_trace.buf = bytes ? buf : nullptr;
+  g_trace.bytes = buf ? bytes : 0;
+  return MOE_OK;
 }
 
 moe_status_t moe_get_tuning(moe_tuning_t* out) {

@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
 }
 
 // ------------------------------------------------------------ host side
+TraceBuf g_trace;  // moe_set_trace (profiling)
+
 static GateKernel pick_gate(const moe_gate_desc_t& d, const GatePlan& p) {
   if (d.kind == MOE_GATE_SAM) return pick_sam(p.L, p.K);
   if (d.kind == MOE_GATE_D2S) return pick_d2s(p.L);
@@ -212,26 +214,27 @@ int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
   return two_kernels(gate_plan_default(d, ngroups)) ? 2 : 3;
 }
 
-// The fused gate + layout plan: tiles of T tokens (tuning gate_layout_tile,
-// default 32: enough tiles that every CTA of the persistent grid gets work
-// while the gate's latency hides behind other CTAs' scatter), doubled while
-// there would be more than 8192 tiles; its control block and status words
-// follow the gate's own workspace.
+// The fused gate + layout kernel uses the separate gate's tiles (its phase G
+// is the gate's select pass); its control block, status words [n_tiles][E]
+// and tile-ready words [n_tiles] follow the gate's own workspace.
 struct FusedPlan {
   GatePlan p;
-  size_t ctrl_off, st_off, bytes;
+  size_t ctrl_off, st_off, rdy_off, bytes;
 };
 
 static FusedPlan fused_plan(const moe_gate_desc_t& d) {
-  int T = tuning().gate_layout_tile;
-  while ((d.S + T - 1) / T > 8192 && T < 256) T *= 2;
   FusedPlan f;
-  f.p = gate_plan(d, 1 << 30, 1, T);
+  f.p = gate_plan_default(d);
   const size_t base = std::max({gate_plan_default(d).bytes, gate_plan(d, 1 << 20, 1, 32).bytes});
   f.ctrl_off = (base + 255) & ~(size_t)255;
   f.st_off = f.ctrl_off + 256;
-  f.bytes = f.st_off + sizeof(unsigned long long) * (size_t)f.p.n_tiles * d.E;
-  f.bytes = (f.bytes + 255) & ~(size_t)255;
+  f.rdy_off = f.st_off + sizeof(unsigned long long) * (size_t)f.p.n_tiles * d.E;
+  f.bytes = f.rdy_off + sizeof(unsigned) * (size_t)f.p.n_tiles;
+  // the status words of the largest tile count any tuning may pick
+  const GatePlan small = gate_plan(d, 1 << 20, 1, 32);
+  const size_t most = f.st_off + (sizeof(unsigned long long) * d.E + sizeof(unsigned)) *
+                                     (size_t)small.n_tiles;
+  f.bytes = (std::max(f.bytes, most) + 255) & ~(size_t)255;
   return f;
 }
 
@@ -366,6 +369,9 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   char* w = static_cast<char*>(ws);
   f.fc = reinterpret_cast<FusedCtrl*>(w + fp.ctrl_off);
   f.st = reinterpret_cast<unsigned long long*>(w + fp.st_off);
+  f.tile_ready = reinterpret_cast<unsigned*>(w + fp.rdy_off);
+  f.trace = static_cast<unsigned long long*>(g_trace.buf);
+  f.trace_n = (long long)(g_trace.bytes / sizeof(unsigned long long));
   const int U = row_bytes <= 2048 ? 2 : 4;  // as k_layout: 2 KiB segments for rows <= 2 KiB
   FusedKernel kern = d.kind == MOE_GATE_HASH    ? pick_fused_hash(U)
                      : d.kind == MOE_GATE_KTOP1 ? pick_fused_ktop1(p.L, p.K, U)

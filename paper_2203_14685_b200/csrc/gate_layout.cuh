@@ -4,49 +4,68 @@
 // latency-bound gate hides behind the bandwidth-bound row scatter.
 //
 // Why it can be one pass.  Under TOKEN priority (R5, the default) the slot of
-// item (t, j) is the number of earlier tokens' items for the same expert plus
-// nothing else (a token names an expert at most once), i.e. an exclusive
-// prefix sum over tokens.  The kernel walks tiles of T tokens in order of a
-// device-side tile counter (so a tile only ever waits on tiles that running
-// CTAs already hold -- no co-residency assumption) and, per tile:
-//   1. bulk-prefetches the tile's x rows into L2 (they do not depend on the
-//      routing), then selects + weighs its tokens (gate_tile, the gate's own
-//      code) and ranks its items per expert inside the tile;
-//   2. publishes its per-expert aggregate, then resolves the exclusive
-//      prefix by a decoupled look-back over earlier tiles (a warp reads 32
-//      predecessors' status words at once: aggregate "A" or inclusive
-//      prefix "P", epoch-tagged so the workspace never needs clearing) and
-//      publishes its inclusive prefix;
-//   3. finishes its slots (>= cap: dropped, weight 0; slot_src), and
-//   4. scatters its x rows (now in L2) to their <= k slots -- in peer mode
-//      straight into the owner rank's receive buffer over NVLink, sending a
-//      token's row once per remote owner (dedupe), as k_layout does.
-// The CTA that finishes the last tile writes load[] and raises a ready
-// word; every CTA then zero-fills its share of the padding rows [min(load,
-// cap), cap) and of slot_src's empty entries.  The last CTA to finish resets
-// the tile counter and advances the epoch (CUDA-graph replay safe).
-// Outputs are bit-identical to moe_gate followed by moe_layout (tested).
+// item (t, j) is the number of earlier tokens' items for the same expert (a
+// token names an expert at most once): an exclusive prefix sum over tokens.
+// Every CTA of the persistent grid runs two phases, each driven by its own
+// device-side counter, so a CTA only ever waits on work that running CTAs
+// already hold (no co-residency assumption):
+//   G. gate tiles (the separate gate's tiles, in order): select + weigh the
+//      tile's tokens and rank its items per expert (gate_tile, the gate's own
+//      code); publish the per-expert aggregate, resolve the exclusive prefix
+//      by a decoupled look-back over earlier tiles (a warp reads 32
+//      predecessors' status words at once: aggregate "A" or inclusive prefix
+//      "P", epoch-tagged so the workspace never needs clearing), publish the
+//      inclusive prefix, write the final slots (>= cap: dropped, weight 0;
+//      slot_src) and raise the tile's ready word;
+//   S. scatter chunks of 32 tokens, in token order: wait for the chunk's
+//      tile to be ready, then a warp per token reads its x row once and
+//      stores it to its <= k slots -- in peer mode straight into the owner
+//      rank's receive buffer over NVLink, a token's row once per remote owner
+//      (dedupe), exactly as k_layout does.
+// Most CTAs hold no gate tile and start scattering as soon as tile 0 is
+// ready, so the gate's latency overlaps the row traffic.  The CTA of the last
+// tile writes load[] and raises the totals word; every CTA then zero-fills
+// its share of the padding rows [min(load, cap), cap) and of slot_src's empty
+// entries.  The last CTA out resets the counters and advances the epoch
+// (CUDA-graph replay safe).  Outputs are bit-identical to moe_gate followed
+// by moe_layout (tested).
 #pragma once
 #include "gate_impl.cuh"
 #include "rows.cuh"
 
 namespace moe {
 
-struct FusedCtrl {        // at FusedLayout::ctrl_off of the gate workspace
-  unsigned tile_next;     // tile counter (reset by the last CTA)
+struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
+  unsigned tile_next;     // phase G counter (reset by the last CTA)
+  unsigned chunk_next;    // phase S counter (reset by the last CTA)
   unsigned done;          // CTAs finished (reset by the last CTA)
-  unsigned epoch;         // launch number, tags the status words
+  unsigned epoch;         // launch number, tags the status and ready words
   unsigned ready;         // = epoch + 1 once load[] of this launch is final
-  unsigned bad;           // unused (invalid hash ids go to GateCtrl::bad)
   unsigned pad[11];
 };
 
+constexpr int kScatterChunk = 32;  // tokens per phase-S work unit (divides every tile)
+
 struct FusedArgs {
-  GateArgs g;              // the gate (tile_tokens, n_tiles of the fused plan; ncols = E)
+  GateArgs g;              // the gate (its tiles; ncols = E)
   RowArgs r;               // the rows: src = x, destinations, peer mode, dedupe
   FusedCtrl* fc;
   unsigned long long* st;  // [n_tiles][E] status: epoch:30 | flag:2 | count:32
+  unsigned* tile_ready;    // [n_tiles] = epoch + 1 once the tile's slots are final
+  // profiling (moe_set_trace): %globaltimer stamps, NULL = off.  Per tile
+  // [claim, aggregate published, prefix published, ready]; per chunk
+  // [claim, tile ready seen]; per CTA [start, end]
+  unsigned long long* trace;
+  long long trace_n;
 };
+
+__device__ __forceinline__ void trace_at(const FusedArgs& f, long long i) {
+  if (f.trace && i < f.trace_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    f.trace[i] = t;
+  }
+}
 
 constexpr unsigned kFlagA = 1, kFlagP = 2;
 
@@ -106,52 +125,49 @@ __device__ __forceinline__ unsigned lookback(const unsigned long long* st, int t
 }
 
 template <int KIND, int L, int K, int U>
-__global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
+__global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   constexpr int VB = 32, SEG = 32 * U * VB;
   extern __shared__ __align__(16) int smem[];
   __shared__ unsigned s_bad;
   __shared__ __align__(8) unsigned long long s_mbar;
-  __shared__ int s_tile;
+  __shared__ int s_work;
   __shared__ unsigned s_epoch;
-  __shared__ int s_agg[256], s_pre[256];
+  __shared__ int s_pre[257], s_agg[256];  // s_pre doubles as the padding prefix [E + 1]
   const GateArgs& a = f.g;
   const RowArgs& ra = f.r;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int items = a.tile_tokens * a.k;
   int* s_exp = smem + a.lg_words;   // gate_tile's arrays (z_words = 0 here)
-  int* s_rank = s_exp + items;
+  const int* s_rank = s_exp + items;
   const int* s_hist = s_rank + items;
   const int per = (items + kGateWarps - 1) / kGateWarps;
 
   pdl_wait();     // the logits' producer / the previous step are complete
   pdl_trigger();
+  const int n_chunks = (a.S + kScatterChunk - 1) / kScatterChunk;
+  const long long tr_chunk = 4LL * a.n_tiles, tr_cta = tr_chunk + 2LL * n_chunks;
   if (tid == 0) {
+    trace_at(f, tr_cta + 2LL * blockIdx.x);
     if (KIND != KIND_HASH) gate_mbar_init(s_mbar);
     s_epoch = *reinterpret_cast<volatile unsigned*>(&f.fc->epoch);
   }
   __syncthreads();
   const unsigned epoch = s_epoch;
   unsigned parity = 0;
+
+  // ---------------- phase G: gate tiles in order
   for (;;) {
-    if (tid == 0) s_tile = (int)atomicAdd(&f.fc->tile_next, 1u);
+    if (tid == 0) s_work = (int)atomicAdd(&f.fc->tile_next, 1u);
     __syncthreads();
-    const int tile = s_tile;
+    const int tile = s_work;
     if (tile >= a.n_tiles) break;
+    if (tid == 0) trace_at(f, 4LL * tile);
     const int t0 = tile * a.tile_tokens;
     const int nt = min(a.tile_tokens, a.S - t0);
-    if (tid == 0) {  // the tile's x rows (contiguous) stream into L2 meanwhile
-      const unsigned long long beg = (unsigned long long)t0 * ra.row_bytes;
-      const unsigned long long n = (unsigned long long)nt * ra.row_bytes;
-      for (unsigned long long o = 0; o < n; o += 65536)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + beg + o),
-                     "r"((unsigned)min(65536ull, n - o))
-                     : "memory");
-    }
-    // ---- 1. select + weights + in-tile ranks (s_exp, s_rank, s_hist, s_agg)
     gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, tile, parity, s_agg);
     parity ^= 1u;
     if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-    // ---- 2. publish the aggregate, look back, publish the inclusive prefix
+    // publish the aggregate, look back, publish the inclusive prefix
     unsigned long long* st = f.st + (size_t)tile * a.E;
     if (tile == 0) {
       for (int c = tid; c < a.E; c += kGateThreads) {
@@ -161,6 +177,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
     } else {
       for (int c = tid; c < a.E; c += kGateThreads)
         st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
+      if (tid == 0) trace_at(f, 4LL * tile + 1);
       for (int c = warp; c < a.E; c += kGateWarps) {
         const unsigned ex = lookback(f.st, tile, c, a.E, epoch, lane);
         if (lane == 0) {
@@ -170,14 +187,8 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
       }
     }
     __syncthreads();
-    if (tile == a.n_tiles - 1) {  // the totals: requests per expert (TOKEN: the column)
-      for (int c = tid; c < a.E; c += kGateThreads) a.load[c] = s_pre[c] + s_agg[c];
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&f.fc->ready),
-                                 "r"(epoch + 1u) : "memory");
-    }
-    // ---- 3. final slots (in s_rank), dropped items, slot_src
+    if (tid == 0) trace_at(f, 4LL * tile + 2);
+    // final slots, dropped items, slot_src
     for (int i = tid; i < nt * a.k; i += kGateThreads) {
       const int e = s_exp[i];
       const size_t gi = (size_t)t0 * a.k + i;
@@ -192,36 +203,71 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
         }
       }
       a.slot_idx[gi] = s;
-      s_rank[i] = s;
+    }
+    const bool last = tile == a.n_tiles - 1;
+    if (last)  // the totals: requests per expert (TOKEN: the column)
+      for (int c = tid; c < a.E; c += kGateThreads) a.load[c] = s_pre[c] + s_agg[c];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      trace_at(f, 4LL * tile + 3);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.tile_ready + tile),
+                   "r"(epoch + 1u) : "memory");
+      if (last)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&f.fc->ready), "r"(epoch + 1u)
+                     : "memory");
+    }
+  }
+
+  // ---------------- phase S: scatter chunks of tokens in order
+  for (;;) {
+    __syncthreads();  // s_work is rewritten
+    if (tid == 0) {
+      const int c = (int)atomicAdd(&f.fc->chunk_next, 1u);
+      s_work = c;
+      if (c < n_chunks) {
+        trace_at(f, tr_chunk + 2LL * c);
+        const unsigned* rdy = f.tile_ready + (c * kScatterChunk) / a.tile_tokens;
+        while (ld_acquire_gpu_u32(rdy) != epoch + 1u) __nanosleep(32);
+        trace_at(f, tr_chunk + 2LL * c + 1);
+      }
     }
     __syncthreads();
-    // ---- 4. scatter the tile's rows, a warp per token
-    for (int tt = warp; tt < nt; tt += kGateWarps) {
-      const int t = t0 + tt;
+    const int c = s_work;
+    if (c >= n_chunks) break;
+    const int t_end = min(a.S, (c + 1) * kScatterChunk);
+    for (int t = c * kScatterChunk + warp; t < t_end; t += kGateWarps) {
+      // lane j < k: slot j of token t (written by another CTA: L2 loads)
+      int my_e = -1, my_s = -1;
+      if (lane < a.k) {
+        my_s = __ldcg(a.slot_idx + (size_t)t * a.k + lane);
+        my_e = __ldcg(a.expert_idx + (size_t)t * a.k + lane);
+      }
       const char* srow = ra.src + (size_t)t * ra.row_bytes;
       for (int seg = 0; seg < ra.row_bytes; seg += SEG) {
         V8 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int off = seg + (lane + 32 * u) * VB;
-          if (off < ra.row_bytes) r[u] = ld_v8(srow + off);
+          if (off < ra.row_bytes) r[u] = ld_stream_v8(srow + off);
         }
         for (int j = 0; j < a.k; ++j) {
-          const int s = s_rank[tt * a.k + j];
+          const int s = __shfl_sync(0xffffffffu, my_s, j);
           if (s < 0) continue;
-          const int e = s_exp[tt * a.k + j];
+          const int e = __shfl_sync(0xffffffffu, my_e, j);
           const int q = e / ra.E_local;
           if (ra.dedupe && q != ra.rank && j > 0) {
             // a row already bound for this remote owner: record "= row of j'"
-            int jj = 0;
+            int jj = 0, e2 = -1, s2 = -1;
             for (; jj < j; ++jj) {
-              const int s2 = s_rank[tt * a.k + jj];
-              if (s2 >= 0 && s_exp[tt * a.k + jj] / ra.E_local == q) break;
+              s2 = __shfl_sync(0xffffffffu, my_s, jj);
+              e2 = __shfl_sync(0xffffffffu, my_e, jj);
+              if (s2 >= 0 && e2 / ra.E_local == q) break;
             }
             if (jj < j) {
               if (seg == 0 && lane == 0)
                 reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
-                    (int)row_index(ra, q, s_exp[tt * a.k + jj], s_rank[tt * a.k + jj]) + 1;
+                    (int)row_index(ra, q, e2, s2) + 1;
               continue;
             }
           }
@@ -234,15 +280,14 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
         }
       }
     }
-    __syncthreads();  // s_tile, s_exp and s_rank are reused by the next tile
   }
 
-  // ---- padding rows [min(load, cap), cap) and empty slot_src entries,
-  // once the CTA of the last tile published load[]
+  // ---------------- padding rows [min(load, cap), cap) and empty slot_src
+  // entries, once the CTA of the last tile published load[]
   if (tid == 0)
     while (ld_acquire_gpu_u32(&f.fc->ready) != epoch + 1u) __nanosleep(64);
   __syncthreads();
-  __shared__ int s_beg[257];
+  int* s_beg = s_pre;  // [E + 1] <= 257
   if (tid < 32) {
     int carry = 0;
     for (int base = 0; base < a.E; base += 32) {
@@ -281,12 +326,14 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_layout(FusedArgs f) {
       for (int s = min(__ldcg(a.load + e), a.cap) + lane; s < a.cap; s += 32)
         a.slot_src[(size_t)e * a.cap + s] = -1;
   if (ra.sys_fence) __threadfence_system();
-  // ---- the last CTA out resets the counters for the next launch
+  // ---------------- the last CTA out resets the counters for the next launch
   __syncthreads();
   if (tid == 0) {
+    trace_at(f, tr_cta + 2LL * blockIdx.x + 1);
     __threadfence();
     if (atomicAdd(&f.fc->done, 1u) == gridDim.x - 1) {
       f.fc->tile_next = 0;
+      f.fc->chunk_next = 0;
       f.fc->done = 0;
       __threadfence();
       f.fc->epoch = epoch + 1u;

@@ -12,6 +12,11 @@ namespace moe {
 // launched) when the shape has no fused kernel: SLOT priority, SAM, D2S,
 // k > 8, rows not a multiple of 32 bytes; callers then launch gate + layout.
 bool gate_layout_supported(const moe_gate_desc_t& d, int row_bytes);
+struct TraceBuf {  // moe_set_trace: a device buffer of %globaltimer stamps
+  void* buf = nullptr;
+  size_t bytes = 0;
+};
+extern TraceBuf g_trace;
 moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
                                 const moe_routing_t& out, void* ws, const void* x,
                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,

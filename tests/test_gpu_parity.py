@@ -314,7 +314,7 @@ def test_gate_layout_fused_equals_gate_then_layout(orc, case):
         assert g.check() == ro.bad
 
 
-@pytest.mark.parametrize("tile", [32, 64, 256])
+@pytest.mark.parametrize("tile", [32, 64, 0, 256])   # gate_max_tile (0: the default)
 @pytest.mark.parametrize("case", [
     dict(kind="topk", S=32768, E=8, k=2, d=1024),           # C2 shape
     dict(kind="topk", S=8192, E=64, k=1, d=2048),           # C3 rows (4 KiB, U = 4)
@@ -329,7 +329,7 @@ def test_gate_layout_fused_replays(orc, case, tile):
     with new inputs each match the oracle, for every tile size."""
     kind, S, E, k, d = case["kind"], case["S"], case["E"], case["k"], case["d"]
     cap = orc.capacity(S, E, k, case.get("C", 1.0))
-    with moe.tuned(gate_layout_tile=tile):
+    with moe.tuned(gate_max_tile=tile):
         g = moe.Gate(S, E, k, cap, kind)
         xd = torch.empty((S, d), dtype=torch.bfloat16, device="cuda")
         lgd = torch.empty((S, E), dtype=torch.float32, device="cuda")

@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default="")
     ap.add_argument("--p2p", action="store_true", help="also time the one-sided NVLink AllToAll")
+    ap.add_argument("--algos", default="flat,hier",
+                    help="comma list of flat, flat_reg (NCCL-registered ncclMemAlloc buffers), "
+                         "a2a (ncclAlltoAll), a2a_reg, hier (leader), hier2d (two-level), p2p")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -55,14 +58,25 @@ def main():
         chunk_words = B // 4 // P
         send = torch.cat([pattern(r, q, chunk_words, dev) for q in range(P)])
         recv = torch.empty_like(send)
-        recv_sym = comm.symm_empty(send.shape, send.dtype) if a.p2p else None
+        recv_sym = comm.symm_empty(send.shape, send.dtype) if (a.p2p or "p2p" in a.algos) else None
         ws = torch.empty(comm.workspace_bytes("hier", G, B // P) if r % G == 0 else 0,
                          dtype=torch.uint8, device=dev)
         res = {"B_mib": mib, "P": P, "G": G, "per_peer_bytes": B // P}
-        for algo in ("flat", "hier") + (("p2p",) if a.p2p else ()):
-            rv = recv_sym if algo == "p2p" else recv
+        algos = [x for x in a.algos.split(",") if x] + (["p2p"] if a.p2p and "p2p" not in a.algos else [])
+        reg = None
+        if any(x.endswith("_reg") for x in algos):
+            reg = (comm.mem_empty(send.shape, send.dtype), comm.mem_empty(send.shape, send.dtype))
+            reg[0].copy_(send)
+        if "hier2d" in algos:
+            ws2 = torch.empty(comm.workspace_bytes("hier2d", G, B // P), dtype=torch.uint8, device=dev)
+        for name in algos:
+            algo = {"flat_reg": "flat", "a2a": "flat", "a2a_reg": "flat"}.get(name, name)
+            moe.set_tuning(nccl_alltoall=1 if name.startswith("a2a") else 0)
+            sd = reg[0] if name.endswith("_reg") else send
+            rv = recv_sym if algo == "p2p" else (reg[1] if name.endswith("_reg") else recv)
+            w_ = ws2 if algo == "hier2d" else ws
             rv.fill_(-1)
-            comm.alltoall(send, rv, algo, G, ws)        # eager warm-up + check
+            comm.alltoall(sd, rv, algo, G, w_)        # eager warm-up + check
             torch.cuda.synchronize()
             want = torch.cat([pattern(q, r, chunk_words, dev) for q in range(P)])
             ok = torch.tensor([1 if torch.equal(rv, want) else 0], device=dev)
@@ -71,7 +85,7 @@ def main():
             with torch.cuda.stream(s):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
-                    comm.alltoall(send, rv, algo, G, ws)
+                    comm.alltoall(sd, rv, algo, G, w_)
             torch.cuda.current_stream().wait_stream(s)
             ts = []
             for _ in range(a.reps):
@@ -91,19 +105,24 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             ms = float(t.item())
-            res[algo] = {"ms": ms, "busbw_gbs": B * (P - 1) / P / (ms / 1e3) / 1e9,
+            res[name] = {"ms": ms, "busbw_gbs": B * (P - 1) / P / (ms / 1e3) / 1e9,
                          "correct": bool(ok.item())}
             del g
-        res["t_flat_over_t_hier"] = res["flat"]["ms"] / res["hier"]["ms"]
-        if a.p2p:
-            res["t_flat_over_t_p2p"] = res["flat"]["ms"] / res["p2p"]["ms"]
-            dist.barrier()
-            torch.cuda.synchronize()
+        moe.set_tuning(nccl_alltoall=0)
+        for name in algos:
+            if name != "flat" and "flat" in res:
+                res["t_flat_over_t_" + name] = res["flat"]["ms"] / res[name]["ms"]
+        dist.barrier()
+        torch.cuda.synchronize()
+        if recv_sym is not None:
             comm.symm_free(recv_sym)
+        if reg is not None:
+            comm.mem_free(reg[0])
+            comm.mem_free(reg[1])
         rows.append(res)
         if r == 0:
             print(json.dumps(res), flush=True)
-        del send, recv, ws, recv_sym
+        del send, recv, ws, recv_sym, reg
         torch.cuda.empty_cache()
         mib *= 2
     if r == 0 and a.out:

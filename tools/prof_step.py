@@ -23,10 +23,10 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--tile", type=int, default=0, help="tuning gate_layout_tile")
+    ap.add_argument("--tile", type=int, default=0, help="tuning gate_max_tile")
     a = ap.parse_args()
     if a.tile:
-        moe.set_tuning(gate_layout_tile=a.tile)
+        moe.set_tuning(gate_max_tile=a.tile)
     w = synthgen.WORKLOADS[a.workload]
     S = w.S
     cap = moe.capacity(S, w.E, w.k, w.C)
