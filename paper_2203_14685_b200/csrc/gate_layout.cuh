@@ -59,7 +59,9 @@ struct FusedArgs {
   long long trace_n;
 };
 
+// trace layout: [0..3] = n_tiles, n_chunks, gridDim.x, 0; stamps from 4 on
 __device__ __forceinline__ void trace_at(const FusedArgs& f, long long i) {
+  i += 4;
   if (f.trace && i < f.trace_n) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -147,6 +149,11 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   const int n_chunks = (a.S + kScatterChunk - 1) / kScatterChunk;
   const long long tr_chunk = 4LL * a.n_tiles, tr_cta = tr_chunk + 2LL * n_chunks;
   if (tid == 0) {
+    if (f.trace && blockIdx.x == 0 && f.trace_n >= 4) {
+      f.trace[0] = (unsigned long long)a.n_tiles;
+      f.trace[1] = (unsigned long long)n_chunks;
+      f.trace[2] = gridDim.x;
+    }
     trace_at(f, tr_cta + 2LL * blockIdx.x);
     if (KIND != KIND_HASH) gate_mbar_init(s_mbar);
     s_epoch = *reinterpret_cast<volatile unsigned*>(&f.fc->epoch);

@@ -61,23 +61,12 @@ def main():
     pipe.step(d[0], d[1], d[2], d[3])
     torch.cuda.synchronize()
     lib().moe_set_trace(None, 0)
-    t = buf.cpu().numpy().astype(np.float64)
-    n_tiles = -(-S // 128) if w.kind != "hash" else -(-S // 256)
-    # the plan's tile count: recover it from the first CTA stamp position
-    nz = np.nonzero(t)[0]
-    n_chunks = -(-S // 32)
-    # try the candidate tile sizes until the layout is consistent
-    for tt in (32, 64, 128, 256):
-        nt = -(-S // tt)
-        base = 4 * nt + 2 * n_chunks
-        if t[base] > 0 and (4 * nt - 1 in nz):
-            n_tiles = nt
-            break
+    raw = buf.cpu().numpy()
+    n_tiles, n_chunks, n_ctas = int(raw[0]), int(raw[1]), int(raw[2])
+    t = raw[4:].astype(np.float64)
     tiles = t[:4 * n_tiles].reshape(n_tiles, 4)
     chunks = t[4 * n_tiles:4 * n_tiles + 2 * n_chunks].reshape(n_chunks, 2)
-    ctas = t[4 * n_tiles + 2 * n_chunks:]
-    ctas = ctas[:2 * (np.nonzero(ctas)[0].max() // 2 + 1)].reshape(-1, 2)
-    ctas = ctas[ctas[:, 0] > 0]
+    ctas = t[4 * n_tiles + 2 * n_chunks:4 * n_tiles + 2 * n_chunks + 2 * n_ctas].reshape(n_ctas, 2)
     t0 = ctas[:, 0].min()
     us = lambda v: (v - t0) / 1e3
     out = {
