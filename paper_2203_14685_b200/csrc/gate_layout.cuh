@@ -126,6 +126,59 @@ __device__ __forceinline__ unsigned lookback(const unsigned long long* st, int t
   }
 }
 
+// The same for CG consecutive columns c0 .. c0+CG-1 at once: each lane
+// reads the CG status words of one predecessor with a single vector load
+// (the tile's words are contiguous; E % CG == 0 keeps it aligned).
+template <int CG>
+__device__ __forceinline__ void lookback_cg(const unsigned long long* st, int tile, int c0, int E,
+                                            unsigned epoch, int lane, unsigned* excl) {
+  static_assert(CG == 4, "vector width");
+#pragma unroll
+  for (int j = 0; j < CG; ++j) excl[j] = 0;
+  unsigned open = (1u << CG) - 1;  // columns still looking back
+  for (int base = tile - 1; open; base -= 32) {
+    const int idx = base - lane;
+    for (;;) {
+      unsigned long long w[CG];
+      if (idx >= 0) {
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+                     : "l"(st + (size_t)idx * E + c0)
+                     : "memory");
+      }
+      bool wait = false;
+      unsigned s[CG];
+      int firstP[CG];
+#pragma unroll
+      for (int j = 0; j < CG; ++j) {
+        const unsigned f = idx >= 0 ? st_flag(w[j], epoch) : kFlagP;
+        const unsigned v = idx >= 0 ? (unsigned)w[j] : 0u;
+        const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
+        const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
+        firstP[j] = pmask ? __ffs(pmask) - 1 : 32;
+        const unsigned need = firstP[j] < 31 ? ((2u << firstP[j]) - 1u) : 0xffffffffu;
+        if ((open >> j & 1u) && (zmask & need)) wait = true;
+        s[j] = lane <= firstP[j] ? v : 0u;
+      }
+      if (wait) {
+        __nanosleep(32);
+        continue;
+      }
+#pragma unroll
+      for (int j = 0; j < CG; ++j) {
+        unsigned t = s[j];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (open >> j & 1u) {
+          excl[j] += t;
+          if (firstP[j] < 32) open &= ~(1u << j);
+        }
+      }
+      break;
+    }
+  }
+}
+
 template <int KIND, int L, int K, int U>
 __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   constexpr int VB = 32, SEG = 32 * U * VB;
@@ -162,8 +215,9 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   const unsigned epoch = s_epoch;
   unsigned parity = 0;
 
-  // ---------------- phase G: gate tiles in order
-  for (;;) {
+  // ---------------- phase G: gate tiles in order (CTAs past the tile count go
+  // straight to phase S: fewer claims contend on the counter)
+  for (; blockIdx.x < a.n_tiles;) {
     if (tid == 0) s_work = (int)atomicAdd(&f.fc->tile_next, 1u);
     __syncthreads();
     const int tile = s_work;
@@ -185,11 +239,23 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
       for (int c = tid; c < a.E; c += kGateThreads)
         st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
       if (tid == 0) trace_at(f, 4LL * tile + 1);
-      for (int c = warp; c < a.E; c += kGateWarps) {
-        const unsigned ex = lookback(f.st, tile, c, a.E, epoch, lane);
-        if (lane == 0) {
-          s_pre[c] = (int)ex;
-          st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, ex + (unsigned)s_agg[c]));
+      if (a.E % 4 == 0) {  // four columns per vector load
+        for (int c0 = warp * 4; c0 < a.E; c0 += kGateWarps * 4) {
+          unsigned ex[4];
+          lookback_cg<4>(f.st, tile, c0, a.E, epoch, lane, ex);
+          if (lane < 4) {
+            const unsigned e = lane == 0 ? ex[0] : lane == 1 ? ex[1] : lane == 2 ? ex[2] : ex[3];
+            s_pre[c0 + lane] = (int)e;
+            st_relaxed_gpu(st + c0 + lane, st_pack(epoch, kFlagP, e + (unsigned)s_agg[c0 + lane]));
+          }
+        }
+      } else {
+        for (int c = warp; c < a.E; c += kGateWarps) {
+          const unsigned ex = lookback(f.st, tile, c, a.E, epoch, lane);
+          if (lane == 0) {
+            s_pre[c] = (int)ex;
+            st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, ex + (unsigned)s_agg[c]));
+          }
         }
       }
     }
@@ -214,9 +280,9 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     const bool last = tile == a.n_tiles - 1;
     if (last)  // the totals: requests per expert (TOKEN: the column)
       for (int c = tid; c < a.E; c += kGateThreads) a.load[c] = s_pre[c] + s_agg[c];
-    __threadfence();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {  // one fence after the barrier covers the CTA's stores
+      __threadfence();
       trace_at(f, 4LL * tile + 3);
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.tile_ready + tile),
                    "r"(epoch + 1u) : "memory");
@@ -234,6 +300,15 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
       s_work = c;
       if (c < n_chunks) {
         trace_at(f, tr_chunk + 2LL * c);
+        // the chunk's x rows (contiguous) do not depend on the routing: they
+        // stream into L2 while the tile may still be resolving
+        const unsigned long long beg = (unsigned long long)c * kScatterChunk * ra.row_bytes;
+        const unsigned long long n =
+            (unsigned long long)(min(a.S, (c + 1) * kScatterChunk) - c * kScatterChunk) * ra.row_bytes;
+        for (unsigned long long o = 0; o < n; o += 65536)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + beg + o),
+                       "r"((unsigned)min(65536ull, n - o))
+                       : "memory");
         const unsigned* rdy = f.tile_ready + (c * kScatterChunk) / a.tile_tokens;
         while (ld_acquire_gpu_u32(rdy) != epoch + 1u) __nanosleep(32);
         trace_at(f, tr_chunk + 2LL * c + 1);
