@@ -11,12 +11,14 @@
 // already hold (no co-residency assumption):
 //   G. gate tiles (the separate gate's tiles, in order): select + weigh the
 //      tile's tokens and rank its items per expert (gate_tile, the gate's own
-//      code); publish the per-expert aggregate, resolve the exclusive prefix
-//      by a decoupled look-back over earlier tiles (a warp reads 32
-//      predecessors' status words at once: aggregate "A" or inclusive prefix
-//      "P", epoch-tagged so the workspace never needs clearing), publish the
-//      inclusive prefix, write the final slots (>= cap: dropped, weight 0;
-//      slot_src) and raise the tile's ready word;
+//      code); publish the per-expert aggregate (epoch-tagged status words, so
+//      the workspace never needs clearing); the tile that completes a group
+//      of 32 tiles publishes the group's per-expert total; the exclusive
+//      prefix of a tile is then the earlier groups' totals plus its own
+//      group's earlier aggregates -- two warp-wide reads, no chain of
+//      prefixes (a look-back chain grows with the tile count and, measured,
+//      dominated the kernel); write the final slots (>= cap: dropped, weight
+//      0; slot_src) and raise the tile's ready word;
 //   S. scatter chunks of 32 tokens, in token order: wait for the chunk's
 //      tile to be ready, then a warp per token reads its x row once and
 //      stores it to its <= k slots -- in peer mode straight into the owner
@@ -44,13 +46,17 @@ struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
   unsigned pad[11];
 };
 
+constexpr int kGroupTiles = 32;  // tiles per group of the two-level prefix
+
 constexpr int kScatterChunk = 32;  // tokens per phase-S work unit (divides every tile)
 
 struct FusedArgs {
   GateArgs g;              // the gate (its tiles; ncols = E)
   RowArgs r;               // the rows: src = x, destinations, peer mode, dedupe
   FusedCtrl* fc;
-  unsigned long long* st;  // [n_tiles][E] status: epoch:30 | flag:2 | count:32
+  unsigned long long* st;  // [n_tiles][E] tile aggregates: epoch:30 | flag:2 | count:32
+  unsigned long long* gt;  // [n_groups][E] group totals, same packing
+  unsigned* gcnt;          // [n_groups] aggregates published (reset by the last CTA)
   unsigned* tile_ready;    // [n_tiles] = epoch + 1 once the tile's slots are final
   // profiling (moe_set_trace): %globaltimer stamps, NULL = off.  Per tile
   // [claim, aggregate published, prefix published, ready]; per chunk
@@ -91,91 +97,75 @@ __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   return v;
 }
 
-// Exclusive prefix over tiles < tile of column c (one warp): look back 32
-// tiles per round; wait until every tile up to the nearest inclusive prefix
-// has published at least its aggregate.
-__device__ __forceinline__ unsigned lookback(const unsigned long long* st, int tile, int c, int E,
-                                             unsigned epoch, int lane) {
-  unsigned excl = 0;
-  for (int base = tile - 1;; base -= 32) {
-    const int idx = base - lane;
-    unsigned f, v;
-    for (;;) {
-      if (idx >= 0) {
-        const unsigned long long w = ld_relaxed_gpu(st + (size_t)idx * E + c);
-        f = st_flag(w, epoch);
-        v = (unsigned)w;
-      } else {
-        f = kFlagP;  // before tile 0: prefix 0
-        v = 0;
-      }
-      const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
-      const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
-      const int firstP = pmask ? __ffs(pmask) - 1 : 32;
-      const unsigned need = firstP < 31 ? ((2u << firstP) - 1u) : 0xffffffffu;
-      if (!(zmask & need)) {
-        unsigned s = lane <= firstP ? v : 0u;
+// Sum over lanes < n of the valid words w[idx(lane)] of one column (one
+// warp; n <= 32), spinning until every one of them carries this epoch's flag.
+__device__ __forceinline__ unsigned warp_sum_words(const unsigned long long* base, size_t stride,
+                                                   int n, unsigned epoch, int lane) {
+  unsigned v = 0;
+  if (lane < n) {
+    const unsigned long long* p = base + (size_t)lane * stride;
+    unsigned long long w = ld_relaxed_gpu(p);
+    while (!st_flag(w, epoch)) {
+      __nanosleep(32);
+      w = ld_relaxed_gpu(p);
+    }
+    v = (unsigned)w;
+  }
 #pragma unroll
-        for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-        excl += s;
-        if (firstP < 32) return excl;
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+
+// The same for four consecutive columns with one vector load per lane
+// (E % 4 == 0 keeps the rows 32-byte aligned).
+__device__ __forceinline__ void warp_sum_words4(const unsigned long long* base, size_t stride,
+                                                int n, unsigned epoch, int lane, unsigned* out) {
+  unsigned v[4] = {0, 0, 0, 0};
+  if (lane < n) {
+    const unsigned long long* p = base + (size_t)lane * stride;
+    unsigned long long w[4];
+    for (;;) {
+      asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+                   : "l"(p)
+                   : "memory");
+      if (st_flag(w[0], epoch) && st_flag(w[1], epoch) && st_flag(w[2], epoch) &&
+          st_flag(w[3], epoch))
         break;
-      }
       __nanosleep(32);
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = (unsigned)w[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], m);
+    out[j] = v[j];
   }
 }
 
-// The same for CG consecutive columns c0 .. c0+CG-1 at once: each lane
-// reads the CG status words of one predecessor with a single vector load
-// (the tile's words are contiguous; E % CG == 0 keeps it aligned).
-template <int CG>
-__device__ __forceinline__ void lookback_cg(const unsigned long long* st, int tile, int c0, int E,
-                                            unsigned epoch, int lane, unsigned* excl) {
-  static_assert(CG == 4, "vector width");
+// Exclusive prefix of column group [c0, c0 + CW) at `tile` (one warp): the
+// totals of the groups before the tile's group plus the aggregates of the
+// tiles before it in its group.  Every word read was (or will be) published
+// by a CTA that holds its tile and does not wait on anyone.
+template <int CW>
+__device__ __forceinline__ void tile_prefix(const unsigned long long* st,
+                                            const unsigned long long* gt, int tile, int c0, int E,
+                                            unsigned epoch, int lane, unsigned* ex) {
+  const int g = tile / kGroupTiles, first = g * kGroupTiles;
+  unsigned t[CW];
+  if constexpr (CW == 4) {
+    warp_sum_words4(st + (size_t)first * E + c0, E, tile - first, epoch, lane, ex);
+    for (int base = 0; base < g; base += 32) {
+      warp_sum_words4(gt + (size_t)base * E + c0, E, min(32, g - base), epoch, lane, t);
 #pragma unroll
-  for (int j = 0; j < CG; ++j) excl[j] = 0;
-  unsigned open = (1u << CG) - 1;  // columns still looking back
-  for (int base = tile - 1; open; base -= 32) {
-    const int idx = base - lane;
-    for (;;) {
-      unsigned long long w[CG];
-      if (idx >= 0) {
-        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
-                     : "l"(st + (size_t)idx * E + c0)
-                     : "memory");
-      }
-      bool wait = false;
-      unsigned s[CG];
-      int firstP[CG];
-#pragma unroll
-      for (int j = 0; j < CG; ++j) {
-        const unsigned f = idx >= 0 ? st_flag(w[j], epoch) : kFlagP;
-        const unsigned v = idx >= 0 ? (unsigned)w[j] : 0u;
-        const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
-        const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
-        firstP[j] = pmask ? __ffs(pmask) - 1 : 32;
-        const unsigned need = firstP[j] < 31 ? ((2u << firstP[j]) - 1u) : 0xffffffffu;
-        if ((open >> j & 1u) && (zmask & need)) wait = true;
-        s[j] = lane <= firstP[j] ? v : 0u;
-      }
-      if (wait) {
-        __nanosleep(32);
-        continue;
-      }
-#pragma unroll
-      for (int j = 0; j < CG; ++j) {
-        unsigned t = s[j];
-#pragma unroll
-        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-        if (open >> j & 1u) {
-          excl[j] += t;
-          if (firstP[j] < 32) open &= ~(1u << j);
-        }
-      }
-      break;
+      for (int j = 0; j < 4; ++j) ex[j] += t[j];
     }
+  } else {
+    ex[0] = warp_sum_words(st + (size_t)first * E + c0, E, tile - first, epoch, lane);
+    for (int base = 0; base < g; base += 32)
+      ex[0] += warp_sum_words(gt + (size_t)base * E + c0, E, min(32, g - base), epoch, lane);
   }
 }
 
@@ -228,35 +218,39 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, tile, parity, s_agg);
     parity ^= 1u;
     if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-    // publish the aggregate, look back, publish the inclusive prefix
+    // publish the aggregate; the tile completing its group publishes the
+    // group total; then the two-level exclusive prefix
     unsigned long long* st = f.st + (size_t)tile * a.E;
-    if (tile == 0) {
-      for (int c = tid; c < a.E; c += kGateThreads) {
-        s_pre[c] = 0;
-        st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, (unsigned)s_agg[c]));
+    for (int c = tid; c < a.E; c += kGateThreads)
+      st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
+    const int grp = tile / kGroupTiles, first = grp * kGroupTiles;
+    const int gsize = min(kGroupTiles, a.n_tiles - first);
+    __syncthreads();
+    if (tid == 0) {
+      trace_at(f, 4LL * tile + 1);
+      __threadfence();
+      s_work = (int)atomicAdd(f.gcnt + grp, 1u) == gsize - 1;  // the group is complete
+    }
+    __syncthreads();
+    if (s_work) {  // group total: every aggregate of the group is published
+      for (int c = warp; c < a.E; c += kGateWarps) {
+        const unsigned tot =
+            warp_sum_words(f.st + (size_t)first * a.E + c, a.E, gsize, epoch, lane);
+        if (lane == 0) st_relaxed_gpu(f.gt + (size_t)grp * a.E + c, st_pack(epoch, kFlagA, tot));
+      }
+    }
+    if (a.E % 4 == 0) {  // four columns per vector load
+      for (int c0 = warp * 4; c0 < a.E; c0 += kGateWarps * 4) {
+        unsigned ex[4];
+        tile_prefix<4>(f.st, f.gt, tile, c0, a.E, epoch, lane, ex);
+        if (lane < 4) s_pre[c0 + lane] = (int)(lane == 0 ? ex[0] : lane == 1 ? ex[1]
+                                                   : lane == 2 ? ex[2] : ex[3]);
       }
     } else {
-      for (int c = tid; c < a.E; c += kGateThreads)
-        st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
-      if (tid == 0) trace_at(f, 4LL * tile + 1);
-      if (a.E % 4 == 0) {  // four columns per vector load
-        for (int c0 = warp * 4; c0 < a.E; c0 += kGateWarps * 4) {
-          unsigned ex[4];
-          lookback_cg<4>(f.st, tile, c0, a.E, epoch, lane, ex);
-          if (lane < 4) {
-            const unsigned e = lane == 0 ? ex[0] : lane == 1 ? ex[1] : lane == 2 ? ex[2] : ex[3];
-            s_pre[c0 + lane] = (int)e;
-            st_relaxed_gpu(st + c0 + lane, st_pack(epoch, kFlagP, e + (unsigned)s_agg[c0 + lane]));
-          }
-        }
-      } else {
-        for (int c = warp; c < a.E; c += kGateWarps) {
-          const unsigned ex = lookback(f.st, tile, c, a.E, epoch, lane);
-          if (lane == 0) {
-            s_pre[c] = (int)ex;
-            st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, ex + (unsigned)s_agg[c]));
-          }
-        }
+      for (int c = warp; c < a.E; c += kGateWarps) {
+        unsigned ex[1];
+        tile_prefix<1>(f.st, f.gt, tile, c, a.E, epoch, lane, ex);
+        if (lane == 0) s_pre[c] = (int)ex[0];
       }
     }
     __syncthreads();
@@ -414,6 +408,7 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     trace_at(f, tr_cta + 2LL * blockIdx.x + 1);
     __threadfence();
     if (atomicAdd(&f.fc->done, 1u) == gridDim.x - 1) {
+      for (int g = 0; g * kGroupTiles < a.n_tiles; ++g) f.gcnt[g] = 0;
       f.fc->tile_next = 0;
       f.fc->chunk_next = 0;
       f.fc->done = 0;
