@@ -219,7 +219,7 @@ int gate_kernel_count(const moe_gate_desc_t& d, int ngroups) {
 // and tile-ready words [n_tiles] follow the gate's own workspace.
 struct FusedPlan {
   GatePlan p;
-  size_t ctrl_off, st_off, gt_off, gc_off, rdy_off, bytes;
+  size_t ctrl_off, st_off, rdy_off, bytes;
 };
 
 static FusedPlan fused_plan(const moe_gate_desc_t& d) {
@@ -227,13 +227,10 @@ static FusedPlan fused_plan(const moe_gate_desc_t& d) {
   f.p = gate_plan_default(d);
   // room for the largest tile count any tuning may pick
   const int most = std::max(f.p.n_tiles, gate_plan(d, 1 << 20, 1, 32).n_tiles);
-  const int groups = (most + kGroupTiles - 1) / kGroupTiles;
   const size_t base = std::max({gate_plan_default(d).bytes, gate_plan(d, 1 << 20, 1, 32).bytes});
   f.ctrl_off = (base + 255) & ~(size_t)255;
   f.st_off = f.ctrl_off + 256;
-  f.gt_off = f.st_off + sizeof(unsigned long long) * (size_t)most * d.E;
-  f.gc_off = f.gt_off + sizeof(unsigned long long) * (size_t)groups * d.E;
-  f.rdy_off = f.gc_off + sizeof(unsigned) * (size_t)groups;
+  f.rdy_off = f.st_off + sizeof(unsigned long long) * (size_t)most * d.E;
   f.bytes = (f.rdy_off + sizeof(unsigned) * (size_t)most + 255) & ~(size_t)255;
   return f;
 }
@@ -370,8 +367,7 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   f.fc = reinterpret_cast<FusedCtrl*>(w + fp.ctrl_off);
   f.st = reinterpret_cast<unsigned long long*>(w + fp.st_off);
   f.tile_ready = reinterpret_cast<unsigned*>(w + fp.rdy_off);
-  f.gt = reinterpret_cast<unsigned long long*>(w + fp.gt_off);
-  f.gcnt = reinterpret_cast<unsigned*>(w + fp.gc_off);
+  f.prefetch = tuning().gate_layout_prefetch;
   f.trace = static_cast<unsigned long long*>(g_trace.buf);
   f.trace_n = (long long)(g_trace.bytes / sizeof(unsigned long long));
   const int U = row_bytes <= 2048 ? 2 : 4;  // as k_layout: 2 KiB segments for rows <= 2 KiB

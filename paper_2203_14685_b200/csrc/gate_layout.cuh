@@ -11,21 +11,21 @@
 // already hold (no co-residency assumption):
 //   G. gate tiles (the separate gate's tiles, in order): select + weigh the
 //      tile's tokens and rank its items per expert (gate_tile, the gate's own
-//      code); publish the per-expert aggregate (epoch-tagged status words, so
-//      the workspace never needs clearing); the tile that completes a group
-//      of 32 tiles publishes the group's per-expert total; the exclusive
-//      prefix of a tile is then the earlier groups' totals plus its own
-//      group's earlier aggregates -- two warp-wide reads, no chain of
-//      prefixes (a look-back chain grows with the tile count and, measured,
-//      dominated the kernel); write the final slots (>= cap: dropped, weight
-//      0; slot_src) and raise the tile's ready word;
-//   S. scatter chunks of 32 tokens, in token order: wait for the chunk's
-//      tile to be ready, then a warp per token reads its x row once and
-//      stores it to its <= k slots -- in peer mode straight into the owner
-//      rank's receive buffer over NVLink, a token's row once per remote owner
-//      (dedupe), exactly as k_layout does.
-// Most CTAs hold no gate tile and start scattering as soon as tile 0 is
-// ready, so the gate's latency overlaps the row traffic.  The CTA of the last
+//      code); publish the per-expert aggregate, resolve the exclusive prefix
+//      by a decoupled look-back over earlier tiles (a warp reads 32
+//      predecessors' status words for 4 experts at once: aggregate "A" or
+//      inclusive prefix "P", epoch-tagged so the workspace never needs
+//      clearing), publish the inclusive prefix, write the final slots (>= cap:
+//      dropped, weight 0; slot_src) and raise the tile's ready word.  (A
+//      two-level form -- group totals published by the tile completing a
+//      group of 32 -- measured slower: C2 prefix 7.7 vs 2.8 us);
+//   S. scatter: a warp per token, tokens interleaved over all warps in
+//      order (as k_layout); a warp waits only until its token's tile is
+//      ready, then reads the x row once and stores it to its <= k slots -- in
+//      peer mode straight into the owner rank's receive buffer over NVLink,
+//      a token's row once per remote owner (dedupe), exactly as k_layout.
+// Most CTAs hold no gate tile and start scattering as soon as the first
+// tiles are ready, so the gate's latency overlaps the row traffic.  The CTA of the last
 // tile writes load[] and raises the totals word; every CTA then zero-fills
 // its share of the padding rows [min(load, cap), cap) and of slot_src's empty
 // entries.  The last CTA out resets the counters and advances the epoch
@@ -39,25 +39,23 @@ namespace moe {
 
 struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
   unsigned tile_next;     // phase G counter (reset by the last CTA)
-  unsigned chunk_next;    // phase S counter (reset by the last CTA)
+  unsigned chunk_next;    // unused
   unsigned done;          // CTAs finished (reset by the last CTA)
   unsigned epoch;         // launch number, tags the status and ready words
   unsigned ready;         // = epoch + 1 once load[] of this launch is final
   unsigned pad[11];
 };
 
-constexpr int kGroupTiles = 32;  // tiles per group of the two-level prefix
 
-constexpr int kScatterChunk = 32;  // tokens per phase-S work unit (divides every tile)
+constexpr int kScatterChunk = 32;  // tokens per trace record of phase S
 
 struct FusedArgs {
   GateArgs g;              // the gate (its tiles; ncols = E)
   RowArgs r;               // the rows: src = x, destinations, peer mode, dedupe
   FusedCtrl* fc;
-  unsigned long long* st;  // [n_tiles][E] tile aggregates: epoch:30 | flag:2 | count:32
-  unsigned long long* gt;  // [n_groups][E] group totals, same packing
-  unsigned* gcnt;          // [n_groups] aggregates published (reset by the last CTA)
+  unsigned long long* st;  // [n_tiles][E] status: epoch:30 | flag:2 | count:32
   unsigned* tile_ready;    // [n_tiles] = epoch + 1 once the tile's slots are final
+  int prefetch;            // bulk-prefetch the next token's x row into L2 (tuning)
   // profiling (moe_set_trace): %globaltimer stamps, NULL = off.  Per tile
   // [claim, aggregate published, prefix published, ready]; per chunk
   // [claim, tile ready seen]; per CTA [start, end]
@@ -97,75 +95,91 @@ __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   return v;
 }
 
-// Sum over lanes < n of the valid words w[idx(lane)] of one column (one
-// warp; n <= 32), spinning until every one of them carries this epoch's flag.
-__device__ __forceinline__ unsigned warp_sum_words(const unsigned long long* base, size_t stride,
-                                                   int n, unsigned epoch, int lane) {
-  unsigned v = 0;
-  if (lane < n) {
-    const unsigned long long* p = base + (size_t)lane * stride;
-    unsigned long long w = ld_relaxed_gpu(p);
-    while (!st_flag(w, epoch)) {
-      __nanosleep(32);
-      w = ld_relaxed_gpu(p);
-    }
-    v = (unsigned)w;
-  }
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  return v;
-}
-
-// The same for four consecutive columns with one vector load per lane
-// (E % 4 == 0 keeps the rows 32-byte aligned).
-__device__ __forceinline__ void warp_sum_words4(const unsigned long long* base, size_t stride,
-                                                int n, unsigned epoch, int lane, unsigned* out) {
-  unsigned v[4] = {0, 0, 0, 0};
-  if (lane < n) {
-    const unsigned long long* p = base + (size_t)lane * stride;
-    unsigned long long w[4];
+// Exclusive prefix over tiles < tile of column c (one warp): look back 32
+// tiles per round; wait until every tile up to the nearest inclusive prefix
+// has published at least its aggregate.
+__device__ __forceinline__ unsigned lookback(const unsigned long long* st, int tile, int c, int E,
+                                             unsigned epoch, int lane) {
+  unsigned excl = 0;
+  for (int base = tile - 1;; base -= 32) {
+    const int idx = base - lane;
+    unsigned f, v;
     for (;;) {
-      asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-                   : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
-                   : "l"(p)
-                   : "memory");
-      if (st_flag(w[0], epoch) && st_flag(w[1], epoch) && st_flag(w[2], epoch) &&
-          st_flag(w[3], epoch))
+      if (idx >= 0) {
+        const unsigned long long w = ld_relaxed_gpu(st + (size_t)idx * E + c);
+        f = st_flag(w, epoch);
+        v = (unsigned)w;
+      } else {
+        f = kFlagP;  // before tile 0: prefix 0
+        v = 0;
+      }
+      const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
+      const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
+      const int firstP = pmask ? __ffs(pmask) - 1 : 32;
+      const unsigned need = firstP < 31 ? ((2u << firstP) - 1u) : 0xffffffffu;
+      if (!(zmask & need)) {
+        unsigned s = lane <= firstP ? v : 0u;
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+        excl += s;
+        if (firstP < 32) return excl;
         break;
+      }
       __nanosleep(32);
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = (unsigned)w[j];
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], m);
-    out[j] = v[j];
   }
 }
 
-// Exclusive prefix of column group [c0, c0 + CW) at `tile` (one warp): the
-// totals of the groups before the tile's group plus the aggregates of the
-// tiles before it in its group.  Every word read was (or will be) published
-// by a CTA that holds its tile and does not wait on anyone.
-template <int CW>
-__device__ __forceinline__ void tile_prefix(const unsigned long long* st,
-                                            const unsigned long long* gt, int tile, int c0, int E,
-                                            unsigned epoch, int lane, unsigned* ex) {
-  const int g = tile / kGroupTiles, first = g * kGroupTiles;
-  unsigned t[CW];
-  if constexpr (CW == 4) {
-    warp_sum_words4(st + (size_t)first * E + c0, E, tile - first, epoch, lane, ex);
-    for (int base = 0; base < g; base += 32) {
-      warp_sum_words4(gt + (size_t)base * E + c0, E, min(32, g - base), epoch, lane, t);
+// The same for CG consecutive columns c0 .. c0+CG-1 at once: each lane
+// reads the CG status words of one predecessor with a single vector load
+// (the tile's words are contiguous; E % CG == 0 keeps it aligned).
+template <int CG>
+__device__ __forceinline__ void lookback_cg(const unsigned long long* st, int tile, int c0, int E,
+                                            unsigned epoch, int lane, unsigned* excl) {
+  static_assert(CG == 4, "vector width");
 #pragma unroll
-      for (int j = 0; j < 4; ++j) ex[j] += t[j];
+  for (int j = 0; j < CG; ++j) excl[j] = 0;
+  unsigned open = (1u << CG) - 1;  // columns still looking back
+  for (int base = tile - 1; open; base -= 32) {
+    const int idx = base - lane;
+    for (;;) {
+      unsigned long long w[CG];
+      if (idx >= 0) {
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+                     : "l"(st + (size_t)idx * E + c0)
+                     : "memory");
+      }
+      bool wait = false;
+      unsigned s[CG];
+      int firstP[CG];
+#pragma unroll
+      for (int j = 0; j < CG; ++j) {
+        const unsigned f = idx >= 0 ? st_flag(w[j], epoch) : kFlagP;
+        const unsigned v = idx >= 0 ? (unsigned)w[j] : 0u;
+        const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
+        const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
+        firstP[j] = pmask ? __ffs(pmask) - 1 : 32;
+        const unsigned need = firstP[j] < 31 ? ((2u << firstP[j]) - 1u) : 0xffffffffu;
+        if ((open >> j & 1u) && (zmask & need)) wait = true;
+        s[j] = lane <= firstP[j] ? v : 0u;
+      }
+      if (wait) {
+        __nanosleep(32);
+        continue;
+      }
+#pragma unroll
+      for (int j = 0; j < CG; ++j) {
+        unsigned t = s[j];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (open >> j & 1u) {
+          excl[j] += t;
+          if (firstP[j] < 32) open &= ~(1u << j);
+        }
+      }
+      break;
     }
-  } else {
-    ex[0] = warp_sum_words(st + (size_t)first * E + c0, E, tile - first, epoch, lane);
-    for (int base = 0; base < g; base += 32)
-      ex[0] += warp_sum_words(gt + (size_t)base * E + c0, E, min(32, g - base), epoch, lane);
   }
 }
 
@@ -205,10 +219,15 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   const unsigned epoch = s_epoch;
   unsigned parity = 0;
 
-  // ---------------- phase G: gate tiles in order (CTAs past the tile count go
-  // straight to phase S: fewer claims contend on the counter)
-  for (; blockIdx.x < a.n_tiles;) {
-    if (tid == 0) s_work = (int)atomicAdd(&f.fc->tile_next, 1u);
+  // ---------------- phase G: gate tiles in order.  A CTA leaves only once
+  // the counter ran out, i.e. every tile is held by a running CTA, so phase
+  // S never waits on a tile nobody holds (a plain read first spares the
+  // atomic once it ran out).
+  for (;;) {
+    if (tid == 0)
+      s_work = *reinterpret_cast<volatile unsigned*>(&f.fc->tile_next) >= (unsigned)a.n_tiles
+                   ? a.n_tiles
+                   : (int)atomicAdd(&f.fc->tile_next, 1u);
     __syncthreads();
     const int tile = s_work;
     if (tile >= a.n_tiles) break;
@@ -218,39 +237,35 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, tile, parity, s_agg);
     parity ^= 1u;
     if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
-    // publish the aggregate; the tile completing its group publishes the
-    // group total; then the two-level exclusive prefix
+    // publish the aggregate, look back, publish the inclusive prefix
     unsigned long long* st = f.st + (size_t)tile * a.E;
-    for (int c = tid; c < a.E; c += kGateThreads)
-      st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
-    const int grp = tile / kGroupTiles, first = grp * kGroupTiles;
-    const int gsize = min(kGroupTiles, a.n_tiles - first);
-    __syncthreads();
-    if (tid == 0) {
-      trace_at(f, 4LL * tile + 1);
-      __threadfence();
-      s_work = (int)atomicAdd(f.gcnt + grp, 1u) == gsize - 1;  // the group is complete
-    }
-    __syncthreads();
-    if (s_work) {  // group total: every aggregate of the group is published
-      for (int c = warp; c < a.E; c += kGateWarps) {
-        const unsigned tot =
-            warp_sum_words(f.st + (size_t)first * a.E + c, a.E, gsize, epoch, lane);
-        if (lane == 0) st_relaxed_gpu(f.gt + (size_t)grp * a.E + c, st_pack(epoch, kFlagA, tot));
-      }
-    }
-    if (a.E % 4 == 0) {  // four columns per vector load
-      for (int c0 = warp * 4; c0 < a.E; c0 += kGateWarps * 4) {
-        unsigned ex[4];
-        tile_prefix<4>(f.st, f.gt, tile, c0, a.E, epoch, lane, ex);
-        if (lane < 4) s_pre[c0 + lane] = (int)(lane == 0 ? ex[0] : lane == 1 ? ex[1]
-                                                   : lane == 2 ? ex[2] : ex[3]);
+    if (tile == 0) {
+      for (int c = tid; c < a.E; c += kGateThreads) {
+        s_pre[c] = 0;
+        st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, (unsigned)s_agg[c]));
       }
     } else {
-      for (int c = warp; c < a.E; c += kGateWarps) {
-        unsigned ex[1];
-        tile_prefix<1>(f.st, f.gt, tile, c, a.E, epoch, lane, ex);
-        if (lane == 0) s_pre[c] = (int)ex[0];
+      for (int c = tid; c < a.E; c += kGateThreads)
+        st_relaxed_gpu(st + c, st_pack(epoch, kFlagA, (unsigned)s_agg[c]));
+      if (tid == 0) trace_at(f, 4LL * tile + 1);
+      if (a.E % 4 == 0) {  // four columns per vector load
+        for (int c0 = warp * 4; c0 < a.E; c0 += kGateWarps * 4) {
+          unsigned ex[4];
+          lookback_cg<4>(f.st, tile, c0, a.E, epoch, lane, ex);
+          if (lane < 4) {
+            const unsigned e = lane == 0 ? ex[0] : lane == 1 ? ex[1] : lane == 2 ? ex[2] : ex[3];
+            s_pre[c0 + lane] = (int)e;
+            st_relaxed_gpu(st + c0 + lane, st_pack(epoch, kFlagP, e + (unsigned)s_agg[c0 + lane]));
+          }
+        }
+      } else {
+        for (int c = warp; c < a.E; c += kGateWarps) {
+          const unsigned ex = lookback(f.st, tile, c, a.E, epoch, lane);
+          if (lane == 0) {
+            s_pre[c] = (int)ex;
+            st_relaxed_gpu(st + c, st_pack(epoch, kFlagP, ex + (unsigned)s_agg[c]));
+          }
+        }
       }
     }
     __syncthreads();
@@ -286,33 +301,37 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     }
   }
 
-  // ---------------- phase S: scatter chunks of tokens in order
-  for (;;) {
-    __syncthreads();  // s_work is rewritten
-    if (tid == 0) {
-      const int c = (int)atomicAdd(&f.fc->chunk_next, 1u);
-      s_work = c;
-      if (c < n_chunks) {
-        trace_at(f, tr_chunk + 2LL * c);
-        // the chunk's x rows (contiguous) do not depend on the routing: they
-        // stream into L2 while the tile may still be resolving
-        const unsigned long long beg = (unsigned long long)c * kScatterChunk * ra.row_bytes;
-        const unsigned long long n =
-            (unsigned long long)(min(a.S, (c + 1) * kScatterChunk) - c * kScatterChunk) * ra.row_bytes;
-        for (unsigned long long o = 0; o < n; o += 65536)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + beg + o),
-                       "r"((unsigned)min(65536ull, n - o))
-                       : "memory");
-        const unsigned* rdy = f.tile_ready + (c * kScatterChunk) / a.tile_tokens;
-        while (ld_acquire_gpu_u32(rdy) != epoch + 1u) __nanosleep(32);
-        trace_at(f, tr_chunk + 2LL * c + 1);
+  // ---------------- phase S: scatter, a warp per token, tokens interleaved
+  // over the grid's warps in order (as k_layout).  A warp keeps the highest
+  // tile it knows to be ready (tiles resolve in about their order) and reads
+  // the ready words only past it; the x row of the warp's next token is
+  // bulk-prefetched into L2 while the current one is stored.
+  {
+    const int gw = blockIdx.x * kGateWarps + warp, nw = gridDim.x * kGateWarps;
+    int known = -1;  // tiles 0..known are ready
+    const bool pf = f.prefetch;
+    if (pf && lane == 0 && gw < a.S)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + (size_t)gw * ra.row_bytes),
+                   "r"((unsigned)ra.row_bytes)
+                   : "memory");
+    for (int t = gw; t < a.S; t += nw) {
+      const int tile = t / a.tile_tokens;
+      if (tile > known) {
+        if (tid % 32 == 0) trace_at(f, tr_chunk + 2LL * (t / kScatterChunk));
+        for (;;) {  // lanes read 32 ready words from known + 1 on
+          const int i = known + 1 + lane;
+          const bool ok = i >= a.n_tiles || ld_acquire_gpu_u32(f.tile_ready + i) == epoch + 1u;
+          const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+          known += bad ? __ffs(bad) - 1 : 32;
+          if (known >= tile) break;
+          __nanosleep(64);
+        }
+        if (lane == 0) trace_at(f, tr_chunk + 2LL * (t / kScatterChunk) + 1);
       }
-    }
-    __syncthreads();
-    const int c = s_work;
-    if (c >= n_chunks) break;
-    const int t_end = min(a.S, (c + 1) * kScatterChunk);
-    for (int t = c * kScatterChunk + warp; t < t_end; t += kGateWarps) {
+      if (pf && lane == 0 && t + nw < a.S)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + (size_t)(t + nw) * ra.row_bytes),
+                     "r"((unsigned)ra.row_bytes)
+                     : "memory");
       // lane j < k: slot j of token t (written by another CTA: L2 loads)
       int my_e = -1, my_s = -1;
       if (lane < a.k) {
@@ -408,7 +427,6 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     trace_at(f, tr_cta + 2LL * blockIdx.x + 1);
     __threadfence();
     if (atomicAdd(&f.fc->done, 1u) == gridDim.x - 1) {
-      for (int g = 0; g * kGroupTiles < a.n_tiles; ++g) f.gcnt[g] = 0;
       f.fc->tile_next = 0;
       f.fc->chunk_next = 0;
       f.fc->done = 0;

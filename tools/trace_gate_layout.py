@@ -78,7 +78,8 @@ def main():
         "tile_gate_us (claim->aggregate)": pct((tiles[tiles[:, 1] > 0, 1] - tiles[tiles[:, 1] > 0, 0]) / 1e3),
         "tile_lookback_us (aggregate->prefix)": pct((tiles[tiles[:, 1] > 0, 2] - tiles[tiles[:, 1] > 0, 1]) / 1e3),
         "tile_finalize_us (prefix->ready)": pct((tiles[:, 3] - tiles[:, 2]) / 1e3),
-        "chunk_claim_us": pct(us(chunks[:, 0])), "chunk_wait_us": pct((chunks[:, 1] - chunks[:, 0]) / 1e3),
+        "chunk_claim_us": pct(us(chunks[chunks[:, 0] > 0, 0])),
+        "chunk_wait_us": pct((chunks[chunks[:, 0] > 0, 1] - chunks[chunks[:, 0] > 0, 0]) / 1e3),
         "ready_by_tile_decile_us": [round(float(us(tiles[int(i), 3])), 2)
                                     for i in np.linspace(0, n_tiles - 1, 11)],
     }
