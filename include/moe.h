@@ -674,8 +674,6 @@ typedef struct {
                                 hash)                                              */
   int32_t gate_two_maxw;     /* gate: tiles x columns <= this -> select + slots2,
                                 else select + scan + slots (4096)                  */
-  int32_t gate_layout_prefetch; /* fused gate + layout: bulk-prefetch each warp's
-                                next x row into L2 (1)                             */
   int32_t layout_u;          /* layout: 32-byte vectors per lane per segment;
                                 0 = auto (2 for rows <= 2 KiB, else 4); 1, 2, 4    */
   int32_t layout_pads_first; /* layout + combine adjoint: zero the padding rows
@@ -721,9 +719,9 @@ moe_status_t moe_set_tuning(const moe_tuning_t* t);
 /* host.  PROFILING: a device buffer of `bytes` that the fused gate + layout
  * kernel (moe_gate_layout, moe_gate_dispatch_p2p) fills with %globaltimer
  * stamps (ns, uint64) on every launch made while it is set: words 0..2 =
- * n_tiles, n_chunks, CTAs; from word 4: per tile of the gate [claim,
- * aggregate published, prefix published, ready] at 4*tile, per 32-token
- * scatter chunk [claim, its tile seen ready] at 4*n_tiles + 2*chunk, per CTA
+ * n_tiles, n_batches, CTAs; from word 4: per tile of the gate [claim,
+ * aggregate published, prefix published, ready] at 4*tile, per 4-token
+ * scatter batch [claim, its tile seen ready] at 4*n_tiles + 2*batch, per CTA
  * [start, end] after those; stamps beyond `bytes` are dropped.
  * NULL (or 0 bytes) turns it off.  Affects launches made after it returns
  * (a captured graph keeps the buffer it was captured with). */

@@ -367,7 +367,6 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   f.fc = reinterpret_cast<FusedCtrl*>(w + fp.ctrl_off);
   f.st = reinterpret_cast<unsigned long long*>(w + fp.st_off);
   f.tile_ready = reinterpret_cast<unsigned*>(w + fp.rdy_off);
-  f.prefetch = tuning().gate_layout_prefetch;
   f.trace = static_cast<unsigned long long*>(g_trace.buf);
   f.trace_n = (long long)(g_trace.bytes / sizeof(unsigned long long));
   const int U = row_bytes <= 2048 ? 2 : 4;  // as k_layout: 2 KiB segments for rows <= 2 KiB

@@ -19,9 +19,9 @@
 //      dropped, weight 0; slot_src) and raise the tile's ready word.  (A
 //      two-level form -- group totals published by the tile completing a
 //      group of 32 -- measured slower: C2 prefix 7.7 vs 2.8 us);
-//   S. scatter: a warp per token, tokens interleaved over all warps in
-//      order (as k_layout); a warp waits only until its token's tile is
-//      ready, then reads the x row once and stores it to its <= k slots -- in
+//   S. scatter: every warp claims batches of 4 consecutive tokens in order
+//      from a device counter, waits until the batch's tile is ready, then
+//      per token reads the x row once and stores it to its <= k slots -- in
 //      peer mode straight into the owner rank's receive buffer over NVLink,
 //      a token's row once per remote owner (dedupe), exactly as k_layout.
 // Most CTAs hold no gate tile and start scattering as soon as the first
@@ -39,7 +39,7 @@ namespace moe {
 
 struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
   unsigned tile_next;     // phase G counter (reset by the last CTA)
-  unsigned chunk_next;    // unused
+  unsigned chunk_next;    // phase S counter, in batches (reset by the last CTA)
   unsigned done;          // CTAs finished (reset by the last CTA)
   unsigned epoch;         // launch number, tags the status and ready words
   unsigned ready;         // = epoch + 1 once load[] of this launch is final
@@ -47,7 +47,7 @@ struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
 };
 
 
-constexpr int kScatterChunk = 32;  // tokens per trace record of phase S
+constexpr int kScatterChunk = 4;  // tokens per phase-S claim (a warp's batch)
 
 struct FusedArgs {
   GateArgs g;              // the gate (its tiles; ncols = E)
@@ -55,7 +55,6 @@ struct FusedArgs {
   FusedCtrl* fc;
   unsigned long long* st;  // [n_tiles][E] status: epoch:30 | flag:2 | count:32
   unsigned* tile_ready;    // [n_tiles] = epoch + 1 once the tile's slots are final
-  int prefetch;            // bulk-prefetch the next token's x row into L2 (tuning)
   // profiling (moe_set_trace): %globaltimer stamps, NULL = off.  Per tile
   // [claim, aggregate published, prefix published, ready]; per chunk
   // [claim, tile ready seen]; per CTA [start, end]
@@ -301,23 +300,28 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     }
   }
 
-  // ---------------- phase S: scatter, a warp per token, tokens interleaved
-  // over the grid's warps in order (as k_layout).  A warp keeps the highest
-  // tile it knows to be ready (tiles resolve in about their order) and reads
-  // the ready words only past it; the x row of the warp's next token is
-  // bulk-prefetched into L2 while the current one is stored.
+  // ---------------- phase S: scatter.  Every warp claims batches of
+  // kScatterChunk consecutive tokens from a device counter, in token order
+  // (the claim of the next batch is issued before the current batch is
+  // stored, so its latency hides), waits until the batch's tile is ready --
+  // it keeps the highest tile it knows to be ready and reads the ready
+  // words only past it -- then, a token at a time, reads the x row once and
+  // stores it to its <= k slots.  Dynamic claims balance the warps of CTAs
+  // that held gate tiles against the others (a static token interleave
+  // measured slower: C3 71 vs 63 us).
   {
-    const int gw = blockIdx.x * kGateWarps + warp, nw = gridDim.x * kGateWarps;
     int known = -1;  // tiles 0..known are ready
-    const bool pf = f.prefetch;
-    if (pf && lane == 0 && gw < a.S)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + (size_t)gw * ra.row_bytes),
-                   "r"((unsigned)ra.row_bytes)
-                   : "memory");
-    for (int t = gw; t < a.S; t += nw) {
-      const int tile = t / a.tile_tokens;
+    unsigned next = 0;
+    if (lane == 0) next = atomicAdd(&f.fc->chunk_next, 1u);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    for (;;) {
+      const int c = (int)next;
+      if (c >= n_chunks) break;
+      if (lane == 0) next = atomicAdd(&f.fc->chunk_next, 1u);  // the following batch
+      const int t_beg = c * kScatterChunk, t_end = min(a.S, t_beg + kScatterChunk);
+      const int tile = t_beg / a.tile_tokens;
       if (tile > known) {
-        if (tid % 32 == 0) trace_at(f, tr_chunk + 2LL * (t / kScatterChunk));
+        if (lane == 0) trace_at(f, tr_chunk + 2LL * c);
         for (;;) {  // lanes read 32 ready words from known + 1 on
           const int i = known + 1 + lane;
           const bool ok = i >= a.n_tiles || ld_acquire_gpu_u32(f.tile_ready + i) == epoch + 1u;
@@ -326,54 +330,53 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
           if (known >= tile) break;
           __nanosleep(64);
         }
-        if (lane == 0) trace_at(f, tr_chunk + 2LL * (t / kScatterChunk) + 1);
+        if (lane == 0) trace_at(f, tr_chunk + 2LL * c + 1);
       }
-      if (pf && lane == 0 && t + nw < a.S)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + (size_t)(t + nw) * ra.row_bytes),
-                     "r"((unsigned)ra.row_bytes)
-                     : "memory");
-      // lane j < k: slot j of token t (written by another CTA: L2 loads)
-      int my_e = -1, my_s = -1;
-      if (lane < a.k) {
-        my_s = __ldcg(a.slot_idx + (size_t)t * a.k + lane);
-        my_e = __ldcg(a.expert_idx + (size_t)t * a.k + lane);
-      }
-      const char* srow = ra.src + (size_t)t * ra.row_bytes;
-      for (int seg = 0; seg < ra.row_bytes; seg += SEG) {
-        V8 r[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int off = seg + (lane + 32 * u) * VB;
-          if (off < ra.row_bytes) r[u] = ld_stream_v8(srow + off);
+      for (int t = t_beg; t < t_end; ++t) {
+        // lane j < k: slot j of token t (written by another CTA: L2 loads)
+        int my_e = -1, my_s = -1;
+        if (lane < a.k) {
+          my_s = __ldcg(a.slot_idx + (size_t)t * a.k + lane);
+          my_e = __ldcg(a.expert_idx + (size_t)t * a.k + lane);
         }
-        for (int j = 0; j < a.k; ++j) {
-          const int s = __shfl_sync(0xffffffffu, my_s, j);
-          if (s < 0) continue;
-          const int e = __shfl_sync(0xffffffffu, my_e, j);
-          const int q = e / ra.E_local;
-          if (ra.dedupe && q != ra.rank && j > 0) {
-            // a row already bound for this remote owner: record "= row of j'"
-            int jj = 0, e2 = -1, s2 = -1;
-            for (; jj < j; ++jj) {
-              s2 = __shfl_sync(0xffffffffu, my_s, jj);
-              e2 = __shfl_sync(0xffffffffu, my_e, jj);
-              if (s2 >= 0 && e2 / ra.E_local == q) break;
-            }
-            if (jj < j) {
-              if (seg == 0 && lane == 0)
-                reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
-                    (int)row_index(ra, q, e2, s2) + 1;
-              continue;
-            }
-          }
-          char* drow = dst_row_of(ra, e, s);
+        const char* srow = ra.src + (size_t)t * ra.row_bytes;
+        for (int seg = 0; seg < ra.row_bytes; seg += SEG) {
+          V8 r[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
-            if (off < ra.row_bytes) st_v8(drow + off, r[u]);
+            if (off < ra.row_bytes) r[u] = ld_stream_v8(srow + off);
+          }
+          for (int j = 0; j < a.k; ++j) {
+            const int s = __shfl_sync(0xffffffffu, my_s, j);
+            if (s < 0) continue;
+            const int e = __shfl_sync(0xffffffffu, my_e, j);
+            const int q = e / ra.E_local;
+            if (ra.dedupe && q != ra.rank && j > 0) {
+              // a row already bound for this remote owner: record "= row of j'"
+              int jj = 0, e2 = -1, s2 = -1;
+              for (; jj < j; ++jj) {
+                s2 = __shfl_sync(0xffffffffu, my_s, jj);
+                e2 = __shfl_sync(0xffffffffu, my_e, jj);
+                if (s2 >= 0 && e2 / ra.E_local == q) break;
+              }
+              if (jj < j) {
+                if (seg == 0 && lane == 0)
+                  reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
+                      (int)row_index(ra, q, e2, s2) + 1;
+                continue;
+              }
+            }
+            char* drow = dst_row_of(ra, e, s);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int off = seg + (lane + 32 * u) * VB;
+              if (off < ra.row_bytes) st_v8(drow + off, r[u]);
+            }
           }
         }
       }
+      next = __shfl_sync(0xffffffffu, next, 0);
     }
   }
 
