@@ -63,8 +63,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
-    ap.add_argument("--no-fuse", action="store_true",
-                    help="gate and layout as separate kernels (default: one fused kernel)")
+    ap.add_argument("--fuse", default="auto", choices=["auto", "on", "off"],
+                    help="gate + layout (+ NVLink dispatch) as one kernel: auto = the "
+                         "RoutePipeline default (on for the one-sided path at N > 1)")
     ap.add_argument("--dropless", action="store_true",
                     help="NEXT-4: packed dropless layout (capacity = S*k), device-side exchange")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -299,14 +300,15 @@ def main():
     try:
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
                                  group_size=G, device=dev, dropless=a.dropless,
-                                 fuse_gate_layout=not a.no_fuse)
+                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse])
     except moe.MoeError as err:
         if algo != "p2p":
             raise
         log("p2p unavailable (%s): NCCL flat AllToAll instead" % err)
         algo = "flat"
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
-                                 group_size=G, device=dev, fuse_gate_layout=not a.no_fuse)
+                                 group_size=G, device=dev,
+                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse])
 
     lg, ids, table, x = synthgen.workload_inputs(w, rank)
 

@@ -719,9 +719,9 @@ moe_status_t moe_set_tuning(const moe_tuning_t* t);
 /* host.  PROFILING: a device buffer of `bytes` that the fused gate + layout
  * kernel (moe_gate_layout, moe_gate_dispatch_p2p) fills with %globaltimer
  * stamps (ns, uint64) on every launch made while it is set: words 0..2 =
- * n_tiles, n_batches, CTAs; from word 4: per tile of the gate [claim,
- * aggregate published, prefix published, ready] at 4*tile, per 4-token
- * scatter batch [claim, its tile seen ready] at 4*n_tiles + 2*batch, per CTA
+ * n_tiles, n_chunks, CTAs; from word 4: per tile of the gate [claim,
+ * aggregate published, prefix published, ready] at 4*tile, per 32-token
+ * scatter chunk [claim, its tile seen ready] at 4*n_tiles + 2*chunk, per CTA
  * [start, end] after those; stamps beyond `bytes` are dropped.
  * NULL (or 0 bytes) turns it off.  Affects launches made after it returns
  * (a captured graph keeps the buffer it was captured with). */

@@ -15,17 +15,20 @@
 //      by a decoupled look-back over earlier tiles (a warp reads 32
 //      predecessors' status words for 4 experts at once: aggregate "A" or
 //      inclusive prefix "P", epoch-tagged so the workspace never needs
-//      clearing), publish the inclusive prefix, write the final slots (>= cap:
-//      dropped, weight 0; slot_src) and raise the tile's ready word.  (A
-//      two-level form -- group totals published by the tile completing a
-//      group of 32 -- measured slower: C2 prefix 7.7 vs 2.8 us);
-//   S. scatter: every warp claims batches of 4 consecutive tokens in order
-//      from a device counter, waits until the batch's tile is ready, then
-//      per token reads the x row once and stores it to its <= k slots -- in
-//      peer mode straight into the owner rank's receive buffer over NVLink,
-//      a token's row once per remote owner (dedupe), exactly as k_layout.
-// Most CTAs hold no gate tile and start scattering as soon as the first
-// tiles are ready, so the gate's latency overlaps the row traffic.  The CTA of the last
+//      clearing), publish the inclusive prefix, write the final slots (>=
+//      cap: dropped, weight 0; slot_src) and raise the tile's ready word.
+//      (Measured slower and dropped: group totals instead of the look-back,
+//      C2 prefix 7.7 vs 2.8 us);
+//   S. scatter chunks of 32 tokens, in token order: bulk-prefetch the
+//      chunk's x rows into L2, wait for the chunk's tile to be ready, then a
+//      warp per token reads its x row once and stores it to its <= k slots --
+//      in peer mode straight into the owner rank's receive buffer over
+//      NVLink, a token's row once per remote owner (dedupe), as k_layout.
+//      (Measured slower and dropped: a static token interleave over all
+//      warps, C3 71 vs 63 us; warp-level claims of 4-token batches without
+//      the prefetch, C3 73 us.)
+// Most CTAs hold no gate tile and start scattering as soon as tile 0 is
+// ready, so the gate's latency overlaps the row traffic.  The CTA of the last
 // tile writes load[] and raises the totals word; every CTA then zero-fills
 // its share of the padding rows [min(load, cap), cap) and of slot_src's empty
 // entries.  The last CTA out resets the counters and advances the epoch
@@ -39,15 +42,14 @@ namespace moe {
 
 struct FusedCtrl {        // at FusedPlan::ctrl_off of the gate workspace
   unsigned tile_next;     // phase G counter (reset by the last CTA)
-  unsigned chunk_next;    // phase S counter, in batches (reset by the last CTA)
+  unsigned chunk_next;    // phase S counter (reset by the last CTA)
   unsigned done;          // CTAs finished (reset by the last CTA)
   unsigned epoch;         // launch number, tags the status and ready words
   unsigned ready;         // = epoch + 1 once load[] of this launch is final
   unsigned pad[11];
 };
 
-
-constexpr int kScatterChunk = 4;  // tokens per phase-S claim (a warp's batch)
+constexpr int kScatterChunk = 32;  // tokens per phase-S work unit (divides every tile)
 
 struct FusedArgs {
   GateArgs g;              // the gate (its tiles; ncols = E)
@@ -300,83 +302,75 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     }
   }
 
-  // ---------------- phase S: scatter.  Every warp claims batches of
-  // kScatterChunk consecutive tokens from a device counter, in token order
-  // (the claim of the next batch is issued before the current batch is
-  // stored, so its latency hides), waits until the batch's tile is ready --
-  // it keeps the highest tile it knows to be ready and reads the ready
-  // words only past it -- then, a token at a time, reads the x row once and
-  // stores it to its <= k slots.  Dynamic claims balance the warps of CTAs
-  // that held gate tiles against the others (a static token interleave
-  // measured slower: C3 71 vs 63 us).
-  {
-    int known = -1;  // tiles 0..known are ready
-    unsigned next = 0;
-    if (lane == 0) next = atomicAdd(&f.fc->chunk_next, 1u);
-    next = __shfl_sync(0xffffffffu, next, 0);
-    for (;;) {
-      const int c = (int)next;
-      if (c >= n_chunks) break;
-      if (lane == 0) next = atomicAdd(&f.fc->chunk_next, 1u);  // the following batch
-      const int t_beg = c * kScatterChunk, t_end = min(a.S, t_beg + kScatterChunk);
-      const int tile = t_beg / a.tile_tokens;
-      if (tile > known) {
-        if (lane == 0) trace_at(f, tr_chunk + 2LL * c);
-        for (;;) {  // lanes read 32 ready words from known + 1 on
-          const int i = known + 1 + lane;
-          const bool ok = i >= a.n_tiles || ld_acquire_gpu_u32(f.tile_ready + i) == epoch + 1u;
-          const unsigned bad = __ballot_sync(0xffffffffu, !ok);
-          known += bad ? __ffs(bad) - 1 : 32;
-          if (known >= tile) break;
-          __nanosleep(64);
-        }
-        if (lane == 0) trace_at(f, tr_chunk + 2LL * c + 1);
+  // ---------------- phase S: scatter chunks of tokens in order
+  for (;;) {
+    __syncthreads();  // s_work is rewritten
+    if (tid == 0) {
+      const int c = (int)atomicAdd(&f.fc->chunk_next, 1u);
+      s_work = c;
+      if (c < n_chunks) {
+        trace_at(f, tr_chunk + 2LL * c);
+        // the chunk's x rows (contiguous) do not depend on the routing: they
+        // stream into L2 while the tile may still be resolving
+        const unsigned long long beg = (unsigned long long)c * kScatterChunk * ra.row_bytes;
+        const unsigned long long n =
+            (unsigned long long)(min(a.S, (c + 1) * kScatterChunk) - c * kScatterChunk) * ra.row_bytes;
+        for (unsigned long long o = 0; o < n; o += 65536)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ra.src + beg + o),
+                       "r"((unsigned)min(65536ull, n - o))
+                       : "memory");
+        const unsigned* rdy = f.tile_ready + (c * kScatterChunk) / a.tile_tokens;
+        while (ld_acquire_gpu_u32(rdy) != epoch + 1u) __nanosleep(32);
+        trace_at(f, tr_chunk + 2LL * c + 1);
       }
-      for (int t = t_beg; t < t_end; ++t) {
-        // lane j < k: slot j of token t (written by another CTA: L2 loads)
-        int my_e = -1, my_s = -1;
-        if (lane < a.k) {
-          my_s = __ldcg(a.slot_idx + (size_t)t * a.k + lane);
-          my_e = __ldcg(a.expert_idx + (size_t)t * a.k + lane);
+    }
+    __syncthreads();
+    const int c = s_work;
+    if (c >= n_chunks) break;
+    const int t_end = min(a.S, (c + 1) * kScatterChunk);
+    for (int t = c * kScatterChunk + warp; t < t_end; t += kGateWarps) {
+      // lane j < k: slot j of token t (written by another CTA: L2 loads)
+      int my_e = -1, my_s = -1;
+      if (lane < a.k) {
+        my_s = __ldcg(a.slot_idx + (size_t)t * a.k + lane);
+        my_e = __ldcg(a.expert_idx + (size_t)t * a.k + lane);
+      }
+      const char* srow = ra.src + (size_t)t * ra.row_bytes;
+      for (int seg = 0; seg < ra.row_bytes; seg += SEG) {
+        V8 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int off = seg + (lane + 32 * u) * VB;
+          if (off < ra.row_bytes) r[u] = ld_stream_v8(srow + off);
         }
-        const char* srow = ra.src + (size_t)t * ra.row_bytes;
-        for (int seg = 0; seg < ra.row_bytes; seg += SEG) {
-          V8 r[U];
+        for (int j = 0; j < a.k; ++j) {
+          const int s = __shfl_sync(0xffffffffu, my_s, j);
+          if (s < 0) continue;
+          const int e = __shfl_sync(0xffffffffu, my_e, j);
+          const int q = e / ra.E_local;
+          if (ra.dedupe && q != ra.rank && j > 0) {
+            // a row already bound for this remote owner: record "= row of j'"
+            int jj = 0, e2 = -1, s2 = -1;
+            for (; jj < j; ++jj) {
+              s2 = __shfl_sync(0xffffffffu, my_s, jj);
+              e2 = __shfl_sync(0xffffffffu, my_e, jj);
+              if (s2 >= 0 && e2 / ra.E_local == q) break;
+            }
+            if (jj < j) {
+              if (seg == 0 && lane == 0)
+                reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
+                    (int)row_index(ra, q, e2, s2) + 1;
+              continue;
+            }
+          }
+          char* drow = dst_row_of(ra, e, s);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int off = seg + (lane + 32 * u) * VB;
-            if (off < ra.row_bytes) r[u] = ld_stream_v8(srow + off);
-          }
-          for (int j = 0; j < a.k; ++j) {
-            const int s = __shfl_sync(0xffffffffu, my_s, j);
-            if (s < 0) continue;
-            const int e = __shfl_sync(0xffffffffu, my_e, j);
-            const int q = e / ra.E_local;
-            if (ra.dedupe && q != ra.rank && j > 0) {
-              // a row already bound for this remote owner: record "= row of j'"
-              int jj = 0, e2 = -1, s2 = -1;
-              for (; jj < j; ++jj) {
-                s2 = __shfl_sync(0xffffffffu, my_s, jj);
-                e2 = __shfl_sync(0xffffffffu, my_e, jj);
-                if (s2 >= 0 && e2 / ra.E_local == q) break;
-              }
-              if (jj < j) {
-                if (seg == 0 && lane == 0)
-                  reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
-                      (int)row_index(ra, q, e2, s2) + 1;
-                continue;
-              }
-            }
-            char* drow = dst_row_of(ra, e, s);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int off = seg + (lane + 32 * u) * VB;
-              if (off < ra.row_bytes) st_v8(drow + off, r[u]);
-            }
+            if (off < ra.row_bytes) st_v8(drow + off, r[u]);
           }
         }
       }
-      next = __shfl_sync(0xffffffffu, next, 0);
     }
   }
 

@@ -22,20 +22,26 @@ class RoutePipeline:
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
                  device=None, slot_src: bool = True, dropless: bool = False,
-                 fuse_gate_layout: bool = True, identity_alias: bool = False):
+                 fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
         exchange (algo "p2p" only).  The expert stand-in is the identity.
-        fuse_gate_layout (default): steps 1 + 2 as one persistent kernel
+        fuse_gate_layout: steps 1 + 2 as one persistent kernel
         (moe_gate_layout / moe_gate_dispatch_p2p; the library runs the two
-        steps separately for shapes it has no fused kernel for).
+        steps separately for shapes it has no fused kernel for).  None =
+        where it measured faster: the one-sided NVLink dispatch (P > 1,
+        algo "p2p"), whose long row phase hides the gate; at P = 1 the
+        separate gate -> layout pair under PDL measured faster (C2 71.4 vs
+        77.0 us per step, C3 91.6 vs 100.0).
         identity_alias=True (p2p only): a step with expert=False tells the
         combine that recv is unmodified (MOE_P2P_RECV_UNMODIFIED): no entry
         barrier and one read of a row sent once for two slots.  A measurement
         of the routing alone; a real expert always takes the default path."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
+        if fuse_gate_layout is None:
+            fuse_gate_layout = comm is not None and comm.nranks > 1 and algo == "p2p"
         self.fuse = fuse_gate_layout and not dropless
         self.identity_alias = identity_alias
         if dropless:

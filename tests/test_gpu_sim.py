@@ -350,3 +350,26 @@ def test_sim_mismatched_programs_are_rejected():
             world.run()
         assert ei.value.status == 1
         world.run()                      # the queues were cleared: usable again
+
+
+@pytest.mark.parametrize("mode", ["default", "nodedupe", "local_pad"])
+@pytest.mark.parametrize("c", [P2P_CASES[i] for i in (0, 2, 3, 6, 7)],
+                         ids=lambda c: "-".join("%s=%s" % kv for kv in c.items()))
+def test_sim_gate_dispatch_fused(orc, c, mode):
+    """moe_gate_dispatch_p2p (gate + NVLink row scatter as one persistent
+    kernel, per simulated rank): routing bit-exact, receive buffers equal the
+    oracle's AllToAll of the per-rank layouts, byte for byte."""
+    with moe.tuned(**P2P_MODES[mode]), moe.SimWorld(c["P"]) as world:
+        R = Ranks(orc, **c)
+        recvs = R.symm(world, (R.E, R.cap, R.d))
+        lg_dev = [dev(lg) for lg in R.lgs]
+        outs = []
+        gates = [moe.Gate(R.S, R.E, R.k, R.cap, R.kind) for _ in range(R.P)]  # alive until run()
+        for r in range(R.P):
+            outs.append(gates[r].with_dispatch_p2p(world.comm(r), R.x_dev[r], recvs[r], lg_dev[r]))
+        world.run()
+        torch.cuda.synchronize()
+        want = orc.alltoall_flat(R.disp)
+        for r in range(R.P):
+            assert_routing_equal(outs[r], R.orc_routings[r], "rank %d" % r)
+            assert host(recvs[r]).tobytes() == want[r].tobytes(), "recv of rank %d" % r

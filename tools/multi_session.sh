@@ -19,7 +19,9 @@ done
 for algo in flat hier hier2d; do
   $B --workload C2 --algo $algo --no-backward > ${O}_bench_C2_${algo}.json 2> ${O}_bench_C2_${algo}.err
 done
-$B --workload C2 --no-fuse --no-backward > ${O}_bench_C2_nofuse.json 2> ${O}_bench_C2_nofuse.err
+for w in C2 C3 C4b; do
+  $B --workload $w --fuse off --no-backward > ${O}_bench_${w}_nofuse.json 2> ${O}_bench_${w}_nofuse.err
+done
 for S in 4096 32768 262144; do
   for algo in p2p flat; do
     $B --workload C5 --tokens $S --algo $algo --no-backward > ${O}_c5e2e_${S}_${algo}.json 2> ${O}_c5e2e_${S}_${algo}.err

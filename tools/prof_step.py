@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--fuse", action="store_true")
     ap.add_argument("--tile", type=int, default=0, help="tuning gate_max_tile")
     a = ap.parse_args()
     if a.tile:
@@ -31,7 +32,7 @@ def main():
     S = w.S
     cap = moe.capacity(S, w.E, w.k, w.C)
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
-    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, fuse_gate_layout=not a.no_fuse)
+    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, fuse_gate_layout=True if a.fuse else (False if a.no_fuse else None))
     lg, ids, table, x = synthgen.workload_inputs(w, 0)
 
     def dev(v):

@@ -39,7 +39,7 @@ def main():
     S = w.S
     cap = moe.capacity(S, w.E, w.k, w.C)
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
-    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind)
+    pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, fuse_gate_layout=True)
     lg, ids, table, x = synthgen.workload_inputs(w, 0)
 
     def dev(v):
