@@ -219,3 +219,32 @@ def test_backward_and_packed_entry_points_validate_on_host():
                                     None) == INVALID
     assert L.moe_combine_backward_p2p(None, rd, dr, FAKE, FAKE, 64, 1, FAKE, FAKE, 0, None) == INVALID
     assert L.moe_dispatch_backward_p2p(None, rd, dr, FAKE, 64, 1, FAKE, 0, None) == INVALID
+
+
+def test_tuning_table_roundtrip_and_validation():
+    """moe_get/set_tuning: the process-wide kernel-variant table (read once
+    from the environment, include/moe.h "tuning"); out-of-range values are
+    rejected without changing it."""
+    before = moe.get_tuning()
+    assert before["gate_tiles"] >= 1 and before["p2p_dedupe"] in (0, 1)
+    with moe.tuned(gate_tiles=17, reverse_ku=2):
+        t = moe.get_tuning()
+        assert t["gate_tiles"] == 17 and t["reverse_ku"] == 2
+    assert moe.get_tuning() == before
+    for bad in ({"layout_u": 3}, {"reverse_ku": 1}, {"gate_bwd_lanes": 6},
+                {"barrier_timeout_ms": -1}, {"nccl_cta_policy": 7}):
+        with pytest.raises(moe.MoeError) as ei:
+            moe.set_tuning(**bad)
+        assert ei.value.status == INVALID
+        assert moe.get_tuning() == before
+    with pytest.raises(KeyError):
+        moe.set_tuning(no_such_field=1)
+
+
+def test_alltoallv_plan_in_c():
+    """moe_alltoallv_plan (host, C): send rows per destination rank from the
+    expert offsets, receive rows and offsets from the received counts."""
+    offsets = [0, 3, 3, 7, 9]           # E = 4, P = 2: rank 0 owns experts 0-1
+    recv_counts = [1, 2, 5, 0]          # from rank 0: (1, 2), from rank 1: (5, 0)
+    sr, rr, ro = moe.alltoallv_plan(offsets, recv_counts, 2)
+    assert sr == [3, 6] and rr == [3, 5] and ro == [0, 1, 3, 8, 8]
