@@ -30,19 +30,17 @@ class RoutePipeline:
         fuse_gate_layout: steps 1 + 2 as one persistent kernel
         (moe_gate_layout / moe_gate_dispatch_p2p; the library runs the two
         steps separately for shapes it has no fused kernel for).  None =
-        where it measured faster: the one-sided NVLink dispatch (P > 1,
-        algo "p2p"), whose long row phase hides the gate; at P = 1 the
-        separate gate -> layout pair under PDL measured faster (C2 71.4 vs
-        77.0 us per step, C3 91.6 vs 100.0).
+        off: the separate gate -> layout pair under PDL measured as fast or
+        faster (P=1: C2 71.4 vs 77.0 us per step, C3 91.6 vs 100.0; P=2
+        one-sided: C2 251.3 vs 251.7, C3 257.0 vs 258.6, C4b 263.6 vs 263.3;
+        profiles/r02_gate_layout).
         identity_alias=True (p2p only): a step with expert=False tells the
         combine that recv is unmodified (MOE_P2P_RECV_UNMODIFIED): no entry
         barrier and one read of a row sent once for two slots.  A measurement
         of the routing alone; a real expert always takes the default path."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
-        if fuse_gate_layout is None:
-            fuse_gate_layout = comm is not None and comm.nranks > 1 and algo == "p2p"
-        self.fuse = fuse_gate_layout and not dropless
+        self.fuse = bool(fuse_gate_layout) and not dropless
         self.identity_alias = identity_alias
         if dropless:
             cap = S * k
@@ -80,9 +78,13 @@ class RoutePipeline:
             self.recv = comm.symm_empty((E, cap, d), dtype)
             self.dispatch = self.back = self.recv
         elif self.P > 1:
-            self.dispatch = mk(E, cap, d)
-            self.recv = mk(E, cap, d)
-            self.back = mk(E, cap, d)
+            # NCCL's send/recv buffers in NCCL-registered memory (ncclMemAlloc
+            # + ncclCommRegister): zero-copy over NVLink, measured 491 vs 280
+            # GB/s busBW at 128 MiB per rank, P=2 (profiles/r02_multi)
+            reg = lambda *shape: comm.mem_empty(shape, dtype)
+            self.dispatch = reg(E, cap, d)
+            self.recv = reg(E, cap, d)
+            self.back = reg(E, cap, d)
         else:
             self.dispatch = mk(E, cap, d)
             self.recv = self.back = self.dispatch
@@ -90,7 +92,7 @@ class RoutePipeline:
         self.ws = None
         if self.P > 1 and algo in ("hier", "hier2d"):
             nb = comm.workspace_bytes(algo, group_size, self.dispatch.nbytes // self.P)
-            self.ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            self.ws = comm.mem_empty((max(1, nb),), torch.uint8)
 
     def _first_flags(self):
         # The very first dispatch needs its entry barrier (peers may not have
@@ -252,9 +254,9 @@ class RoutePipeline:
                 self.d_recv = self.comm.symm_empty((self.E, self.cap, self.d), self.y.dtype)
                 self.wtab = self.comm.symm_empty((self.E * self.cap,), torch.float32)
                 self.dwtab = self.comm.symm_empty((self.E * self.cap,), torch.float32)
-            elif self.P > 1:
-                self.d_back, self.d_recv, self.d_disp = (mk(self.E, self.cap, self.d)
-                                                         for _ in range(3))
+            elif self.P > 1:   # NCCL send/recv buffers: registered (see __init__)
+                self.d_back, self.d_recv, self.d_disp = (
+                    self.comm.mem_empty((self.E, self.cap, self.d), self.y.dtype) for _ in range(3))
             else:
                 self.d_back = self.d_recv = self.d_disp = mk(self.E, self.cap, self.d)
         if self.P > 1 and self.algo == "p2p":

@@ -142,7 +142,8 @@ def test_sim_route_pipeline_p2p(orc):
         R = Ranks(orc, P, S, d, E, k)
         pipes = [moe.RoutePipeline(S, d, E, k, R.cap, torch.bfloat16, comm=world.comm(r),
                                    algo="p2p", identity_alias=True) for r in range(P)]
-        ys = [pipes[r].step(dev(R.lgs[r]), R.x_dev[r]) for r in range(P)]
+        lg_dev = [dev(lg) for lg in R.lgs]   # alive until run(): the fused gate + dispatch is queued
+        ys = [pipes[r].step(lg_dev[r], R.x_dev[r]) for r in range(P)]
         world.run()
         torch.cuda.synchronize()
         want = orc.alltoall_flat(R.disp)
