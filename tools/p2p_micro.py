@@ -30,6 +30,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--variants", action="store_true",
+                    help="also time the row kernels under other tuning values")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -70,6 +72,28 @@ def main():
         "step": lambda: pipe.step(lg_d, x_d, ids_d, tb_d),
     }
     out = {"P": P, "workload": w.name, "recv_bytes": pipe.recv.numel() * 2}
+    runs = [("", {}, pieces)]
+    if a.variants:
+        rows = {k: pieces[k] for k in ("dispatch_rows_only", "dispatch_with_exit",
+                                       "combine_reads_only")}
+        for tag, tu in (("u4", {"layout_u": 4}), ("u1", {"layout_u": 1}),
+                        ("cta8", {"row_ctas_per_sm": 8}), ("cta3", {"row_ctas_per_sm": 3}),
+                        ("ku2", {"reverse_ku": 2}), ("nodedupe", {"p2p_dedupe": 0}),
+                        ("rev", {"reverse_backwards": 1})):
+            runs.append(("@" + tag, tu, rows))
+    for tag, tu, group in runs:
+        old_t = moe.set_tuning(**tu)
+        _time_pieces(group, tag, out, comm, flush, a.reps)
+        moe.set_tuning(**old_t)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+def _time_pieces(pieces, tag, out, comm, flush, reps):
     for name, fn in pieces.items():
         fn()
         torch.cuda.synchronize()
@@ -83,7 +107,7 @@ def main():
         g.replay()
         torch.cuda.synchronize()
         ts = []
-        for _ in range(a.reps):
+        for _ in range(reps):
             flush.zero_()
             comm.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -94,14 +118,8 @@ def main():
             ts.append(e0.elapsed_time(e1) * 1e3)
         t = torch.tensor([float(np.median(ts))], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        out[name + "_us"] = round(float(t[0]), 2)
+        out[name + tag + "_us"] = round(float(t[0]), 2)
         del g
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    torch.cuda.synchronize()
-    dist.barrier()
-    comm.destroy()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
