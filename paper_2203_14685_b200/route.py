@@ -22,7 +22,8 @@ class RoutePipeline:
                  kind: str = "topk", weight_mode: str = "renorm", priority: str = "token",
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
                  device=None, slot_src: bool = True, dropless: bool = False,
-                 fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False):
+                 fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False,
+                 nvtx: bool = False):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
@@ -37,11 +38,14 @@ class RoutePipeline:
         identity_alias=True (p2p only): a step with expert=False tells the
         combine that recv is unmodified (MOE_P2P_RECV_UNMODIFIED): no entry
         barrier and one read of a row sent once for two slots.  A measurement
-        of the routing alone; a real expert always takes the default path."""
+        of the routing alone; a real expert always takes the default path.
+        nvtx=True: every stage of step() is an NVTX range ("moe/gate",
+        "moe/layout", ...) for Nsight timelines."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
         self.fuse = bool(fuse_gate_layout) and not dropless
         self.identity_alias = identity_alias
+        self.nvtx = nvtx
         if dropless:
             cap = S * k
             slot_src = False
@@ -118,6 +122,15 @@ class RoutePipeline:
                 return self.step(logits, x, token_ids, table, expert, mark)
             finally:
                 self.y = saved
+        if self.nvtx:   # NVTX ranges between the stage marks; the last mark is "reverse"
+            inner = mark
+            torch.cuda.nvtx.range_push("moe/gate")
+
+            def mark(name, _inner=inner):
+                _inner(name)
+                torch.cuda.nvtx.range_pop()
+                if name != "reverse":
+                    torch.cuda.nvtx.range_push("moe/after_" + name)
         if self.fuse:
             return self._step_fused(logits, x, token_ids, table, expert, mark)
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
