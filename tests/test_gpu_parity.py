@@ -381,3 +381,21 @@ def test_gate_layout_fused_replays(orc, case, tile):
             graph.replay()
             torch.cuda.synchronize()
             check(*v, "replay %d" % it)
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_route_pipeline_nvtx_and_fuse(orc, fuse):
+    """RoutePipeline with NVTX ranges and with / without the fused gate +
+    layout: the same routing, dispatch and y as the oracle."""
+    S, d, E, k = 3000, 256, 16, 2
+    cap = orc.capacity(S, E, k, 1.0)
+    lg = synthgen.logits(4242, S, E, k)
+    x = synthgen.tokens(4343, S, d, "bf16")
+    pipe = moe.RoutePipeline(S, d, E, k, cap, torch.bfloat16, nvtx=True, fuse_gate_layout=fuse)
+    y = host(pipe.step(dev(lg), dev(x)))
+    torch.cuda.synchronize()
+    ro = orc.gate(lg, E=E, k=k, cap=cap)
+    assert_routing_equal(pipe.routing, ro)
+    disp = orc.layout(x, ro)
+    assert host(pipe.dispatch).tobytes() == disp.tobytes()
+    assert_y_close(y, orc.reverse_layout(disp, ro), combine_bound(as_f64(disp), ro), True)
