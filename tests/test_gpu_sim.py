@@ -374,3 +374,54 @@ def test_sim_gate_dispatch_fused(orc, c, mode):
         for r in range(R.P):
             assert_routing_equal(outs[r], R.orc_routings[r], "rank %d" % r)
             assert host(recvs[r]).tobytes() == want[r].tobytes(), "recv of rank %d" % r
+
+
+FULL = [("C2", 2), ("C2", 8), ("C3", 8), ("C4a", 8), ("C4b", 8)]
+
+
+@pytest.mark.parametrize("wname,P", FULL, ids=lambda v: str(v))
+def test_sim_full_size(orc, wname, P):
+    """BASELINE.json's full per-rank sizes on P simulated ranks, the bench's
+    launch configuration (RoutePipeline, one-sided path, s_e expert in place):
+    every receive buffer byte-exact against the oracle's AllToAll, y within
+    tolerance on a sample of 2048 tokens per rank (the oracle's combine of
+    those tokens, from the oracle's own expert outputs)."""
+    w = synthgen.WORKLOADS[wname]
+    S, d, E, k = w.S, w.d, w.E, w.k
+    cap = orc.capacity(S, E, k, w.C)
+    El = E // P
+    with moe.SimWorld(P) as world:
+        ins = [synthgen.workload_inputs(w, r) for r in range(P)]
+        pipes = [moe.RoutePipeline(S, d, E, k, cap, torch.bfloat16, w.kind, comm=world.comm(r),
+                                   algo="p2p") for r in range(P)]
+        dins = [[None if v is None else dev(v) for v in inp] for inp in ins]
+        for r in range(P):   # gate (immediate) + dispatch (queued)
+            lg, ids, table, x = dins[r]
+            pipes[r].gate(lg, ids, table, out=pipes[r].routing)
+            world.comm(r).dispatch_p2p(x, pipes[r].routing, pipes[r].recv)
+        world.run()
+        torch.cuda.synchronize()
+        ros = [orc.gate(ins[r][0], E=E, k=k, cap=cap, kind=w.kind, token_ids=ins[r][1],
+                        table=ins[r][2]) for r in range(P)]
+        for r in range(P):
+            assert_routing_equal(pipes[r].routing, ros[r], "rank %d" % r)
+        recvs = orc.alltoall_flat([orc.layout(ins[r][3], ros[r]) for r in range(P)])
+        for r in range(P):
+            assert host(pipes[r].recv).tobytes() == recvs[r].tobytes(), "recv of rank %d" % r
+        for r in range(P):   # the s_e stand-in, then the combine
+            moe.expert_scale(pipes[r].recv, P, El, r * El, out=pipes[r].recv)
+        for r in range(P):
+            world.comm(r).combine_p2p(pipes[r].recv, pipes[r].routing, pipes[r].y)
+        world.run()
+        torch.cuda.synchronize()
+        backs = orc.alltoall_flat([orc.expert_scale(recvs[q].reshape(P, El, cap, d), q * El)
+                                   .reshape(E, cap, d) for q in range(P)])
+        rng = np.random.default_rng(P * 7 + len(wname))
+        for r in range(P):
+            t = np.sort(rng.choice(S, 2048, replace=False))
+            ro = ros[r]
+            sub = type(ro)(**{**ro.__dict__, "expert_idx": ro.expert_idx[t], "slot_idx": ro.slot_idx[t],
+                              "weight": ro.weight[t], "S": len(t)})
+            y_o = orc.reverse_layout(backs[r], sub)
+            assert_y_close(host(pipes[r].y)[t], y_o, combine_bound(as_f64(backs[r]), sub), True,
+                           "rank %d" % r)
