@@ -674,9 +674,6 @@ typedef struct {
                                 hash)                                              */
   int32_t gate_two_maxw;     /* gate: tiles x columns <= this -> select + slots2,
                                 else select + scan + slots (4096)                  */
-  int32_t gate_single;       /* gate: one launch (selection, decoupled look-back
-                                prefix and slots in one kernel; TOKEN priority,
-                                TOPK/KTOP1 k <= 8, HASH) instead of 2-3 (0)       */
   int32_t layout_u;          /* layout: 32-byte vectors per lane per segment;
                                 0 = auto (2 for rows <= 2 KiB, else 4); 1, 2, 4    */
   int32_t layout_pads_first; /* layout + combine adjoint: zero the padding rows

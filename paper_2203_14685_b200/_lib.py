@@ -41,7 +41,7 @@ class A2AOp(ctypes.Structure):
                 ("src_off", i64), ("dst_off", i64), ("chunks", i64)]
 
 
-TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "gate_single", "layout_u",
+TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "layout_u",
                  "layout_pads_first", "reverse_ku", "reverse_tpw", "reverse_kspec",
                  "reverse_backwards", "reverse_y_ef", "row_ctas_per_sm", "combine_bwd_kspec",
                  "gate_bwd_lanes", "p2p_dedupe", "p2p_local_pad", "a2a_ctas_per_sm",

@@ -55,7 +55,6 @@ const TuneField kTune[] = {
     {"MOE_GATE_TILES", &moe_tuning_t::gate_tiles, 256, 1, 1 << 20},
     {"MOE_GATE_MAX_TILE", &moe_tuning_t::gate_max_tile, 0, 0, 256},
     {"MOE_GATE_TWO_MAXW", &moe_tuning_t::gate_two_maxw, 4096, 0, 1 << 30},
-    {"MOE_GATE_SINGLE", &moe_tuning_t::gate_single, 0, 0, 1},
     {"MOE_LAYOUT_U", &moe_tuning_t::layout_u, 0, 0, 4},
     {"MOE_LAYOUT_PADS_FIRST", &moe_tuning_t::layout_pads_first, -1, -1, 1},
     {"MOE_REVERSE_KU", &moe_tuning_t::reverse_ku, 0, 0, 4},

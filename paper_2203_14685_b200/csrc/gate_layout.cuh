@@ -34,10 +34,7 @@
 // entries.  The last CTA out resets the counters and advances the epoch
 // (CUDA-graph replay safe).  Outputs are bit-identical to moe_gate followed
 // by moe_layout (tested).
-//
-// With no rows (ra.src == NULL, a grid of one CTA per tile) the same kernel
-// is the gate alone in ONE launch: selection, the look-back prefix and the
-// final slots, instead of select -> (scan ->) slots.
+
 #pragma once
 #include "gate_impl.cuh"
 #include "rows.cuh"
@@ -306,9 +303,8 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     }
   }
 
-  // ---------------- phase S: scatter chunks of tokens in order (gate-only
-  // launches, ra.src == NULL, have no rows to move)
-  for (; ra.src;) {
+  // ---------------- phase S: scatter chunks of tokens in order
+  for (;;) {
     __syncthreads();  // s_work is rewritten
     if (tid == 0) {
       const int c = (int)atomicAdd(&f.fc->chunk_next, 1u);
@@ -385,7 +381,7 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
     while (ld_acquire_gpu_u32(&f.fc->ready) != epoch + 1u) __nanosleep(64);
   __syncthreads();
   int* s_beg = s_pre;  // [E + 1] <= 257
-  if (tid < 32 && ra.src) {
+  if (tid < 32) {
     int carry = 0;
     for (int base = 0; base < a.E; base += 32) {
       const int e = base + lane;
@@ -409,7 +405,7 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
   __syncthreads();
   const int gw = blockIdx.x * kGateWarps + warp, nw = gridDim.x * kGateWarps;
   const V8 z = V8{{0, 0, 0, 0, 0, 0, 0, 0}};
-  for (int p = gw; ra.src && p < s_beg[a.E]; p += nw) {
+  for (int p = gw; p < s_beg[a.E]; p += nw) {
     int lo = 0, hi = a.E - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;

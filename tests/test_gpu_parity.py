@@ -93,8 +93,7 @@ GATE_CASES = [
 
 
 # kernel variants selected by the library's tuning table (moe.tuned)
-GATE_PATHS = {"two": {}, "three": {"gate_two_maxw": 0}, "single": {"gate_single": 1},
-              "single_tile32": {"gate_single": 1, "gate_max_tile": 32},
+GATE_PATHS = {"two": {}, "three": {"gate_two_maxw": 0},
               "two_forced": {"gate_two_maxw": 1000000},
               "tile256": {"gate_max_tile": 256, "gate_tiles": 1},
               "tile32": {"gate_max_tile": 32}}
