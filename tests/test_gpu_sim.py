@@ -267,7 +267,8 @@ def test_sim_dropless_p2p(orc, P, E, k):
 @pytest.mark.parametrize("form", ["pull", "push"])
 @pytest.mark.parametrize("P,E,k,C,local_pad", [(2, 16, 2, 0.8, -1), (4, 16, 2, 1.0, -1),
                                                (8, 32, 1, 1.25, -1), (4, 32, 1, 1.25, 0),
-                                               (2, 8, 2, 1.25, 1)])
+                                               (2, 8, 2, 1.25, 1),
+                                               (8, 8, 2, 1.0, -1)])   # C2 at N=8: 1 expert per rank
 def test_sim_backward_p2p(orc, form, P, E, k, C, local_pad):
     """combine_backward (pull: reads expert rows and stores w*dy at the owner;
     push: dy rows + weights to the owners, dots there) and the dispatch
