@@ -192,10 +192,12 @@ __global__ void k_barrier(PeerPtrs sig, int P, int rank, unsigned long long time
 }
 
 moe_status_t barrier_launch(const PeerPtrs& sig, int nranks, int rank, cudaStream_t stream) {
-  // a plain launch (with PDL it measured slower in the step graph)
+  // a plain launch by default (round 1 measured PDL slower in the step graph)
   unsigned long long to = (unsigned long long)tuning().barrier_timeout_ms * 1000000ull;
   void* args[] = {(void*)&sig, &nranks, &rank, &to};
-  cudaError_t e = cudaLaunchKernel((const void*)k_barrier, dim3(1), dim3(32), args, 0, stream);
+  cudaError_t e = tuning().barrier_pdl
+                      ? launch_pdl((const void*)k_barrier, dim3(1), dim3(32), 0, stream, args)
+                      : cudaLaunchKernel((const void*)k_barrier, dim3(1), dim3(32), args, 0, stream);
   if (e != cudaSuccess) return cuda_status(e, "moe_comm_barrier: launch");
   return MOE_OK;
 }

@@ -30,6 +30,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--barrier-pdl", action="store_true",
+                    help="also time the barrier-heavy pieces with PDL-launched barriers")
     ap.add_argument("--variants", action="store_true",
                     help="also time the row kernels under other tuning values")
     a = ap.parse_args()
@@ -73,6 +75,10 @@ def main():
     }
     out = {"P": P, "workload": w.name, "recv_bytes": pipe.recv.numel() * 2}
     runs = [("", {}, pieces)]
+    if a.barrier_pdl:   # the step and the barrier-heavy pieces with PDL-launched barriers
+        bar = {k: pieces[k] for k in ("barrier", "dispatch_with_exit", "combine_with_barriers",
+                                      "step")}
+        runs.append(("@bpdl", {"barrier_pdl": 1}, bar))
     if a.variants:
         rows = {k: pieces[k] for k in ("dispatch_rows_only", "dispatch_with_exit",
                                        "combine_reads_only")}
