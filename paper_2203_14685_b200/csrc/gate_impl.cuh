@@ -480,7 +480,7 @@ __device__ __forceinline__ void gate_mbar_init(unsigned long long& s_mbar) {
 template <int KIND, int L, int K>
 __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned& s_bad,
                                           unsigned long long& s_mbar, int tile, unsigned parity,
-                                          int* s_agg = nullptr) {
+                                          int* s_agg = nullptr, bool init_mbar = false) {
   const int items = a.tile_tokens * a.k;
   float* s_lg = reinterpret_cast<float*>(smem);  // [tile_tokens][E] staged logits
   double* s_z = reinterpret_cast<double*>(smem + a.lg_words);  // D2S: [tile_tokens][E]
@@ -489,35 +489,38 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
   int* s_hist = s_rank + items;               // [warps][ncols]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = tile * a.tile_tokens;
+  const int nt = min(a.tile_tokens, a.S - t0);
+  // Stage the tile's logits (nt*E contiguous floats) into shared memory with
+  // one TMA bulk copy (one DRAM latency for the whole tile), issued first so
+  // the clears below overlap it (the staging area is disjoint from them); the
+  // sub-16-byte tail with plain loads.
+  const unsigned lg_bytes = KIND != KIND_HASH ? (unsigned)nt * a.E * 4u : 0u;
+  const unsigned bulk = lg_bytes & ~15u;
+  const float* g = a.logits + (size_t)t0 * a.E;
+  const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar);
+  if (KIND != KIND_HASH && tid == 0) {
+    if (init_mbar) gate_mbar_init(s_mbar);
+    // the previous tile's generic-proxy reads of the buffer come first
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bulk)
+                 : "memory");
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(s_lg);
+    for (unsigned o = 0; o < bulk; o += 65536u) {
+      const unsigned n = min(65536u, bulk - o);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(dst + o), "l"(reinterpret_cast<const char*>(g) + o), "r"(n), "r"(mbar)
+          : "memory");
+    }
+  }
   if (tid == 0) s_bad = 0;
   for (int i = tid; i < items; i += kGateThreads) s_exp[i] = -1;
   for (int i = tid; i < kGateWarps * a.ncols; i += kGateThreads) s_hist[i] = 0;
-  __syncthreads();
-  const int t0 = tile * a.tile_tokens;
-  const int nt = min(a.tile_tokens, a.S - t0);
+  if constexpr (KIND != KIND_HASH)
+    for (unsigned i = bulk / 4 + tid; i < lg_bytes / 4; i += kGateThreads) s_lg[i] = __ldg(g + i);
+  __syncthreads();  // the clears, the tail's stores (and the mbarrier's init)
   if constexpr (KIND != KIND_HASH) {
-    // Stage the tile's logits (nt*E contiguous floats) into shared memory
-    // with one TMA bulk copy (one DRAM latency for the whole tile); the
-    // sub-16-byte tail, if any, with plain loads.
-    const unsigned bytes = (unsigned)nt * a.E * 4u, bulk = bytes & ~15u;
-    const float* g = a.logits + (size_t)t0 * a.E;
-    const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    if (tid == 0) {
-      // the previous tile's generic-proxy reads of the buffer come first
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bulk)
-                   : "memory");
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(s_lg);
-      for (unsigned o = 0; o < bulk; o += 65536u) {
-        const unsigned n = min(65536u, bulk - o);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(dst + o), "l"(reinterpret_cast<const char*>(g) + o), "r"(n), "r"(mbar)
-            : "memory");
-      }
-    }
-    for (unsigned i = bulk / 4 + tid; i < bytes / 4; i += kGateThreads) s_lg[i] = __ldg(g + i);
-    __syncthreads();  // the tail's plain stores
     unsigned done = 0;
     while (!done)
       asm volatile(
@@ -627,9 +630,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   __shared__ __align__(8) unsigned long long s_mbar;
   pdl_wait();     // the producer of the logits / the previous step must be done
   pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
-  if (threadIdx.x == 0) gate_mbar_init(s_mbar);
-  __syncthreads();
-  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, blockIdx.x, 0);
+  gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, blockIdx.x, 0, nullptr, true);
   const int tid = threadIdx.x;
   const int items = a.tile_tokens * a.k;
   const int* s_exp = smem + a.lg_words + a.z_words;
