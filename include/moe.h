@@ -701,7 +701,7 @@ typedef struct {
                                 report MOE_ERR_TIMEOUT (moe_comm_check); 0 = wait
                                 forever (60000)                                    */
   int32_t barrier_pdl;       /* device barrier launched with programmatic dependent
-                                launch (0)                                         */
+                                launch (1)                                         */
   int32_t disable_p2p;       /* moe_comm_init: do not map peer memory (0)          */
   int32_t nccl_alltoall;     /* moe_alltoall(FLAT): 1 = ncclAlltoAll, 0 = one group
                                 of ncclSend/ncclRecv pairs (0)                     */

@@ -69,7 +69,7 @@ const TuneField kTune[] = {
     {"MOE_P2P_LOCAL_PAD", &moe_tuning_t::p2p_local_pad, -1, -1, 1},
     {"MOE_A2A_CTAS_PER_SM", &moe_tuning_t::a2a_ctas_per_sm, 4, 1, 64},
     {"MOE_BARRIER_TIMEOUT_MS", &moe_tuning_t::barrier_timeout_ms, 60000, 0, 1 << 30},
-    {"MOE_BARRIER_PDL", &moe_tuning_t::barrier_pdl, 0, 0, 1},
+    {"MOE_BARRIER_PDL", &moe_tuning_t::barrier_pdl, 1, 0, 1},
     {"MOE_DISABLE_P2P", &moe_tuning_t::disable_p2p, 0, 0, 1},
     {"MOE_NCCL_ALLTOALL", &moe_tuning_t::nccl_alltoall, 0, 0, 1},
     {"MOE_NCCL_MAX_CTAS", &moe_tuning_t::nccl_max_ctas, 0, 0, 64},
