@@ -43,7 +43,8 @@ class A2AOp(ctypes.Structure):
 
 TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "layout_u",
                  "layout_pads_first", "reverse_ku", "reverse_tpw", "reverse_kspec",
-                 "reverse_backwards", "reverse_y_ef", "row_ctas_per_sm", "combine_bwd_kspec",
+                 "reverse_backwards", "reverse_y_ef", "row_ctas_per_sm", "reverse_ctas_per_sm",
+                 "combine_ctas_per_sm", "combine_bwd_kspec",
                  "gate_bwd_lanes", "p2p_dedupe", "p2p_local_pad", "a2a_ctas_per_sm",
                  "barrier_timeout_ms", "barrier_pdl", "disable_p2p", "nccl_alltoall", "nccl_max_ctas",
                  "nccl_min_ctas", "nccl_cta_policy")

@@ -504,7 +504,11 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
   }
   void* args[] = {&a};
-  cudaError_t e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
+  // CTAs per SM: the tuning's per-mode value (peer = the NVLink combine),
+  // else the row movers' setting, else the occupancy limit
+  const int cps = E_local != d.E ? tu.combine_ctas_per_sm : tu.reverse_ctas_per_sm;
+  const int grid = cps > 0 ? cps * device_sm_count() : row_grid(kern);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
   return MOE_OK;
 }

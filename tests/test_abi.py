@@ -248,3 +248,11 @@ def test_alltoallv_plan_in_c():
     recv_counts = [1, 2, 5, 0]          # from rank 0: (1, 2), from rank 1: (5, 0)
     sr, rr, ro = moe.alltoallv_plan(offsets, recv_counts, 2)
     assert sr == [3, 6] and rr == [3, 5] and ro == [0, 1, 3, 8, 8]
+
+
+def test_tuning_fields_match_the_header():
+    """The binding's moe_tuning_t mirror lists the header's fields in order."""
+    from paper_2203_14685_b200._lib import TUNING_FIELDS
+    src = open(HEADER).read()
+    body = src[src.index("typedef struct {\n  int32_t gate_tiles;"):src.index("} moe_tuning_t;")]
+    assert re.findall(r"int32_t\s+(\w+);", body) == list(TUNING_FIELDS)

@@ -84,6 +84,8 @@ def main():
                                        "combine_reads_only")}
         for tag, tu in (("u4", {"layout_u": 4}), ("u1", {"layout_u": 1}),
                         ("cta8", {"row_ctas_per_sm": 8}), ("cta3", {"row_ctas_per_sm": 3}),
+                        ("ccta6", {"combine_ctas_per_sm": 6}), ("ccta8", {"combine_ctas_per_sm": 8}),
+                        ("ccta12", {"combine_ctas_per_sm": 12}), ("ccta16", {"combine_ctas_per_sm": 16}),
                         ("ku2", {"reverse_ku": 2}), ("nodedupe", {"p2p_dedupe": 0}),
                         ("rev", {"reverse_backwards": 1})):
             runs.append(("@" + tag, tu, rows))
