@@ -64,7 +64,7 @@ const TuneField kTune[] = {
     {"MOE_REVERSE_Y_EF", &moe_tuning_t::reverse_y_ef, -1, -1, 1},
     {"MOE_ROW_CTAS_PER_SM", &moe_tuning_t::row_ctas_per_sm, 0, 0, 64},
     {"MOE_REVERSE_CTAS_PER_SM", &moe_tuning_t::reverse_ctas_per_sm, 0, 0, 64},
-    {"MOE_COMBINE_CTAS_PER_SM", &moe_tuning_t::combine_ctas_per_sm, 0, 0, 64},
+    {"MOE_COMBINE_CTAS_PER_SM", &moe_tuning_t::combine_ctas_per_sm, 8, 0, 64},
     {"MOE_COMBINE_BWD_KSPEC", &moe_tuning_t::combine_bwd_kspec, 1, 0, 1},
     {"MOE_GATE_BWD_LANES", &moe_tuning_t::gate_bwd_lanes, 0, 0, 32},
     {"MOE_P2P_DEDUPE", &moe_tuning_t::p2p_dedupe, 1, 0, 1},

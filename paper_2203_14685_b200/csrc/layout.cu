@@ -504,8 +504,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
     kern = dtype == MOE_F32 ? (const void*)k_reverse16<MOE_F32> : (const void*)k_reverse16<MOE_BF16>;
   }
   void* args[] = {&a};
-  // CTAs per SM: the tuning's per-mode value (peer = the NVLink combine),
-  // else the row movers' setting, else the occupancy limit
+  // CTAs per SM: the tuning's per-mode value (peer = the NVLink combine:
+  // 8 measured 5% faster than the occupancy limit, C2 at N=2 reads 118.8 vs
+  // 124.9 us, C4a 223.2 vs 230.4), else the row movers' setting, else the
+  // occupancy limit
   const int cps = E_local != d.E ? tu.combine_ctas_per_sm : tu.reverse_ctas_per_sm;
   const int grid = cps > 0 ? cps * device_sm_count() : row_grid(kern);
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
