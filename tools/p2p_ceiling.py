@@ -46,11 +46,10 @@ def main():
         recv = comm.symm_empty((P * B,), torch.uint8)
         remote = (P - 1) * B
         for cps in ((1, 2, 4, 8) if mb == 64 else (4, 8)):
-            os.environ["MOE_A2A_CTAS_PER_SM"] = str(cps)
-            us = timed(lambda: comm.alltoall(send, recv, "p2p"), comm)
+            with moe.tuned(a2a_ctas_per_sm=cps):
+                us = timed(lambda: comm.alltoall(send, recv, "p2p"), comm)
             out["a2a_p2p_%dM_cps%d" % (mb, cps)] = {"us": round(us, 1),
                                                    "GBs": round(remote / us / 1e3, 1)}
-        os.environ.pop("MOE_A2A_CTAS_PER_SM")
         if mb == 64:
             # back to back: is the fixed cost per copy, or per burst?
             us = timed(lambda: [comm.alltoall(send, recv, "p2p") for _ in range(10)], comm) / 10
@@ -90,21 +89,16 @@ def main():
     r = moe.Gate(S, E, k, cap)(lg)
     buf = comm.symm_empty((P, E // P, cap, d), torch.bfloat16)
     rb = E * cap * d * 2 * (P - 1) / P
-    for name, env in (("default", {}), ("tma0", {"MOE_P2P_LAYOUT_TMA": "0"})):
-        os.environ.update(env)
-        us = timed(lambda: comm.dispatch_p2p(x, r, buf), comm)
+    for name, tu in (("default", {}), ("nodedupe", {"p2p_dedupe": 0})):
+        with moe.tuned(**tu):
+            us = timed(lambda: comm.dispatch_p2p(x, r, buf), comm)
         out["dispatch_" + name] = {"us": round(us, 1), "GBs": round(rb / us / 1e3, 1)}
-        for kk in env:
-            os.environ.pop(kk)
     y = torch.empty_like(x)
-    for name, env in (("default", {}), ("rev", {"MOE_REVERSE_BACKWARDS": "1"}),
-                      ("ku2", {"MOE_REVERSE_KU": "2"}), ("tma", {"MOE_P2P_REVERSE_TMA": "1"}),
-                      ("v16", {"MOE_REVERSE_V16": "1"})):
-        os.environ.update(env)
-        us = timed(lambda: comm.combine_p2p(buf, r, y), comm)
+    for name, tu in (("default", {}), ("rev", {"reverse_backwards": 1}), ("ku2", {"reverse_ku": 2}),
+                     ("cta_occupancy", {"combine_ctas_per_sm": 0})):
+        with moe.tuned(**tu):
+            us = timed(lambda: comm.combine_p2p(buf, r, y), comm)
         out["combine_" + name] = {"us": round(us, 1), "GBs": round(rb / us / 1e3, 1)}
-        for kk in env:
-            os.environ.pop(kk)
     if rank == 0:
         print(json.dumps(out))
     torch.cuda.synchronize()
