@@ -714,6 +714,10 @@ typedef struct {
   int32_t nccl_min_ctas;     /* moe_comm_init: ncclConfig_t minCTAs; 0 = NCCL's    */
   int32_t nccl_cta_policy;   /* moe_comm_init: ncclConfig_t CTAPolicy (0 default, 1
                                 efficiency, 2 zero); -1 = NCCL's                   */
+  int32_t layout_tokens_per_warp; /* local layout: grid of ceil(S / (8 warps x this))
+                                CTAs (at least the persistent grid), which the
+                                block scheduler balances over the SMs; 0 = the
+                                persistent grid (row_ctas_per_sm) (2)              */
 } moe_tuning_t;
 
 /* host.  Copy of the current table (after the one-time environment read). */
@@ -729,7 +733,17 @@ moe_status_t moe_set_tuning(const moe_tuning_t* t);
  * n_tiles, n_chunks, CTAs; from word 4: per tile of the gate [claim,
  * aggregate published, prefix published, ready] at 4*tile, per 32-token
  * scatter chunk [claim, its tile seen ready] at 4*n_tiles + 2*chunk, per CTA
- * [start, end] after those; stamps beyond `bytes` are dropped.
+ * [start, end] after those; stamps beyond `bytes` are dropped.  The separate
+ * gate (moe_gate, select -> slots2) fills the same buffer with words 0..3 =
+ * n_tiles, 16, 0, 2 and, per tile, 16 words from 4 + 16*tile: k_gate_select
+ * [entry, after its grid-dependency wait, logits staged, selection done,
+ * in-tile ranks, tile aggregate, end] at 0..6, k_gate_slots2 [entry, after
+ * its wait, prefixes reduced, end] at 8..11 (select -> scan -> slots:
+ * k_gate_slots [entry, after its wait, end] at 8, 9, 11 and k_gate_scan's
+ * CTA b [entry, after its wait] at 12, 13 of tile b's words).  The row kernels of moe_layout / the one-sided
+ * dispatch and of moe_reverse_layout / the one-sided combine stamp [entry,
+ * after the grid-dependency wait, end] per CTA at word 4*cta of the buffer's
+ * second half (layout) and last quarter (reverse).
  * NULL (or 0 bytes) turns it off.  Affects launches made after it returns
  * (a captured graph keeps the buffer it was captured with). */
 moe_status_t moe_set_trace(void* buf, size_t bytes);

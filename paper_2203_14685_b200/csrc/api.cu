@@ -77,6 +77,7 @@ const TuneField kTune[] = {
     {"MOE_NCCL_MAX_CTAS", &moe_tuning_t::nccl_max_ctas, 0, 0, 64},
     {"MOE_NCCL_MIN_CTAS", &moe_tuning_t::nccl_min_ctas, 0, 0, 64},
     {"MOE_NCCL_CTA_POLICY", &moe_tuning_t::nccl_cta_policy, -1, -1, 2},
+    {"MOE_LAYOUT_TOKENS_PER_WARP", &moe_tuning_t::layout_tokens_per_warp, 2, 0, 1 << 20},
 };
 moe_tuning_t g_tune;
 std::once_flag g_tune_once;

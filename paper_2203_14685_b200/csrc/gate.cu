@@ -37,8 +37,10 @@ namespace moe {
 __global__ void __launch_bounds__(kGateThreads) k_gate_scan(GateArgs a) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kGateWarps + (threadIdx.x >> 5);
+  gate_trace(a, blockIdx.x, 12);
   pdl_wait();
   pdl_trigger();
+  gate_trace(a, blockIdx.x, 13);
   if (c >= a.ncols) return;
   unsigned* col = reinterpret_cast<unsigned*>(a.status) + (size_t)c * a.n_tiles;
   unsigned carry = 0;
@@ -85,8 +87,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
   const int t0 = tile * a.tile_tokens;
   const int nt = min(a.tile_tokens, a.S - t0);
   const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  gate_trace(a, tile, 8);
   pdl_wait();
   pdl_trigger();
+  gate_trace(a, tile, 9);
   const unsigned* pre = reinterpret_cast<const unsigned*>(a.status);
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const size_t gi = (size_t)t0 * a.k + i;
@@ -119,6 +123,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
     if (a.slot_src)
       for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
   }
+  if (a.trace) {
+    __syncthreads();
+    gate_trace(a, tile, 11);
+  }
 }
 
 // Two-kernel variant of scan + slots: every CTA reduces the column
@@ -133,8 +141,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
   const int t0 = tile * a.tile_tokens;
   const int nt = min(a.tile_tokens, a.S - t0);
   const bool slot_prio = a.prio == MOE_PRIO_SLOT;
+  gate_trace(a, tile, 8);
   pdl_wait();
   pdl_trigger();
+  gate_trace(a, tile, 9);
   const unsigned* agg = reinterpret_cast<const unsigned*>(a.status);
   for (int c = warp; c < a.ncols; c += kGateWarps) {
     const unsigned* col = agg + (size_t)c * a.n_tiles;
@@ -163,6 +173,7 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
     }
   }
   __syncthreads();
+  gate_trace(a, tile, 10);
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const size_t gi = (size_t)t0 * a.k + i;
     const int e = a.expert_idx[gi];
@@ -189,6 +200,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
     if (lane == 0) a.load[e] = ld;
     if (a.slot_src)
       for (int s = min(ld, a.cap) + lane; s < a.cap; s += 32) a.slot_src[(size_t)e * a.cap + s] = -1;
+  }
+  if (a.trace) {
+    __syncthreads();
+    gate_trace(a, tile, 11);
   }
 }
 
@@ -308,6 +323,8 @@ moe_status_t gate_launch(const moe_gate_desc_t& d, const moe_gate_inputs_t& in,
   const GatePlan p = gate_plan_default(d, ng);
   GateArgs a;
   fill_args(a, d, in, out, ws, p, ng);
+  a.trace = static_cast<unsigned long long*>(g_trace.buf);
+  a.trace_n = (long long)(g_trace.bytes / sizeof(unsigned long long));
   moe_status_t s = select_launch(d, p, a, stream);
   if (s != MOE_OK) return s;
   void* args[] = {&a};

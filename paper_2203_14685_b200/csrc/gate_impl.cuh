@@ -46,7 +46,32 @@ struct GateArgs {
   GateCtrl* ctrl;
   unsigned long long* status;  // [ncols][n_tiles] u32 tile aggregates, then prefixes
   int32_t* totals;             // [ncols] (SLOT priority)
+  // profiling (moe_set_trace, the separate select -> (scan ->) slots path):
+  // %globaltimer stamps per tile, NULL = off; see gate_trace
+  unsigned long long* trace;
+  long long trace_n;
 };
+
+// Gate trace layout: [0..3] = n_tiles, 16, 0, 2 (kind: separate gate); tile b's
+// stamps at 4 + 16 b + i: k_gate_select i = 0 entry, 1 after pdl_wait, 2 logits
+// staged, 3 selection done, 4 in-tile ranks, 5 tile aggregate, 6 end;
+// k_gate_slots2 i = 8 entry, 9 after pdl_wait, 10 prefixes reduced, 11 end;
+// select -> scan -> slots: k_gate_slots at 8, 9, 11 and k_gate_scan CTA b at
+// 12 (entry), 13 (after pdl_wait) of "tile" b.
+__device__ __forceinline__ void gate_trace(const GateArgs& a, int tile, int i) {
+  const long long w = 4 + 16LL * tile + i;
+  if (a.trace && threadIdx.x == 0 && w < a.trace_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[w] = t;
+    if (tile == 0 && i == 0) {
+      a.trace[0] = (unsigned long long)a.n_tiles;
+      a.trace[1] = 16;
+      a.trace[2] = 0;
+      a.trace[3] = 2;
+    }
+  }
+}
 
 
 
@@ -529,6 +554,7 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
           : "r"(mbar), "r"(parity)
           : "memory");
   }
+  gate_trace(a, tile, 2);
 
   // ---------------- Phase A: selection + weights
   if constexpr (KIND == KIND_HASH) {
@@ -571,6 +597,7 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
     }
   }
   __syncthreads();
+  gate_trace(a, tile, 3);
 
   // ---------------- Phase B1: ranks inside the tile, per warp
   const bool slot_prio = a.prio == MOE_PRIO_SLOT;
@@ -604,6 +631,7 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
     }
   }
   __syncthreads();
+  gate_trace(a, tile, 4);
 
   // ---------------- Phase B2: per-column warp prefix and tile aggregate
   unsigned* agg = reinterpret_cast<unsigned*>(a.status);  // [ncols][n_tiles]
@@ -621,6 +649,7 @@ __device__ __forceinline__ void gate_tile(const GateArgs& a, int* smem, unsigned
       agg[(size_t)c * a.n_tiles + tile] = run;
   }
   __syncthreads();
+  gate_trace(a, tile, 5);
 }
 
 template <int KIND, int L, int K>
@@ -628,8 +657,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
   extern __shared__ __align__(16) int smem[];
   __shared__ unsigned s_bad;
   __shared__ __align__(8) unsigned long long s_mbar;
+  gate_trace(a, blockIdx.x, 0);
   pdl_wait();     // the producer of the logits / the previous step must be done
   pdl_trigger();  // k_gate_scan may launch now; it waits for our completion
+  gate_trace(a, blockIdx.x, 1);
   gate_tile<KIND, L, K>(a, smem, s_bad, s_mbar, blockIdx.x, 0, nullptr, true);
   const int tid = threadIdx.x;
   const int items = a.tile_tokens * a.k;
@@ -655,6 +686,10 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_select(GateArgs a) {
     a.slot_idx[gi] = s_hist[(pos / per) * a.ncols + col] + s_rank[i];
   }
   if (KIND == KIND_HASH && tid == 0 && s_bad) atomicAdd(&a.ctrl->bad, s_bad);
+  if (a.trace) {
+    __syncthreads();
+    gate_trace(a, tile, 6);
+  }
 }
 
 // ------------------------------------------------------------ kernel pickers

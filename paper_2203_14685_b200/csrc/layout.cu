@@ -25,8 +25,10 @@ template <int VB, int U>
 __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
   using V = Vec<VB>;
   __shared__ int s_beg[257];
+  row_trace(a, 0);
   pdl_wait();     // routing comes from moe_gate
   pdl_trigger();
+  row_trace(a, 1);
   pad_prefix(a, s_beg);
   const int lane = threadIdx.x & 31;
   const long long npad = s_beg[a.E];
@@ -74,6 +76,7 @@ __global__ void __launch_bounds__(kRowThreads) k_layout(RowArgs a) {
     }
   }
   if (a.sys_fence) __threadfence_system();
+  row_trace_end(a);
 }
 
 // ------------------------------------------------------------ Reverse + combine
@@ -84,8 +87,10 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
   constexpr int SEG = 32 * U * VB;
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * kRowWarps;
+  row_trace(a, 0);
   pdl_wait();     // expert outputs come from the AllToAll / the layout
   pdl_trigger();
+  row_trace(a, 1);
   for (int tl = blockIdx.x * kRowWarps + (threadIdx.x >> 5); tl < a.S; tl += wstride) {
     const int t = a.rev ? a.S - 1 - tl : tl;  // rev: last tokens first (L2 reuse)
     char* yrow = a.dst + (size_t)t * a.row_bytes;
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse(RowArgs a) {
       }
     }
   }
+  row_trace_end(a);
 }
 
 // k <= 2 specialisation: every load of a U-vector segment of the KK rows of
@@ -160,8 +166,10 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   constexpr int SEG = 32 * U * VB;
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * kRowWarps * TPW;
+  row_trace(a, 0);
   pdl_wait();
   pdl_trigger();
+  row_trace(a, 1);
   for (int tb = (blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * TPW; tb < a.S; tb += wstride) {
     const char* b[TPW][KK];
     float w[TPW][KK];
@@ -227,6 +235,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
       }
     }
   }
+  row_trace_end(a);
 }
 
 // 16-byte fallback of the combine for rows that are not a multiple of 32 B.
@@ -235,8 +244,10 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * kRowWarps;
   constexpr int NA = DT == MOE_F32 ? 4 : 8;
+  row_trace(a, 0);
   pdl_wait();
   pdl_trigger();
+  row_trace(a, 1);
   for (int tl = blockIdx.x * kRowWarps + (threadIdx.x >> 5); tl < a.S; tl += wstride) {
     const int t = a.rev ? a.S - 1 - tl : tl;
     char* yrow = a.dst + (size_t)t * a.row_bytes;
@@ -272,6 +283,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse16(RowArgs a) {
       st_v4(yrow + off, o);
     }
   }
+  row_trace_end(a);
 }
 
 // ------------------------------------------------------------ expert stand-in
@@ -371,12 +383,22 @@ moe_status_t expert_offsets_launch(const int32_t* load, int E, int cap, int32_t*
 
 // ------------------------------------------------------------ host side
 
+// moe_set_trace: the row kernels' per-CTA stamps go to the trace buffer's
+// second half (layout, dispatch) and last quarter (reverse, combine)
+static void row_trace_set(RowArgs& a, bool reverse) {
+  if (!g_trace.buf) return;
+  const long long n = (long long)(g_trace.bytes / sizeof(unsigned long long));
+  a.trace = static_cast<unsigned long long*>(g_trace.buf) + (reverse ? 3 * n / 4 : n / 2);
+  a.trace_n = n / 4;
+}
+
 moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r, const void* x,
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets,
                                  const int32_t* peer_base, const PeerPtrs* pad_tab,
                                  const PeerPtrs* dup_tab) {
   RowArgs a{};
+  row_trace_set(a, false);
   if (dup_tab && !offsets) {
     a.dedupe = 1;
     a.dup = *dup_tab;
@@ -418,8 +440,21 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   } else {
     kern = (const void*)k_layout<16, 4>;
   }
+  // Local layout: a grid of ~2 tokens per warp, not the persistent one.  The
+  // persistent grid's CTAs end up to 15 us apart at C2 (moe_set_trace: some
+  // SMs get less of the write bandwidth), an idle tail the block scheduler
+  // removes when it hands out small CTAs as SMs free up (measured: C2 layout
+  // 37.0 -> 34.9 us, C3 44.6 -> 43.0, C4a 70.4 -> 66.1, C4b 52.1 -> 50.0;
+  // the reverse, whose reversed walk reuses L2, measured slower that way and
+  // stays persistent).  The one-sided dispatch (stores to peers, a system
+  // fence per CTA) keeps the persistent grid.
+  int grid = row_grid(kern);
+  if (tu.layout_tokens_per_warp > 0 && !a.sys_fence) {
+    const long long per_cta = (long long)kRowWarps * tu.layout_tokens_per_warp;
+    grid = (int)std::max<long long>(grid, (d.S + per_cta - 1) / per_cta);
+  }
   void* args[] = {&a};
-  cudaError_t e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout launch");
   return MOE_OK;
 }
@@ -438,6 +473,7 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
                                   const int32_t* offsets, const int32_t* peer_base,
                                   int dup_alias) {
   RowArgs a{};
+  row_trace_set(a, true);
   a.dedupe = dup_alias;  // reverse: read deduped slots from their first row (src_row_item)
   a.offsets = offsets;
   a.peer_base = peer_base;

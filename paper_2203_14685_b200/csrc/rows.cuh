@@ -58,7 +58,27 @@ struct RowArgs {
   // src_row_item.
   int dedupe;
   PeerPtrs dup;
+  // profiling (moe_set_trace): per CTA [entry, after the grid-dependency
+  // wait, end] %globaltimer stamps at trace[4 * blockIdx.x + i], NULL = off
+  unsigned long long* trace;
+  long long trace_n;
 };
+
+__device__ __forceinline__ void row_trace(const RowArgs& a, int i) {
+  const long long w = 4LL * blockIdx.x + i;
+  if (a.trace && threadIdx.x == 0 && w < a.trace_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[w] = t;
+  }
+}
+// the CTA's end stamp: after every warp of it is done
+__device__ __forceinline__ void row_trace_end(const RowArgs& a) {
+  if (a.trace) {
+    __syncthreads();
+    row_trace(a, 2);
+  }
+}
 
 __device__ __forceinline__ size_t row_index(const RowArgs& a, int q, int e, int s) {
   if (a.offsets) {

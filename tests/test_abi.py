@@ -232,7 +232,8 @@ def test_tuning_table_roundtrip_and_validation():
         assert t["gate_tiles"] == 17 and t["reverse_ku"] == 2
     assert moe.get_tuning() == before
     for bad in ({"layout_u": 3}, {"reverse_ku": 1}, {"gate_bwd_lanes": 6},
-                {"barrier_timeout_ms": -1}, {"nccl_cta_policy": 7}):
+                {"barrier_timeout_ms": -1}, {"nccl_cta_policy": 7},
+                {"layout_tokens_per_warp": -1}):
         with pytest.raises(moe.MoeError) as ei:
             moe.set_tuning(**bad)
         assert ei.value.status == INVALID

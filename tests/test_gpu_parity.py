@@ -104,7 +104,9 @@ ROW_PATHS = {"default": {}, "layout_u4_rev_ku4": {"layout_u": 4, "reverse_ku": 4
              "forward_order": {"reverse_backwards": 0, "reverse_y_ef": 0},
              "reverse_generic_fwd": {"reverse_kspec": 0, "reverse_backwards": 0},
              "pads_first": {"layout_pads_first": 1}, "pads_last": {"layout_pads_first": 0},
-             "one_cta_per_sm": {"row_ctas_per_sm": 1}}
+             "one_cta_per_sm": {"row_ctas_per_sm": 1},
+             "layout_persistent": {"layout_tokens_per_warp": 0},
+             "layout_one_token_per_warp": {"layout_tokens_per_warp": 1}}
 
 
 @pytest.mark.parametrize("path", sorted(GATE_PATHS))
