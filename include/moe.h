@@ -740,7 +740,8 @@ moe_status_t moe_set_tuning(const moe_tuning_t* t);
  * in-tile ranks, tile aggregate, end] at 0..6, k_gate_slots2 [entry, after
  * its wait, prefixes reduced, end] at 8..11 (select -> scan -> slots:
  * k_gate_slots [entry, after its wait, end] at 8, 9, 11 and k_gate_scan's
- * CTA b [entry, after its wait] at 12, 13 of tile b's words).  The row kernels of moe_layout / the one-sided
+ * CTA b [entry, after its wait, its warp 0 done] at 12..14 of tile b's
+ * words).  The row kernels of moe_layout / the one-sided
  * dispatch and of moe_reverse_layout / the one-sided combine stamp [entry,
  * after the grid-dependency wait, end] per CTA at word 4*cta of the buffer's
  * second half (layout) and last quarter (reverse).

@@ -32,8 +32,12 @@
 namespace moe {
 
 // Exclusive scan of every column's tile aggregates (in place), warp per
-// column, 8 consecutive tiles per lane per round; totals[c] = column total.
-// TOKEN priority: the column is the expert, so load[e] = totals[e].
+// column, 8 consecutive tiles per lane per round of 256; the loads of up to
+// kScanRounds rounds are issued before the first is scanned (one L2 round
+// trip for <= 1024 tiles instead of one per round: C4a's 512 tiles).
+// totals[c] = column total.  TOKEN priority: the column is the expert, so
+// load[e] = totals[e].
+constexpr int kScanRounds = 4;
 __global__ void __launch_bounds__(kGateThreads) k_gate_scan(GateArgs a) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kGateWarps + (threadIdx.x >> 5);
@@ -44,37 +48,46 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_scan(GateArgs a) {
   if (c >= a.ncols) return;
   unsigned* col = reinterpret_cast<unsigned*>(a.status) + (size_t)c * a.n_tiles;
   unsigned carry = 0;
-  for (int base = 0; base < a.n_tiles; base += 256) {
-    unsigned v[8], run = 0;
+  for (int blk = 0; blk < a.n_tiles; blk += 256 * kScanRounds) {
+    unsigned v[kScanRounds][8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + lane * 8 + u;
-      v[u] = i < a.n_tiles ? col[i] : 0u;
-    }
+    for (int r = 0; r < kScanRounds; ++r)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const unsigned x = v[u];
-      v[u] = run;
-      run += x;
-    }
-    unsigned incl = run;
+      for (int u = 0; u < 8; ++u) {
+        const int i = blk + r * 256 + lane * 8 + u;
+        v[r][u] = i < a.n_tiles ? __ldcg(col + i) : 0u;
+      }
 #pragma unroll
-    for (int m = 1; m < 32; m <<= 1) {
-      const unsigned o = __shfl_up_sync(0xffffffffu, incl, m);
-      if (lane >= m) incl += o;
-    }
-    const unsigned lane_excl = carry + incl - run;
+    for (int r = 0; r < kScanRounds; ++r) {
+      const int base = blk + r * 256;
+      if (base >= a.n_tiles) break;
+      unsigned run = 0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + lane * 8 + u;
-      if (i < a.n_tiles) col[i] = lane_excl + v[u];
+      for (int u = 0; u < 8; ++u) {
+        const unsigned x = v[r][u];
+        v[r][u] = run;
+        run += x;
+      }
+      unsigned incl = run;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += o;
+      }
+      const unsigned lane_excl = carry + incl - run;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + lane * 8 + u;
+        if (i < a.n_tiles) col[i] = lane_excl + v[r][u];
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
   if (lane == 0) {
     a.totals[c] = (int)carry;
     if (a.prio != MOE_PRIO_SLOT) a.load[c] = (int)carry;
   }
+  gate_trace(a, blockIdx.x, 14);  // warp 0's end
 }
 
 // Final slots: slot = (SLOT priority: items of earlier j of this expert) +

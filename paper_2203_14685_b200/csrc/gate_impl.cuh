@@ -57,7 +57,7 @@ struct GateArgs {
 // staged, 3 selection done, 4 in-tile ranks, 5 tile aggregate, 6 end;
 // k_gate_slots2 i = 8 entry, 9 after pdl_wait, 10 prefixes reduced, 11 end;
 // select -> scan -> slots: k_gate_slots at 8, 9, 11 and k_gate_scan CTA b at
-// 12 (entry), 13 (after pdl_wait) of "tile" b.
+// 12 (entry), 13 (after pdl_wait), 14 (its warp 0 done) of "tile" b.
 __device__ __forceinline__ void gate_trace(const GateArgs& a, int tile, int i) {
   const long long w = 4 + 16LL * tile + i;
   if (a.trace && threadIdx.x == 0 && w < a.trace_n) {
@@ -264,9 +264,15 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, const float*
     bv[p] = -INFINITY;
     bi[p] = INT_MAX;
   }
+  // the lane's experts are consecutive: its prototype pe = e / n is stepped
+  // at prototype boundaries instead of divided per logit
+  int pe = (l * epl) / n, next = (pe + 1) * n;
   if (valid)
     for_lane_logits(row, l, epl, vec4, [&](float x, int e) {
-      const int pe = e / n;
+      if (e == next) {
+        ++pe;
+        next += n;
+      }
 #pragma unroll
       for (int p = 0; p < K; ++p)
         if (p == pe && beats(x, e, bv[p], bi[p])) {
@@ -293,12 +299,16 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, const float*
     double part[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) part[p] = 0.0;
+    int qe = (l * epl) / n, qnext = (qe + 1) * n;
     if (valid)
       for_lane_logits(row, l, epl, vec4, [&](float x, int e) {
-        const int pe = e / n;
+        if (e == qnext) {
+          ++qe;
+          qnext += n;
+        }
 #pragma unroll
         for (int p = 0; p < K; ++p)
-          if (p == pe) part[p] += exp((double)x - (double)bv[p]);
+          if (p == qe) part[p] += exp((double)x - (double)bv[p]);
       });
 #pragma unroll
     for (int p = 0; p < K; ++p) den[p] = group_sum<L>(part[p]);

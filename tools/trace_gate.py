@@ -95,6 +95,7 @@ def main():
             sc = t[t[:, 12] > 0]
             r["scan_entry_us"] = pct(us(sc[:, 12]))
             r["scan_waited_us"] = pct(us(sc[:, 13]))
+            r["scan_end_us"] = pct(us(sc[:, 14]))
         r["select_end_to_slots_waited_us"] = round(float((t[:, 9].min() - t[:, 6].max()) / 1e3), 2)
         r["gate_us"] = round(float(us(t[:, 11].max())), 2)
         n = raw.size
