@@ -447,7 +447,8 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   // 37.0 -> 34.9 us, C3 44.6 -> 43.0, C4a 70.4 -> 66.1, C4b 52.1 -> 50.0;
   // the reverse, whose reversed walk reuses L2, measured slower that way and
   // stays persistent).  The one-sided dispatch (stores to peers, a system
-  // fence per CTA) keeps the persistent grid.
+  // fence per CTA) keeps the persistent grid: measured slower on 2 GPUs with
+  // the small-CTA grid (C2 step 249.3 -> 257.0 us; 1 token per warp 271.4).
   int grid = row_grid(kern);
   if (tu.layout_tokens_per_warp > 0 && !a.sys_fence) {
     const long long per_cta = (long long)kRowWarps * tu.layout_tokens_per_warp;
