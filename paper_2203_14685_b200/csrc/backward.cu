@@ -302,6 +302,8 @@ moe_status_t combine_bwd_launch(const moe_gate_desc_t& d, const moe_routing_t& r
   else
     kern = f ? (const void*)k_combine_bwd16<MOE_F32> : (const void*)k_combine_bwd16<MOE_BF16>;
   void* args[] = {&a, &d_weight};
+  // persistent grid: the layout's small-CTA grid (scatter_grid) measured
+  // slower here (C2 backward 97.5 -> 101.0 us, C4a 175.8 -> 183.6)
   cudaError_t e = launch_pdl(kern, dim3(row_grid(kern)), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout_backward: launch");
   return MOE_OK;

@@ -449,11 +449,7 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   // stays persistent).  The one-sided dispatch (stores to peers, a system
   // fence per CTA) keeps the persistent grid: measured slower on 2 GPUs with
   // the small-CTA grid (C2 step 249.3 -> 257.0 us; 1 token per warp 271.4).
-  int grid = row_grid(kern);
-  if (tu.layout_tokens_per_warp > 0 && !a.sys_fence) {
-    const long long per_cta = (long long)kRowWarps * tu.layout_tokens_per_warp;
-    grid = (int)std::max<long long>(grid, (d.S + per_cta - 1) / per_cta);
-  }
+  const int grid = scatter_grid(kern, d.S, a.sys_fence);
   void* args[] = {&a};
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_layout: k_layout launch");

@@ -260,4 +260,17 @@ inline int row_grid(const void* kern) {
   return std::max(1, per_sm) * device_sm_count();
 }
 
+// Grid of the local layout: ~layout_tokens_per_warp tokens per warp, at
+// least the persistent grid, so the block scheduler balances the tail over
+// the SMs (DESIGN.md §6 k_layout); stores to peers keep the persistent grid.
+inline int scatter_grid(const void* kern, long long S, bool peer) {
+  int grid = row_grid(kern);
+  const int tpw = tuning().layout_tokens_per_warp;
+  if (tpw > 0 && !peer) {
+    const long long per_cta = (long long)kRowWarps * tpw;
+    grid = (int)std::max<long long>(grid, (S + per_cta - 1) / per_cta);
+  }
+  return grid;
+}
+
 }  // namespace moe
