@@ -65,7 +65,10 @@ def parse():
     ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--fuse", default="auto", choices=["auto", "on", "off"],
                     help="gate + layout (+ NVLink dispatch) as one kernel: auto = the "
-                         "RoutePipeline default (on for the one-sided path at N > 1)")
+                         "RoutePipeline default (off: the separate pair measured as fast)")
+    ap.add_argument("--single-buffer", action="store_true",
+                    help="one-sided path: one receive buffer (combine keeps its exit barrier) "
+                         "instead of the default two used in turn")
     ap.add_argument("--dropless", action="store_true",
                     help="NEXT-4: packed dropless layout (capacity = S*k), device-side exchange")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -300,7 +303,8 @@ def main():
     try:
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
                                  group_size=G, device=dev, dropless=a.dropless,
-                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse])
+                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse],
+                                 double_buffer=not a.single_buffer)
     except moe.MoeError as err:
         if algo != "p2p":
             raise
@@ -308,7 +312,8 @@ def main():
         algo = "flat"
         pipe = moe.RoutePipeline(S, w.d, w.E, w.k, cap, dt, w.kind, comm=comm, algo=algo,
                                  group_size=G, device=dev,
-                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse])
+                                 fuse_gate_layout={"auto": None, "on": True, "off": False}[a.fuse],
+                                 double_buffer=not a.single_buffer)
 
     lg, ids, table, x = synthgen.workload_inputs(w, rank)
 
@@ -636,7 +641,8 @@ def main():
             load = pipe.routing.load.view(P, El)
             padrows = cap - load.clamp(max=cap)
             pads = int(padrows.sum().item() - padrows[rank].sum().item())
-        p2p_flags = {"dedupe": bool(dedupe), "local_pad": bool(local_pad)}
+        p2p_flags = {"dedupe": bool(dedupe), "local_pad": bool(local_pad),
+                     "double_buffer": pipe.double_buffered}
         ab["a2a_buffer"] = ab["a2a"]
         ab["a2a_dispatch"] = ((pairs if dedupe else remote_slots) + pads) * row
         ab["a2a_combine"] = remote_slots * row
@@ -704,6 +710,7 @@ def main():
         else:
             bw = {s_: ab["a2a"] / (stage_ms[s_] / 1e3) / 1e9 for s_ in ("a2a_dispatch", "a2a_combine")}
         a2a = {"bytes_out_per_rank": ab["a2a"], "busbw_gbs": bw, "peak_gbs": NVLINK_GBS,
+               "p2p": p2p_flags if algo == "p2p" else None,
                "algo": algo, "group_size": G if algo in ("hier", "hier2d") else None}
         if "a2a_buffer" in ab:
             a2a["buffer_bytes_per_rank"] = ab["a2a_buffer"]
@@ -751,8 +758,9 @@ def main():
     # our kernels per step: gate (k_gate_select, k_gate_scan, k_gate_slots),
     # layout, reverse; on hierarchical leaders one chunk permute per AllToAll,
     # with the two-level form two transposes per AllToAll on every rank; on
-    # the one-sided path three barriers (dispatch exit, combine entry and
-    # exit), the owners' duplicate-row copies (dedupe) and padding fill
+    # the one-sided path the barriers (dispatch exit, combine entry, and the
+    # combine's exit unless the pipeline alternates two receive buffers), the
+    # owners' duplicate-row copies (dedupe) and padding fill
     import ctypes
     from paper_2203_14685_b200._lib import lib as _moelib
     gate_k = _moelib().moe_gate_kernel_count(ctypes.byref(pipe.routing.desc()), 1)
@@ -767,7 +775,8 @@ def main():
         elif P > 1 and algo == "hier2d":
             launches_per_step += 4
         elif P > 1 and algo == "p2p":
-            launches_per_step += 3 + int(p2p_flags["dedupe"]) + int(p2p_flags["local_pad"])
+            launches_per_step += (2 + (0 if pipe.double_buffered else 1) +
+                                  int(p2p_flags["dedupe"]) + int(p2p_flags["local_pad"]))
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,

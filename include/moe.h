@@ -448,7 +448,15 @@ moe_status_t moe_comm_barrier(moe_comm_t* comm, moe_stream_t stream);
  * store landed (dispatch) / every read finished (combine).  A caller that
  * orders its steps itself (e.g. moe_comm_barrier after its expert) may skip
  * redundant ones, e.g. dispatch(NO_ENTRY) after a combine with its exit
- * barrier.  Exception: a combine of a buffer whose last moe_dispatch_p2p
+ * barrier.  The tables the senders write into an owner during a dispatch
+ * (padding counts, duplicate rows) belong to its receive buffer (allocated
+ * collectively on the first dispatch into that buffer outside stream capture;
+ * released with it), so a caller that ALTERNATES two receive buffers A, B --
+ * dispatch(A) combine(A) dispatch(B) combine(B) dispatch(A) ... on every
+ * rank -- may give every combine NO_EXIT_BARRIER and every dispatch after the
+ * first into its buffer NO_ENTRY_BARRIER: a rank that dispatches into A again
+ * has passed the exit barrier of the dispatch into B, which no rank reaches
+ * before its combine of A has finished reading.  Exception: a combine of a buffer whose last moe_dispatch_p2p
  * sent some token rows once for two slots (k >= 2, two experts of the token
  * on one remote owner, tuning p2p_dedupe) keeps its entry barrier under
  * NO_ENTRY_BARRIER, because the owners' duplicate-row copies run after the

@@ -238,7 +238,7 @@ moe_status_t moe_comm_destroy(moe_comm_t* comm) {
   release_regs(comm);
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
-  if (comm->dup.base) symm_release(comm, comm->dup);
+  for (RecvTables& t : comm->tables) symm_release(comm, t.buf);
   moe_status_t s = nccl_status(ncclCommDestroy(comm->nccl), "moe_comm_destroy");
   delete comm;
   return s;
@@ -285,7 +285,7 @@ moe_status_t moe_comm_abort(moe_comm_t* comm) {
   comm->regs.clear();
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
-  if (comm->dup.base) symm_release(comm, comm->dup);
+  for (RecvTables& t : comm->tables) symm_release(comm, t.buf);
   delete comm;
   return s;
 }

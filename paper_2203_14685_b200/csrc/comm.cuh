@@ -12,14 +12,16 @@
 namespace moe {
 
 constexpr int kMaxRanks = 32;
-// The comm's signal buffer: barrier words at offset 0, then the padding-count
-// table of the padded one-sided dispatch: [kMaxRanks source ranks][256 local
-// experts] int32 (admitted rows per (source, local expert)).
-constexpr size_t kPadTabOff = 4096;
-constexpr int kPadTabStride = 256;
-// device error word of this rank (a barrier that timed out sets it)
+// The comm's signal buffer: barrier words at offset 0, the device error word
+// of this rank (a barrier that timed out sets it) at kErrOff.
 constexpr size_t kErrOff = 2048;
-constexpr size_t kSigBytes = kPadTabOff + sizeof(int) * kMaxRanks * kPadTabStride;
+constexpr size_t kSigBytes = 4096;
+// Side tables of a receive buffer of the padded one-sided dispatch
+// (RecvTables): the padding-count table [kMaxRanks source ranks][256 local
+// experts] int32 (admitted rows per (source, local expert)), then the
+// duplicate-row table (int32 per recv row).
+constexpr int kPadTabStride = 256;
+constexpr size_t kPadTabBytes = sizeof(int) * kMaxRanks * kPadTabStride;
 enum { kErrBarrierTimeout = 1 };
 
 // P pointers to the same symmetric buffer as mapped on every rank
@@ -32,6 +34,16 @@ struct SymmBuf {
   char* base;
   size_t bytes;
   PeerPtrs peer;
+};
+
+// The side tables the senders of a padded one-sided dispatch write into an
+// owner and the owner reads after the exit barrier (padding counts, duplicate
+// rows), one set PER RECEIVE BUFFER: a caller that alternates two receive
+// buffers may then drop the combine's exit barrier (moe.h, MOE_P2P_*).
+struct RecvTables {
+  const void* recv;   // this rank's receive buffer they belong to
+  SymmBuf buf;        // [kPadTabBytes padding counts][dup_rows int32]
+  size_t dup_rows;    // capacity of the duplicate-row table
 };
 
 // One step of a rank's program on a SIMULATED communicator (moe_sim_*):
@@ -63,7 +75,7 @@ struct moe_comm {
   int nranks, rank, device;
   std::vector<moe::SymmBuf> symm;  // live symmetric buffers
   moe::SymmBuf sig;                // barrier signals: [kMaxRanks] flags + local epoch
-  moe::SymmBuf dup{};              // one-sided dispatch: duplicate-row table (int32 per recv row)
+  std::vector<moe::RecvTables> tables;  // one-sided dispatch: side tables per receive buffer
   const void* dup_recv = nullptr;  // recv of the last dispatch whose owners fill duplicate rows
                                    // after its exit barrier (the combine must not skip its entry one)
   bool p2p_ok;                     // peer mappings could be made (NVLink / P2P)

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256) k_pad_fill(char* recv, const int* tab, in
   }
 }
 
-// tab: this rank's padding-count table (sig + kPadTabOff)
+// tab: this rank's padding-count table (RecvTables of recv)
 static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, int cap,
                                     int row_bytes, cudaStream_t stream) {
   const int nrows_pad_max = P * El * cap;
@@ -372,35 +372,51 @@ moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_byt
   return MOE_OK;
 }
 
-// The duplicate-row table for a padded one-sided dispatch of E*cap recv
-// rows: used when k >= 2, two experts can share an owner (E/P >= 2) and the
-// exit barrier runs.  Allocated (collectively: every rank makes the same call)
-// on first use outside stream capture; inside a capture without a table the
-// dispatch just sends every row (same result).  Returns false: no dedupe.
-static bool dup_table(moe_comm* c, const moe_gate_desc_t& d, int32_t flags, cudaStream_t stream,
-                      PeerPtrs* out, moe_status_t* st) {
+// The side tables of receive buffer `recv` (this rank's pointer), with room
+// for a duplicate-row table of `dup_rows` rows (0: padding counts only).
+// Allocated (collectively: every rank makes the same call) on first use
+// outside stream capture, grown the same way; inside a capture without a
+// large enough set: nullptr, and the dispatch sends every row, padding
+// included (same result).
+static RecvTables* recv_tables(moe_comm* c, const void* recv, size_t dup_rows, cudaStream_t stream,
+                               moe_status_t* st) {
   *st = MOE_OK;
-  const int P = c->nranks;
-  if (P < 2 || d.k < 2 || d.E / P < 2 || (flags & MOE_P2P_NO_EXIT_BARRIER) || !tuning().p2p_dedupe)
-    return false;
-  const size_t want = (size_t)d.E * d.capacity * sizeof(int);
-  if (!(c->dup.base && c->dup.bytes >= want)) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-      return false;
-    if (c->dup.base) {  // grow: collectively, after every rank is done with the old table
-      *st = symm_release_coll(c, c->dup);
-      c->dup = SymmBuf{};
-      if (*st != MOE_OK) return false;
-    }
-    *st = symm_alloc(c, want, &c->dup);
-    if (*st != MOE_OK) {
-      c->dup = SymmBuf{};
-      return false;
+  RecvTables* t = nullptr;
+  for (RecvTables& u : c->tables)
+    if (u.recv == recv) t = &u;
+  if (t && t->dup_rows >= dup_rows) return t;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  if (t) {  // grow: collectively, after every rank is done with the old set
+    *st = symm_release_coll(c, t->buf);
+    c->tables.erase(c->tables.begin() + (t - c->tables.data()));
+    if (*st != MOE_OK) return nullptr;
+  }
+  RecvTables n{};
+  n.recv = recv;
+  n.dup_rows = dup_rows;
+  *st = symm_alloc(c, kPadTabBytes + dup_rows * sizeof(int), &n.buf);  // zero-filled
+  if (*st != MOE_OK) return nullptr;
+  c->tables.push_back(n);
+  return &c->tables.back();
+}
+
+// Collective: release the side tables of every receive buffer inside
+// [base, base + bytes) (before that buffer is freed).
+static moe_status_t release_tables_in(moe_comm* c, const char* base, size_t bytes) {
+  moe_status_t s = MOE_OK;
+  for (size_t i = 0; i < c->tables.size();) {
+    const char* q = static_cast<const char*>(c->tables[i].recv);
+    if (q >= base && q < base + bytes) {
+      moe_status_t s2 = symm_release_coll(c, c->tables[i].buf);
+      if (s == MOE_OK) s = s2;
+      c->tables.erase(c->tables.begin() + i);
+    } else {
+      ++i;
     }
   }
-  *out = c->dup.peer;
-  return true;
+  return s;
 }
 
 // ------------------------------------------------------------ dropless exchange
@@ -532,12 +548,6 @@ static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate
   return symm_peers(fn, comm, buf, (size_t)rows * d * *ds, peers);
 }
 
-static PeerPtrs pad_tables(const moe_comm* c) {
-  PeerPtrs tab{};
-  for (int q = 0; q < c->nranks; ++q) tab.p[q] = c->sig.peer.p[q] + kPadTabOff;
-  return tab;
-}
-
 // Padded one-sided dispatch after the entry barrier (shared by the dispatch,
 // the fused gate + dispatch and the push-form combine adjoint's dy scatter):
 // rows into the owners' `dst` by `rows` (k_layout in peer mode, or the fused
@@ -557,12 +567,25 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int 
   // (E*cap > 1.05*S*k, e.g. the hash config's C = 1.25: C4b dispatch 165 ->
   // 132 us at N=2); with C = 1 the padding is only the imbalance and the
   // extra kernel costs more than it saves (C2: +1.7 us).
-  const bool local_pad = exit_bar && El <= kPadTabStride && local_pad_on(D);
-  const PeerPtrs tab = pad_tables(comm);
-  PeerPtrs dup{};
-  moe_status_t s;
-  const bool dedupe = dup_table(comm, D, flags, stream, &dup, &s);
-  if (s != MOE_OK) return s;
+  bool local_pad = exit_bar && El <= kPadTabStride && local_pad_on(D);
+  // dedupe: k >= 2 and two experts can share an owner; the owners' copies
+  // need the exit barrier
+  bool dedupe = exit_bar && P >= 2 && D.k >= 2 && El >= 2 && tuning().p2p_dedupe;
+  PeerPtrs tab{}, dup{};
+  moe_status_t s = MOE_OK;
+  if (local_pad || dedupe) {
+    const RecvTables* t =
+        recv_tables(comm, dst.p[r], dedupe ? (size_t)D.E * D.capacity : 0, stream, &s);
+    if (s != MOE_OK) return s;
+    if (!t) {
+      local_pad = dedupe = false;
+    } else {
+      for (int q = 0; q < P; ++q) {
+        tab.p[q] = t->buf.peer.p[q];
+        dup.p[q] = t->buf.peer.p[q] + kPadTabBytes;
+      }
+    }
+  }
   s = run_or_queue(comm, stream, [=](cudaStream_t st) {
     return rows(st, local_pad ? &tab : nullptr, dedupe ? &dup : nullptr);
   });
@@ -625,9 +648,11 @@ moe_status_t moe_comm_symm_free(moe_comm_t* comm, void* p) {
   }
   for (size_t i = 0; i < comm->symm.size(); ++i) {
     if (comm->symm[i].base == p) {
-      moe_status_t s = symm_release_coll(comm, comm->symm[i]);
+      // the side tables of receive buffers inside it go first (collective)
+      moe_status_t s = release_tables_in(comm, comm->symm[i].base, comm->symm[i].bytes);
+      moe_status_t s2 = symm_release_coll(comm, comm->symm[i]);
       comm->symm.erase(comm->symm.begin() + i);
-      return s;
+      return s != MOE_OK ? s : s2;
     }
   }
   set_error("moe_comm_symm_free: %p is not a symmetric buffer of this communicator", p);

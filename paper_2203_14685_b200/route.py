@@ -23,7 +23,7 @@ class RoutePipeline:
                  comm: Optional[Comm] = None, algo: str = "flat", group_size: int = 1,
                  device=None, slot_src: bool = True, dropless: bool = False,
                  fuse_gate_layout: Optional[bool] = None, identity_alias: bool = False,
-                 nvtx: bool = False):
+                 nvtx: bool = False, double_buffer: bool = True, bwd_push: bool = True):
         """dropless=True (NEXT-4): capacity is ignored (cap = S*k, nothing is
         dropped) and the packed layout is used -- locally moe_layout_packed /
         moe_reverse_layout_packed, across ranks the device-side NVLink
@@ -40,12 +40,20 @@ class RoutePipeline:
         barrier and one read of a row sent once for two slots.  A measurement
         of the routing alone; a real expert always takes the default path.
         nvtx=True: every stage of step() is an NVTX range ("moe/gate",
-        "moe/layout", ...) for Nsight timelines."""
+        "moe/layout", ...) for Nsight timelines.
+        double_buffer (padded one-sided path, P > 1): steps alternate two
+        symmetric receive buffers, so the combine needs no exit barrier (the
+        next dispatch into the same buffer is two steps later, behind another
+        dispatch's exit barrier; include/moe.h MOE_P2P_*).  `recv` is the
+        buffer of the latest step.
+        bwd_push (p2p backward): the push-form combine adjoint (dy rows cross
+        once, dots at the owners) instead of reading expert outputs across."""
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.dropless = dropless
         self.fuse = bool(fuse_gate_layout) and not dropless
         self.identity_alias = identity_alias
         self.nvtx = nvtx
+        self.bwd_push = bwd_push
         if dropless:
             cap = S * k
             slot_src = False
@@ -78,8 +86,12 @@ class RoutePipeline:
         elif self.P > 1 and algo == "p2p":
             # one-sided NVLink path: layout fused into the dispatch (rows are
             # stored into the owner's symmetric recv), combine fused into the
-            # reverse (rows are read from the owner's recv); no staging buffers
-            self.recv = comm.symm_empty((E, cap, d), dtype)
+            # reverse (rows are read from the owner's recv); no staging
+            # buffers; two receive buffers used in turn (double_buffer)
+            self._recvs = [comm.symm_empty((E, cap, d), dtype)
+                           for _ in range(2 if double_buffer else 1)]
+            self._parity = 0
+            self.recv = self._recvs[0]
             self.dispatch = self.back = self.recv
         elif self.P > 1:
             # NCCL's send/recv buffers in NCCL-registered memory (ncclMemAlloc
@@ -99,12 +111,32 @@ class RoutePipeline:
             self.ws = comm.mem_empty((max(1, nb),), torch.uint8)
 
     def _first_flags(self):
-        # The very first dispatch needs its entry barrier (peers may not have
-        # allocated / zeroed recv yet); later ones follow a combine's exit one.
-        if not getattr(self, "_started", False):
-            self._started = True
+        # The first dispatch into a receive buffer needs its entry barrier
+        # (peers may not have reached it yet); later ones follow a combine's
+        # exit barrier, or (two buffers) the exit barrier of the dispatch into
+        # the other buffer, which no rank passes before its combine of this
+        # one has finished reading.
+        used = getattr(self, "_used", None)
+        if used is None:
+            used = self._used = set()
+        key = self.recv.data_ptr()
+        if key not in used:
+            used.add(key)
             return 0
         return self.comm.NO_ENTRY_BARRIER
+
+    @property
+    def double_buffered(self) -> bool:
+        return len(getattr(self, "_recvs", ())) == 2
+
+    def _p2p_begin(self):
+        """The padded one-sided path: this step's receive buffer."""
+        if hasattr(self, "_recvs"):
+            self.recv = self.dispatch = self.back = self._recvs[self._parity]
+
+    def _p2p_end(self):
+        if hasattr(self, "_recvs"):
+            self._parity = (self._parity + 1) % len(self._recvs)
 
     def alltoall(self, send, recv):
         if self.P > 1:
@@ -132,42 +164,58 @@ class RoutePipeline:
                 if name != "reverse":
                     torch.cuda.nvtx.range_push("moe/after_" + name)
         if self.fuse:
+            if self.P > 1 and self.algo == "p2p":
+                self._p2p_begin()
+                try:
+                    return self._step_fused(logits, x, token_ids, table, expert, mark)
+                finally:
+                    self._p2p_end()
             return self._step_fused(logits, x, token_ids, table, expert, mark)
+        if self.P > 1 and self.algo == "p2p" and not self.dropless:
+            self._p2p_begin()
+            try:
+                return self._step_p2p(logits, x, token_ids, table, expert, mark)
+            finally:
+                self._p2p_end()
         r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
         if self.dropless:
             return self._step_dropless(r, x, mark)
         mark("gate")
-        if self.P > 1 and self.algo == "p2p":                              # steps 2+3 fused
-            # no entry barrier: the previous step's combine ended with one
-            self.comm.dispatch_p2p(x, r, self.recv, flags=self._first_flags())
-            mark("layout")
-            mark("a2a_dispatch")
-        else:
-            layout(x, r, out=self.dispatch)                                # step 2
-            mark("layout")
-            self.alltoall(self.dispatch, self.recv)                        # step 3
-            mark("a2a_dispatch")
+        layout(x, r, out=self.dispatch)                                    # step 2
+        mark("layout")
+        self.alltoall(self.dispatch, self.recv)                            # step 3
+        mark("a2a_dispatch")
         if expert:                                                         # step 4 (stand-in)
             expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
             mark("expert")
-        if self.P > 1 and self.algo == "p2p":                              # steps 5+6 fused
-            # the entry barrier orders every rank's expert (and the owners'
-            # duplicate-row copies) before the reads; the exit barrier frees
-            # recv for the next step
-            self.comm.combine_p2p(self.recv, r, self.y, flags=self._combine_flags(expert))
-            mark("a2a_combine")
-            mark("reverse")
-            return self.y
         self.alltoall(self.recv, self.back)                                # step 5
         mark("a2a_combine")
         reverse_layout(self.back, r, out=self.y)                           # step 6
         mark("reverse")
         return self.y
 
+    def _step_p2p(self, logits, x, token_ids, table, expert, mark):
+        """The padded step on the one-sided NVLink path."""
+        r = self.gate(logits, token_ids, table, out=self.routing)          # step 1
+        mark("gate")
+        self.comm.dispatch_p2p(x, r, self.recv, flags=self._first_flags())  # steps 2+3
+        mark("layout")
+        mark("a2a_dispatch")
+        if expert:                                                         # step 4 (stand-in)
+            expert_scale(self.recv, self.P, self.E_local, self.rank * self.E_local, out=self.recv)
+            mark("expert")
+        # steps 5+6: the entry barrier orders every rank's expert (and the
+        # owners' duplicate-row copies) before the reads
+        self.comm.combine_p2p(self.recv, r, self.y, flags=self._combine_flags(expert))
+        mark("a2a_combine")
+        mark("reverse")
+        return self.y
+
     def _combine_flags(self, expert: bool) -> int:
+        f = self.comm.NO_EXIT_BARRIER if self.double_buffered else 0
         if self.identity_alias and not expert:
-            return self.comm.NO_ENTRY_BARRIER | self.comm.RECV_UNMODIFIED
-        return 0
+            f |= self.comm.NO_ENTRY_BARRIER | self.comm.RECV_UNMODIFIED
+        return f
 
     def _step_fused(self, logits, x, token_ids, table, expert, mark):
         """The step with the gate and the layout as one kernel (P=1, NCCL
@@ -275,8 +323,7 @@ class RoutePipeline:
         if self.P > 1 and self.algo == "p2p":
             # d_back rows are stored straight into the owners' d_recv, then
             # every dx row gathers its gradient rows back over NVLink
-            import os
-            if os.environ.get("MOE_BWD_PUSH", "1") != "0":
+            if self.bwd_push:
                 # push form: dy rows travel once, dots are taken at the owners
                 self.comm.combine_backward_push_p2p(dy, self.recv, r, self.d_recv, self.wtab,
                                                     self.dwtab, self.d_weight)
@@ -303,7 +350,22 @@ class RoutePipeline:
         the whole step; with `events` (len(STAGES)+1 torch.cuda.Event(
         enable_timing=True, external=True)) event-record nodes bracket every
         stage inside that graph.  stages=True: {stage: graph}.  Run one eager
-        step first (NCCL's lazy setup must not happen inside a capture)."""
+        step first (NCCL's lazy setup must not happen inside a capture).
+        Double-buffered one-sided path (stages=False): one graph per receive
+        buffer (an eager step first initialises a buffer not used yet),
+        returned as one object whose replay() runs the graph of the buffer
+        whose turn it is -- graphs and eager steps may be mixed freely."""
+        if self.double_buffered and not stages:
+            graphs = {}
+            while not all(b.data_ptr() in getattr(self, "_used", ()) for b in self._recvs):
+                self.step(logits, x, token_ids, table, expert)
+            for _ in range(2):
+                p = self._parity
+                graphs[p] = self._capture_one(logits, x, token_ids, table, expert, False, events)
+            return _AlternatingGraph(self, graphs)
+        return self._capture_one(logits, x, token_ids, table, expert, stages, events)
+
+    def _capture_one(self, logits, x, token_ids, table, expert, stages, events):
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         graphs = {}
@@ -420,3 +482,18 @@ class RoutePipeline:
             y_h = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
         y_h.copy_(y, non_blocking=True)
         return y_h
+
+
+class _AlternatingGraph:
+    """The step graphs of a double-buffered pipeline, one per receive buffer:
+    replay() runs the one whose turn it is and advances the turn (shared with
+    eager steps)."""
+
+    def __init__(self, pipe: RoutePipeline, graphs: dict):
+        self.pipe, self.graphs = pipe, graphs
+
+    def replay(self):
+        p = self.pipe._parity
+        self.pipe.recv = self.pipe.dispatch = self.pipe.back = self.pipe._recvs[p]
+        self.graphs[p].replay()
+        self.pipe._parity = (p + 1) % len(self.pipe._recvs)

@@ -39,7 +39,25 @@ def _rank_main(rank, world, algo, G, port, q):
     y_id = host(pipe.y).copy()
     y = host(pipe.step(dev(lg), dev(x), expert=True))
     torch.cuda.synchronize()
-    q.put((rank, lg, x, recv, y_id, y.copy(), host(pipe.routing.slot_idx)))
+    y = y.copy()
+    # more steps on the same inputs: the double-buffered one-sided path reuses
+    # each receive buffer with no entry barrier after combines with no exit
+    # barrier; eager steps and graph replays alternate buffers (the results
+    # must not change: compared byte for byte with the first two steps)
+    lg_d, x_d = dev(lg), dev(x)
+    again = []
+    for expert in (False, True, False):
+        again.append(host(pipe.step(lg_d, x_d, expert=expert)).copy())
+    g = pipe.capture(lg_d, x_d)
+    for _ in range(3):
+        pipe.y.fill_(0)
+        g.replay()
+        torch.cuda.synchronize()
+        again.append(host(pipe.y).copy())
+    del g   # a graph holding NCCL work must go before the communicator
+    torch.cuda.synchronize()
+    ok = [a.tobytes() == (y if i == 1 else y_id).tobytes() for i, a in enumerate(again)]
+    q.put((rank, lg, x, recv, y_id, y, host(pipe.routing.slot_idx), ok))
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
@@ -101,7 +119,8 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     routings, disp, recvs, ys = orc.route_multi(xs, lgs, E=E, k=K, cap=cap)
     _, _, _, ys_id = orc.route_multi(xs, lgs, E=E, k=K, cap=cap, scale=False)
     for r in range(world):
-        _, _, recv, y_id, y, slots = out[r]
+        _, _, recv, y_id, y, slots, again_ok = out[r]
+        assert all(again_ok), "rank %d: repeated steps / graph replays differ: %s" % (r, again_ok)
         assert (slots == routings[r].slot_idx).all()
         assert recv.tobytes() == recvs[r].tobytes()          # AllToAll bit-exact
         # identity expert, k=2 RENORM: y == combine of the original rows

@@ -154,6 +154,41 @@ def test_sim_route_pipeline_p2p(orc):
                          for r in range(P)])
 
 
+@pytest.mark.parametrize("double_buffer", [True, False])
+def test_sim_route_pipeline_p2p_steps(orc, double_buffer):
+    """Four RoutePipeline steps on simulated ranks over two alternating token
+    sets: with double buffering the steps alternate two receive buffers,
+    every combine skips its exit barrier and every dispatch after a buffer's
+    first skips its entry barrier (include/moe.h MOE_P2P_*); each step's
+    receive buffer and y equal the oracle's for that step's tokens.  (Identity
+    expert: on a simulated rank only the library's calls are queued, so an
+    in-place expert would run before its dispatch; the multi-GPU test covers
+    the s_e expert.)"""
+    P, S, d, E, k = 4, 768, 64, 16, 2
+    with moe.SimWorld(P) as world:
+        R = Ranks(orc, P, S, d, E, k)
+        xs_b = [synthgen.tokens(synthgen.seed_for(29, r, 2), S, d, "bf16") for r in range(P)]
+        sets = [(R.x_dev, R.disp),
+                ([dev(x) for x in xs_b], [orc.layout(x, ro) for x, ro in zip(xs_b, R.orc_routings)])]
+        pipes = [moe.RoutePipeline(S, d, E, k, R.cap, torch.bfloat16, comm=world.comm(r),
+                                   algo="p2p", double_buffer=double_buffer) for r in range(P)]
+        lg_dev = [dev(lg) for lg in R.lgs]
+        recv_ptrs = set()
+        for i in range(4):
+            x_dev, disp = sets[i % 2]
+            ys = [pipes[r].step(lg_dev[r], x_dev[r]) for r in range(P)]
+            world.run()
+            torch.cuda.synchronize()
+            recv_ptrs.add(pipes[0].recv.data_ptr())
+            want = orc.alltoall_flat(disp)
+            for r in range(P):
+                assert host(pipes[r].recv).tobytes() == want[r].tobytes(), (i, r)
+            backs = orc.alltoall_flat(want)
+            _check_y(R, ys, [(backs[r], orc.reverse_layout(backs[r], R.orc_routings[r]))
+                             for r in range(P)])
+        assert len(recv_ptrs) == (2 if double_buffer else 1)
+
+
 # ------------------------------------------------------------ AllToAll algorithms
 A2A_CASES = [(2, "flat", 1), (4, "flat", 1), (8, "flat", 1), (2, "hier", 2), (4, "hier", 2),
              (4, "hier", 4), (8, "hier", 4), (8, "hier", 2), (8, "hier", 1), (4, "hier2d", 2),
