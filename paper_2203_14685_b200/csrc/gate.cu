@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots(GateArgs a) {
   pdl_trigger();
   gate_trace(a, tile, 9);
   const unsigned* pre = reinterpret_cast<const unsigned*>(a.status);
+  // (staging this tile's column prefixes in shared memory together with the
+  // first item, as k_gate_slots2 does, measured no faster here: C4a gate
+  // stage 21.0 -> 22.1 us)
   for (int i = tid; i < nt * a.k; i += kGateThreads) {
     const size_t gi = (size_t)t0 * a.k + i;
     const int e = a.expert_idx[gi];
@@ -158,6 +161,14 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
   pdl_wait();
   pdl_trigger();
   gate_trace(a, tile, 9);
+  // this thread's first item, loaded before the column reduction so the two
+  // L2 round trips overlap
+  const int n_items = nt * a.k;
+  int e0 = -1, s0 = 0;
+  if (tid < n_items) {
+    e0 = __ldcg(a.expert_idx + (size_t)t0 * a.k + tid);
+    s0 = __ldcg(a.slot_idx + (size_t)t0 * a.k + tid);
+  }
   const unsigned* agg = reinterpret_cast<const unsigned*>(a.status);
   for (int c = warp; c < a.ncols; c += kGateWarps) {
     const unsigned* col = agg + (size_t)c * a.n_tiles;
@@ -187,13 +198,14 @@ __global__ void __launch_bounds__(kGateThreads) k_gate_slots2(GateArgs a) {
   }
   __syncthreads();
   gate_trace(a, tile, 10);
-  for (int i = tid; i < nt * a.k; i += kGateThreads) {
+  for (int i = tid; i < n_items; i += kGateThreads) {
     const size_t gi = (size_t)t0 * a.k + i;
-    const int e = a.expert_idx[gi];
+    const bool first = i == tid;
+    const int e = first ? e0 : a.expert_idx[gi];
     if (e < 0) continue;
     const int j = i % a.k;
     const int col = slot_prio ? j * a.E + e : e;
-    int s = a.slot_idx[gi] + s_pre[col];
+    int s = (first ? s0 : a.slot_idx[gi]) + s_pre[col];
     if (slot_prio)
       for (int jj = 0; jj < j; ++jj) s += s_tot[jj * a.E + e];
     if (s < a.cap) {
