@@ -132,8 +132,11 @@ inline GatePlan gate_plan_default(const moe_gate_desc_t& d, int ngroups = 1) {
 }
 
 // ------------------------------------------------------------ selection
+// (va, ia) ranks before (vb, ib): larger value, then lower index (R2, R3).
+// Bitwise, not short-circuit: predicates and selects, no branches (the
+// branchy form cost C4a's k-top-1 selection a reconvergence per logit).
 __device__ __forceinline__ bool beats(float va, int ia, float vb, int ib) {
-  return va > vb || (va == vb && ia < ib);
+  return (va > vb) | ((va == vb) & (ia < ib));
 }
 
 template <int K>
@@ -147,21 +150,20 @@ struct TopList {
       i[p] = INT_MAX;
     }
   }
+  // Sorted insertion as a select network (no branches): b[p] = x beats
+  // entry p is monotone in p (the list is sorted), so entry p becomes entry
+  // p-1 where x beats it, x where x beats p but not p-1, else stays.
   __device__ __forceinline__ void insert(float x, int e) {
-    if (!beats(x, e, v[K - 1], i[K - 1])) return;
-    v[K - 1] = x;
-    i[K - 1] = e;
+    bool b[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) b[p] = beats(x, e, v[p], i[p]);
 #pragma unroll
     for (int p = K - 1; p > 0; --p) {
-      if (beats(v[p], i[p], v[p - 1], i[p - 1])) {
-        float tv = v[p];
-        v[p] = v[p - 1];
-        v[p - 1] = tv;
-        int ti = i[p];
-        i[p] = i[p - 1];
-        i[p - 1] = ti;
-      }
+      v[p] = b[p - 1] ? v[p - 1] : (b[p] ? x : v[p]);
+      i[p] = b[p - 1] ? i[p - 1] : (b[p] ? e : i[p]);
     }
+    v[0] = b[0] ? x : v[0];
+    i[0] = b[0] ? e : i[0];
   }
 };
 
@@ -269,16 +271,15 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, const float*
   int pe = (l * epl) / n, next = (pe + 1) * n;
   if (valid)
     for_lane_logits(row, l, epl, vec4, [&](float x, int e) {
-      if (e == next) {
-        ++pe;
-        next += n;
-      }
+      const bool adv = e == next;
+      pe += adv;
+      next += adv ? n : 0;
 #pragma unroll
-      for (int p = 0; p < K; ++p)
-        if (p == pe && beats(x, e, bv[p], bi[p])) {
-          bv[p] = x;
-          bi[p] = e;
-        }
+      for (int p = 0; p < K; ++p) {
+        const bool take = (p == pe) & beats(x, e, bv[p], bi[p]);
+        bv[p] = take ? x : bv[p];
+        bi[p] = take ? e : bi[p];
+      }
     });
 #pragma unroll
   for (int m = 1; m < L; m <<= 1) {
@@ -286,10 +287,9 @@ __device__ __forceinline__ void select_ktop1_reg(const GateArgs& a, const float*
     for (int p = 0; p < K; ++p) {
       float ov = __shfl_xor_sync(0xffffffffu, bv[p], m);
       int oi = __shfl_xor_sync(0xffffffffu, bi[p], m);
-      if (beats(ov, oi, bv[p], bi[p])) {
-        bv[p] = ov;
-        bi[p] = oi;
-      }
+      const bool take = beats(ov, oi, bv[p], bi[p]);
+      bv[p] = take ? ov : bv[p];
+      bi[p] = take ? oi : bi[p];
     }
   }
   double den[K];
