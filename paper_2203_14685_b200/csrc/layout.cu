@@ -499,7 +499,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   a.rank = rank;
   // Measured alternatives, removed: a TMA-staged combine (won for Switch on
   // >= 4 KiB rows only in the forward walk; the reversed register walk is
-  // faster, C3 40.0 vs 52.3 us), 16-byte vectors, two segments per round.
+  // faster, C3 40.0 vs 52.3 us), 16-byte vectors, two segments per round; a
+  // small-CTA grid (as the layout's) with blocks of 2-8 consecutive tokens
+  // per warp (C2 step 70.2 -> 71.2 us, C3 89.7 -> 90.6, C4b 94.9 -> 95.0,
+  // C4a 139.0 -> 138.6; profiles/r02_n1_grid/ab_rev_blocked.txt).
   const void* kern;
   // k <= 2 path: vectors per lane per round (x k rows); measured: 2 for
   // k = 2 (one 1 KiB segment of both rows: C2 36.3 -> 35.6 us), 4 for k = 1
