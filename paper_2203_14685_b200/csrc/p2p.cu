@@ -324,13 +324,18 @@ static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, 
 
 // ------------------------------------------------------------ dispatch dedupe
 // Owner side: a warp per 32 table entries (coalesced), each nonzero entry
-// "= row v-1" copied by the warp (16-byte vectors, local HBM), then cleared
-// for the next step.  The entries were stored by the senders before their
-// exit barrier (release) and this kernel runs after it (acquire).
+// "= row v-1" copied (16-byte vectors, local HBM), then cleared for the next
+// step.  The warp copies up to kDupRows rows at a time, all their loads
+// issued before the first store (one HBM latency per group of rows instead
+// of per row: a trace of C2 at N=2 showed the serial per-row copy as ~8 us
+// between the dispatch and the combine).  The entries were stored by the
+// senders before their exit barrier (release) and this kernel runs after it
+// (acquire).
+constexpr int kDupRows = 4;
 __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes) {
   pdl_wait();
   pdl_trigger();
-  constexpr int kV = 8;  // 16-byte vectors per lane in flight: 4 KiB of a row per warp round
+  constexpr int kV = 4;  // 16-byte vectors per lane per row segment: 2 KiB of a row per round
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
   for (long long base = gw * 32; base < n; base += nw * 32) {
@@ -338,23 +343,38 @@ __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long lon
     const int v = i < n ? tab[i] : 0;
     unsigned m = __ballot_sync(0xffffffffu, v != 0);
     while (m) {
-      const int l = __ffs(m) - 1;
-      m &= m - 1;
-      const long long src = (long long)__shfl_sync(0xffffffffu, v, l) - 1;
-      const char* sr = recv + src * row_bytes;
-      char* dr = recv + (base + l) * row_bytes;
+      const char* sr[kDupRows];
+      char* dr[kDupRows];
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < kDupRows; ++q) {
+        sr[q] = nullptr;
+        dr[q] = nullptr;
+        if (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const long long src = (long long)__shfl_sync(0xffffffffu, v, l) - 1;
+          sr[q] = recv + src * row_bytes;
+          dr[q] = recv + (base + l) * row_bytes;
+          cnt = q + 1;
+        }
+      }
       for (int o0 = 0; o0 < row_bytes; o0 += 32 * 16 * kV) {
-        V4 r[kV];
+        V4 r[kDupRows][kV];
 #pragma unroll
-        for (int u = 0; u < kV; ++u) {
-          const int off = o0 + (lane + 32 * u) * 16;
-          if (off < row_bytes) r[u] = ld_stream_v4(sr + off);
-        }
+        for (int q = 0; q < kDupRows; ++q)
 #pragma unroll
-        for (int u = 0; u < kV; ++u) {
-          const int off = o0 + (lane + 32 * u) * 16;
-          if (off < row_bytes) st_v4(dr + off, r[u]);
-        }
+          for (int u = 0; u < kV; ++u) {
+            const int off = o0 + (lane + 32 * u) * 16;
+            if (q < cnt && off < row_bytes) r[q][u] = ld_stream_v4(sr[q] + off);
+          }
+#pragma unroll
+        for (int q = 0; q < kDupRows; ++q)
+#pragma unroll
+          for (int u = 0; u < kV; ++u) {
+            const int off = o0 + (lane + 32 * u) * 16;
+            if (q < cnt && off < row_bytes) st_v4(dr[q] + off, r[q][u]);
+          }
       }
     }
     if (v) tab[i] = 0;
