@@ -8,9 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# MOE_LIB_VARIANT=trace selects the instrumented build (libmoe_b200_trace.so)
-_VARIANT = os.environ.get("MOE_LIB_VARIANT", "")
-SO_PATH = os.path.join(_HERE, "libmoe_b200%s.so" % ("_" + _VARIANT if _VARIANT else ""))
+SO_PATH = os.path.join(_HERE, "libmoe_b200.so")
 
 i32, i64, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
 vp = ctypes.c_void_p

@@ -23,8 +23,6 @@ ROOT = os.path.dirname(PKG)
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "moe_b200")
 SO = os.path.join(PKG, "libmoe_b200.so")
-# variants: extra -D flags, their own object dir and library name
-VARIANTS = {"": []}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -53,15 +51,14 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+def build(force: bool = False, verbose: bool = False) -> str:
     nd = nccl_dir()
-    build_dir = BUILD + ("_" + variant if variant else "")
-    so = SO[:-3] + ("_" + variant if variant else "") + ".so"
+    build_dir, so = BUILD, SO
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "moe.h"),
                                                              os.path.abspath(__file__)]
     os.makedirs(build_dir, exist_ok=True)
-    flags = ARCH + VARIANTS[variant] + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+    flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                     "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC,
                     "-I", os.path.join(nd, "include")]
     if verbose:
@@ -96,6 +93,5 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
-    ap.add_argument("--variant", default="", choices=sorted(VARIANTS))
     a = ap.parse_args()
-    print(build(a.force, a.verbose, a.variant))
+    print(build(a.force, a.verbose))
