@@ -448,6 +448,41 @@ def main():
     log("stage timing done")
     eager = timed_eager(max(3, a.steps // 2))
     log("eager timing done")
+    # N > 1 one-sided path: the row kernels' own spans (moe_set_trace stamps
+    # per CTA, one traced graph replay after the timed steps, max over ranks):
+    # the dispatch kernel (k_layout in peer mode) and the combine kernel
+    # (k_reverse_k in peer mode), without the barriers and owner-side copies
+    # that the stage times include
+    kernel_spans = None
+    if P > 1 and algo == "p2p" and not a.dropless:
+        from paper_2203_14685_b200._lib import lib as _tlib
+        tbuf = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
+        _tlib().moe_set_trace(tbuf.data_ptr(), tbuf.numel() * 8)
+        g_tr = pipe.capture(d_in["logits"], d_in["x"], d_in["token_ids"], d_in["table"])
+        _tlib().moe_set_trace(None, 0)
+        spans = []
+        for _ in range(3):
+            flush_l2()
+            tbuf.zero_()
+            torch.cuda.synchronize()
+            barrier()
+            align()
+            g_tr.replay()
+            torch.cuda.synchronize()
+            raw = tbuf.cpu().numpy()
+            n = raw.size
+            sp = []
+            for lo in (n // 2, 3 * n // 4):
+                c = raw[lo:lo + n // 4].reshape(-1, 4)[:, :3]
+                c = c[c[:, 0] > 0]
+                sp.append(float(c[:, 2].max() - c[:, 1].min()) / 1e3 if c.size else 0.0)
+            spans.append(sp)
+        del g_tr
+        sp_t = torch.tensor([statistics.median(x[0] for x in spans),
+                             statistics.median(x[1] for x in spans)], dtype=torch.float64, device=dev)
+        dist.all_reduce(sp_t, op=dist.ReduceOp.MAX)
+        kernel_spans = {"dispatch_us": float(sp_t[0]), "combine_us": float(sp_t[1])}
+        log("row-kernel spans done")
     # N > 1 one-sided path: the identity-expert alias form, an extra (the
     # headline above keeps the combine's entry barrier and reads every slot)
     alias_ms = None
@@ -608,7 +643,7 @@ def main():
     ab = algorithmic_bytes(w, S, cap, P, row)
     ab["reverse"] = admitted * row + S * row + 12 * S * w.k
     tun = moe.get_tuning()
-    p2p_flags = {"dedupe": False, "local_pad": False}
+    p2p_flags = {"dedupe": False, "local_pad": False, "precombine": False}
     if a.dropless:
         # packed: no padding rows; the rows leaving this rank are the admitted
         # rows of other ranks' experts
@@ -641,11 +676,15 @@ def main():
             load = pipe.routing.load.view(P, El)
             padrows = cap - load.clamp(max=cap)
             pads = int(padrows.sum().item() - padrows[rank].sum().item())
+        precombine = bool(dedupe and w.k == 2 and tun["p2p_precombine"] and tun["reverse_kspec"]
+                          and row % 32 == 0)
         p2p_flags = {"dedupe": bool(dedupe), "local_pad": bool(local_pad),
-                     "double_buffer": pipe.double_buffered}
+                     "double_buffer": pipe.double_buffered, "precombine": precombine}
         ab["a2a_buffer"] = ab["a2a"]
         ab["a2a_dispatch"] = ((pairs if dedupe else remote_slots) + pads) * row
-        ab["a2a_combine"] = remote_slots * row
+        # the combine reads every admitted remote slot, except that a
+        # pre-combined pair (both slots on one remote owner) is one row
+        ab["a2a_combine"] = (pairs if precombine else remote_slots) * row
         ab["a2a_combine_alias"] = (pairs if dedupe else remote_slots) * row
         ab["a2a"] = ab["a2a_dispatch"]
     elif P > 1:
@@ -719,8 +758,20 @@ def main():
             a2a["note"] = ("bytes that cross NVLink per rank and direction: the dispatch sends a "
                            "token's row once per remote owner (dedupe) plus the padding rows the "
                            "owners do not write themselves; the combine reads every admitted "
-                           "remote slot (entry barrier kept, as with a real expert)")
+                           "remote slot, a token's two slots on one remote owner as the one row "
+                           "that owner pre-combined after its expert (entry barrier kept, as "
+                           "with a real expert)")
         a2a["frac"] = min(bw.values()) / NVLINK_GBS
+        if kernel_spans and "a2a_buffer" in ab:
+            # the same bytes over the row kernels' own spans (max over ranks)
+            kg = {"dispatch": ab["a2a_dispatch"] / (kernel_spans["dispatch_us"] / 1e6) / 1e9,
+                  "combine": ab["a2a_combine"] / (kernel_spans["combine_us"] / 1e6) / 1e9}
+            a2a["row_kernels"] = {
+                "span_us": kernel_spans, "gbs": kg, "frac": min(kg.values()) / NVLINK_GBS,
+                "what": "bytes that cross over the dispatch / combine kernel's own span (first "
+                        "CTA released -> last CTA end, moe_set_trace, one traced replay, max "
+                        "over ranks): the link rate of the row kernels; the stage figures above "
+                        "add the device barriers and the owners' duplicate-row copies"}
         if alias_ms is not None:
             a2a["identity_alias"] = {
                 "ms_per_step": alias_ms, "value": P * S / (alias_ms / 1e3),
@@ -776,7 +827,8 @@ def main():
             launches_per_step += 4
         elif P > 1 and algo == "p2p":
             launches_per_step += (2 + (0 if pipe.double_buffered else 1) +
-                                  int(p2p_flags["dedupe"]) + int(p2p_flags["local_pad"]))
+                                  int(p2p_flags["dedupe"]) + int(p2p_flags["local_pad"]) +
+                                  int(p2p_flags["precombine"]))
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,

@@ -726,6 +726,10 @@ typedef struct {
                                 CTAs (at least the persistent grid), which the
                                 block scheduler balances over the SMs; 0 = the
                                 persistent grid (row_ctas_per_sm) (2)              */
+  int32_t p2p_precombine;    /* NVLink combine, k = 2 after a deduped dispatch: each
+                                owner first combines the token pairs it received
+                                once (one rounding, the same result), and the
+                                token's owner reads one row instead of two (1)    */
 } moe_tuning_t;
 
 /* host.  Copy of the current table (after the one-time environment read). */

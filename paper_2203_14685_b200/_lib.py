@@ -45,7 +45,8 @@ TUNING_FIELDS = ("gate_tiles", "gate_max_tile", "gate_two_maxw", "layout_u",
                  "combine_ctas_per_sm", "combine_bwd_kspec",
                  "gate_bwd_lanes", "p2p_dedupe", "p2p_local_pad", "a2a_ctas_per_sm",
                  "barrier_timeout_ms", "barrier_pdl", "disable_p2p", "nccl_alltoall", "nccl_max_ctas",
-                 "nccl_min_ctas", "nccl_cta_policy", "layout_tokens_per_warp")
+                 "nccl_min_ctas", "nccl_cta_policy", "layout_tokens_per_warp",
+                 "p2p_precombine")
 
 
 class Tuning(ctypes.Structure):

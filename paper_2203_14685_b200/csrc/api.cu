@@ -78,6 +78,7 @@ const TuneField kTune[] = {
     {"MOE_NCCL_MIN_CTAS", &moe_tuning_t::nccl_min_ctas, 0, 0, 64},
     {"MOE_NCCL_CTA_POLICY", &moe_tuning_t::nccl_cta_policy, -1, -1, 2},
     {"MOE_LAYOUT_TOKENS_PER_WARP", &moe_tuning_t::layout_tokens_per_warp, 2, 0, 1 << 20},
+    {"MOE_P2P_PRECOMBINE", &moe_tuning_t::p2p_precombine, 1, 0, 1},
 };
 moe_tuning_t g_tune;
 std::once_flag g_tune_once;

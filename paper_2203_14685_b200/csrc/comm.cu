@@ -238,7 +238,10 @@ moe_status_t moe_comm_destroy(moe_comm_t* comm) {
   release_regs(comm);
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
-  for (RecvTables& t : comm->tables) symm_release(comm, t.buf);
+  for (RecvTables& t : comm->tables) {
+    symm_release(comm, t.buf);
+    if (t.pre.base) symm_release(comm, t.pre);
+  }
   moe_status_t s = nccl_status(ncclCommDestroy(comm->nccl), "moe_comm_destroy");
   delete comm;
   return s;
@@ -285,7 +288,10 @@ moe_status_t moe_comm_abort(moe_comm_t* comm) {
   comm->regs.clear();
   for (SymmBuf& b : comm->symm) symm_release(comm, b);
   if (comm->sig.base) symm_release(comm, comm->sig);
-  for (RecvTables& t : comm->tables) symm_release(comm, t.buf);
+  for (RecvTables& t : comm->tables) {
+    symm_release(comm, t.buf);
+    if (t.pre.base) symm_release(comm, t.pre);
+  }
   delete comm;
   return s;
 }

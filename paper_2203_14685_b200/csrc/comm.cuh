@@ -42,8 +42,15 @@ struct SymmBuf {
 // buffers may then drop the combine's exit barrier (moe.h, MOE_P2P_*).
 struct RecvTables {
   const void* recv;   // this rank's receive buffer they belong to
-  SymmBuf buf;        // [kPadTabBytes padding counts][dup_rows int32]
-  size_t dup_rows;    // capacity of the duplicate-row table
+  // [kPadTabBytes padding counts][dup_rows int32 duplicate-row table]
+  // [dup_rows int32 pair table][dup_rows float slot weights]
+  SymmBuf buf;
+  size_t dup_rows;    // capacity of the per-row tables
+  SymmBuf pre{};      // pre-combined rows of token pairs (moe_combine_p2p), lazily
+  size_t pre_bytes = 0;
+  char* dup(int q) const { return buf.peer.p[q] + kPadTabBytes; }
+  char* pairs(int q) const { return dup(q) + dup_rows * sizeof(int); }
+  char* wts(int q) const { return pairs(q) + dup_rows * sizeof(int); }
 };
 
 // One step of a rank's program on a SIMULATED communicator (moe_sim_*):

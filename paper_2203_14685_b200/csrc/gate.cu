@@ -372,7 +372,8 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
                                 const moe_routing_t& out, void* ws, const void* x,
                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                 int rank, const PeerPtrs* pad_tab, const PeerPtrs* dup_tab,
-                                cudaStream_t stream) {
+                                cudaStream_t stream,
+                                const PeerPtrs* wt_tab) {
   const int row_bytes = dtype_size * dcols;
   if (!gate_layout_supported(d, row_bytes)) {
     set_error("moe_gate_layout: no fused kernel for this gate (SLOT priority, SAM, D2S, k > 8 "
@@ -406,6 +407,7 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
   if (dup_tab) {
     a.dedupe = 1;
     a.dup = *dup_tab;
+    if (wt_tab) a.wt = *wt_tab;
   }
   char* w = static_cast<char*>(ws);
   f.fc = reinterpret_cast<FusedCtrl*>(w + fp.ctrl_off);

@@ -358,9 +358,15 @@ __global__ void __launch_bounds__(kGateThreads, 4) k_gate_layout(FusedArgs f) {
               if (s2 >= 0 && e2 / ra.E_local == q) break;
             }
             if (jj < j) {
-              if (seg == 0 && lane == 0)
-                reinterpret_cast<int*>(ra.dup.p[q])[row_index(ra, q, e, s)] =
-                    (int)row_index(ra, q, e2, s2) + 1;
+              if (seg == 0 && lane == 0) {
+                const size_t rb = row_index(ra, q, e, s), rr = row_index(ra, q, e2, s2);
+                reinterpret_cast<int*>(ra.dup.p[q])[rb] = (int)rr + 1;
+                if (ra.wt.p[q] && ra.weight) {  // this kernel wrote the weights: plain loads
+                  const size_t it = (size_t)t * a.k;
+                  reinterpret_cast<float*>(ra.wt.p[q])[rr] = __ldcg(ra.weight + it + jj);
+                  reinterpret_cast<float*>(ra.wt.p[q])[rb] = __ldcg(ra.weight + it + j);
+                }
+              }
               continue;
             }
           }

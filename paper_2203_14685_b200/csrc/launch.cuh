@@ -21,7 +21,8 @@ moe_status_t gate_layout_launch(const moe_gate_desc_t& d, const moe_gate_inputs_
                                 const moe_routing_t& out, void* ws, const void* x,
                                 int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                 int rank, const PeerPtrs* pad_tab, const PeerPtrs* dup_tab,
-                                cudaStream_t stream);
+                                cudaStream_t stream,
+                                const PeerPtrs* wt_tab = nullptr);
 size_t gate_workspace_bytes(const moe_gate_desc_t& d);
 // host checks of moe_gate_ex's arguments (api.cu), without launching
 moe_status_t gate_validate(const moe_gate_desc_t* desc, const moe_gate_inputs_t* in,
@@ -46,17 +47,22 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
                                  int rank, cudaStream_t stream, const int32_t* offsets = nullptr,
                                  const int32_t* peer_base = nullptr,
                                  const PeerPtrs* pad_tab = nullptr,
-                                 const PeerPtrs* dup_tab = nullptr);
+                                 const PeerPtrs* dup_tab = nullptr,
+                                 const PeerPtrs* wt_tab = nullptr);
 // The owner's half of the dispatch dedupe (RowArgs::dedupe): after the exit
 // barrier, copy every recv row whose table entry says "= row i" and clear
 // the entry.  tab: this rank's table, n_rows entries.
 moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_bytes,
-                             cudaStream_t stream);
+                             cudaStream_t stream, int* pairs = nullptr);
 moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& r,
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,
                                   const int32_t* offsets = nullptr,
-                                  const int32_t* peer_base = nullptr, int dup_alias = 0);
+                                  const int32_t* peer_base = nullptr, int dup_alias = 0,
+                                  const PeerPtrs* pre = nullptr);
+// The peer combine kernel (k_reverse_k) serves this shape: k <= 2, rows a
+// multiple of 32 bytes, tuning reverse_kspec (the pre-combined pairs need it).
+bool reverse_kspec_used(const moe_gate_desc_t& d, int row_bytes);
 // At least ~5% of the padded rows are padding by construction (E*cap >
 // 1.05*S*k, e.g. the hash gate's C = 1.25): local padding over NVLink, and
 // the padding rows zeroed first in local mode (L2 order for the combine).

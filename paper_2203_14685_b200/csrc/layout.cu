@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   for (int tb = (blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * TPW; tb < a.S; tb += wstride) {
     const char* b[TPW][KK];
     float w[TPW][KK];
+    int ee[TPW][KK], ss[TPW][KK];
 #pragma unroll
     for (int p = 0; p < TPW; ++p)
 #pragma unroll
@@ -182,12 +183,34 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
         const int s = tl < a.S ? __ldg(a.slot_idx + (size_t)t * KK + j) : -1;
         b[p][j] = nullptr;
         w[p][j] = 0.f;
+        ss[p][j] = s;
+        ee[p][j] = 0;
         if (s >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * KK + j);
+          ee[p][j] = e;
           b[p][j] = AL ? src_row_item(a, t, j, e, s) : src_row(a, e, s);
           w[p][j] = row_weight(a, (size_t)t * KK + j);
         }
       }
+    // pre-combined pairs (RowArgs::pre): both admitted slots on one remote
+    // owner -> that owner already computed the token's y row (same fp32 FMA
+    // order, one rounding) into its pre row of the second slot: one read,
+    // stored as is
+    bool pc[TPW];
+#pragma unroll
+    for (int p = 0; p < TPW; ++p) {
+      pc[p] = false;
+      if constexpr (KK == 2 && !AL) {
+        if (a.pre.p[0] && ss[p][0] >= 0 && ss[p][1] >= 0) {
+          const int q = ee[p][1] / a.E_local;
+          if (q == ee[p][0] / a.E_local && q != a.rank) {
+            pc[p] = true;
+            b[p][0] = a.pre.p[q] + row_index(a, q, ee[p][1], ss[p][1]) * a.row_bytes;
+            b[p][1] = nullptr;
+          }
+        }
+      }
+    }
     // alias-mode combine (src_row_item): both slots of a token may name the
     // same row (sent once by the deduped dispatch); it is loaded once
     bool dup1[TPW];
@@ -228,8 +251,9 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
 #pragma unroll
             for (int j = 0; j < KK; ++j)
               if (b[p][j]) fma_vec<DT>(acc, w[p][j], r[p][j][u]);
-            if (a.y_ef) st_v8_ef(yrow + off, pack_vec<DT>(acc));
-            else st_v8(yrow + off, pack_vec<DT>(acc));
+            const V8 o = pc[p] ? r[p][0][u] : pack_vec<DT>(acc);
+            if (a.y_ef) st_v8_ef(yrow + off, o);
+            else st_v8(yrow + off, o);
           }
         }
       }
@@ -396,12 +420,13 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
                                  int dtype_size, int dcols, const PeerPtrs& dst, int E_local,
                                  int rank, cudaStream_t stream, const int32_t* offsets,
                                  const int32_t* peer_base, const PeerPtrs* pad_tab,
-                                 const PeerPtrs* dup_tab) {
+                                 const PeerPtrs* dup_tab, const PeerPtrs* wt_tab) {
   RowArgs a{};
   row_trace_set(a, false);
   if (dup_tab && !offsets) {
     a.dedupe = 1;
     a.dup = *dup_tab;
+    if (wt_tab) a.wt = *wt_tab;
   }
   if (pad_tab) {
     a.skip_pads = 1;
@@ -412,6 +437,7 @@ moe_status_t layout_launch_peers(const moe_gate_desc_t& d, const moe_routing_t& 
   a.src = static_cast<const char*>(x);
   a.expert_idx = r.expert_idx;
   a.slot_idx = r.slot_idx;
+  a.weight = r.weight;  // read only by the dedupe's slot-weight stores
   a.load = r.load;
   a.S = d.S;
   a.E = d.E;
@@ -468,8 +494,9 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
                                   const PeerPtrs& src, int E_local, int rank, int dtype,
                                   int dtype_size, int dcols, void* y, cudaStream_t stream,
                                   const int32_t* offsets, const int32_t* peer_base,
-                                  int dup_alias) {
+                                  int dup_alias, const PeerPtrs* pre) {
   RowArgs a{};
+  if (pre) a.pre = *pre;
   row_trace_set(a, true);
   a.dedupe = dup_alias;  // reverse: read deduped slots from their first row (src_row_item)
   a.offsets = offsets;
@@ -509,7 +536,7 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   // (peer mode: 4 -- both 2 KiB rows in flight hide the NVLink latency better,
   // C2 at P=2: 129.2 -> 127.3 us)
   const int KU = tu.reverse_ku > 0 ? tu.reverse_ku : (d.k == 2 && E_local == d.E) ? 2 : 4;
-  const bool kspec = tu.reverse_kspec && a.row_bytes % 32 == 0 && a.k <= 2;
+  const bool kspec = reverse_kspec_used(d, a.row_bytes);
   if (kspec) {
     // TPW * k * U = KU vectors in flight per lane, U covering at most one
     // row (1 KiB of row per U step)
@@ -549,6 +576,10 @@ moe_status_t reverse_launch_peers(const moe_gate_desc_t& d, const moe_routing_t&
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kRowThreads), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "moe_reverse_layout: launch");
   return MOE_OK;
+}
+
+bool reverse_kspec_used(const moe_gate_desc_t& d, int row_bytes) {
+  return tuning().reverse_kspec && row_bytes % 32 == 0 && d.k <= 2;
 }
 
 moe_status_t reverse_launch(const moe_gate_desc_t& d, const moe_routing_t& r, const void* back,

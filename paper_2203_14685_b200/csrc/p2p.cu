@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include "launch.cuh"
+#include "rows.cuh"
 
 namespace moe {
 
@@ -332,7 +333,8 @@ static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, 
 // senders before their exit barrier (release) and this kernel runs after it
 // (acquire).
 constexpr int kDupRows = 4;
-__global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes) {
+__global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes,
+                                                  int* pairs) {
   pdl_wait();
   pdl_trigger();
   constexpr int kV = 4;  // 16-byte vectors per lane per row segment: 2 KiB of a row per round
@@ -341,6 +343,9 @@ __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long lon
   for (long long base = gw * 32; base < n; base += nw * 32) {
     const long long i = base + lane;
     const int v = i < n ? tab[i] : 0;
+    // the pair table (read by the combine's pre-combine) gets this step's
+    // entries, zeros included, so no stale pair survives a step
+    if (pairs && i < n) pairs[i] = v;
     unsigned m = __ballot_sync(0xffffffffu, v != 0);
     while (m) {
       const char* sr[kDupRows];
@@ -382,13 +387,104 @@ __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long lon
 }
 
 moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_bytes,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, int* pairs) {
   const long long groups = (n_rows + 31) / 32;
   const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 7) / 8,
                                                                     (long long)device_sm_count() * 4));
-  void* args[] = {&recv, &tab, &n_rows, &row_bytes};
+  void* args[] = {&recv, &tab, &n_rows, &row_bytes, &pairs};
   cudaError_t e = launch_pdl((const void*)k_dup_fill, dim3(grid), dim3(256), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "k_dup_fill launch");
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------ combine pre-combine
+// Owner side, before the combine's entry barrier: for every pair "row B =
+// row A" of this step (the pair table k_dup_fill refreshed: one token's two
+// slots, both here), pre[B] = the token's combined row, w_A * out[A] + w_B *
+// out[B] in fp32 from 0 in slot order, rounded once -- exactly what the
+// token's owner would compute from the two rows -- so the combine reads one
+// row over NVLink instead of two.  A warp per 32 table entries; the weights
+// came with the dispatch (RowArgs::wt).  Rows are 32-byte multiples.
+template <int DT>
+__global__ void __launch_bounds__(256) k_precombine(const char* recv, const int* pairs,
+                                                    const float* wt, char* pre, long long n,
+                                                    int row_bytes) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NA = DT == MOE_F32 ? 8 : 16;
+  constexpr int kS = 2;      // 1 KiB segments per round
+  constexpr int kPairs = 2;  // pairs per warp with all their loads in flight
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  for (long long base = gw * 32; base < n; base += nw * 32) {
+    const long long i = base + lane;
+    const int v = i < n ? pairs[i] : 0;
+    unsigned m = __ballot_sync(0xffffffffu, v != 0);
+    while (m) {
+      const char* xa[kPairs];
+      const char* xb[kPairs];
+      char* out[kPairs];
+      float wa[kPairs], wb[kPairs];
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) {
+        xa[q] = xb[q] = nullptr;
+        out[q] = nullptr;
+        wa[q] = wb[q] = 0.f;
+        if (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const long long ra = (long long)__shfl_sync(0xffffffffu, v, l) - 1, rb = base + l;
+          wa[q] = wt[ra];
+          wb[q] = wt[rb];
+          xa[q] = recv + ra * row_bytes;
+          xb[q] = recv + rb * row_bytes;
+          out[q] = pre + rb * row_bytes;
+          cnt = q + 1;
+        }
+      }
+      for (int o0 = 0; o0 < row_bytes; o0 += 1024 * kS) {
+        V8 va[kPairs][kS], vb[kPairs][kS];
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q)
+#pragma unroll
+          for (int u = 0; u < kS; ++u) {
+            const int off = o0 + (lane + 32 * u) * 32;
+            if (q < cnt && off < row_bytes) {
+              va[q][u] = ld_stream_v8(xa[q] + off);
+              vb[q][u] = ld_stream_v8(xb[q] + off);
+            }
+          }
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q)
+#pragma unroll
+          for (int u = 0; u < kS; ++u) {
+            const int off = o0 + (lane + 32 * u) * 32;
+            if (q < cnt && off < row_bytes) {
+              float acc[NA];
+#pragma unroll
+              for (int z = 0; z < NA; ++z) acc[z] = 0.f;
+              fma_vec<DT>(acc, wa[q], va[q][u]);
+              fma_vec<DT>(acc, wb[q], vb[q][u]);
+              st_v8(out[q] + off, pack_vec<DT>(acc));
+            }
+          }
+      }
+    }
+  }
+}
+
+static moe_status_t precombine_launch(const char* recv, const int* pairs, const float* wt,
+                                      char* pre, long long n_rows, int row_bytes, int dtype,
+                                      cudaStream_t stream) {
+  const long long groups = (n_rows + 31) / 32;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 7) / 8,
+                                                                    (long long)device_sm_count() * 4));
+  void* args[] = {&recv, &pairs, &wt, &pre, &n_rows, &row_bytes};
+  const void* kern = dtype == MOE_F32 ? (const void*)k_precombine<MOE_F32>
+                                      : (const void*)k_precombine<MOE_BF16>;
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(256), 0, stream, args);
+  if (e != cudaSuccess) return cuda_status(e, "k_precombine launch");
   return MOE_OK;
 }
 
@@ -410,13 +506,14 @@ static RecvTables* recv_tables(moe_comm* c, const void* recv, size_t dup_rows, c
     return nullptr;
   if (t) {  // grow: collectively, after every rank is done with the old set
     *st = symm_release_coll(c, t->buf);
+    if (*st == MOE_OK && t->pre.base) *st = symm_release_coll(c, t->pre);
     c->tables.erase(c->tables.begin() + (t - c->tables.data()));
     if (*st != MOE_OK) return nullptr;
   }
   RecvTables n{};
   n.recv = recv;
   n.dup_rows = dup_rows;
-  *st = symm_alloc(c, kPadTabBytes + dup_rows * sizeof(int), &n.buf);  // zero-filled
+  *st = symm_alloc(c, kPadTabBytes + 3 * dup_rows * sizeof(int), &n.buf);  // zero-filled
   if (*st != MOE_OK) return nullptr;
   c->tables.push_back(n);
   return &c->tables.back();
@@ -431,6 +528,10 @@ static moe_status_t release_tables_in(moe_comm* c, const char* base, size_t byte
     if (q >= base && q < base + bytes) {
       moe_status_t s2 = symm_release_coll(c, c->tables[i].buf);
       if (s == MOE_OK) s = s2;
+      if (c->tables[i].pre.base) {
+        s2 = symm_release_coll(c, c->tables[i].pre);
+        if (s == MOE_OK) s = s2;
+      }
       c->tables.erase(c->tables.begin() + i);
     } else {
       ++i;
@@ -574,7 +675,7 @@ static moe_status_t packed_args(const char* fn, moe_comm_t* comm, const moe_gate
 // gate + layout kernel), then (unless NO_EXIT) the exit barrier, the owners'
 // duplicate-row copies and local padding.  *dup_pending: copies enqueued.
 using RowLauncher = std::function<moe_status_t(cudaStream_t, const PeerPtrs* pad_tab,
-                                               const PeerPtrs* dup_tab)>;
+                                               const PeerPtrs* dup_tab, const PeerPtrs* wt_tab)>;
 
 static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int row_bytes,
                                   const PeerPtrs& dst, int32_t flags, cudaStream_t stream,
@@ -591,7 +692,8 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int 
   // dedupe: k >= 2 and two experts can share an owner; the owners' copies
   // need the exit barrier
   bool dedupe = exit_bar && P >= 2 && D.k >= 2 && El >= 2 && tuning().p2p_dedupe;
-  PeerPtrs tab{}, dup{};
+  PeerPtrs tab{}, dup{}, wts{};
+  int* pairs_mine = nullptr;
   moe_status_t s = MOE_OK;
   if (local_pad || dedupe) {
     const RecvTables* t =
@@ -602,12 +704,14 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int 
     } else {
       for (int q = 0; q < P; ++q) {
         tab.p[q] = t->buf.peer.p[q];
-        dup.p[q] = t->buf.peer.p[q] + kPadTabBytes;
+        dup.p[q] = t->dup(q);
+        wts.p[q] = t->wts(q);
       }
+      pairs_mine = reinterpret_cast<int*>(t->pairs(r));
     }
   }
   s = run_or_queue(comm, stream, [=](cudaStream_t st) {
-    return rows(st, local_pad ? &tab : nullptr, dedupe ? &dup : nullptr);
+    return rows(st, local_pad ? &tab : nullptr, dedupe ? &dup : nullptr, dedupe ? &wts : nullptr);
   });
   if (s != MOE_OK) return s;
   *dup_pending = false;
@@ -619,7 +723,7 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int 
   if (dedupe) {
     int* dtab = reinterpret_cast<int*>(dup.p[r]);
     s = run_or_queue(comm, stream, [=](cudaStream_t st) {
-      return dup_fill_launch(mine, dtab, nrows, row_bytes, st);
+      return dup_fill_launch(mine, dtab, nrows, row_bytes, st, pairs_mine);
     });
     if (s != MOE_OK) return s;
     *dup_pending = true;
@@ -635,8 +739,8 @@ static moe_status_t dispatch_body(moe_comm* comm, const moe_gate_desc_t& D, int 
 // k_layout in peer mode as the dispatch's row kernel
 static RowLauncher layout_rows(const moe_gate_desc_t& D, const moe_routing_t& R, const void* x,
                                int ds, int d, const PeerPtrs& dst, int El, int r) {
-  return [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup) {
-    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, nullptr, nullptr, pad, dup);
+  return [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup, const PeerPtrs* wt) {
+    return layout_launch_peers(D, R, x, ds, d, dst, El, r, st, nullptr, nullptr, pad, dup, wt);
   };
 }
 
@@ -735,6 +839,51 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   comm->dup_recv = nullptr;
   const bool no_entry = flags & MOE_P2P_NO_ENTRY_BARRIER;
   const int alias = dup_pending && (flags & MOE_P2P_RECV_UNMODIFIED) ? 1 : 0;
+  // Pre-combine (k = 2, an expert may have written the rows): every owner
+  // first combines the token pairs the dispatch sent it once (k_precombine,
+  // on its own rows, after its expert), so a token whose two slots sit on
+  // one remote owner is one row read over NVLink; the symmetric pre-row
+  // buffer is allocated with the receive buffer's tables on first use
+  // outside capture (collectively).
+  PeerPtrs pre{};
+  bool pre_on = false;
+  const int row_bytes = d * ds;
+  if (dup_pending && !alias && desc->k == 2 && tuning().p2p_precombine &&
+      reverse_kspec_used(*desc, row_bytes)) {
+    RecvTables* t = nullptr;
+    for (RecvTables& u : comm->tables)
+      if (u.recv == expert_out) t = &u;
+    const size_t want = (size_t)desc->E * desc->capacity * row_bytes;
+    if (t && t->dup_rows >= (size_t)desc->E * desc->capacity && !(t->pre.base && t->pre_bytes >= want)) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+        if (t->pre.base) {
+          s = symm_release_coll(comm, t->pre);
+          t->pre = SymmBuf{};
+          if (s != MOE_OK) return s;
+        }
+        s = symm_alloc(comm, want, &t->pre);
+        if (s != MOE_OK) {
+          t->pre = SymmBuf{};
+          return s;
+        }
+        t->pre_bytes = want;
+      }
+    }
+    if (t && t->pre.base && t->pre_bytes >= want) {
+      pre_on = true;
+      for (int q = 0; q < P; ++q) pre.p[q] = t->pre.peer.p[q];
+      const char* mine = static_cast<const char*>(expert_out);
+      const int* pairs = reinterpret_cast<const int*>(t->pairs(r));
+      const float* wts = reinterpret_cast<const float*>(t->wts(r));
+      char* pre_mine = t->pre.peer.p[r];
+      const long long nrows = (long long)desc->E * desc->capacity;
+      s = run_or_queue(comm, stream, [=](cudaStream_t st) {
+        return precombine_launch(mine, pairs, wts, pre_mine, nrows, row_bytes, dtype, st);
+      });
+      if (s != MOE_OK) return s;
+    }
+  }
   if (!no_entry || (dup_pending && !alias)) {  // every rank's expert is done
     s = comm_barrier(comm, stream);
     if (s != MOE_OK) return s;
@@ -743,7 +892,7 @@ moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
   const moe_routing_t R = *routing;
   s = run_or_queue(comm, stream, [=](cudaStream_t st) {
     return reverse_launch_peers(D, R, src, D.E / P, r, dtype, ds, d, y, st, nullptr, nullptr,
-                                alias);
+                                alias, pre_on ? &pre : nullptr);
   });
   if (s != MOE_OK) return s;
   if (flags & MOE_P2P_NO_EXIT_BARRIER) return MOE_OK;
@@ -780,9 +929,10 @@ moe_status_t moe_gate_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc
   }
   bool dup_pending = false;
   s = dispatch_body(comm, D, d * ds, dst, flags, stream,
-                    [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup) {
+                    [=](cudaStream_t st, const PeerPtrs* pad, const PeerPtrs* dup,
+                        const PeerPtrs* wt) {
                       return gate_layout_launch(D, I, R, ws, x, ds, d, dst, D.E / P, r, pad, dup,
-                                                st);
+                                                st, wt);
                     },
                     &dup_pending);
   if (s != MOE_OK) return s;

@@ -58,6 +58,15 @@ struct RowArgs {
   // src_row_item.
   int dedupe;
   PeerPtrs dup;
+  // with dedupe: the owners' slot-weight tables (float per recv row): a pair
+  // sent once gets both slots' combine weights, for the combine's
+  // pre-combine (p == nullptr: not written)
+  PeerPtrs wt;
+  // peer combine (k_reverse_k, k = 2): a token whose two admitted slots sit
+  // on one remote owner reads that owner's pre-combined row (pre.p[q], the
+  // row of its second slot) instead of both expert rows; pre.p[0] == nullptr
+  // = off
+  PeerPtrs pre;
   // profiling (moe_set_trace): per CTA [entry, after the grid-dependency
   // wait, end] %globaltimer stamps at trace[4 * blockIdx.x + i], NULL = off
   unsigned long long* trace;
@@ -111,8 +120,14 @@ __device__ __forceinline__ bool dedupe_row(const RowArgs& a, int t, int j, int e
     if (s2 < 0) continue;
     const int e2 = __ldg(a.expert_idx + i);
     if (e2 / a.E_local != q) continue;
-    if (lane == 0)
-      reinterpret_cast<int*>(a.dup.p[q])[row_index(a, q, e, s)] = (int)row_index(a, q, e2, s2) + 1;
+    if (lane == 0) {
+      const size_t rb = row_index(a, q, e, s), ra = row_index(a, q, e2, s2);
+      reinterpret_cast<int*>(a.dup.p[q])[rb] = (int)ra + 1;
+      if (a.wt.p[q] && a.weight) {
+        reinterpret_cast<float*>(a.wt.p[q])[ra] = __ldg(a.weight + i);
+        reinterpret_cast<float*>(a.wt.p[q])[rb] = __ldg(a.weight + (size_t)t * a.k + j);
+      }
+    }
     return true;
   }
   return false;

@@ -89,12 +89,15 @@ def _run(world, algo, G, port):
                                               (4, "flat", 1, None), (4, "hier", 2, None),
                                               (4, "hier", 4, None), (4, "p2p", 1, None),
                                               (4, "p2p", 1, "alias"),
-                                              (4, "p2p", 1, "local_pad")])
+                                              (4, "p2p", 1, "local_pad"),
+                                              (2, "p2p", 1, "no_precombine")])
 def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
     if env == "local_pad":   # the owners zero their own padding rows (inherited by the ranks)
         monkeypatch.setenv("MOE_P2P_LOCAL_PAD", "1")
+    if env == "no_precombine":  # the combine reads both rows of a token's pair
+        monkeypatch.setenv("MOE_P2P_PRECOMBINE", "0")
     if env == "nodedupe":    # every row sent, even when a token's two experts share an owner
         monkeypatch.setenv("MOE_P2P_DEDUPE", "0")
     if env == "rev":         # peer combine walking the tokens last to first
@@ -111,7 +114,7 @@ def test_multi_gpu_route(orc, world, algo, G, env, monkeypatch):
         monkeypatch.setenv("MOE_TEST_DTYPE", "f32")
     out = _run(world, algo, G, 29600 + world * 10 + G + {"flat": 0, "hier": 3, "p2p": 6}[algo] +
                {None: 0, "local_pad": 1, "f32": 2, "rev": 3, "nodedupe": 5, "f32_alias": 7,
-                "alias": 8, "k4": 9, "k4_f32": 10, "k4_alias": 11}[env] +
+                "alias": 8, "k4": 9, "k4_f32": 10, "k4_alias": 11, "no_precombine": 12}[env] +
                (40 if env and world == 4 else 0))
     lgs = [out[r][0] for r in range(world)]
     xs = [out[r][1] for r in range(world)]

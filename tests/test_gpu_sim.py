@@ -72,7 +72,7 @@ P2P_CASES = [
     dict(P=2, S=999, d=96, E=8, k=2, C=0.6, skew=3.0),   # heavy drops, ragged
 ]
 P2P_MODES = {"default": {}, "nodedupe": {"p2p_dedupe": 0}, "local_pad": {"p2p_local_pad": 1},
-             "no_local_pad": {"p2p_local_pad": 0}}
+             "no_local_pad": {"p2p_local_pad": 0}, "no_precombine": {"p2p_precombine": 0}}
 
 
 def _route_p2p(orc, R, world, mode, expert):
@@ -120,6 +120,35 @@ def test_sim_dispatch_combine_p2p(orc, c, mode):
     with moe.tuned(**P2P_MODES[mode]), moe.SimWorld(c["P"]) as world:
         R = Ranks(orc, **c)
         _route_p2p(orc, R, world, mode, expert=True)
+
+
+@pytest.mark.parametrize("c", [c for c in P2P_CASES if c["k"] == 2],
+                         ids=lambda c: "-".join("%s=%s" % kv for kv in c.items()))
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_sim_precombine_bit_identical(orc, c, dtype):
+    """The owners' pre-combine of token pairs (k = 2, both slots on one
+    remote owner, MOE_P2P_PRECOMBINE) gives y byte for byte equal to reading
+    both rows (same fp32 FMA order, one rounding), with the s_e expert in
+    place between the dispatch and the combine."""
+    ys = {}
+    for pre in (1, 0):
+        with moe.tuned(p2p_precombine=pre), moe.SimWorld(c["P"]) as world:
+            R = Ranks(orc, **{**c, "dtype": dtype})
+            recvs = R.symm(world, (R.E, R.cap, R.d))
+            out = [torch.empty((R.S, R.d), dtype=TORCH_DT[R.dtype], device="cuda")
+                   for _ in range(R.P)]
+            for r in range(R.P):
+                world.comm(r).dispatch_p2p(R.x_dev[r], R.routings[r], recvs[r])
+            world.run()
+            torch.cuda.synchronize()
+            for r in range(R.P):
+                moe.expert_scale(recvs[r], R.P, R.El, r * R.El, out=recvs[r])
+            for r in range(R.P):
+                world.comm(r).combine_p2p(recvs[r], R.routings[r], out[r])
+            world.run()
+            torch.cuda.synchronize()
+            ys[pre] = [host(t).tobytes() for t in out]
+    assert ys[1] == ys[0]
 
 
 @pytest.mark.parametrize("c", P2P_CASES[:4] + P2P_CASES[5:6],
