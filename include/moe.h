@@ -487,8 +487,15 @@ moe_status_t moe_dispatch_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
  * every admitted row read straight from its owner rank q's `expert_out` over
  * NVLink (fp32 accumulate in ascending j, one RNE store, 0 if all slots
  * dropped), then moe_comm_barrier (the buffers may be reused).  Same result
- * as moe_alltoall(FLAT) back + moe_reverse_layout.  Flags: see above
- * (NO_ENTRY_BARRIER, NO_EXIT_BARRIER, RECV_UNMODIFIED).  expert_out:
+ * as moe_alltoall(FLAT) back + moe_reverse_layout.  With k = 2 after a
+ * deduped moe_dispatch_p2p into expert_out (and no RECV_UNMODIFIED), every
+ * rank first combines, on its own rows, the token pairs that dispatch sent
+ * it once (both slots of a token on this owner; tuning p2p_precombine), and
+ * such a token's y row is then read as that one pre-combined row: the same
+ * fp32 FMA order and rounding, byte-identical y, half the NVLink reads for
+ * those tokens (a symmetric pre-row buffer the size of expert_out is
+ * allocated collectively on first use outside stream capture).  Flags: see
+ * above (NO_ENTRY_BARRIER, NO_EXIT_BARRIER, RECV_UNMODIFIED).  expert_out:
  * symmetric, [P][E/P][cap][d] of dtype (e.g. the recv of moe_dispatch_p2p). */
 moe_status_t moe_combine_p2p(moe_comm_t* comm, const moe_gate_desc_t* desc,
                              const moe_routing_t* routing, const void* expert_out, int32_t d,
