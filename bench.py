@@ -725,7 +725,10 @@ def main():
                 else "k_reverse_k (peer combine)", "achieved": achieved, "peak": NVLINK_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_GBS, "traffic": None,
                 "algorithmic_bytes": nb,
-                "peak_source": "measured peer copy per direction (B200_PROFILING.md), 900 nominal"}
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md), 900 nominal",
+                "note": "stage time from CUDA-event nodes in the step graph: it includes the "
+                        "device barriers and owner-side copies enqueued with the row kernel; "
+                        "the row kernels' own spans are alltoall.row_kernels"}
     if fused:
         # the layout / reverse stages ARE the NVLink dispatch / combine (the
         # "reverse" and "a2a_dispatch" marks are empty stages: event resolution)
