@@ -173,9 +173,15 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
   for (int tb = (blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * TPW; tb < a.S; tb += wstride) {
     const char* b[TPW][KK];
     float w[TPW][KK];
-    int ee[TPW][KK], ss[TPW][KK];
+    // pre-combined pairs (RowArgs::pre, k = 2 only): both admitted slots on
+    // one remote owner -> that owner already computed the token's y row
+    // (same fp32 FMA order, one rounding) into its pre row of the second
+    // slot: one read, stored as is
+    bool pc[TPW];
 #pragma unroll
-    for (int p = 0; p < TPW; ++p)
+    for (int p = 0; p < TPW; ++p) {
+      pc[p] = false;
+      int e_first = 0, s_first = -1;
 #pragma unroll
       for (int j = 0; j < KK; ++j) {
         const int tl = tb + p;
@@ -183,30 +189,22 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
         const int s = tl < a.S ? __ldg(a.slot_idx + (size_t)t * KK + j) : -1;
         b[p][j] = nullptr;
         w[p][j] = 0.f;
-        ss[p][j] = s;
-        ee[p][j] = 0;
         if (s >= 0) {
           const int e = __ldg(a.expert_idx + (size_t)t * KK + j);
-          ee[p][j] = e;
           b[p][j] = AL ? src_row_item(a, t, j, e, s) : src_row(a, e, s);
           w[p][j] = row_weight(a, (size_t)t * KK + j);
-        }
-      }
-    // pre-combined pairs (RowArgs::pre): both admitted slots on one remote
-    // owner -> that owner already computed the token's y row (same fp32 FMA
-    // order, one rounding) into its pre row of the second slot: one read,
-    // stored as is
-    bool pc[TPW];
-#pragma unroll
-    for (int p = 0; p < TPW; ++p) {
-      pc[p] = false;
-      if constexpr (KK == 2 && !AL) {
-        if (a.pre.p[0] && ss[p][0] >= 0 && ss[p][1] >= 0) {
-          const int q = ee[p][1] / a.E_local;
-          if (q == ee[p][0] / a.E_local && q != a.rank) {
-            pc[p] = true;
-            b[p][0] = a.pre.p[q] + row_index(a, q, ee[p][1], ss[p][1]) * a.row_bytes;
-            b[p][1] = nullptr;
+          if constexpr (KK == 2 && !AL) {
+            if (j == 0) {
+              e_first = e;
+              s_first = s;
+            } else if (a.pre.p[0] && s_first >= 0) {
+              const int q = e / a.E_local;
+              if (q == e_first / a.E_local && q != a.rank) {
+                pc[p] = true;
+                b[p][0] = a.pre.p[q] + row_index(a, q, e, s) * a.row_bytes;
+                b[p][1] = nullptr;
+              }
+            }
           }
         }
       }
@@ -251,9 +249,14 @@ __global__ void __launch_bounds__(kRowThreads) k_reverse_k(RowArgs a) {
 #pragma unroll
             for (int j = 0; j < KK; ++j)
               if (b[p][j]) fma_vec<DT>(acc, w[p][j], r[p][j][u]);
-            const V8 o = pc[p] ? r[p][0][u] : pack_vec<DT>(acc);
-            if (a.y_ef) st_v8_ef(yrow + off, o);
-            else st_v8(yrow + off, o);
+            if constexpr (KK == 2 && !AL) {
+              const V8 o = pc[p] ? r[p][0][u] : pack_vec<DT>(acc);
+              if (a.y_ef) st_v8_ef(yrow + off, o);
+              else st_v8(yrow + off, o);
+            } else {
+              if (a.y_ef) st_v8_ef(yrow + off, pack_vec<DT>(acc));
+              else st_v8(yrow + off, pack_vec<DT>(acc));
+            }
           }
         }
       }

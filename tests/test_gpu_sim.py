@@ -184,7 +184,8 @@ def test_sim_route_pipeline_p2p(orc):
 
 
 @pytest.mark.parametrize("double_buffer", [True, False])
-def test_sim_route_pipeline_p2p_steps(orc, double_buffer):
+@pytest.mark.parametrize("P,E", [(4, 16), (8, 8), (8, 32)])
+def test_sim_route_pipeline_p2p_steps(orc, double_buffer, P, E):
     """Four RoutePipeline steps on simulated ranks over two alternating token
     sets: with double buffering the steps alternate two receive buffers,
     every combine skips its exit barrier and every dispatch after a buffer's
@@ -193,7 +194,7 @@ def test_sim_route_pipeline_p2p_steps(orc, double_buffer):
     expert: on a simulated rank only the library's calls are queued, so an
     in-place expert would run before its dispatch; the multi-GPU test covers
     the s_e expert.)"""
-    P, S, d, E, k = 4, 768, 64, 16, 2
+    S, d, k = 768, 64, 2
     with moe.SimWorld(P) as world:
         R = Ranks(orc, P, S, d, E, k)
         xs_b = [synthgen.tokens(synthgen.seed_for(29, r, 2), S, d, "bf16") for r in range(P)]
