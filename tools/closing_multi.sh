@@ -10,5 +10,12 @@ echo "EXIT $?" >> ${O}_pytest.log
 for N in 2 4; do
   [ $N -le $NMAX ] || continue
   timeout 900 python bench.py --gpus $N > ${O}_bench_N$N.json 2> ${O}_bench_N$N.err
+  echo "N=$N rc=$?" >> ${O}_rc.txt
+done
+# back-to-back repeats of the short form (start-up robustness, spread)
+for R in 1 2 3; do
+  timeout 600 python bench.py --gpus 2 --no-e2e --no-backward --cpu-seconds 1 \
+    > ${O}_rep_N2_$R.json 2> ${O}_rep_N2_$R.err
+  echo "rep N=2 $R rc=$?" >> ${O}_rc.txt
 done
 echo done > ${O}_done.txt
