@@ -233,7 +233,7 @@ def test_tuning_table_roundtrip_and_validation():
     assert moe.get_tuning() == before
     for bad in ({"layout_u": 3}, {"reverse_ku": 1}, {"gate_bwd_lanes": 6},
                 {"barrier_timeout_ms": -1}, {"nccl_cta_policy": 7},
-                {"layout_tokens_per_warp": -1}):
+                {"layout_tokens_per_warp": -1}, {"p2p_precombine": 2}):
         with pytest.raises(moe.MoeError) as ei:
             moe.set_tuning(**bad)
         assert ei.value.status == INVALID
