@@ -765,7 +765,9 @@ def main():
                            "that owner pre-combined after its expert (entry barrier kept, as "
                            "with a real expert)")
         a2a["frac"] = min(bw.values()) / NVLINK_GBS
-        if kernel_spans and "a2a_buffer" in ab:
+        if kernel_spans and "a2a_buffer" in ab and min(kernel_spans.values()) > 0:
+            # (the fused gate + dispatch kernel keeps its own trace format: no
+            # per-CTA dispatch span there, so no row-kernel figure)
             # the same bytes over the row kernels' own spans (max over ranks)
             kg = {"dispatch": ab["a2a_dispatch"] / (kernel_spans["dispatch_us"] / 1e6) / 1e9,
                   "combine": ab["a2a_combine"] / (kernel_spans["combine_us"] / 1e6) / 1e9}
