@@ -329,10 +329,11 @@ static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, 
 // step.  The warp copies up to kDupRows rows at a time, all their loads
 // issued before the first store (one HBM latency per group of rows instead
 // of per row: a trace of C2 at N=2 showed the serial per-row copy as ~8 us
-// between the dispatch and the combine).  The entries were stored by the
+// between the dispatch and the combine; 4 rows: step 242.4 -> 236.8 us, 8
+// rows with the pre-combine at 4 pairs: 225.5 -> 223.1 us).  The entries were stored by the
 // senders before their exit barrier (release) and this kernel runs after it
 // (acquire).
-constexpr int kDupRows = 4;
+constexpr int kDupRows = 8;
 __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes,
                                                   int* pairs) {
   pdl_wait();
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(256) k_precombine(const char* recv, const int*
   pdl_trigger();
   constexpr int NA = DT == MOE_F32 ? 8 : 16;
   constexpr int kS = 2;      // 1 KiB segments per round
-  constexpr int kPairs = 2;  // pairs per warp with all their loads in flight
+  constexpr int kPairs = 4;  // pairs per warp with all their loads in flight
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
   for (long long base = gw * 32; base < n; base += nw * 32) {
