@@ -334,13 +334,14 @@ static moe_status_t pad_fill_launch(char* local, const int* tab, int P, int El, 
 // senders before their exit barrier (release) and this kernel runs after it
 // (acquire).
 constexpr int kDupRows = 8;
-__global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long long n, int row_bytes,
+__global__ void __launch_bounds__(128) k_dup_fill(char* recv, int* tab, long long n, int row_bytes,
                                                   int* pairs) {
   pdl_wait();
   pdl_trigger();
   constexpr int kV = 4;  // 16-byte vectors per lane per row segment: 2 KiB of a row per round
   const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  const int wpc = blockDim.x >> 5;  // warps per CTA
+  const long long gw = (long long)blockIdx.x * wpc + (threadIdx.x >> 5), nw = (long long)gridDim.x * wpc;
   for (long long base = gw * 32; base < n; base += nw * 32) {
     const long long i = base + lane;
     const int v = i < n ? tab[i] : 0;
@@ -390,10 +391,12 @@ __global__ void __launch_bounds__(256) k_dup_fill(char* recv, int* tab, long lon
 moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_bytes,
                              cudaStream_t stream, int* pairs) {
   const long long groups = (n_rows + 31) / 32;
-  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 7) / 8,
-                                                                    (long long)device_sm_count() * 4));
+  // 128-thread CTAs: two fit per SM at ~200 registers, so every warp of
+  // the (single) pass is resident at once
+  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 3) / 4,
+                                                                    (long long)device_sm_count() * 8));
   void* args[] = {&recv, &tab, &n_rows, &row_bytes, &pairs};
-  cudaError_t e = launch_pdl((const void*)k_dup_fill, dim3(grid), dim3(256), 0, stream, args);
+  cudaError_t e = launch_pdl((const void*)k_dup_fill, dim3(grid), dim3(128), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "k_dup_fill launch");
   return MOE_OK;
 }
@@ -407,7 +410,7 @@ moe_status_t dup_fill_launch(char* recv, int* tab, long long n_rows, int row_byt
 // row over NVLink instead of two.  A warp per 32 table entries; the weights
 // came with the dispatch (RowArgs::wt).  Rows are 32-byte multiples.
 template <int DT>
-__global__ void __launch_bounds__(256) k_precombine(const char* recv, const int* pairs,
+__global__ void __launch_bounds__(128) k_precombine(const char* recv, const int* pairs,
                                                     const float* wt, char* pre, long long n,
                                                     int row_bytes) {
   pdl_wait();
@@ -416,7 +419,8 @@ __global__ void __launch_bounds__(256) k_precombine(const char* recv, const int*
   constexpr int kS = 2;      // 1 KiB segments per round
   constexpr int kPairs = 4;  // pairs per warp with all their loads in flight
   const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  const int wpc = blockDim.x >> 5;  // warps per CTA
+  const long long gw = (long long)blockIdx.x * wpc + (threadIdx.x >> 5), nw = (long long)gridDim.x * wpc;
   for (long long base = gw * 32; base < n; base += nw * 32) {
     const long long i = base + lane;
     const int v = i < n ? pairs[i] : 0;
@@ -479,12 +483,14 @@ static moe_status_t precombine_launch(const char* recv, const int* pairs, const 
                                       char* pre, long long n_rows, int row_bytes, int dtype,
                                       cudaStream_t stream) {
   const long long groups = (n_rows + 31) / 32;
-  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 7) / 8,
-                                                                    (long long)device_sm_count() * 4));
+  // 128-thread CTAs: two fit per SM at ~200 registers, so every warp of
+  // the (single) pass is resident at once
+  const int grid = (int)std::max<long long>(1, std::min<long long>((groups + 3) / 4,
+                                                                    (long long)device_sm_count() * 8));
   void* args[] = {&recv, &pairs, &wt, &pre, &n_rows, &row_bytes};
   const void* kern = dtype == MOE_F32 ? (const void*)k_precombine<MOE_F32>
                                       : (const void*)k_precombine<MOE_BF16>;
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(256), 0, stream, args);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(128), 0, stream, args);
   if (e != cudaSuccess) return cuda_status(e, "k_precombine launch");
   return MOE_OK;
 }
